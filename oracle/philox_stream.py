@@ -1,0 +1,107 @@
+"""CPU emulation of the device noise stream (csrc/philox.cuh).
+
+TEST INFRASTRUCTURE ONLY.  Philox4x32-10 (Salmon, Moraes, Dror, Shaw, SC'11;
+the Random123 reference algorithm -- restated here from the published round
+function, pinned by the Random123 known-answer vectors in
+tests/test_oracle_golden.py) with the repo's counter layout and Box-Muller
+mapping.  Integer outputs (Philox words, jump indicators) are bit-exact with
+the device; normals agree to ~1e-6 relative (the device uses MUFU
+lg2/sqrt/sin/cos approximations, this emulation float64 libm).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+M0, M1 = np.uint64(0xD2511F53), np.uint64(0xCD9E8D57)
+W0, W1 = np.uint32(0x9E3779B9), np.uint32(0xBB67AE85)
+MASK = np.uint64(0xFFFFFFFF)
+
+SLOT_DIFFUSION, SLOT_JUMP_UNIFORM, SLOT_MARK, SLOT_PLANT = 0, 1, 2, 3
+
+
+def philox4x32_10(c0, c1, c2, c3, k0, k1):
+    """Vectorised Philox4x32-10 on uint32 arrays; returns 4 uint32 arrays."""
+    c0, c1, c2, c3 = (np.asarray(v, dtype=np.uint32) for v in (c0, c1, c2, c3))
+    c0, c1, c2, c3 = np.broadcast_arrays(c0, c1, c2, c3)
+    k0 = np.uint32(k0)
+    k1 = np.uint32(k1)
+    with np.errstate(over="ignore"):
+        for _ in range(10):
+            p0 = M0 * c0.astype(np.uint64)
+            p1 = M1 * c2.astype(np.uint64)
+            hi0, lo0 = (p0 >> np.uint64(32)).astype(np.uint32), (p0 & MASK).astype(np.uint32)
+            hi1, lo1 = (p1 >> np.uint64(32)).astype(np.uint32), (p1 & MASK).astype(np.uint32)
+            c0, c1, c2, c3 = hi1 ^ c1 ^ k0, lo1, hi0 ^ c3 ^ k1, lo0
+            k0 = np.uint32(k0 + W0)
+            k1 = np.uint32(k1 + W1)
+    return c0, c1, c2, c3
+
+
+def stream_key(seed: int, iteration: int):
+    seed, iteration = int(seed), int(iteration)
+    return (seed & 0xFFFFFFFF, (seed >> 32) & 0xFFFFFFFF, iteration & 0xFFFFFFFF,
+            (iteration >> 32) & 0xFFFFFF)
+
+
+def draw(key, slot, block, sample):
+    k0, k1, c2, c3 = key
+    c3s = np.uint32(c3 | (slot << 24))
+    return philox4x32_10(block, sample, np.uint32(c2), c3s, k0, k1)
+
+
+def _f32_from_bits(bits):
+    return np.asarray(bits, dtype=np.uint32).view(np.float32)
+
+
+def box_muller(a, b):
+    """Device mapping: u1 = 2 - [1,2) in (0,1], angle = [1,2)*2pi - 3pi."""
+    one = np.uint32(0x3F800000)
+    u1 = (np.float32(2.0) - _f32_from_bits(one | (np.asarray(a, np.uint32) >> np.uint32(9)))).astype(np.float64)
+    f = _f32_from_bits(one | (np.asarray(b, np.uint32) >> np.uint32(9))).astype(np.float64)
+    ang = np.float32(f * np.float64(np.float32(6.2831853071795865)) + np.float64(np.float32(-9.4247779607693797)))
+    r = np.sqrt(-2.0 * np.log(u1))
+    return r * np.cos(np.float64(ang)), r * np.sin(np.float64(ang))
+
+
+def jump_threshold(p: float) -> int:
+    if not p > 0:
+        return 0
+    thr = min(int(np.ceil(p * 16777216.0)), 16777215)
+    return thr << 8
+
+
+def device_noise(seed, iteration, K, T, m, q, Ld, Lj, mark_mean, jthr, jump_channel="control",
+                 sample_offset=0):
+    """(eps_d, ind, eps_j, eps_c) as the device sampler draws them (float64).
+
+    Ld (m x m) = chol(c Sigma_D), Lj (q x q) = chol(Sigma_J), jthr from
+    jump_threshold(nu dt) (0 = no jumps)."""
+    key = stream_key(seed, iteration)
+    MP = 4 if m == 3 else m
+    k = (np.arange(K, dtype=np.int64) + sample_offset).astype(np.uint32)[:, None]
+    # diffusion normals: index i = t*MP + j, block i>>2
+    nblk = (T * MP + 3) // 4
+    blocks = np.arange(nblk, dtype=np.uint32)[None, :]
+    w = draw(key, SLOT_DIFFUSION, blocks, k)
+    z01 = box_muller(w[0], w[1])
+    z23 = box_muller(w[2], w[3])
+    z = np.stack([z01[0], z01[1], z23[0], z23[1]], axis=-1).reshape(K, nblk * 4)[:, : T * MP]
+    z = z.reshape(K, T, MP)[:, :, :m]
+    eps_d = np.einsum("jl,ktl->ktj", np.tril(Ld), z)
+    ind = np.zeros((K, T), dtype=np.int64)
+    eps_j = np.zeros((K, T, q))
+    if jthr:
+        ublk = np.arange((T + 3) // 4, dtype=np.uint32)[None, :]
+        uw = draw(key, SLOT_JUMP_UNIFORM, ublk, k)
+        words = np.stack(uw, axis=-1).reshape(K, -1)[:, :T]
+        ind = (words < np.uint32(jthr)).astype(np.int64)
+        rows, cols = np.nonzero(ind)
+        if rows.size:
+            mw = draw(key, SLOT_MARK, cols.astype(np.uint32), k[rows, 0])
+            a01 = box_muller(mw[0], mw[1])
+            a23 = box_muller(mw[2], mw[3])
+            zz = np.stack([a01[0], a01[1], a23[0], a23[1]], axis=-1)[:, :q]
+            eps_j[rows, cols] = np.asarray(mark_mean, float)[:q] + zz @ np.tril(Lj).T
+    eps_c = eps_d + eps_j if jump_channel == "control" else eps_d.copy()
+    return eps_d, ind, eps_j, eps_c

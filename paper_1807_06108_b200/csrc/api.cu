@@ -1,0 +1,848 @@
+// api.cu -- the extern "C" boundary (include/jmppi.h).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#define JM_COMMON_KERNELS
+#include "internal.h"
+
+using jm::DiagOut;
+using jm::LoopState;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(jm_ctx* c, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  if (c) c->err = buf;
+  return code;
+}
+
+#define CK(expr)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (expr);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(ctx, JM_ERR_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, \
+                  __LINE__);                                                              \
+  } while (0)
+
+// Lower Cholesky of an n x n row-major matrix (reads the lower triangle, like
+// numpy.linalg.cholesky / LAPACK potrf 'L'; noise.py:63-68).
+bool cholesky(const double* A, int n, double* L) {
+  for (int i = 0; i < 16; ++i) L[i] = 0.0;
+  for (int i = 0; i < n; ++i) {
+    for (int j = 0; j <= i; ++j) {
+      double s = A[i * n + j];
+      for (int k = 0; k < j; ++k) s -= L[i * n + k] * L[j * n + k];
+      if (i == j) {
+        if (!(s > 0.0) || !std::isfinite(s)) return false;
+        L[i * n + i] = std::sqrt(s);
+      } else {
+        L[i * n + j] = s / L[j * n + j];
+      }
+    }
+  }
+  return true;
+}
+
+uint32_t jump_threshold(double p) {
+  // jump iff (word >> 8) * 2^-24 < p  <=>  word < ceil(p 2^24) << 8
+  if (!(p > 0.0)) return 0u;
+  double thr = std::ceil(p * 16777216.0);
+  if (thr > 16777215.0) thr = 16777215.0;
+  return ((uint32_t)thr) << 8;
+}
+
+template <typename T>
+cudaError_t dalloc(T** p, size_t count) {
+  *p = nullptr;
+  if (count == 0) return cudaSuccess;
+  return cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+}
+
+void dfree(void* p) {
+  if (p) cudaFree(p);
+}
+
+// ---------------------------------------------------------------- update_controls kernels
+// compute_weights (controller.py:62-71): one CTA, fixed-order reduction.
+__global__ void cw_kernel(const double* costs, int64_t K, double inv_lam, double* w, double* out2) {
+  __shared__ double s[1024];
+  __shared__ double s_rho;
+  const int tid = threadIdx.x;
+  double m = CUDART_INF;
+  for (int64_t k = tid; k < K; k += blockDim.x) {
+    const double c = costs[k];
+    if (isfinite(c)) m = fmin(m, c);
+  }
+  s[tid] = m;
+  __syncthreads();
+  if (tid == 0) {
+    double mm = CUDART_INF;
+    for (int i = 0; i < (int)blockDim.x; ++i) mm = fmin(mm, s[i]);
+    s_rho = mm;
+  }
+  __syncthreads();
+  const double rho = s_rho;
+  double z = 0.0;
+  for (int64_t k = tid; k < K; k += blockDim.x) {
+    const double c = costs[k];
+    const double e = (isfinite(c) && rho != CUDART_INF) ? exp(-(c - rho) * inv_lam) : 0.0;
+    w[k] = e;
+    z += e;
+  }
+  __syncthreads();
+  s[tid] = z;
+  __syncthreads();
+  if (tid == 0) {
+    double zz = 0.0;
+    for (int i = 0; i < (int)blockDim.x; ++i) zz += s[i];
+    out2[0] = rho;
+    out2[1] = zz;
+  }
+  __syncthreads();
+  const double Z = out2[1];
+  for (int64_t k = tid; k < K; k += blockDim.x) w[k] = (Z > 0.0) ? w[k] / Z : 0.0;
+}
+
+// _weighted_noise_average + update (controller.py:74-93): column r of the
+// stacked (K, T*m) eps, fixed k order.
+__global__ void wavg_kernel(const double* w, const double* eps, int64_t K, int TM, int M,
+                            double inv_sdt, const double* u_nom, const double* mapping,
+                            double* u_new) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t * M >= TM) return;
+  double d[4] = {0, 0, 0, 0};
+  for (int64_t k = 0; k < K; ++k) {
+    const double wk = w[k];
+    for (int j = 0; j < M; ++j) d[j] = fma(wk, eps[k * TM + t * M + j], d[j]);
+  }
+  for (int j = 0; j < M; ++j) {
+    double out = 0.0;
+    if (mapping) {
+      for (int l = 0; l < M; ++l) out += (d[l] * inv_sdt) * mapping[j * M + l];
+    } else {
+      out = d[j] * inv_sdt;
+    }
+    u_new[t * M + j] = u_nom[t * M + j] + out;
+  }
+}
+
+int rollout_and_finalize(jm_ctx* ctx, const jm::RolloutCall& rc, const double* mapping_dev,
+                         bool want_weights) {
+  CK(ctx->eng->rollout(ctx, rc));
+  jm::FinArgs f{};
+  f.rec = ctx->d_records;
+  f.nrec = ctx->grid;
+  f.rec_stride = ctx->rec_stride;
+  f.TM = ctx->TM;
+  f.M = ctx->M;
+  f.inv_lam = 1.0 / ctx->mppi.lambda_;
+  f.inv_sdt = 1.0 / std::sqrt(ctx->mppi.dt);
+  f.u_nom = rc.u_nom;
+  f.mapping = mapping_dev;
+  f.u_new = ctx->d_small + ctx->off_unew();
+  f.norms = ctx->d_small + ctx->off_norms();
+  f.diag = ctx->d_diag();
+  f.status = ctx->d_status();
+  const int fgrid = (ctx->TM + jm::kFinCols - 1) / jm::kFinCols;
+  jm::finalize_kernel<<<fgrid, jm::kFinThreads, 0, ctx->stream>>>(f);
+  CK(cudaGetLastError());
+  if (want_weights) {
+    const int b = 256, g = (ctx->K + b - 1) / b;
+    jm::weights_kernel<<<g, b, 0, ctx->stream>>>(ctx->d_costs, ctx->d_diag(), 1.0 / ctx->mppi.lambda_,
+                                                 ctx->K, ctx->d_weights);
+    CK(cudaGetLastError());
+  }
+  return JM_OK;
+}
+
+int ensure_trace(jm_ctx* ctx) {
+  const size_t need = (size_t)ctx->K * (ctx->T + 1) * ctx->N;
+  if (ctx->states_cap >= need) return JM_OK;
+  dfree(ctx->d_states);
+  dfree(ctx->d_div);
+  ctx->d_states = nullptr;
+  ctx->d_div = nullptr;
+  CK(dalloc(&ctx->d_states, need));
+  CK(dalloc(&ctx->d_div, (size_t)ctx->K));
+  ctx->states_cap = need;
+  return JM_OK;
+}
+
+int capture_loop_graph(jm_ctx* ctx) {
+  if (ctx->graph_exec) return JM_OK;
+  cudaStream_t saved = ctx->stream;
+  ctx->stream = ctx->own_stream;
+  CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  jm::RolloutCall rc;
+  rc.u_nom = ctx->d_loop_unom;
+  rc.costs = ctx->d_costs;
+  rc.loop = ctx->d_loop;
+  cudaError_t e1 = ctx->eng->rollout(ctx, rc);
+  jm::FinArgs f{};
+  f.rec = ctx->d_records;
+  f.nrec = ctx->grid;
+  f.rec_stride = ctx->rec_stride;
+  f.TM = ctx->TM;
+  f.M = ctx->M;
+  f.inv_lam = 1.0 / ctx->mppi.lambda_;
+  f.inv_sdt = 1.0 / std::sqrt(ctx->mppi.dt);
+  f.u_nom = ctx->d_loop_unom;
+  f.u_new = ctx->d_loop_unew;
+  f.loop = ctx->d_loop;
+  const int fgrid = (ctx->TM + jm::kFinCols - 1) / jm::kFinCols;
+  jm::finalize_kernel<<<fgrid, jm::kFinThreads, 0, ctx->stream>>>(f);
+  cudaError_t e2 = cudaGetLastError();
+  cudaError_t e3 = ctx->eng->plant(ctx, ctx->d_loop, ctx->d_loop_unew, ctx->d_loop_unom);
+  cudaGraph_t g = nullptr;
+  cudaError_t e4 = cudaStreamEndCapture(ctx->stream, &g);
+  ctx->stream = saved;
+  CK(e1);
+  CK(e2);
+  CK(e3);
+  CK(e4);
+  ctx->graph = g;
+  CK(cudaGraphInstantiate(&ctx->graph_exec, g, 0));
+  return JM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int jm_abi_version(void) { return JM_ABI_VERSION; }
+
+const char* jm_last_error(const jm_ctx* ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
+
+int jm_device_count(int* out) {
+  jm_ctx* ctx = nullptr;
+  CK(cudaGetDeviceCount(out));
+  return JM_OK;
+}
+
+int jm_create(const jm_model_desc* model, const jm_cost_desc* cost, const jm_mppi_desc* mppi,
+              int device, jm_ctx** out) {
+  jm_ctx* ctx = nullptr;
+  if (!model || !cost || !mppi || !out) return fail(nullptr, JM_ERR_VALUE, "null argument");
+  *out = nullptr;
+  const jm_mppi_desc& p = *mppi;
+  // MppiConfig invariants (types.py:90-113)
+  if (!(p.lambda_ > 0)) return fail(nullptr, JM_ERR_CONFIG, "invalid configuration: lambda must be positive");
+  if (!(p.c >= 1.0)) return fail(nullptr, JM_ERR_CONFIG, "invalid configuration: c must be at least 1");
+  if (!(p.dt > 0)) return fail(nullptr, JM_ERR_CONFIG, "invalid configuration: dt must be positive");
+  if (!(p.nu >= 0)) return fail(nullptr, JM_ERR_CONFIG, "invalid configuration: nu must be nonnegative");
+  if (p.horizon < 1) return fail(nullptr, JM_ERR_CONFIG, "invalid configuration: horizon_n must be a positive integer");
+  if (p.samples < 1) return fail(nullptr, JM_ERR_CONFIG, "invalid configuration: samples_m must be a positive integer");
+  if (!(cost->lambda_ > 0)) return fail(nullptr, JM_ERR_CONFIG, "invalid configuration: cost lambda must be positive");
+  if (!(cost->c >= 1.0)) return fail(nullptr, JM_ERR_CONFIG, "invalid configuration: cost c must be at least 1");
+  const int m = model->control_dim, n = model->state_dim;
+  if (m != p.control_dim) return fail(nullptr, JM_ERR_CONFIG, "control_dim mismatch between model (%d) and config (%d)", m, p.control_dim);
+  if (p.jump_enabled && !(p.nu * p.dt < 0.1))  // noise.py:148-149
+    return fail(nullptr, JM_ERR_VALUE, "zero-one jump law violated (nu*dt = %g)", p.nu * p.dt);
+
+  ctx = new jm_ctx();
+  ctx->model = *model;
+  ctx->cost = *cost;
+  ctx->mppi = p;
+  ctx->device = device;
+  ctx->N = n;
+  ctx->M = m;
+  ctx->T = p.horizon;
+  ctx->K = p.samples;
+  ctx->TM = ctx->T * m;
+  ctx->Q = model->jump_channel == JM_JUMP_CONTROL ? m : model->jump_dim;
+  ctx->rec_stride = 4 + ctx->TM + (ctx->TM & 1);
+  ctx->real_size = p.precision == JM_F64 ? 8 : 4;
+  ctx->block = p.block_threads > 0 ? p.block_threads : 128;
+  if (ctx->block % 32 != 0 || ctx->block > 256) {
+    delete ctx;
+    return fail(nullptr, JM_ERR_CONFIG, "block_threads must be a multiple of 32 and <= 256");
+  }
+  // factors (noise.py:143, :150; harness.py:123-124)
+  double cs[16];
+  for (int i = 0; i < m * m; ++i) cs[i] = p.c * p.sigma_d[i];
+  if (!cholesky(cs, m, ctx->Ld)) {
+    delete ctx;
+    return fail(nullptr, JM_ERR_NOISE, "covariance factorization failed for c*sigma_d");
+  }
+  if (!cholesky(p.sigma_d, m, ctx->Lp)) {
+    delete ctx;
+    return fail(nullptr, JM_ERR_NOISE, "covariance factorization failed for sigma_d");
+  }
+  if (!cholesky(p.sigma_j, ctx->Q, ctx->Lj)) {
+    delete ctx;
+    return fail(nullptr, JM_ERR_NOISE, "covariance factorization failed for sigma_j");
+  }
+  ctx->jthr = p.jump_enabled ? jump_threshold(p.nu * p.dt) : 0u;
+  ctx->jthr_plant = jump_threshold(p.nu * p.dt);
+
+  // plugin -> kernel family
+  switch (model->kind) {
+    case JM_MODEL_INTEGRATOR:
+      if (n != m) break;
+      ctx->eng = jm::make_engine_integrator(cost->kind, p.precision, n);
+      break;
+    case JM_MODEL_CARTPOLE:
+      if (n != 4 || m != 1) break;
+      ctx->eng = jm::make_engine_cartpole(cost->kind, p.precision);
+      break;
+    case JM_MODEL_QUADROTOR:
+      if (n != 12 || m != 4) break;
+      ctx->eng = jm::make_engine_quadrotor(cost->kind, p.precision);
+      break;
+    default:
+      break;
+  }
+  if (!ctx->eng) {
+    delete ctx;
+    return fail(nullptr, JM_ERR_UNSUPPORTED, "no kernel for model kind %d (n=%d, m=%d) with cost kind %d",
+                model->kind, n, m, cost->kind);
+  }
+  if (model->jump_channel == JM_JUMP_STATE) {
+    // the state-jump selector rows are compiled into each model
+    const int expect_q = model->kind == JM_MODEL_CARTPOLE ? 1 : (model->kind == JM_MODEL_QUADROTOR ? 3 : n);
+    bool ok = ctx->Q == expect_q;
+    for (int i = 0; ok && i < ctx->Q; ++i) {
+      const int row = model->kind == JM_MODEL_CARTPOLE ? 3 : (model->kind == JM_MODEL_QUADROTOR ? 3 + i : i);
+      ok = model->jump_rows[i] == row;
+    }
+    if (!ok) {
+      delete ctx->eng;
+      delete ctx;
+      return fail(nullptr, JM_ERR_UNSUPPORTED,
+                  "state-jump selector not supported for this model (cartpole: row 3; quadrotor: rows 3,4,5)");
+    }
+  }
+
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = ctx->eng->configure(ctx);
+  ctx->stream = ctx->own_stream;
+  if (e == cudaSuccess && p.noise_source == JM_NOISE_PHILOX)
+    e = cudaMalloc(&ctx->d_scratch, (size_t)ctx->grid * ctx->TM * ctx->block * ctx->real_size);
+  if (e == cudaSuccess) e = dalloc(&ctx->d_costs, (size_t)ctx->K);
+  if (e == cudaSuccess) e = dalloc(&ctx->d_weights, (size_t)ctx->K);
+  if (e == cudaSuccess) e = dalloc(&ctx->d_records, (size_t)ctx->grid * ctx->rec_stride);
+  if (e == cudaSuccess) e = dalloc(&ctx->d_small, ctx->small_doubles());
+  if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_small, ctx->small_doubles() * sizeof(double));
+  if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_big, 2 * (size_t)ctx->K * sizeof(double));
+  if (e == cudaSuccess) e = cudaMemsetAsync(ctx->d_small, 0, ctx->small_doubles() * sizeof(double), ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) {
+    const std::string msg = cudaGetErrorString(e);
+    jm_destroy(ctx);
+    return fail(nullptr, JM_ERR_CUDA, "jm_create: %s", msg.c_str());
+  }
+  *out = ctx;
+  return JM_OK;
+}
+
+int jm_destroy(jm_ctx* ctx) {
+  if (!ctx) return JM_OK;
+  cudaSetDevice(ctx->device);
+  if (ctx->own_stream) cudaStreamSynchronize(ctx->own_stream);
+  if (ctx->graph_exec) cudaGraphExecDestroy(ctx->graph_exec);
+  if (ctx->graph) cudaGraphDestroy(ctx->graph);
+  dfree(ctx->d_scratch);
+  dfree(ctx->d_hbm_eps);
+  dfree(ctx->d_hbm_jump);
+  dfree(ctx->d_costs);
+  dfree(ctx->d_weights);
+  dfree(ctx->d_records);
+  dfree(ctx->d_small);
+  dfree(ctx->d_states);
+  dfree(ctx->d_div);
+  dfree(ctx->d_loop);
+  dfree(ctx->d_loop_unom);
+  dfree(ctx->d_loop_unew);
+  dfree(ctx->d_hist);
+  dfree(ctx->d_hist_jumps);
+  dfree(ctx->d_hist_t);
+  if (ctx->h_small) cudaFreeHost(ctx->h_small);
+  if (ctx->h_big) cudaFreeHost(ctx->h_big);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  delete ctx->eng;
+  delete ctx;
+  return JM_OK;
+}
+
+int jm_set_stream(jm_ctx* ctx, void* stream) {
+  if (!ctx) return fail(nullptr, JM_ERR_VALUE, "null context");
+  ctx->stream = stream ? reinterpret_cast<cudaStream_t>(stream) : ctx->own_stream;
+  return JM_OK;
+}
+
+int jm_record_doubles(const jm_ctx* ctx, int64_t* out) {
+  if (!ctx || !out) return fail(nullptr, JM_ERR_VALUE, "null argument");
+  *out = ctx->rec_stride;
+  return JM_OK;
+}
+
+int jm_iteration_host(jm_ctx* ctx, const double* x0, const double* u_nom, uint64_t seed,
+                      uint64_t iteration, const void* eps_c, const void* jump,
+                      const double* mapping, double* u_new, double* costs, double* weights,
+                      double* step_norms, double* states, int64_t* diverged_step, jm_diag* diag) {
+  if (!ctx || !x0 || !u_nom || !u_new) return fail(ctx, JM_ERR_VALUE, "null argument");
+  CK(cudaSetDevice(ctx->device));
+  const bool hbm = ctx->mppi.noise_source == JM_NOISE_HBM;
+  if (hbm && !eps_c) return fail(ctx, JM_ERR_VALUE, "HBM noise mode needs eps_combined");
+  if (hbm && ctx->model.jump_channel == JM_JUMP_STATE && ctx->jthr && !jump)
+    return fail(ctx, JM_ERR_VALUE, "HBM noise mode with state jumps needs the jump tensor");
+  const int N = ctx->N, M = ctx->M, TM = ctx->TM, T = ctx->T, K = ctx->K;
+  double* hs = ctx->h_small;
+  double* ds = ctx->d_small;
+  std::memcpy(hs + ctx->off_x0(), x0, sizeof(double) * N);
+  std::memcpy(hs + ctx->off_unom(), u_nom, sizeof(double) * TM);
+  if (mapping) std::memcpy(hs + ctx->off_map(), mapping, sizeof(double) * M * M);
+  CK(cudaMemcpyAsync(ds, hs, sizeof(double) * ctx->off_unew(), cudaMemcpyHostToDevice, ctx->stream));
+  jm::RolloutCall rc;
+  rc.x0 = ds + ctx->off_x0();
+  rc.u_nom = ds + ctx->off_unom();
+  rc.seed = seed;
+  rc.iteration = iteration;
+  rc.costs = ctx->d_costs;
+  if (hbm) {
+    const size_t eb = (size_t)TM * K * ctx->real_size;
+    if (!ctx->d_hbm_eps) CK(cudaMalloc(&ctx->d_hbm_eps, eb));
+    CK(cudaMemcpyAsync(ctx->d_hbm_eps, eps_c, eb, cudaMemcpyHostToDevice, ctx->stream));
+    rc.eps_in = ctx->d_hbm_eps;
+    if (jump && ctx->model.jump_channel == JM_JUMP_STATE) {
+      const size_t jb = (size_t)T * ctx->Q * K * ctx->real_size;
+      if (!ctx->d_hbm_jump) CK(cudaMalloc(&ctx->d_hbm_jump, jb));
+      CK(cudaMemcpyAsync(ctx->d_hbm_jump, jump, jb, cudaMemcpyHostToDevice, ctx->stream));
+      rc.jump_in = ctx->d_hbm_jump;
+    }
+  }
+  const bool trace = states != nullptr || diverged_step != nullptr;
+  if (trace) {
+    const int r = ensure_trace(ctx);
+    if (r != JM_OK) return r;
+    rc.states = ctx->d_states;
+    rc.diverged = ctx->d_div;
+  }
+  const int r = rollout_and_finalize(ctx, rc, mapping ? ds + ctx->off_map() : nullptr, weights != nullptr);
+  if (r != JM_OK) return r;
+  const size_t out_n = ctx->off_rec() - ctx->off_unew();
+  CK(cudaMemcpyAsync(hs + ctx->off_unew(), ds + ctx->off_unew(), sizeof(double) * out_n,
+                     cudaMemcpyDeviceToHost, ctx->stream));
+  if (costs) CK(cudaMemcpyAsync(ctx->h_big, ctx->d_costs, sizeof(double) * K, cudaMemcpyDeviceToHost, ctx->stream));
+  if (weights)
+    CK(cudaMemcpyAsync(ctx->h_big + K, ctx->d_weights, sizeof(double) * K, cudaMemcpyDeviceToHost, ctx->stream));
+  if (states)
+    CK(cudaMemcpyAsync(states, ctx->d_states, sizeof(double) * (size_t)K * (T + 1) * N,
+                       cudaMemcpyDeviceToHost, ctx->stream));
+  if (diverged_step)
+    CK(cudaMemcpyAsync(diverged_step, ctx->d_div, sizeof(int64_t) * K, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  const int32_t status = *reinterpret_cast<int32_t*>(hs + ctx->off_status());
+  const DiagOut* dg = reinterpret_cast<const DiagOut*>(hs + ctx->off_diag());
+  if (costs) std::memcpy(costs, ctx->h_big, sizeof(double) * K);
+  if (status == JM_ERR_NO_VIABLE) return fail(ctx, JM_ERR_NO_VIABLE, "no viable rollout");
+  std::memcpy(u_new, hs + ctx->off_unew(), sizeof(double) * TM);
+  if (step_norms) std::memcpy(step_norms, hs + ctx->off_norms(), sizeof(double) * T);
+  if (weights) std::memcpy(weights, ctx->h_big + K, sizeof(double) * K);
+  if (diag) {
+    diag->min_cost = dg->min_cost;
+    diag->ess = dg->ess;
+    diag->normaliser = dg->normaliser;
+    diag->n_finite = dg->n_finite;
+  }
+  return JM_OK;
+}
+
+int jm_rollout_dev(jm_ctx* ctx, const double* x0_dev, const double* u_nom_dev, uint64_t seed,
+                   uint64_t iteration, const uint64_t* iteration_dev, const void* eps_c_dev,
+                   const void* jump_dev, double* costs_dev, double* states_dev, int64_t* diverged_dev) {
+  if (!ctx || !x0_dev || !u_nom_dev) return fail(ctx, JM_ERR_VALUE, "null argument");
+  if (ctx->mppi.noise_source == JM_NOISE_HBM && !eps_c_dev)
+    return fail(ctx, JM_ERR_VALUE, "HBM noise mode needs eps_combined");
+  CK(cudaSetDevice(ctx->device));
+  jm::RolloutCall rc;
+  rc.x0 = x0_dev;
+  rc.u_nom = u_nom_dev;
+  rc.seed = seed;
+  rc.iteration = iteration;
+  rc.iteration_dev = iteration_dev;
+  rc.eps_in = eps_c_dev;
+  rc.jump_in = ctx->model.jump_channel == JM_JUMP_STATE ? jump_dev : nullptr;
+  rc.costs = costs_dev ? costs_dev : ctx->d_costs;
+  rc.states = states_dev;
+  rc.diverged = diverged_dev;
+  if ((states_dev == nullptr) != (diverged_dev == nullptr))
+    return fail(ctx, JM_ERR_VALUE, "states and diverged buffers go together");
+  CK(ctx->eng->rollout(ctx, rc));
+  return JM_OK;
+}
+
+int jm_reduce_dev(jm_ctx* ctx, double* record_dev) {
+  if (!ctx || !record_dev) return fail(ctx, JM_ERR_VALUE, "null argument");
+  CK(cudaSetDevice(ctx->device));
+  jm::FinArgs f{};
+  f.rec = ctx->d_records;
+  f.nrec = ctx->grid;
+  f.rec_stride = ctx->rec_stride;
+  f.TM = ctx->TM;
+  f.M = ctx->M;
+  f.inv_lam = 1.0 / ctx->mppi.lambda_;
+  f.inv_sdt = 1.0 / std::sqrt(ctx->mppi.dt);
+  f.rec_out = record_dev;
+  const int fgrid = (ctx->TM + jm::kFinCols - 1) / jm::kFinCols;
+  jm::finalize_kernel<<<fgrid, jm::kFinThreads, 0, ctx->stream>>>(f);
+  CK(cudaGetLastError());
+  return JM_OK;
+}
+
+int jm_finalize_dev(jm_ctx* ctx, const double* records_dev, int32_t nrec, const double* u_nom_dev,
+                    const double* mapping_dev, double* u_new_dev, double* step_norms_dev,
+                    jm_diag* diag_dev, int32_t* status_dev) {
+  if (!ctx || !u_nom_dev || !u_new_dev) return fail(ctx, JM_ERR_VALUE, "null argument");
+  CK(cudaSetDevice(ctx->device));
+  jm::FinArgs f{};
+  f.rec = records_dev ? records_dev : ctx->d_records;
+  f.nrec = records_dev ? nrec : ctx->grid;
+  f.rec_stride = ctx->rec_stride;
+  f.TM = ctx->TM;
+  f.M = ctx->M;
+  f.inv_lam = 1.0 / ctx->mppi.lambda_;
+  f.inv_sdt = 1.0 / std::sqrt(ctx->mppi.dt);
+  f.u_nom = u_nom_dev;
+  f.mapping = mapping_dev;
+  f.u_new = u_new_dev;
+  f.norms = step_norms_dev;
+  f.diag = reinterpret_cast<DiagOut*>(diag_dev);
+  f.status = status_dev;
+  const int fgrid = (ctx->TM + jm::kFinCols - 1) / jm::kFinCols;
+  jm::finalize_kernel<<<fgrid, jm::kFinThreads, 0, ctx->stream>>>(f);
+  CK(cudaGetLastError());
+  return JM_OK;
+}
+
+int jm_weights_dev(jm_ctx* ctx, const double* costs_dev, const jm_diag* diag_dev, double* weights_dev) {
+  if (!ctx || !costs_dev || !diag_dev || !weights_dev) return fail(ctx, JM_ERR_VALUE, "null argument");
+  CK(cudaSetDevice(ctx->device));
+  const int b = 256, g = (ctx->K + b - 1) / b;
+  jm::weights_kernel<<<g, b, 0, ctx->stream>>>(costs_dev, reinterpret_cast<const DiagOut*>(diag_dev),
+                                               1.0 / ctx->mppi.lambda_, ctx->K, weights_dev);
+  CK(cudaGetLastError());
+  return JM_OK;
+}
+
+int jm_shift_dev(jm_ctx* ctx, const double* u_dev, const double* u_init_dev, double* out_dev) {
+  if (!ctx || !u_dev || !u_init_dev || !out_dev) return fail(ctx, JM_ERR_VALUE, "null argument");
+  CK(cudaSetDevice(ctx->device));
+  const int b = 128, g = (ctx->TM + b - 1) / b;
+  jm::shift_kernel<<<g, b, 0, ctx->stream>>>(u_dev, u_init_dev, ctx->T, ctx->M, out_dev);
+  CK(cudaGetLastError());
+  return JM_OK;
+}
+
+int jm_shift_host(int device, int32_t T, int32_t m, const double* u, const double* u_init, double* out) {
+  jm_ctx* ctx = nullptr;
+  if (T < 1 || m < 1 || !u || !u_init || !out) return fail(nullptr, JM_ERR_VALUE, "bad arguments");
+  CK(cudaSetDevice(device));
+  const int TM = T * m;
+  double *d_u = nullptr, *d_i = nullptr, *d_o = nullptr;
+  CK(dalloc(&d_u, (size_t)TM));
+  CK(dalloc(&d_i, (size_t)m));
+  CK(dalloc(&d_o, (size_t)TM));
+  CK(cudaMemcpy(d_u, u, sizeof(double) * TM, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_i, u_init, sizeof(double) * m, cudaMemcpyHostToDevice));
+  jm::shift_kernel<<<(TM + 127) / 128, 128>>>(d_u, d_i, T, m, d_o);
+  CK(cudaGetLastError());
+  CK(cudaMemcpy(out, d_o, sizeof(double) * TM, cudaMemcpyDeviceToHost));
+  dfree(d_u);
+  dfree(d_i);
+  dfree(d_o);
+  return JM_OK;
+}
+
+int jm_compute_weights_host(int device, int64_t K, const double* costs, double lambda_, double* weights) {
+  jm_ctx* ctx = nullptr;
+  if (K < 1 || !costs || !weights) return fail(nullptr, JM_ERR_VALUE, "bad arguments");
+  CK(cudaSetDevice(device));
+  double *d_c = nullptr, *d_w = nullptr, *d_o = nullptr;
+  CK(dalloc(&d_c, (size_t)K));
+  CK(dalloc(&d_w, (size_t)K));
+  CK(dalloc(&d_o, 2));
+  CK(cudaMemcpy(d_c, costs, sizeof(double) * K, cudaMemcpyHostToDevice));
+  cw_kernel<<<1, 1024>>>(d_c, K, 1.0 / lambda_, d_w, d_o);
+  CK(cudaGetLastError());
+  double o[2];
+  CK(cudaMemcpy(weights, d_w, sizeof(double) * K, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(o, d_o, sizeof(o), cudaMemcpyDeviceToHost));
+  dfree(d_c);
+  dfree(d_w);
+  dfree(d_o);
+  if (o[0] == INFINITY) return fail(nullptr, JM_ERR_NO_VIABLE, "no viable rollout");
+  return JM_OK;
+}
+
+int jm_update_controls_host(int device, int64_t K, int32_t T, int32_t m, const double* costs,
+                            const double* eps_c, double lambda_, double dt, const double* u_nom,
+                            const double* mapping, double* u_new, double* weights) {
+  jm_ctx* ctx = nullptr;
+  if (K < 1 || T < 1 || m < 1 || m > 4 || !costs || !eps_c || !u_nom || !u_new)
+    return fail(nullptr, JM_ERR_VALUE, "bad arguments");
+  CK(cudaSetDevice(device));
+  const int TM = T * m;
+  double *d_c, *d_w, *d_o, *d_e, *d_u, *d_n, *d_m = nullptr;
+  CK(dalloc(&d_c, (size_t)K));
+  CK(dalloc(&d_w, (size_t)K));
+  CK(dalloc(&d_o, 2));
+  CK(dalloc(&d_e, (size_t)K * TM));
+  CK(dalloc(&d_u, (size_t)TM));
+  CK(dalloc(&d_n, (size_t)TM));
+  CK(cudaMemcpy(d_c, costs, sizeof(double) * K, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_e, eps_c, sizeof(double) * K * TM, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_u, u_nom, sizeof(double) * TM, cudaMemcpyHostToDevice));
+  if (mapping) {
+    CK(dalloc(&d_m, (size_t)m * m));
+    CK(cudaMemcpy(d_m, mapping, sizeof(double) * m * m, cudaMemcpyHostToDevice));
+  }
+  cw_kernel<<<1, 1024>>>(d_c, K, 1.0 / lambda_, d_w, d_o);
+  CK(cudaGetLastError());
+  wavg_kernel<<<(T + 127) / 128, 128>>>(d_w, d_e, K, TM, m, 1.0 / std::sqrt(dt), d_u, d_m, d_n);
+  CK(cudaGetLastError());
+  double o[2];
+  CK(cudaMemcpy(o, d_o, sizeof(o), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(u_new, d_n, sizeof(double) * TM, cudaMemcpyDeviceToHost));
+  if (weights) CK(cudaMemcpy(weights, d_w, sizeof(double) * K, cudaMemcpyDeviceToHost));
+  for (double* p : {d_c, d_w, d_o, d_e, d_u, d_n, d_m}) dfree(p);
+  if (o[0] == INFINITY) return fail(nullptr, JM_ERR_NO_VIABLE, "no viable rollout");
+  return JM_OK;
+}
+
+static jm::NoiseArgs noise_args(const jm_ctx* ctx, uint64_t seed, uint64_t iteration) {
+  jm::NoiseArgs na{};
+  na.K = ctx->K;
+  na.T = ctx->T;
+  na.q = ctx->Q;
+  na.jmode = ctx->model.jump_channel;
+  na.jthr = ctx->jthr;
+  na.jump_on = ctx->jthr != 0;
+  na.sample_offset = ctx->mppi.sample_offset;
+  na.seed = seed;
+  na.iteration = iteration;
+  for (int i = 0; i < 16; ++i) {
+    na.Ld[i] = ctx->Ld[i];
+    na.Lj[i] = ctx->Lj[i];
+  }
+  for (int i = 0; i < 4; ++i) na.mu_j[i] = ctx->mppi.mark_mean[i];
+  return na;
+}
+
+int jm_sample_noise_host(jm_ctx* ctx, uint64_t seed, uint64_t iteration, double* eps_d,
+                         int64_t* indicators, double* eps_j, double* eps_c) {
+  if (!ctx) return fail(nullptr, JM_ERR_VALUE, "null context");
+  CK(cudaSetDevice(ctx->device));
+  const size_t KT = (size_t)ctx->K * ctx->T;
+  double *d_ed = nullptr, *d_ej = nullptr, *d_ec = nullptr;
+  int64_t* d_ind = nullptr;
+  if (eps_d) CK(dalloc(&d_ed, KT * ctx->M));
+  if (eps_j) CK(dalloc(&d_ej, KT * ctx->Q));
+  if (eps_c) CK(dalloc(&d_ec, KT * ctx->M));
+  if (indicators) CK(dalloc(&d_ind, KT));
+  jm::NoiseArgs na = noise_args(ctx, seed, iteration);
+  na.eps_d = d_ed;
+  na.eps_j = d_ej;
+  na.eps_c = d_ec;
+  na.ind = d_ind;
+  CK(ctx->eng->noise(ctx, na));
+  if (eps_d) CK(cudaMemcpyAsync(eps_d, d_ed, sizeof(double) * KT * ctx->M, cudaMemcpyDeviceToHost, ctx->stream));
+  if (eps_j) CK(cudaMemcpyAsync(eps_j, d_ej, sizeof(double) * KT * ctx->Q, cudaMemcpyDeviceToHost, ctx->stream));
+  if (eps_c) CK(cudaMemcpyAsync(eps_c, d_ec, sizeof(double) * KT * ctx->M, cudaMemcpyDeviceToHost, ctx->stream));
+  if (indicators) CK(cudaMemcpyAsync(indicators, d_ind, sizeof(int64_t) * KT, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  for (void* p : {(void*)d_ed, (void*)d_ej, (void*)d_ec, (void*)d_ind}) dfree(p);
+  return JM_OK;
+}
+
+int jm_sample_noise_dev(jm_ctx* ctx, uint64_t seed, uint64_t iteration, void* eps_c_dev, void* jump_dev) {
+  if (!ctx || !eps_c_dev) return fail(ctx, JM_ERR_VALUE, "null argument");
+  CK(cudaSetDevice(ctx->device));
+  jm::NoiseArgs na = noise_args(ctx, seed, iteration);
+  na.eps_c_sm = eps_c_dev;
+  na.jump_sm = ctx->model.jump_channel == JM_JUMP_STATE ? jump_dev : nullptr;
+  CK(ctx->eng->noise(ctx, na));
+  return JM_OK;
+}
+
+int jm_loop_init(jm_ctx* ctx, const double* x0, const double* u_init, uint64_t seed,
+                 uint64_t first_iteration, int32_t max_steps) {
+  if (!ctx || !x0 || !u_init || max_steps < 1) return fail(ctx, JM_ERR_VALUE, "bad arguments");
+  if (ctx->mppi.noise_source != JM_NOISE_PHILOX)
+    return fail(ctx, JM_ERR_UNSUPPORTED, "the device closed loop samples its own (Philox) noise");
+  CK(cudaSetDevice(ctx->device));
+  const int N = ctx->N, M = ctx->M, TM = ctx->TM;
+  if (max_steps > ctx->loop_cap) {
+    if (ctx->graph_exec) cudaGraphExecDestroy(ctx->graph_exec);
+    if (ctx->graph) cudaGraphDestroy(ctx->graph);
+    ctx->graph_exec = nullptr;
+    ctx->graph = nullptr;
+    dfree(ctx->d_hist);
+    dfree(ctx->d_hist_jumps);
+    dfree(ctx->d_hist_t);
+    if (!ctx->d_loop) {
+      CK(dalloc(reinterpret_cast<char**>(&ctx->d_loop), sizeof(LoopState)));
+      CK(dalloc(&ctx->d_loop_unom, (size_t)TM));
+      CK(dalloc(&ctx->d_loop_unew, (size_t)TM));
+    }
+    CK(dalloc(&ctx->d_hist, (size_t)(max_steps + 1) * N + (size_t)max_steps * M));
+    CK(dalloc(&ctx->d_hist_jumps, (size_t)max_steps));
+    CK(dalloc(&ctx->d_hist_t, 2 * (size_t)max_steps));
+    ctx->loop_cap = max_steps;
+  }
+  LoopState h{};
+  for (int i = 0; i < N; ++i) h.x[i] = x0[i];
+  for (int j = 0; j < M; ++j) h.u_init[j] = u_init[j];
+  h.seed = seed;
+  h.iteration = first_iteration;
+  h.step = 0;
+  h.max_steps = max_steps;
+  h.halted = 0;
+  h.status = 0;
+  h.diverged_at = -1;
+  h.hist_states = ctx->d_hist;
+  h.hist_controls = ctx->d_hist + (size_t)(ctx->loop_cap + 1) * N;
+  h.hist_jumps = ctx->d_hist_jumps;
+  h.t_start = ctx->d_hist_t;
+  h.t_end = ctx->d_hist_t + ctx->loop_cap;
+  std::vector<double> unom((size_t)TM);
+  for (int t = 0; t < ctx->T; ++t)
+    for (int j = 0; j < M; ++j) unom[(size_t)t * M + j] = u_init[j];  // initial_controller_state (controller.py:56-59)
+  cudaStream_t s = ctx->own_stream;
+  CK(cudaMemcpyAsync(ctx->d_loop, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(ctx->d_loop_unom, unom.data(), sizeof(double) * TM, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(ctx->d_hist, x0, sizeof(double) * N, cudaMemcpyHostToDevice, s));
+  CK(cudaStreamSynchronize(s));
+  return capture_loop_graph(ctx);
+}
+
+int jm_loop_step(jm_ctx* ctx) {
+  if (!ctx || !ctx->graph_exec) return fail(ctx, JM_ERR_VALUE, "loop not initialised");
+  CK(cudaGraphLaunch(ctx->graph_exec, ctx->own_stream));
+  return JM_OK;
+}
+
+int jm_loop_read(jm_ctx* ctx, double* x_out, uint64_t* iteration_out, int32_t* step_out,
+                 int32_t* halted_out, int32_t* status_out) {
+  if (!ctx || !ctx->d_loop) return fail(ctx, JM_ERR_VALUE, "loop not initialised");
+  CK(cudaSetDevice(ctx->device));
+  LoopState h{};
+  CK(cudaMemcpyAsync(&h, ctx->d_loop, sizeof(h), cudaMemcpyDeviceToHost, ctx->own_stream));
+  CK(cudaStreamSynchronize(ctx->own_stream));
+  if (x_out) std::memcpy(x_out, h.x, sizeof(double) * ctx->N);
+  if (iteration_out) *iteration_out = h.iteration;
+  if (step_out) *step_out = h.step;
+  if (halted_out) *halted_out = h.halted;
+  if (status_out) *status_out = h.status;
+  return JM_OK;
+}
+
+int jm_closed_loop_host(jm_ctx* ctx, const double* x0, const double* u_init, uint64_t seed,
+                        int32_t steps, double* states, double* controls, int64_t* jumps,
+                        double* step_ns, int32_t* diverged_at, int32_t* status) {
+  int r = jm_loop_init(ctx, x0, u_init, seed, 0, steps);
+  if (r != JM_OK) return r;
+  for (int s = 0; s < steps; ++s) {
+    r = jm_loop_step(ctx);
+    if (r != JM_OK) return r;
+  }
+  LoopState h{};
+  CK(cudaMemcpyAsync(&h, ctx->d_loop, sizeof(h), cudaMemcpyDeviceToHost, ctx->own_stream));
+  const int N = ctx->N, M = ctx->M;
+  std::vector<double> hs((size_t)(steps + 1) * N), hc((size_t)steps * M);
+  std::vector<int64_t> hj((size_t)steps);
+  std::vector<uint64_t> ht(2 * (size_t)ctx->loop_cap);
+  CK(cudaMemcpyAsync(hs.data(), ctx->d_hist, sizeof(double) * hs.size(), cudaMemcpyDeviceToHost, ctx->own_stream));
+  CK(cudaMemcpyAsync(hc.data(), ctx->d_hist + (size_t)(ctx->loop_cap + 1) * N, sizeof(double) * hc.size(),
+                     cudaMemcpyDeviceToHost, ctx->own_stream));
+  CK(cudaMemcpyAsync(hj.data(), ctx->d_hist_jumps, sizeof(int64_t) * hj.size(), cudaMemcpyDeviceToHost, ctx->own_stream));
+  CK(cudaMemcpyAsync(ht.data(), ctx->d_hist_t, sizeof(uint64_t) * ht.size(), cudaMemcpyDeviceToHost, ctx->own_stream));
+  CK(cudaStreamSynchronize(ctx->own_stream));
+  // steps actually executed (h.step), then the reference's post-divergence fill
+  // (harness.py:144-148): states[k+1:] = states[k], controls[k+1:] = 0.
+  const int done = h.step;
+  const int last = (h.diverged_at >= 0) ? h.diverged_at : done;  // last valid state row
+  for (int k = 0; k <= steps; ++k) {
+    const int src = std::min(k, last);
+    if (states)
+      for (int i = 0; i < N; ++i) states[(size_t)k * N + i] = hs[(size_t)src * N + i];
+  }
+  for (int k = 0; k < steps; ++k) {
+    const bool valid = (h.diverged_at >= 0) ? k <= h.diverged_at : k < done;
+    if (controls)
+      for (int j = 0; j < M; ++j) controls[(size_t)k * M + j] = valid ? hc[(size_t)k * M + j] : 0.0;
+    if (jumps) jumps[k] = valid ? hj[k] : 0;
+    if (step_ns) step_ns[k] = valid ? double(ht[ctx->loop_cap + k] - ht[k]) : 0.0;
+  }
+  if (diverged_at) *diverged_at = h.diverged_at;
+  if (status) *status = h.status;
+  if (h.status == JM_ERR_NO_VIABLE) return fail(ctx, JM_ERR_NO_VIABLE, "no viable rollout");
+  return JM_OK;
+}
+
+int jm_microbench(int device, double* fp32_tflops, double* mufu_tops, double* fp64_tflops) {
+  jm_ctx* ctx = nullptr;
+  CK(cudaSetDevice(device));
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  float* d_out = nullptr;
+  CK(dalloc(&d_out, (size_t)sms * 64));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  const int blocks = sms * 8, threads = 256;
+  float best = 0.f;
+  auto timeit = [&](auto launch) -> float {
+    launch();  // warm-up (clocks ramp)
+    launch();
+    cudaEventRecord(e0);
+    launch();
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    return ms;
+  };
+  const int it_f = 8192, it_m = 2048, it_d = 2048;
+  float ms = timeit([&] { jm::mb_ffma_kernel<<<blocks, threads>>>(d_out, it_f, 0.9999f, 1e-7f); });
+  CK(cudaGetLastError());
+  best = ms;
+  if (fp32_tflops) *fp32_tflops = (double)blocks * threads * it_f * 32.0 * 2.0 / (best * 1e-3) / 1e12;
+  ms = timeit([&] { jm::mb_mufu_kernel<<<blocks, threads>>>(d_out, it_m); });
+  CK(cudaGetLastError());
+  if (mufu_tops) *mufu_tops = (double)blocks * threads * it_m * 16.0 / (ms * 1e-3) / 1e12;
+  ms = timeit([&] { jm::mb_dfma_kernel<<<blocks, threads>>>(reinterpret_cast<double*>(d_out), it_d, 0.9999, 1e-7); });
+  CK(cudaGetLastError());
+  if (fp64_tflops) *fp64_tflops = (double)blocks * threads * it_d * 16.0 * 2.0 / (ms * 1e-3) / 1e12;
+  CK(cudaDeviceSynchronize());
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  dfree(d_out);
+  return JM_OK;
+}
+
+const char* jm_kernel_name(const jm_ctx* ctx) { return ctx && ctx->eng ? ctx->eng->kernel_name(false) : ""; }
+
+int jm_launches_per_iteration(const jm_ctx* ctx, int32_t* iteration, int32_t* loop_step) {
+  if (!ctx) return fail(nullptr, JM_ERR_VALUE, "null context");
+  if (iteration) *iteration = 2;  // rollout + finalize (+1 weights kernel when weights are requested)
+  if (loop_step) *loop_step = 3;  // rollout + finalize + plant/shift
+  return JM_OK;
+}
+
+}  // extern "C"

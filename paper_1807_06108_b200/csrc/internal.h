@@ -1,0 +1,101 @@
+// internal.h -- context object shared by the C-ABI host code and the
+// per-system engines.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../../include/jmppi.h"
+#include "kernels.cuh"
+
+namespace jm {
+
+struct RolloutCall {
+  const double* x0 = nullptr;
+  const double* u_nom = nullptr;
+  uint64_t seed = 0, iteration = 0;
+  const uint64_t* iteration_dev = nullptr;
+  const void* eps_in = nullptr;
+  const void* jump_in = nullptr;
+  double* costs = nullptr;
+  double* states = nullptr;
+  int64_t* diverged = nullptr;
+  LoopState* loop = nullptr;
+};
+
+struct EngineBase {
+  virtual ~EngineBase() = default;
+  // occupancy-derived launch shape; sets ctx->grid/ntiles/smem
+  virtual cudaError_t configure(jm_ctx* c) = 0;
+  virtual cudaError_t rollout(jm_ctx* c, const RolloutCall& rc) = 0;
+  virtual cudaError_t noise(jm_ctx* c, NoiseArgs& na) = 0;
+  virtual cudaError_t plant(jm_ctx* c, LoopState* loop, const double* u_new, double* u_nom) = 0;
+  virtual const char* kernel_name(bool trace) const = 0;
+};
+
+EngineBase* make_engine_integrator(int cost_kind, int precision, int n);
+EngineBase* make_engine_cartpole(int cost_kind, int precision);
+EngineBase* make_engine_quadrotor(int cost_kind, int precision);
+
+}  // namespace jm
+
+struct jm_ctx {
+  jm_model_desc model{};
+  jm_cost_desc cost{};
+  jm_mppi_desc mppi{};
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  cudaStream_t own_stream = nullptr;
+  int N = 0, M = 0, Q = 0, T = 0, K = 0, TM = 0, rec_stride = 0;
+  int block = 128, grid = 1, ntiles = 1;
+  size_t smem = 0;
+  size_t real_size = 4;
+  double Ld[16] = {0}, Lj[16] = {0}, Lp[16] = {0};  // chol(c Sigma_D), chol(Sigma_J), chol(Sigma_D)
+  uint32_t jthr = 0;      // sampler jump threshold (0 = no jumps)
+  uint32_t jthr_plant = 0;
+  jm::EngineBase* eng = nullptr;
+  // device workspace
+  void* d_scratch = nullptr;      // per-CTA eps_combined slabs (Philox mode)
+  void* d_hbm_eps = nullptr;      // HBM-mode input staging (host API)
+  void* d_hbm_jump = nullptr;
+  double* d_costs = nullptr;      // K
+  double* d_weights = nullptr;    // K
+  double* d_records = nullptr;    // grid * rec_stride
+  double* d_small = nullptr;      // x0 | u_nom | u_new | norms | mapping | u_init | record
+  double* h_big = nullptr;        // pinned 2K doubles: costs | weights
+  double* d_states = nullptr;     // trace
+  int64_t* d_div = nullptr;
+  size_t states_cap = 0;
+  // pinned staging for the host API
+  double* h_small = nullptr;
+  jm::DiagOut* d_diag() const { return reinterpret_cast<jm::DiagOut*>(d_small + off_diag()); }
+  int32_t* d_status() const { return reinterpret_cast<int32_t*>(d_small + off_status()); }
+  // closed loop
+  jm::LoopState* d_loop = nullptr;
+  double* d_loop_unom = nullptr;
+  double* d_loop_unew = nullptr;
+  double* d_hist = nullptr;       // states | controls
+  int64_t* d_hist_jumps = nullptr;
+  uint64_t* d_hist_t = nullptr;   // t_start | t_end
+  int loop_cap = 0;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
+  std::string err;
+
+  // d_small / h_small layout (doubles):
+  //   inputs  [x0:16][u_nom:TM][mapping:16][u_init:16]
+  //   outputs [u_new:TM][norms:T][diag:4][status:2]
+  //   [record:rec_stride]  (this context's reduced record)
+  size_t off_x0() const { return 0; }
+  size_t off_unom() const { return 16; }
+  size_t off_map() const { return 16 + (size_t)TM; }
+  size_t off_uinit() const { return off_map() + 16; }
+  size_t off_unew() const { return off_uinit() + 16; }
+  size_t off_norms() const { return off_unew() + (size_t)TM; }
+  size_t off_diag() const { return off_norms() + (size_t)T; }
+  size_t off_status() const { return off_diag() + 4; }
+  size_t off_rec() const { return off_status() + 2; }
+  size_t small_doubles() const { return off_rec() + (size_t)rec_stride; }
+};

@@ -1,0 +1,798 @@
+// kernels.cuh -- the sm_100a kernels of one MPC iteration.
+//
+//   rollout_kernel   K1 (in-register Philox noise, or the HBM wire-format
+//                    reader) + K2 fused rollout/modified cost + the per-CTA
+//                    half of K3/K4 (online-softmax partials: rho, Z, sum w^2,
+//                    N[t,j] = sum_k w_k eps[k,t,j]).  Reference:
+//                    controller.py:118-158, noise.py:129-161,
+//                    dynamics.py:87-135, costs.py:80-111.
+//   finalize_kernel  K3/K4/K5 across CTAs (or across GPUs): log-sum-exp merge
+//                    of the partial records, u_new = u_nom + N/(Z sqrt dt)
+//                    (@ mapping^T), diagnostics.  controller.py:62-78,
+//                    :157-169.
+//   weights_kernel   per-sample weights (controller.py:62-71) on demand.
+//   shift_kernel     K6 warm_start_shift (controller.py:96-100).
+//   plant_kernel     K7 closed-loop plant step + shift (harness.py:131-150).
+//   noise_kernel     K1 in write mode (sample_noise_batch on device).
+// All reductions are fixed-order (no float atomics): results are bitwise
+// reproducible run to run for a given launch configuration, and the noise is
+// independent of it.
+#pragma once
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include <cstdint>
+
+#include "philox.cuh"
+#include "systems.cuh"
+
+namespace jm {
+
+constexpr int kFinCols = 128;   // finalize: columns per CTA (multiple of m for m in {1,2,4})
+constexpr int kFinThreads = 256;
+
+// Device-resident closed-loop controller state (ControllerState +
+// the plant state of run_trial).
+struct LoopState {
+  double x[12];            // plant state
+  double u_init[4];        // MppiConfig.u_init
+  uint64_t seed;           // master_seed
+  uint64_t iteration;      // ControllerState.iteration_index (RNG stream id)
+  int32_t step;            // control step k
+  int32_t max_steps;
+  int32_t halted;          // 1 after divergence / no viable rollout / max_steps
+  int32_t status;          // jm_status
+  int32_t diverged_at;     // step index or -1
+  int32_t pad_;
+  // history buffers (device)
+  double* hist_states;     // (max_steps+1) * n
+  double* hist_controls;   // max_steps * m
+  int64_t* hist_jumps;     // max_steps
+  uint64_t* t_start;       // max_steps, %globaltimer ns
+  uint64_t* t_end;         // max_steps
+};
+
+struct DiagOut {
+  double min_cost, ess, normaliser;
+  int64_t n_finite;
+};
+
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ T warp_min(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
+  return v;
+}
+
+template <typename Real>
+__device__ __forceinline__ Real r_inf();
+template <>
+__device__ __forceinline__ float r_inf<float>() { return CUDART_INF_F; }
+template <>
+__device__ __forceinline__ double r_inf<double>() { return CUDART_INF; }
+
+template <typename Real>
+__device__ __forceinline__ Real r_exp(Real v);
+template <>
+__device__ __forceinline__ float r_exp<float>(float v) { return expf(v); }
+template <>
+__device__ __forceinline__ double r_exp<double>(double v) { return exp(v); }
+
+template <typename Real>
+struct RolloutArgs {
+  int K, T, TM, ntiles;
+  long long sample_offset;
+  Real dt, sdt, inv_lam, cq, lam_sdt;  // cq = 0.5*lam*(1-1/c); lam_sdt = lam*sqrt(dt)
+  Real R[16];
+  Real u_lo[4], u_hi[4];
+  int has_limits;
+  int q;            // jump mark dimension
+  int jmode;        // 0 control channel, 1 state selector
+  int jump_on;      // sampler draws jumps (jump_sampling_enabled && nu > 0)
+  uint32_t jthr;    // jump iff uniform word < jthr
+  Real jscale;      // state-jump scale (1 or sqrt dt)
+  Real Ld[16];      // chol(c * Sigma_D), m x m row-major
+  Real Lj[16];      // chol(Sigma_J), q x q
+  Real mu_j[4];     // mark mean
+  SysParams<Real> sp;
+  uint64_t seed, iteration;
+  const uint64_t* iteration_dev;
+  const double* x0;
+  const double* u_nom;
+  const Real* eps_in;    // HBM mode: step-major eps_combined
+  const Real* jump_in;   // HBM mode, state jumps: step-major ind*mark
+  Real* eps_out;         // Philox mode: per-CTA eps_combined scratch [cta][t*m+j][lane] (re-read by the epilogue)
+  double* costs;         // K
+  double* states;        // trace: K*(T+1)*n
+  int64_t* diverged;     // trace: K
+  double* records;       // gridDim.x * rec_stride
+  int rec_stride;
+  LoopState* loop;
+};
+
+// ---------------------------------------------------------------- noise
+// Normals of one 4-step group for sample kg: z[s*MP + j] for step t0+s.
+template <int MP>
+__device__ __forceinline__ void group_normals(const StreamKey& sk, uint32_t t0, uint32_t kg, float* z) {
+#pragma unroll
+  for (int b = 0; b < MP; ++b) {
+    const P4 r = draw(sk, kSlotDiffusion, (t0 * MP >> 2) + b, kg);
+    box_muller(r.x, r.y, z[4 * b + 0], z[4 * b + 1]);
+    box_muller(r.z, r.w, z[4 * b + 2], z[4 * b + 3]);
+  }
+}
+
+// eps = L z (lower triangular, fixed fma order so every kernel that
+// regenerates a draw gets the same bits).
+template <int M, typename Real>
+__device__ __forceinline__ void apply_chol(const Real* L, const float* z, Real* eps) {
+#pragma unroll
+  for (int j = 0; j < M; ++j) {
+    Real acc = L[j * M] * Real(z[0]);
+#pragma unroll
+    for (int l = 1; l <= j; ++l) acc = fma(L[j * M + l], Real(z[l]), acc);
+    eps[j] = acc;
+  }
+}
+
+// Jump marks for (kg, t): mk = mu + Lj z (q <= 4).
+template <typename Real>
+__device__ __forceinline__ void draw_marks(const StreamKey& sk, uint32_t t, uint32_t kg, const Real* Lj,
+                                        const Real* mu, int q, Real* mk) {
+  const P4 r = draw(sk, kSlotMark, t, kg);
+  float z[4];
+  box_muller(r.x, r.y, z[0], z[1]);
+  box_muller(r.z, r.w, z[2], z[3]);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    Real acc = Real(0);
+#pragma unroll
+    for (int l = 0; l < 4; ++l)
+      if (l <= i && i < q) acc = fma(Lj[i * q + l], Real(z[l]), acc);
+    mk[i] = (i < q) ? mu[i] + acc : Real(0);
+  }
+}
+
+__device__ __forceinline__ uint32_t word_of(const P4& w, int s) {
+  return s == 0 ? w.x : (s == 1 ? w.y : (s == 2 ? w.z : w.w));
+}
+
+// ---------------------------------------------------------------- rollout
+template <class Sys, typename Real, bool PHILOX, bool TRACE>
+__global__ void __launch_bounds__(256) rollout_kernel(const RolloutArgs<Real> a) {
+  using Dyn = typename Sys::Dyn;
+  using Cost = typename Sys::Cost;
+  constexpr int N = Sys::N, M = Sys::M;
+  constexpr int MP = (M == 3) ? 4 : M;
+  constexpr int TS = 2 * M + 1;
+  constexpr int QJ = Dyn::QJ;
+
+  extern __shared__ double smem_d[];
+  __shared__ double s_red[3][32];
+  __shared__ double s_acc[4];  // rho, Z, W2, nfinite of this CTA
+  __shared__ double s_bc[2];
+
+  const int TM = a.TM, T = a.T, K = a.K;
+  double* Nacc = smem_d;
+  Real* tab = reinterpret_cast<Real*>(Nacc + TM);
+  Real* sw = tab + T * TS;
+
+  LoopState* L = a.loop;
+  if (L != nullptr && L->halted) return;
+  const uint64_t iter = L ? L->iteration : (a.iteration_dev ? *a.iteration_dev : a.iteration);
+  const double* x0 = L ? L->x : a.x0;
+  if (L != nullptr && blockIdx.x == 0 && threadIdx.x == 0) L->t_start[L->step] = globaltimer();
+
+  // per-step table: clamped u (controller.py:128) hoisted into
+  //   udt = u dt, a_t = 1/2 u'Ru dt, b_t = lambda u sqrt(dt)   (costs.py:98-111 times dt)
+  for (int t = threadIdx.x; t < T; t += blockDim.x) {
+    Real u[M];
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      Real v = Real(a.u_nom[t * M + j]);
+      if (a.has_limits) v = fmin(fmax(v, a.u_lo[j]), a.u_hi[j]);
+      u[j] = v;
+    }
+    Real uru = Real(0);
+#pragma unroll
+    for (int j = 0; j < M; ++j)
+#pragma unroll
+      for (int l = 0; l < M; ++l) uru += u[j] * a.R[j * M + l] * u[l];
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      tab[t * TS + j] = u[j] * a.dt;
+      tab[t * TS + M + 1 + j] = a.lam_sdt * u[j];
+    }
+    tab[t * TS + M] = Real(0.5) * uru * a.dt;
+  }
+  for (int r = threadIdx.x; r < TM; r += blockDim.x) Nacc[r] = 0.0;
+  if (threadIdx.x == 0) {
+    s_acc[0] = CUDART_INF;
+    s_acc[1] = 0.0;
+    s_acc[2] = 0.0;
+    s_acc[3] = 0.0;
+  }
+  __syncthreads();
+
+  const StreamKey sk = make_stream_key(L ? L->seed : a.seed, iter);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const Real dt = a.dt, sdt = a.sdt, cq = a.cq;
+
+  for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+    const int kl = tile * blockDim.x + threadIdx.x;
+    const bool active = kl < K;
+    const uint32_t kg = (uint32_t)(a.sample_offset + kl);
+    Real S = Real(0);
+    if (active) {
+      Real x[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) x[i] = Real(x0[i]);
+      int dstep = -1;
+      if (TRACE) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) a.states[((size_t)kl * (T + 1)) * N + i] = double(x[i]);
+      }
+      for (int t0 = 0; t0 < T; t0 += 4) {
+        float z[4 * MP];
+        P4 jw = P4{0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
+        if (PHILOX) {
+          group_normals<MP>(sk, (uint32_t)t0, kg, z);
+          if (a.jump_on) jw = draw(sk, kSlotJumpUniform, (uint32_t)(t0 >> 2), kg);
+        }
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+          const int t = t0 + s;
+          if (t >= T) break;
+          Real eps[M];
+          Real sj[4] = {Real(0), Real(0), Real(0), Real(0)};  // state-space jump increment
+          bool has_sj = false;
+          if (PHILOX) {
+            apply_chol<M, Real>(a.Ld, z + s * MP, eps);
+            if (word_of(jw, s) < a.jthr) {  // zero-one law, noise.py:151
+              Real mk[4];
+              draw_marks<Real>(sk, (uint32_t)t, kg, a.Lj, a.mu_j, a.q, mk);
+              if (a.jmode == 0) {
+#pragma unroll
+                for (int j = 0; j < M; ++j) eps[j] += mk[j];  // eps_c = eps_d + eps_j (noise.py:156-157)
+              } else {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) sj[i] = a.jscale * mk[i];
+                has_sj = true;
+              }
+            }
+#pragma unroll
+            for (int j = 0; j < M; ++j) a.eps_out[((size_t)blockIdx.x * TM + t * M + j) * blockDim.x + threadIdx.x] = eps[j];
+          } else {
+#pragma unroll
+            for (int j = 0; j < M; ++j) eps[j] = __ldg(a.eps_in + (size_t)(t * M + j) * K + kl);
+            if (a.jump_in != nullptr) {
+#pragma unroll
+              for (int i = 0; i < QJ; ++i) sj[i] = a.jscale * __ldg(a.jump_in + (size_t)(t * QJ + i) * K + kl);
+              has_sj = true;
+            }
+          }
+          // modified running cost on x_t (controller.py:140-142)
+          const auto ax = Dyn::template aux<Real>(x, a.sp);
+          const Real qv = Cost::template q<Dyn, Real>(x, ax, a.sp);
+          const Real* st = tab + t * TS;
+          // q dt + 1/2 u'Ru dt + lambda sqrt(dt) u'eps + 1/2 lambda (1-1/c) eps'eps
+          // (the eps'eps sum is formed first, as costs.py:101/:514 does, so an
+          // overflowing eps gives NaN even when c = 1)
+          Real inc = fma(qv, dt, st[M]);
+          Real quad = eps[0] * eps[0];
+#pragma unroll
+          for (int j = 1; j < M; ++j) quad = fma(eps[j], eps[j], quad);
+#pragma unroll
+          for (int j = 0; j < M; ++j) inc = fma(st[M + 1 + j], eps[j], inc);
+          S += fma(cq, quad, inc);
+          // Euler step (dynamics.py:130-135 / :115-129 with B = G)
+          Real xold[N];
+          if (TRACE) {
+#pragma unroll
+            for (int i = 0; i < N; ++i) xold[i] = x[i];
+          }
+          Real v[M];
+#pragma unroll
+          for (int j = 0; j < M; ++j) v[j] = fma(eps[j], sdt, st[j]);
+          Dyn::template advance<Real>(x, ax, v, dt, a.sp);
+          if (has_sj) {
+#pragma unroll
+            for (int i = 0; i < QJ; ++i) x[Dyn::jump_row(i)] += sj[i];
+          }
+          if (TRACE) {
+            // divergence mask, controller.py:144-151
+            bool fin = true;
+#pragma unroll
+            for (int i = 0; i < N; ++i) fin = fin && isfinite(x[i]);
+            if (dstep >= 0 || !fin) {
+              if (dstep < 0) dstep = t;
+#pragma unroll
+              for (int i = 0; i < N; ++i) x[i] = xold[i];
+            }
+#pragma unroll
+            for (int i = 0; i < N; ++i) a.states[((size_t)kl * (T + 1) + t + 1) * N + i] = double(x[i]);
+          }
+        }
+      }
+      // Once non-finite, an Euler state x += dx stays non-finite, so the
+      // final state decides divergence (the reference checks every step).
+      bool fin = true;
+#pragma unroll
+      for (int i = 0; i < N; ++i) fin = fin && isfinite(x[i]);
+      if (TRACE) {
+        fin = dstep < 0;
+        a.diverged[kl] = dstep;
+      }
+      if (fin) {
+        const auto ax = Dyn::template aux<Real>(x, a.sp);
+        S += a.sp.term_scale * Cost::template q<Dyn, Real>(x, ax, a.sp);  // controller.py:155
+      } else {
+        S = r_inf<Real>();
+      }
+      if (a.costs) a.costs[kl] = double(S);
+    }
+
+    // ---- per-CTA online softmax over this tile (K3/K4 partials) ----
+    const Real Sf = active ? S : r_inf<Real>();
+    Real m = warp_min(Sf);
+    if (lane == 0) s_red[0][warp] = double(m);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double mm = CUDART_INF;
+      for (int w = 0; w < nwarps; ++w) mm = fmin(mm, s_red[0][w]);
+      const double rho_prev = s_acc[0];
+      const double rho_new = fmin(rho_prev, mm);
+      s_bc[0] = rho_new;
+      s_bc[1] = (rho_prev == CUDART_INF) ? 0.0 : exp((rho_new - rho_prev) * double(a.inv_lam));
+    }
+    __syncthreads();
+    const double rho_new = s_bc[0], scale_old = s_bc[1];
+    if (rho_new == CUDART_INF) continue;  // no finite cost yet in this CTA (uniform)
+    const Real w = (Sf < r_inf<Real>()) ? r_exp<Real>(-(Sf - Real(rho_new)) * a.inv_lam) : Real(0);
+    sw[threadIdx.x] = w;
+    {
+      const double z1 = warp_sum(double(w)), z2 = warp_sum(double(w) * double(w));
+      const double nf = warp_sum((Sf < r_inf<Real>()) ? 1.0 : 0.0);
+      __syncwarp();
+      if (lane == 0) {
+        s_red[0][warp] = z1;
+        s_red[1][warp] = z2;
+        s_red[2][warp] = nf;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double z1 = 0.0, z2 = 0.0, nf = 0.0;
+      for (int w2 = 0; w2 < nwarps; ++w2) {
+        z1 += s_red[0][w2];
+        z2 += s_red[1][w2];
+        nf += s_red[2][w2];
+      }
+      s_acc[0] = rho_new;
+      s_acc[1] = s_acc[1] * scale_old + z1;
+      s_acc[2] = s_acc[2] * scale_old * scale_old + z2;
+      s_acc[3] += nf;
+    }
+    // N[r] += sum_k w_k eps[r, k] over the tile: warp-per-row, lanes over k
+    const int base = tile * blockDim.x;
+    const int nk = min((int)blockDim.x, K - base);
+    // Philox: this CTA's scratch slab (rows of blockDim.x, written above);
+    // HBM: the input tensor itself (rows of K).
+    const Real* src = PHILOX ? a.eps_out + (size_t)blockIdx.x * TM * blockDim.x : a.eps_in + base;
+    const size_t rstride = PHILOX ? (size_t)blockDim.x : (size_t)K;
+    for (int r = warp; r < TM; r += nwarps) {
+      const Real* row = src + (size_t)r * rstride;
+      Real acc = Real(0);
+#pragma unroll 4
+      for (int kk = lane; kk < nk; kk += 32) {
+        acc = fma(sw[kk], row[kk], acc);  // einsum semantics: 0 * inf = NaN like controller.py:78
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) Nacc[r] = Nacc[r] * scale_old + double(acc);
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  double* rec = a.records + (size_t)blockIdx.x * a.rec_stride;
+  if (threadIdx.x == 0) {
+    rec[0] = s_acc[0];
+    rec[1] = s_acc[1];
+    rec[2] = s_acc[2];
+    rec[3] = s_acc[3];
+  }
+  for (int r = threadIdx.x; r < TM; r += blockDim.x) rec[4 + r] = Nacc[r];
+}
+
+// ---------------------------------------------------------------- finalize
+struct FinArgs {
+  const double* rec;
+  int nrec, rec_stride, TM, M;
+  double inv_lam, inv_sdt;
+  const double* u_nom;
+  const double* mapping;  // m x m or null
+  double* u_new;
+  double* norms;          // T or null
+  DiagOut* diag;          // or null
+  int32_t* status;        // or null
+  double* rec_out;        // reduce mode: write the merged record instead of finalizing
+  LoopState* loop;
+};
+
+#ifdef JM_COMMON_KERNELS  // non-template kernels: defined in api.cu only
+__global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a) {
+  __shared__ double s_red[3][kFinThreads / 32];
+  __shared__ double s_part[kFinThreads / 32][kFinCols];
+  __shared__ double s_delta[kFinCols];
+  __shared__ double s_bc[4];
+  LoopState* L = a.loop;
+  if (L != nullptr && L->halted) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = kFinThreads / 32;
+  const int rs = a.rec_stride;
+  // global rho (controller.py:69: min over finite costs)
+  double m = CUDART_INF;
+  for (int b = tid; b < a.nrec; b += kFinThreads) m = fmin(m, a.rec[(size_t)b * rs]);
+  m = warp_min(m);
+  if (lane == 0) s_red[0][warp] = m;
+  __syncthreads();
+  if (tid == 0) {
+    double mm = CUDART_INF;
+    for (int w = 0; w < nw; ++w) mm = fmin(mm, s_red[0][w]);
+    s_bc[0] = mm;
+  }
+  __syncthreads();
+  const double rho = s_bc[0];
+  double z = 0.0, w2 = 0.0, nf = 0.0;
+  if (rho != CUDART_INF) {
+    for (int b = tid; b < a.nrec; b += kFinThreads) {
+      const double* r = a.rec + (size_t)b * rs;
+      const double e = (r[0] == CUDART_INF) ? 0.0 : exp(-(r[0] - rho) * a.inv_lam);
+      z += r[1] * e;
+      w2 += r[2] * e * e;
+      nf += r[3];
+    }
+  }
+  z = warp_sum(z);
+  w2 = warp_sum(w2);
+  nf = warp_sum(nf);
+  __syncthreads();
+  if (lane == 0) {
+    s_red[0][warp] = z;
+    s_red[1][warp] = w2;
+    s_red[2][warp] = nf;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double zz = 0.0, ww = 0.0, nn = 0.0;
+    for (int w = 0; w < nw; ++w) {
+      zz += s_red[0][w];
+      ww += s_red[1][w];
+      nn += s_red[2][w];
+    }
+    s_bc[1] = zz;
+    s_bc[2] = ww;
+    s_bc[3] = nn;
+  }
+  __syncthreads();
+  const double Z = s_bc[1], W2 = s_bc[2], NF = s_bc[3];
+  const int c0 = blockIdx.x * kFinCols;
+  const bool reduce_mode = a.rec_out != nullptr;
+  if (rho == CUDART_INF) {  // controller.py:66-67
+    if (blockIdx.x == 0 && tid == 0) {
+      if (a.status) *a.status = 3;  // JM_ERR_NO_VIABLE
+      if (a.diag) *a.diag = DiagOut{CUDART_INF, 0.0, 0.0, 0};
+      if (L) {
+        L->status = 3;
+        L->halted = 1;
+      }
+      if (reduce_mode) {
+        a.rec_out[0] = CUDART_INF;
+        a.rec_out[1] = 0.0;
+        a.rec_out[2] = 0.0;
+        a.rec_out[3] = 0.0;
+      }
+    }
+    for (int c = c0 + tid; c < min(c0 + kFinCols, a.TM); c += kFinThreads) {
+      if (reduce_mode)
+        a.rec_out[4 + c] = 0.0;
+      else
+        a.u_new[c] = a.u_nom[c];
+    }
+    return;
+  }
+  // columns: warps split records, lanes split columns
+  constexpr int CPL = kFinCols / 32;
+  double acc[CPL];
+#pragma unroll
+  for (int i = 0; i < CPL; ++i) acc[i] = 0.0;
+  for (int b = warp; b < a.nrec; b += nw) {
+    const double* r = a.rec + (size_t)b * rs;
+    const double rb = r[0];
+    if (rb == CUDART_INF) continue;
+    const double e = exp(-(rb - rho) * a.inv_lam);
+#pragma unroll
+    for (int i = 0; i < CPL; ++i) {
+      const int c = c0 + lane + 32 * i;
+      if (c < a.TM) acc[i] = fma(r[4 + c], e, acc[i]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < CPL; ++i) s_part[warp][lane + 32 * i] = acc[i];
+  __syncthreads();
+  if (tid < kFinCols) {
+    double n = 0.0;
+    for (int w = 0; w < nw; ++w) n += s_part[w][tid];
+    s_delta[tid] = n;
+  }
+  __syncthreads();
+  if (reduce_mode) {
+    if (blockIdx.x == 0 && tid == 0) {
+      a.rec_out[0] = rho;
+      a.rec_out[1] = Z;
+      a.rec_out[2] = W2;
+      a.rec_out[3] = NF;
+    }
+    if (tid < kFinCols && c0 + tid < a.TM) a.rec_out[4 + c0 + tid] = s_delta[tid];
+    return;
+  }
+  // delta = N / (Z sqrt(dt))  (controller.py:158), then mapping (:159-160)
+  const double scale = a.inv_sdt / Z;
+  double out = 0.0;
+  const int c = c0 + tid;
+  const int M = a.M;
+  if (tid < kFinCols && c < a.TM) {
+    const int j = c % M, cb = tid - j;
+    if (a.mapping) {
+      for (int l = 0; l < M; ++l) out = fma(a.mapping[j * M + l], s_delta[cb + l] * scale, out);
+    } else {
+      out = s_delta[tid] * scale;
+    }
+  }
+  __syncthreads();
+  if (tid < kFinCols && c < a.TM) {
+    s_delta[tid] = out;
+    a.u_new[c] = a.u_nom[c] + out;  // u_nom + delta, unclamped (controller.py:161)
+  }
+  __syncthreads();
+  if (a.norms) {  // per_step_update_norm (controller.py:168)
+    const int tl = tid, t = c0 / M + tl;
+    if (tl < kFinCols / M && t * M < a.TM) {
+      double s2 = 0.0;
+      for (int j = 0; j < M; ++j) s2 += s_delta[tl * M + j] * s_delta[tl * M + j];
+      a.norms[t] = sqrt(s2);
+    }
+  }
+  if (blockIdx.x == 0 && tid == 0) {
+    if (a.status) *a.status = 0;
+    if (a.diag) *a.diag = DiagOut{rho, Z * Z / W2, Z, (int64_t)NF};  // ESS = 1/sum w^2 (:167)
+  }
+}
+
+// ---------------------------------------------------------------- weights
+__global__ void weights_kernel(const double* costs, const DiagOut* diag, double inv_lam, int K,
+                               double* w) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  const double rho = diag->min_cost, Z = diag->normaliser;
+  const double s = costs[k];
+  w[k] = (isfinite(s) && Z > 0.0) ? exp(-(s - rho) * inv_lam) / Z : 0.0;
+}
+
+// ---------------------------------------------------------------- shift
+__global__ void shift_kernel(const double* u, const double* u_init, int T, int M, double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int TM = T * M;
+  if (i >= TM) return;
+  out[i] = (i < TM - M) ? u[i + M] : u_init[i - (TM - M)];
+}
+
+#endif  // JM_COMMON_KERNELS
+
+// ---------------------------------------------------------------- noise (write mode)
+struct NoiseArgs {
+  int K, T, q, jmode, jump_on;
+  uint32_t jthr;
+  long long sample_offset;
+  uint64_t seed, iteration;
+  double Ld[16], Lj[16], mu_j[4];
+  // sample-major float64 outputs (host API mirror of sample_noise_batch)
+  double* eps_d;
+  int64_t* ind;
+  double* eps_j;
+  double* eps_c;
+  // step-major Real outputs (HBM-mode inputs)
+  void* eps_c_sm;
+  void* jump_sm;
+};
+
+template <int M, typename Real>
+__global__ void __launch_bounds__(256) noise_kernel(const NoiseArgs a) {
+  constexpr int MP = (M == 3) ? 4 : M;
+  const int kl = blockIdx.x * blockDim.x + threadIdx.x;
+  if (kl >= a.K) return;
+  const uint32_t kg = (uint32_t)(a.sample_offset + kl);
+  const StreamKey sk = make_stream_key(a.seed, a.iteration);
+  Real Ld[16], Lj[16], mu[4];
+  for (int i = 0; i < 16; ++i) {
+    Ld[i] = Real(a.Ld[i]);
+    Lj[i] = Real(a.Lj[i]);
+  }
+  for (int i = 0; i < 4; ++i) mu[i] = Real(a.mu_j[i]);
+  const int T = a.T, K = a.K;
+  for (int t0 = 0; t0 < T; t0 += 4) {
+    float z[4 * MP];
+    group_normals<MP>(sk, (uint32_t)t0, kg, z);
+    P4 jw = P4{0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
+    if (a.jump_on) jw = draw(sk, kSlotJumpUniform, (uint32_t)(t0 >> 2), kg);
+    for (int s = 0; s < 4 && t0 + s < T; ++s) {
+      const int t = t0 + s;
+      Real ed[M], ec[M], mk[4] = {Real(0), Real(0), Real(0), Real(0)};
+      apply_chol<M, Real>(Ld, z + s * MP, ed);
+      const bool jump = word_of(jw, s) < a.jthr;
+      if (jump) draw_marks<Real>(sk, (uint32_t)t, kg, Lj, mu, a.q, mk);
+      for (int j = 0; j < M; ++j) ec[j] = (jump && a.jmode == 0) ? ed[j] + mk[j] : ed[j];
+      const size_t row = (size_t)kl * T + t;
+      if (a.eps_d)
+        for (int j = 0; j < M; ++j) a.eps_d[row * M + j] = double(ed[j]);
+      if (a.ind) a.ind[row] = jump ? 1 : 0;
+      if (a.eps_j)
+        for (int i = 0; i < a.q; ++i) a.eps_j[row * a.q + i] = jump ? double(mk[i]) : 0.0;
+      if (a.eps_c)
+        for (int j = 0; j < M; ++j) a.eps_c[row * M + j] = double(ec[j]);
+      if (a.eps_c_sm)
+        for (int j = 0; j < M; ++j) reinterpret_cast<Real*>(a.eps_c_sm)[(size_t)(t * M + j) * K + kl] = ec[j];
+      if (a.jump_sm)
+        for (int i = 0; i < a.q; ++i)
+          reinterpret_cast<Real*>(a.jump_sm)[(size_t)(t * a.q + i) * K + kl] = jump ? mk[i] : Real(0);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- plant + shift (closed loop)
+struct PlantArgs {
+  SysParams<double> sp;
+  double dt, sdt, jscale;
+  double Lp[16];   // chol(Sigma_D)  (plant: Sigma_D, not c*Sigma_D; harness.py:123)
+  double Lj[16];   // chol(Sigma_J)
+  double mu_j[4];
+  uint32_t jthr;   // plant always has jumps (harness.py:138)
+  int q, jmode, has_limits, T, M;
+  double u_lo[4], u_hi[4];
+  LoopState* loop;
+  const double* u_new;
+  double* u_nom;
+};
+
+template <class Dyn>
+__global__ void plant_kernel(const PlantArgs a) {
+  constexpr int N = Dyn::N, M = Dyn::M;
+  LoopState* L = a.loop;
+  __shared__ int s_ok;
+  if (L->halted) return;
+  if (threadIdx.x == 0) {
+    const int k = L->step;
+    L->t_end[k] = globaltimer();
+    double u0[M];
+    for (int j = 0; j < M; ++j) {
+      double v = a.u_new[j];
+      if (a.has_limits) v = fmin(fmax(v, a.u_lo[j]), a.u_hi[j]);  // harness.py:136
+      u0[j] = v;
+    }
+    const StreamKey sk = make_stream_key(L->seed, 0);
+    // eps_d = L_D N(0,I); has_jump = U < nu dt; eps_j = L_J N(0,I) drawn every step (:137-139)
+    P4 r = draw(sk, kSlotPlant, 3u * k + 0u, 0u);
+    float z[4];
+    box_muller(r.x, r.y, z[0], z[1]);
+    box_muller(r.z, r.w, z[2], z[3]);
+    double ed[M];
+    apply_chol<M, double>(a.Lp, z, ed);
+    const P4 ju = draw(sk, kSlotPlant, 3u * k + 1u, 0u);
+    const bool jump = ju.x < a.jthr;
+    r = draw(sk, kSlotPlant, 3u * k + 2u, 0u);
+    box_muller(r.x, r.y, z[0], z[1]);
+    box_muller(r.z, r.w, z[2], z[3]);
+    double mk[4];
+    for (int i = 0; i < 4; ++i) {
+      double acc = 0.0;
+      for (int l = 0; l <= i && i < a.q; ++l) acc = fma(a.Lj[i * a.q + l], double(z[l]), acc);
+      mk[i] = (i < a.q) ? a.mu_j[i] + acc : 0.0;
+    }
+    double x[N];
+    for (int i = 0; i < N; ++i) x[i] = L->x[i];
+    const auto ax = Dyn::template aux<double>(x, a.sp);
+    double v[M];
+    for (int j = 0; j < M; ++j) {
+      const double e = (jump && a.jmode == 0) ? ed[j] + mk[j] : ed[j];
+      v[j] = fma(e, a.sdt, u0[j] * a.dt);
+    }
+    Dyn::template advance<double>(x, ax, v, a.dt, a.sp);
+    if (jump && a.jmode == 1)
+#pragma unroll
+      for (int i = 0; i < Dyn::QJ; ++i) x[Dyn::jump_row(i)] += a.jscale * mk[i];
+    bool fin = true;
+    for (int i = 0; i < N; ++i) fin = fin && isfinite(x[i]);
+    for (int j = 0; j < M; ++j) L->hist_controls[(size_t)k * M + j] = u0[j];
+    L->hist_jumps[k] = jump ? 1 : 0;
+    if (!fin) {  // StateDivergedError -> trial failure (harness.py:144-148)
+      L->halted = 1;
+      L->status = 7;
+      L->diverged_at = k;
+      s_ok = 0;
+    } else {
+      for (int i = 0; i < N; ++i) {
+        L->x[i] = x[i];
+        L->hist_states[(size_t)(k + 1) * N + i] = x[i];
+      }
+      s_ok = 1;
+    }
+  }
+  __syncthreads();
+  if (!s_ok) return;
+  const int TM = a.T * M;
+  for (int i = threadIdx.x; i < TM; i += blockDim.x)
+    a.u_nom[i] = (i < TM - M) ? a.u_new[i + M] : L->u_init[i - (TM - M)];  // warm_start_shift
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    L->iteration += 1;  // ControllerState(..., k+1, cfg) (harness.py:150)
+    L->step += 1;
+    if (L->step >= L->max_steps) L->halted = 1;
+  }
+}
+
+#ifdef JM_COMMON_KERNELS
+// ---------------------------------------------------------------- microbenchmarks
+__global__ void mb_ffma_kernel(float* out, int iters, float b, float c) {
+  float a0 = threadIdx.x * 1e-7f, a1 = a0 + 1e-7f, a2 = a0 + 2e-7f, a3 = a0 + 3e-7f;
+  float a4 = a0 + 4e-7f, a5 = a0 + 5e-7f, a6 = a0 + 6e-7f, a7 = a0 + 7e-7f;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      a0 = fmaf(a0, b, c); a1 = fmaf(a1, b, c); a2 = fmaf(a2, b, c); a3 = fmaf(a3, b, c);
+      a4 = fmaf(a4, b, c); a5 = fmaf(a5, b, c); a6 = fmaf(a6, b, c); a7 = fmaf(a7, b, c);
+    }
+  }
+  const float s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+  if (s == 12345.678f) out[blockIdx.x] = s;
+}
+
+__global__ void mb_mufu_kernel(float* out, int iters) {
+  float a0 = threadIdx.x * 1e-9f, a1 = a0 + 1e-9f, a2 = a0 + 2e-9f, a3 = a0 + 3e-9f;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a0));
+      asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a1));
+      asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a2));
+      asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a3));
+    }
+  }
+  const float s = a0 + a1 + a2 + a3;
+  if (s == 12345.678f) out[blockIdx.x] = s;
+}
+
+__global__ void mb_dfma_kernel(double* out, int iters, double b, double c) {
+  double a0 = threadIdx.x * 1e-7, a1 = a0 + 1e-7, a2 = a0 + 2e-7, a3 = a0 + 3e-7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      a0 = fma(a0, b, c); a1 = fma(a1, b, c); a2 = fma(a2, b, c); a3 = fma(a3, b, c);
+    }
+  }
+  const double s = a0 + a1 + a2 + a3;
+  if (s == 12345.678) out[blockIdx.x] = s;
+}
+
+#endif  // JM_COMMON_KERNELS
+
+}  // namespace jm

@@ -1,0 +1,167 @@
+"""Dynamics plugins, mirroring jump_mppi.dynamics
+(/root/reference/pkg/src/jump_mppi/dynamics.py).
+
+The reference's DynamicsModel carries numpy callables f, G, B, H.  Here a model
+is a *description* the device kernels are compiled for (csrc/systems.cuh): the
+physical parameter object (CartpoleModel / QuadrotorModel / IntegratorModel),
+control limits and the noise routing.  Evaluation happens only on the GPU,
+inside mppi_iteration / run_trial; there is no numpy path.
+
+Noise routing:
+  jump_channel="control"  B = H = G (the reference's cartpole_dynamics /
+                          quadrotor_dynamics, dynamics.py:274-283, :399-409)
+  jump_channel="state"    B = G, H = constant selector on `jump_rows`
+                          (theta-dot for the cartpole, the linear velocities
+                          for the quadrotor: the BASELINE configs; SURVEY
+                          Appendix A), jump_scale_mode "unit" = O(1) increment.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional, Tuple
+
+import numpy as np
+
+
+class StateDivergedError(RuntimeError):
+    """Non-finite state (dynamics.py:29-33)."""
+
+    def __init__(self, step_index=None):
+        self.step_index = step_index
+        at = "" if step_index is None else f" at step {step_index}"
+        super().__init__(f"state diverged{at}")
+
+
+@dataclass(frozen=True)
+class CartpoleModel:
+    """Cart with a point-mass pole, theta = pi upright (dynamics.py:194-203)."""
+
+    cart_mass: float = 1.0
+    pole_mass: float = 0.1
+    pole_half_length: float = 0.5
+    gravity: float = 9.81
+
+    def __post_init__(self):
+        if min(self.cart_mass, self.pole_mass, self.pole_half_length, self.gravity) <= 0:
+            raise ValueError("cartpole parameters must be positive")
+
+
+@dataclass(frozen=True)
+class QuadrotorModel:
+    """12-state Euler-angle rigid body (dynamics.py:296-305)."""
+
+    mass: float = 1.0
+    arm_length: float = 0.2
+    inertia_diag: Tuple[float, float, float] = (0.01, 0.01, 0.02)
+    gravity: float = 9.81
+
+    def __post_init__(self):
+        if self.mass <= 0 or self.arm_length <= 0 or min(self.inertia_diag) <= 0:
+            raise ValueError("quadrotor parameters must be positive")
+
+    def hover_control(self) -> np.ndarray:
+        return np.array([self.mass * self.gravity, 0.0, 0.0, 0.0])
+
+
+@dataclass(frozen=True)
+class IntegratorModel:
+    """dx = u dt + eps sqrt(dt) with G = B = H = I (tests/conftest.py:19-30)."""
+
+    dim: int = 1
+
+    def __post_init__(self):
+        if self.dim not in (1, 2):
+            raise ValueError("the device integrator is compiled for dim 1 or 2")
+
+
+@dataclass(frozen=True)
+class DynamicsModel:
+    """Device-evaluable control-affine jump-diffusion model (dynamics.py:45-65)."""
+
+    state_dim: int
+    control_dim: int
+    plant: object
+    control_limits: Optional[Tuple[np.ndarray, np.ndarray]] = None
+    noise_through_controls: bool = True
+    jump_channel: str = "control"
+    jump_rows: Tuple[int, ...] = ()
+    jump_scale_mode: str = "sqrt_dt"
+
+    def __post_init__(self):
+        if self.jump_channel not in ("control", "state"):
+            raise ValueError("jump_channel must be 'control' or 'state'")
+        if self.jump_scale_mode not in ("sqrt_dt", "unit"):
+            raise ValueError("jump_scale_mode must be 'sqrt_dt' or 'unit'")
+        if self.jump_channel == "control" and self.jump_scale_mode != "sqrt_dt":
+            raise ValueError("control-channel jumps use the sqrt(dt) scaling (controller.py:143)")
+
+    @property
+    def jump_dim(self) -> int:
+        return self.control_dim if self.jump_channel == "control" else len(self.jump_rows)
+
+    def clamp(self, u: np.ndarray) -> np.ndarray:
+        """np.clip to control_limits (dynamics.py:61-65); a host helper for callers."""
+        if self.control_limits is None:
+            return u
+        lo, hi = self.control_limits
+        return np.clip(u, lo, hi)
+
+
+def _limits(control_limits, m):
+    if control_limits is None:
+        return None
+    lo, hi = control_limits
+    lo = np.broadcast_to(np.atleast_1d(np.asarray(lo, float)), (m,)).copy()
+    hi = np.broadcast_to(np.atleast_1d(np.asarray(hi, float)), (m,)).copy()
+    return lo, hi
+
+
+def cartpole_dynamics(
+    params: Optional[CartpoleModel] = None,
+    control_limits=None,
+    jump_channel: str = "control",
+    jump_scale_mode: str = "sqrt_dt",
+) -> DynamicsModel:
+    """Cartpole (dynamics.py:264-284).  jump_channel="state" puts the jump on
+    theta-dot (BASELINE configs 0/1)."""
+    return DynamicsModel(
+        state_dim=4,
+        control_dim=1,
+        plant=params or CartpoleModel(),
+        control_limits=_limits(control_limits, 1),
+        noise_through_controls=jump_channel == "control",
+        jump_channel=jump_channel,
+        jump_rows=(3,) if jump_channel == "state" else (),
+        jump_scale_mode=jump_scale_mode,
+    )
+
+
+def quadrotor_dynamics(
+    params: Optional[QuadrotorModel] = None,
+    control_limits=None,
+    jump_channel: str = "control",
+    jump_scale_mode: str = "sqrt_dt",
+) -> DynamicsModel:
+    """Quadrotor (dynamics.py:389-409).  jump_channel="state" puts 3-axis
+    gusts on the linear velocities (BASELINE configs 2/3)."""
+    return DynamicsModel(
+        state_dim=12,
+        control_dim=4,
+        plant=params or QuadrotorModel(),
+        control_limits=_limits(control_limits, 4),
+        noise_through_controls=jump_channel == "control",
+        jump_channel=jump_channel,
+        jump_rows=(3, 4, 5) if jump_channel == "state" else (),
+        jump_scale_mode=jump_scale_mode,
+    )
+
+
+def integrator_dynamics(dim: int = 1, control_limits=None) -> DynamicsModel:
+    """The conftest scalar integrator (tests/conftest.py:19-30), dim in {1, 2}."""
+    return DynamicsModel(
+        state_dim=dim,
+        control_dim=dim,
+        plant=IntegratorModel(dim),
+        control_limits=_limits(control_limits, dim),
+    )

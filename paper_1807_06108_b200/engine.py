@@ -1,0 +1,344 @@
+"""Plugin introspection and the device-context cache.
+
+`describe(model, cost_model, cfg)` turns a dynamics/cost plugin pair -- ours
+(paper_1807_06108_b200.dynamics / .costs) or the reference's own objects
+(jump_mppi.dynamics.DynamicsModel built by cartpole_dynamics /
+quadrotor_dynamics, jump_mppi.costs.CartpoleStateCost / QuadrotorStateCost /
+ScaledTerminalCost) -- into the POD descriptors of include/jmppi.h.  Plugins
+without a compiled kernel raise NotImplementedError: there is no CPU path.
+
+A `Context` owns one jm_ctx (device workspace for K samples) and is cached
+per (model, cost, config, precision, noise source, device).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from collections import OrderedDict
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from . import _lib as L
+from .errors import ConfigError, ControllerError, DeviceError, NoiseError, StateDivergedError
+
+_PRECISIONS = {"f32": L.JM_F32, "fp32": L.JM_F32, "float32": L.JM_F32,
+               "f64": L.JM_F64, "fp64": L.JM_F64, "float64": L.JM_F64}
+
+
+def default_precision() -> str:
+    """Compute precision of the product path: fp32 unless JM_B200_PRECISION says f64."""
+    return os.environ.get("JM_B200_PRECISION", "f32")
+
+
+def _prec(precision: Optional[str]) -> int:
+    p = (precision or default_precision()).lower()
+    if p not in _PRECISIONS:
+        raise ValueError(f"precision must be f32 or f64, got {precision!r}")
+    return _PRECISIONS[p]
+
+
+def raise_status(code: int, ctx_handle=None):
+    if code == L.JM_OK:
+        return
+    msg = L.last_error(ctx_handle)
+    if code == L.JM_ERR_CONFIG:
+        raise ConfigError([msg.replace("invalid configuration: ", "")])
+    if code == L.JM_ERR_VALUE:
+        raise ValueError(msg)
+    if code == L.JM_ERR_NO_VIABLE:
+        raise ControllerError("no viable rollout")
+    if code == L.JM_ERR_NOISE:
+        raise NoiseError(msg)
+    if code == L.JM_ERR_UNSUPPORTED:
+        raise NotImplementedError(msg)
+    if code == L.JM_ERR_DIVERGED:
+        raise StateDivergedError()
+    raise DeviceError(msg or f"libjmppi error {code}")
+
+
+# ---------------------------------------------------------------- plugin descriptions
+def _plant_of(model):
+    plant = getattr(model, "plant", None)
+    if plant is not None:
+        return plant
+    # reference DynamicsModel: the fused (f, G) evaluator is a bound method of
+    # the CartpoleModel / QuadrotorModel parameter object (dynamics.py:283, :408)
+    fused = getattr(model, "fused_drift_control", None)
+    plant = getattr(fused, "__self__", None)
+    if plant is None:
+        raise NotImplementedError(
+            "dynamics plugin has no device kernel (expected a cartpole / quadrotor / integrator model)"
+        )
+    if not getattr(model, "noise_through_controls", False):
+        raise NotImplementedError("reference plugins are supported with noise through the control channel")
+    return plant
+
+
+def describe_model(model) -> L.ModelDesc:
+    d = L.ModelDesc()
+    plant = _plant_of(model)
+    name = type(plant).__name__
+    n, m = int(model.state_dim), int(model.control_dim)
+    d.state_dim, d.control_dim = n, m
+    if name == "CartpoleModel":
+        d.kind = L.JM_MODEL_CARTPOLE
+        vals = [plant.cart_mass, plant.pole_mass, plant.pole_half_length, plant.gravity]
+    elif name == "QuadrotorModel":
+        d.kind = L.JM_MODEL_QUADROTOR
+        ixx, iyy, izz = plant.inertia_diag
+        vals = [plant.mass, plant.arm_length, ixx, iyy, izz, plant.gravity]
+    elif name == "IntegratorModel":
+        d.kind = L.JM_MODEL_INTEGRATOR
+        vals = []
+    else:
+        raise NotImplementedError(f"no device kernel for dynamics parameter object {name}")
+    for i, v in enumerate(vals):
+        d.params[i] = float(v)
+    lim = getattr(model, "control_limits", None)
+    if lim is not None:
+        lo = np.broadcast_to(np.atleast_1d(np.asarray(lim[0], float)), (m,))
+        hi = np.broadcast_to(np.atleast_1d(np.asarray(lim[1], float)), (m,))
+        d.has_limits = 1
+        for j in range(m):
+            d.u_lo[j], d.u_hi[j] = float(lo[j]), float(hi[j])
+    channel = getattr(model, "jump_channel", "control")
+    if channel == "control":
+        d.jump_channel, d.jump_dim = L.JM_JUMP_CONTROL, m
+    else:
+        rows = tuple(getattr(model, "jump_rows", ()))
+        d.jump_channel, d.jump_dim = L.JM_JUMP_STATE, len(rows)
+        for i, r in enumerate(rows):
+            d.jump_rows[i] = int(r)
+    d.jump_scale_unit = 1 if getattr(model, "jump_scale_mode", "sqrt_dt") == "unit" else 0
+    return d
+
+
+def _cost_kind(cost, n):
+    name = type(cost).__name__
+    w, tgt = [0.0] * 12, [0.0] * 12
+    if name == "CartpoleStateCost":
+        w[:4] = [cost.w_pos, cost.w_vel, cost.w_angle, cost.w_avel]
+        return L.JM_COST_CARTPOLE_SWINGUP, w, tgt
+    if name == "QuadrotorStateCost":
+        w[:4] = [cost.w_pos, cost.w_vel, cost.w_att, cost.w_rate]
+        tgt[:3] = list(cost.target)
+        return L.JM_COST_QUADROTOR_HOVER, w, tgt
+    if name == "DiagQuadraticCost":
+        ww = list(cost.weights)
+        if len(ww) != n:
+            raise ValueError(f"DiagQuadraticCost has {len(ww)} weights for a {n}-state model")
+        w[:n] = ww
+        if cost.target is not None:
+            tgt[:n] = list(cost.target)
+        return L.JM_COST_DIAG_QUADRATIC, w, tgt
+    raise NotImplementedError(f"no device kernel for state cost {name}")
+
+
+def describe_cost(cost_model, n: int, m: int) -> L.CostDesc:
+    if not getattr(cost_model, "control_channel", True):
+        raise NotImplementedError("only the control-channel modified cost (calB = bb = I) has a kernel")
+    d = L.CostDesc()
+    sc, tc = cost_model.state_cost, cost_model.terminal_cost
+    kind, w, tgt = _cost_kind(sc, n)
+    if type(tc).__name__ == "ScaledTerminalCost":
+        run = tc.running
+        if not (run is sc or run == sc):
+            raise NotImplementedError("terminal cost must scale the running state cost")
+        scale = float(tc.scale)
+    elif tc is sc or tc == sc:
+        scale = 1.0
+    else:
+        raise NotImplementedError("terminal cost must be ScaledTerminalCost(state_cost) or state_cost")
+    d.kind = kind
+    for i in range(12):
+        d.weights[i], d.target[i] = float(w[i]), float(tgt[i])
+    d.terminal_scale = scale
+    r = np.atleast_2d(np.asarray(cost_model.control_cost_matrix, float))
+    if r.shape != (m, m):
+        raise ValueError(f"control_cost_matrix must be {m}x{m}")
+    for i in range(m):
+        for j in range(m):
+            d.R[i * m + j] = float(r[i, j])
+    d.lambda_ = float(cost_model.lambda_)
+    d.c = float(cost_model.c)
+    return d
+
+
+def describe_mppi(cfg, m: int, q: int, *, samples=None, precision=None, hbm=False,
+                  sample_offset=0, block_threads=0) -> L.MppiDesc:
+    d = L.MppiDesc()
+    d.lambda_, d.c, d.dt, d.nu = float(cfg.lambda_), float(cfg.c), float(cfg.dt), float(cfg.nu)
+    d.horizon = int(cfg.horizon_n)
+    d.samples = int(cfg.samples_m if samples is None else samples)
+    d.control_dim = m
+    d.jump_enabled = 1 if getattr(cfg, "jump_sampling_enabled", True) else 0
+    sd = np.asarray(cfg.sigma_d, float)
+    sj = np.asarray(cfg.sigma_j, float)
+    if sd.shape != (m, m):
+        raise ValueError(f"sigma_d must be {m}x{m}")
+    if sj.shape != (q, q):
+        raise ValueError(f"sigma_j must be {q}x{q} for this jump channel")
+    for i in range(m):
+        for j in range(m):
+            d.sigma_d[i * m + j] = sd[i, j]
+    for i in range(q):
+        for j in range(q):
+            d.sigma_j[i * q + j] = sj[i, j]
+    mm = getattr(cfg, "mark_mean", None)
+    if mm is not None:
+        mm = np.atleast_1d(np.asarray(mm, float))
+        for i in range(min(q, mm.shape[0])):
+            d.mark_mean[i] = mm[i]
+    d.precision = _prec(precision)
+    d.noise_source = L.JM_NOISE_HBM if hbm else L.JM_NOISE_PHILOX
+    d.sample_offset = int(sample_offset)
+    d.block_threads = int(block_threads)
+    return d
+
+
+# ---------------------------------------------------------------- context
+@dataclass
+class IterationOut:
+    u_new: np.ndarray
+    norms: np.ndarray
+    diag: L.Diag
+    costs: Optional[np.ndarray]
+    weights: Optional[np.ndarray]
+    states: Optional[np.ndarray]
+    diverged: Optional[np.ndarray]
+
+
+class Context:
+    """One jm_ctx: device workspace + kernels for a (model, cost, config)."""
+
+    def __init__(self, mdesc: L.ModelDesc, cdesc: L.CostDesc, pdesc: L.MppiDesc, device: int = 0):
+        self.lib = L.load()
+        self.mdesc, self.cdesc, self.pdesc = mdesc, cdesc, pdesc
+        self.device = device
+        h = C.c_void_p()
+        rc = self.lib.jm_create(C.byref(mdesc), C.byref(cdesc), C.byref(pdesc), device, C.byref(h))
+        raise_status(rc, None)
+        self.h = h
+        self.N, self.M = mdesc.state_dim, mdesc.control_dim
+        self.Q = mdesc.jump_dim if mdesc.jump_channel == L.JM_JUMP_STATE else self.M
+        self.T, self.K = pdesc.horizon, pdesc.samples
+        self.real = np.float64 if pdesc.precision == L.JM_F64 else np.float32
+        self.hbm = pdesc.noise_source == L.JM_NOISE_HBM
+
+    def close(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            self.lib.jm_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def check(self, rc):
+        raise_status(rc, self.h)
+
+    # -- wire format helpers
+    def step_major(self, a: np.ndarray, width: int) -> np.ndarray:
+        """(K, T, width) sample-major -> (T, width, K) contiguous in the compute precision."""
+        a = np.asarray(a, dtype=float).reshape(self.K, self.T, width)
+        return np.ascontiguousarray(a.transpose(1, 2, 0), dtype=self.real)
+
+    def iteration(self, x0, u_nom, seed, iteration, *, eps_c=None, jump=None, mapping=None,
+                  want_costs=False, want_weights=True, trace=False) -> IterationOut:
+        x0 = np.ascontiguousarray(x0, dtype=float).reshape(self.N)
+        u_nom = np.ascontiguousarray(u_nom, dtype=float).reshape(self.T * self.M)
+        u_new = np.empty(self.T * self.M)
+        norms = np.empty(self.T)
+        costs = np.empty(self.K) if (want_costs or trace) else None
+        weights = np.empty(self.K) if want_weights else None
+        states = np.empty((self.K, self.T + 1, self.N)) if trace else None
+        div = np.empty(self.K, dtype=np.int64) if trace else None
+        mp = None if mapping is None else np.ascontiguousarray(mapping, dtype=float).reshape(self.M, self.M)
+        diag = L.Diag()
+        rc = self.lib.jm_iteration_host(
+            self.h, L.dptr(x0), L.dptr(u_nom), C.c_uint64(int(seed)), C.c_uint64(int(iteration)),
+            L.vptr(eps_c), L.vptr(jump), L.dptr(mp), L.dptr(u_new), L.dptr(costs), L.dptr(weights),
+            L.dptr(norms), L.dptr(states), L.i64ptr(div), C.byref(diag))
+        self.check(rc)
+        return IterationOut(u_new.reshape(self.T, self.M), norms, diag, costs, weights, states, div)
+
+    def sample_noise(self, seed, iteration):
+        KT = self.K * self.T
+        ed = np.empty((self.K, self.T, self.M))
+        ind = np.empty((self.K, self.T), dtype=np.int64)
+        ej = np.empty((self.K, self.T, self.Q))
+        ec = np.empty((self.K, self.T, self.M))
+        rc = self.lib.jm_sample_noise_host(self.h, C.c_uint64(int(seed)), C.c_uint64(int(iteration)),
+                                           L.dptr(ed), L.i64ptr(ind), L.dptr(ej), L.dptr(ec))
+        self.check(rc)
+        del KT
+        return ed, ind, ej, ec
+
+    def closed_loop(self, x0, u_init, seed, steps):
+        x0 = np.ascontiguousarray(x0, dtype=float).reshape(self.N)
+        u_init = np.ascontiguousarray(u_init, dtype=float).reshape(self.M)
+        states = np.empty((steps + 1, self.N))
+        controls = np.empty((steps, self.M))
+        jumps = np.empty(steps, dtype=np.int64)
+        step_ns = np.empty(steps)
+        div = C.c_int32(-1)
+        status = C.c_int32(0)
+        rc = self.lib.jm_closed_loop_host(self.h, L.dptr(x0), L.dptr(u_init), C.c_uint64(int(seed)),
+                                          int(steps), L.dptr(states), L.dptr(controls),
+                                          L.i64ptr(jumps), L.dptr(step_ns), C.byref(div),
+                                          C.byref(status))
+        if rc not in (L.JM_OK,):
+            self.check(rc)
+        return states, controls, jumps, step_ns, int(div.value), int(status.value)
+
+    def kernel_name(self) -> str:
+        return self.lib.jm_kernel_name(self.h).decode()
+
+
+_cache: "OrderedDict[tuple, Context]" = OrderedDict()
+_cache_lock = threading.Lock()
+_CACHE_MAX = 12
+
+
+def get_context(model, cost_model, cfg, *, samples=None, precision=None, hbm=False,
+                sample_offset=0, device=None, block_threads=0) -> Context:
+    mdesc = describe_model(model)
+    cdesc = describe_cost(cost_model, mdesc.state_dim, mdesc.control_dim)
+    q = mdesc.jump_dim
+    pdesc = describe_mppi(cfg, mdesc.control_dim, q, samples=samples, precision=precision, hbm=hbm,
+                          sample_offset=sample_offset, block_threads=block_threads)
+    dev = int(os.environ.get("JM_B200_DEVICE", "0")) if device is None else int(device)
+    key = (bytes(mdesc), bytes(cdesc), bytes(pdesc), dev)
+    with _cache_lock:
+        ctx = _cache.get(key)
+        if ctx is not None:
+            _cache.move_to_end(key)
+            return ctx
+    ctx = Context(mdesc, cdesc, pdesc, dev)
+    with _cache_lock:
+        _cache[key] = ctx
+        while len(_cache) > _CACHE_MAX:
+            _, old = _cache.popitem(last=False)
+            old.close()
+    return ctx
+
+
+def clear_cache():
+    with _cache_lock:
+        for ctx in _cache.values():
+            ctx.close()
+        _cache.clear()
+
+
+def microbench(device: int = 0):
+    """Measured FP32 FFMA TFLOP/s, MUFU Tops/s, FP64 DFMA TFLOP/s on this GPU."""
+    lib = L.load()
+    f32, mufu, f64 = C.c_double(), C.c_double(), C.c_double()
+    raise_status(lib.jm_microbench(device, C.byref(f32), C.byref(mufu), C.byref(f64)))
+    return {"fp32_tflops": f32.value, "mufu_tops": mufu.value, "fp64_tflops": f64.value}
