@@ -214,6 +214,17 @@ int jm_loop_read(jm_ctx* ctx, double* x_out, uint64_t* iteration_out, int32_t* s
                  int32_t* halted_out, int32_t* status_out);
 
 /* ---- measurement helpers ---- */
+/* Time `steps` closed-loop control steps (jm_loop_init first) with CUDA events
+ * on the context's stream; before each step a cudaMemsetAsync of flush_bytes
+ * (> L2) evicts the L2.  use_graph=1: one graph launch per step (step_ms);
+ * use_graph=0: direct launches, step_ms and rollout_ms (the rollout kernel
+ * alone).  Either output may be NULL. */
+int jm_bench_loop(jm_ctx* ctx, int32_t steps, int64_t flush_bytes, int32_t use_graph, double* step_ms,
+                  double* rollout_ms);
+/* Time `reps` device-resident iterations (rollout + finalize, no host copies)
+ * from the context's current x0/u_nom; HBM mode first fills device noise
+ * tensors from the Philox sampler.  iter_ms / rollout_ms per rep. */
+int jm_bench_iteration(jm_ctx* ctx, int32_t reps, int64_t flush_bytes, double* iter_ms, double* rollout_ms);
 /* FP32 FFMA and MUFU throughput microbenchmarks (the roofline denominators
  * SURVEY 8(d) asks to measure): returns TFLOP/s and Tops/s. */
 int jm_microbench(int device, double* fp32_tflops, double* mufu_tops, double* fp64_tflops);

@@ -98,6 +98,8 @@ SIGNATURES = {
     "jm_loop_step": (C.c_int, [_vp]),
     "jm_loop_read": (C.c_int, [_vp, _pd, _pu64, _pi32, _pi32, _pi32]),
     "jm_microbench": (C.c_int, [C.c_int, _pd, _pd, _pd]),
+    "jm_bench_loop": (C.c_int, [_vp, _i32, _i64, _i32, _pd, _pd]),
+    "jm_bench_iteration": (C.c_int, [_vp, _i32, _i64, _pd, _pd]),
     "jm_kernel_name": (C.c_char_p, [_vp]),
     "jm_launches_per_iteration": (C.c_int, [_vp, _pi32, _pi32]),
 }

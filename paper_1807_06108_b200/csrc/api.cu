@@ -371,6 +371,7 @@ int jm_destroy(jm_ctx* ctx) {
   dfree(ctx->d_hist);
   dfree(ctx->d_hist_jumps);
   dfree(ctx->d_hist_t);
+  dfree(ctx->d_flush);
   if (ctx->h_small) cudaFreeHost(ctx->h_small);
   if (ctx->h_big) cudaFreeHost(ctx->h_big);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
@@ -833,6 +834,145 @@ int jm_microbench(int device, double* fp32_tflops, double* mufu_tops, double* fp
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   dfree(d_out);
+  return JM_OK;
+}
+
+static int ensure_flush(jm_ctx* ctx, int64_t bytes) {
+  if (bytes <= 0 || (size_t)bytes <= ctx->flush_cap) return JM_OK;
+  dfree(ctx->d_flush);
+  ctx->d_flush = nullptr;
+  ctx->flush_cap = 0;
+  CK(cudaMalloc(&ctx->d_flush, (size_t)bytes));
+  ctx->flush_cap = (size_t)bytes;
+  return JM_OK;
+}
+
+static int loop_direct(jm_ctx* ctx, cudaEvent_t mid) {
+  // the graph's three kernels, launched directly on the own stream
+  cudaStream_t saved = ctx->stream;
+  ctx->stream = ctx->own_stream;
+  jm::RolloutCall rc;
+  rc.u_nom = ctx->d_loop_unom;
+  rc.costs = ctx->d_costs;
+  rc.loop = ctx->d_loop;
+  cudaError_t e = ctx->eng->rollout(ctx, rc);
+  if (e == cudaSuccess && mid) e = cudaEventRecord(mid, ctx->stream);
+  if (e == cudaSuccess) {
+    jm::FinArgs f{};
+    f.rec = ctx->d_records;
+    f.nrec = ctx->grid;
+    f.rec_stride = ctx->rec_stride;
+    f.TM = ctx->TM;
+    f.M = ctx->M;
+    f.inv_lam = 1.0 / ctx->mppi.lambda_;
+    f.inv_sdt = 1.0 / std::sqrt(ctx->mppi.dt);
+    f.u_nom = ctx->d_loop_unom;
+    f.u_new = ctx->d_loop_unew;
+    f.loop = ctx->d_loop;
+    const int fgrid = (ctx->TM + jm::kFinCols - 1) / jm::kFinCols;
+    jm::finalize_kernel<<<fgrid, jm::kFinThreads, 0, ctx->stream>>>(f);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = ctx->eng->plant(ctx, ctx->d_loop, ctx->d_loop_unew, ctx->d_loop_unom);
+  ctx->stream = saved;
+  CK(e);
+  return JM_OK;
+}
+
+int jm_bench_loop(jm_ctx* ctx, int32_t steps, int64_t flush_bytes, int32_t use_graph, double* step_ms,
+                  double* rollout_ms) {
+  if (!ctx || !ctx->graph_exec || steps < 1) return fail(ctx, JM_ERR_VALUE, "loop not initialised");
+  CK(cudaSetDevice(ctx->device));
+  int r = ensure_flush(ctx, flush_bytes);
+  if (r != JM_OK) return r;
+  cudaStream_t s = ctx->own_stream;
+  std::vector<cudaEvent_t> ev(3 * (size_t)steps);
+  for (auto& e : ev) CK(cudaEventCreate(&e));
+  for (int i = 0; i < steps; ++i) {
+    if (flush_bytes > 0) CK(cudaMemsetAsync(ctx->d_flush, i & 0xFF, (size_t)flush_bytes, s));
+    CK(cudaEventRecord(ev[3 * i], s));
+    if (use_graph) {
+      CK(cudaGraphLaunch(ctx->graph_exec, s));
+    } else {
+      r = loop_direct(ctx, ev[3 * i + 1]);
+      if (r != JM_OK) return r;
+    }
+    CK(cudaEventRecord(ev[3 * i + 2], s));
+  }
+  CK(cudaStreamSynchronize(s));
+  for (int i = 0; i < steps; ++i) {
+    float a = 0.f, b = 0.f;
+    CK(cudaEventElapsedTime(&a, ev[3 * i], ev[3 * i + 2]));
+    if (step_ms) step_ms[i] = a;
+    if (rollout_ms) {
+      if (!use_graph) CK(cudaEventElapsedTime(&b, ev[3 * i], ev[3 * i + 1]));
+      rollout_ms[i] = use_graph ? 0.0 : b;
+    }
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  return JM_OK;
+}
+
+int jm_bench_iteration(jm_ctx* ctx, int32_t reps, int64_t flush_bytes, double* iter_ms, double* rollout_ms) {
+  if (!ctx || reps < 1) return fail(ctx, JM_ERR_VALUE, "bad arguments");
+  CK(cudaSetDevice(ctx->device));
+  int r = ensure_flush(ctx, flush_bytes);
+  if (r != JM_OK) return r;
+  const bool hbm = ctx->mppi.noise_source == JM_NOISE_HBM;
+  jm::RolloutCall rc;
+  rc.x0 = ctx->d_small + ctx->off_x0();
+  rc.u_nom = ctx->d_small + ctx->off_unom();
+  rc.seed = 1;
+  rc.iteration = 0;
+  rc.costs = ctx->d_costs;
+  if (hbm) {
+    const size_t eb = (size_t)ctx->TM * ctx->K * ctx->real_size;
+    if (!ctx->d_hbm_eps) CK(cudaMalloc(&ctx->d_hbm_eps, eb));
+    const bool sj = ctx->model.jump_channel == JM_JUMP_STATE;
+    if (sj && !ctx->d_hbm_jump) CK(cudaMalloc(&ctx->d_hbm_jump, (size_t)ctx->T * ctx->Q * ctx->K * ctx->real_size));
+    jm::NoiseArgs na = noise_args(ctx, 1, 0);
+    na.eps_c_sm = ctx->d_hbm_eps;
+    na.jump_sm = sj ? ctx->d_hbm_jump : nullptr;
+    CK(ctx->eng->noise(ctx, na));
+    rc.eps_in = ctx->d_hbm_eps;
+    rc.jump_in = sj ? ctx->d_hbm_jump : nullptr;
+  }
+  cudaStream_t s = ctx->stream;
+  std::vector<cudaEvent_t> ev(3 * (size_t)reps);
+  for (auto& e : ev) CK(cudaEventCreate(&e));
+  for (int i = 0; i < reps; ++i) {
+    rc.iteration = (uint64_t)i;
+    if (flush_bytes > 0) CK(cudaMemsetAsync(ctx->d_flush, i & 0xFF, (size_t)flush_bytes, s));
+    CK(cudaEventRecord(ev[3 * i], s));
+    CK(ctx->eng->rollout(ctx, rc));
+    CK(cudaEventRecord(ev[3 * i + 1], s));
+    jm::FinArgs f{};
+    f.rec = ctx->d_records;
+    f.nrec = ctx->grid;
+    f.rec_stride = ctx->rec_stride;
+    f.TM = ctx->TM;
+    f.M = ctx->M;
+    f.inv_lam = 1.0 / ctx->mppi.lambda_;
+    f.inv_sdt = 1.0 / std::sqrt(ctx->mppi.dt);
+    f.u_nom = rc.u_nom;
+    f.u_new = ctx->d_small + ctx->off_unew();
+    f.norms = ctx->d_small + ctx->off_norms();
+    f.diag = ctx->d_diag();
+    f.status = ctx->d_status();
+    const int fgrid = (ctx->TM + jm::kFinCols - 1) / jm::kFinCols;
+    jm::finalize_kernel<<<fgrid, jm::kFinThreads, 0, s>>>(f);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(ev[3 * i + 2], s));
+  }
+  CK(cudaStreamSynchronize(s));
+  for (int i = 0; i < reps; ++i) {
+    float a = 0.f, b = 0.f;
+    CK(cudaEventElapsedTime(&a, ev[3 * i], ev[3 * i + 2]));
+    CK(cudaEventElapsedTime(&b, ev[3 * i], ev[3 * i + 1]));
+    if (iter_ms) iter_ms[i] = a;
+    if (rollout_ms) rollout_ms[i] = b;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
   return JM_OK;
 }
 

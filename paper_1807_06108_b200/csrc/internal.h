@@ -80,6 +80,8 @@ struct jm_ctx {
   int64_t* d_hist_jumps = nullptr;
   uint64_t* d_hist_t = nullptr;   // t_start | t_end
   int loop_cap = 0;
+  void* d_flush = nullptr;         // L2 flush buffer (bench)
+  size_t flush_cap = 0;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
   std::string err;
