@@ -62,6 +62,7 @@ def parse():
     p.add_argument("--horizon", type=int, default=None, help="override T")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--profile", action="store_true", help="ncu mode: no clock settle, e2e or CPU legs")
     p.add_argument("--_cpu-worker", dest="cpu_worker", default=None, help=argparse.SUPPRESS)
     return p.parse_args()
 
@@ -286,6 +287,8 @@ def ours_arm(a):
     ctx.iteration(x0, np.tile(cfg.u_init, (T, 1)), 0, 0)  # uploads x0 / u_nom into the context; warm-up
 
     def settle():
+        if a.profile:
+            return
         # ~1 s of back-to-back device iterations (not timed) so the clock record covers a loaded GPU
         buf = np.zeros(64)
         t_end = time.time() + 1.0
@@ -366,7 +369,7 @@ def ours_arm(a):
         line["clocks"] = clocks
 
     # ---- e2e through the public drop-in API with host buffers
-    if not a.no_e2e:
+    if not (a.no_e2e or a.profile):
         ctrl = jb.initial_controller_state(cfg)
         x0 = np.asarray(task.x0, float)
         e2e = []
@@ -386,7 +389,7 @@ def ours_arm(a):
                                "the reference's `jump-mppi bench` loop (cli.py:157-183)"}
 
     # ---- CPU baseline (rank 0, N=1): the reference on one host core, bounded sample
-    if not a.no_cpu_baseline:
+    if not (a.no_cpu_baseline or a.profile):
         try:
             per_step, kind, Kdone, _ = run_cpu(system, min(K, 65536 if system == "cartpole" else 8192), T, 3, 1)
             cs = statistics.mean(per_step)

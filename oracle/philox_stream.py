@@ -98,10 +98,15 @@ def device_noise(seed, iteration, K, T, m, q, Ld, Lj, mark_mean, jthr, jump_chan
         ind = (words < np.uint32(jthr)).astype(np.int64)
         rows, cols = np.nonzero(ind)
         if rows.size:
-            mw = draw(key, SLOT_MARK, cols.astype(np.uint32), k[rows, 0])
+            # mark normals: index t*QP + i, Philox block index>>2, lane index&3
+            QP = 4 if q == 3 else q
+            idx = cols[:, None].astype(np.int64) * QP + np.arange(q)[None, :]
+            blk = (idx >> 2).astype(np.uint32)
+            mw = draw(key, SLOT_MARK, blk, k[rows, 0][:, None])
             a01 = box_muller(mw[0], mw[1])
             a23 = box_muller(mw[2], mw[3])
-            zz = np.stack([a01[0], a01[1], a23[0], a23[1]], axis=-1)[:, :q]
+            allz = np.stack([a01[0], a01[1], a23[0], a23[1]], axis=-1)  # (events, q, 4)
+            zz = np.take_along_axis(allz, (idx & 3)[..., None], axis=-1)[..., 0]
             eps_j[rows, cols] = np.asarray(mark_mean, float)[:q] + zz @ np.tril(Lj).T
     eps_c = eps_d + eps_j if jump_channel == "control" else eps_d.copy()
     return eps_d, ind, eps_j, eps_c

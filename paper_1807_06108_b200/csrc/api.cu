@@ -139,26 +139,29 @@ __global__ void wavg_kernel(const double* w, const double* eps, int64_t K, int T
   }
 }
 
-int rollout_and_finalize(jm_ctx* ctx, const jm::RolloutCall& rc, const double* mapping_dev,
-                         bool want_weights) {
-  CK(ctx->eng->rollout(ctx, rc));
+jm::FinArgs fin_args(const jm_ctx* ctx, const double* records, int nrec) {
   jm::FinArgs f{};
-  f.rec = ctx->d_records;
-  f.nrec = ctx->grid;
+  f.rec = records ? records : ctx->d_records;
+  f.nrec = records ? nrec : ctx->grid;
   f.rec_stride = ctx->rec_stride;
   f.TM = ctx->TM;
   f.M = ctx->M;
   f.inv_lam = 1.0 / ctx->mppi.lambda_;
   f.inv_sdt = 1.0 / std::sqrt(ctx->mppi.dt);
+  return f;
+}
+
+int rollout_and_finalize(jm_ctx* ctx, const jm::RolloutCall& rc, const double* mapping_dev,
+                         bool want_weights) {
+  CK(ctx->eng->rollout(ctx, rc));
+  jm::FinArgs f = fin_args(ctx, nullptr, 0);
   f.u_nom = rc.u_nom;
   f.mapping = mapping_dev;
   f.u_new = ctx->d_small + ctx->off_unew();
   f.norms = ctx->d_small + ctx->off_norms();
   f.diag = ctx->d_diag();
   f.status = ctx->d_status();
-  const int fgrid = (ctx->TM + jm::kFinCols - 1) / jm::kFinCols;
-  jm::finalize_kernel<<<fgrid, jm::kFinThreads, 0, ctx->stream>>>(f);
-  CK(cudaGetLastError());
+  CK(ctx->eng->finalize(ctx, f, nullptr, nullptr));
   if (want_weights) {
     const int b = 256, g = (ctx->K + b - 1) / b;
     jm::weights_kernel<<<g, b, 0, ctx->stream>>>(ctx->d_costs, ctx->d_diag(), 1.0 / ctx->mppi.lambda_,
@@ -181,37 +184,32 @@ int ensure_trace(jm_ctx* ctx) {
   return JM_OK;
 }
 
+// one control step of the closed loop on ctx->stream: rollout, then finalize
+// whose last CTA runs the plant step + shift (2 launches)
+cudaError_t loop_step_launches(jm_ctx* ctx, cudaEvent_t mid) {
+  jm::RolloutCall rc;
+  rc.u_nom = ctx->d_loop_unom;
+  rc.costs = ctx->d_costs;
+  rc.loop = ctx->d_loop;
+  cudaError_t e = ctx->eng->rollout(ctx, rc);
+  if (e == cudaSuccess && mid) e = cudaEventRecord(mid, ctx->stream);
+  if (e != cudaSuccess) return e;
+  jm::FinArgs f = fin_args(ctx, nullptr, 0);
+  f.u_nom = ctx->d_loop_unom;
+  f.u_new = ctx->d_loop_unew;
+  return ctx->eng->finalize(ctx, f, ctx->d_loop, ctx->d_loop_unom);
+}
+
 int capture_loop_graph(jm_ctx* ctx) {
   if (ctx->graph_exec) return JM_OK;
   cudaStream_t saved = ctx->stream;
   ctx->stream = ctx->own_stream;
   CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-  jm::RolloutCall rc;
-  rc.u_nom = ctx->d_loop_unom;
-  rc.costs = ctx->d_costs;
-  rc.loop = ctx->d_loop;
-  cudaError_t e1 = ctx->eng->rollout(ctx, rc);
-  jm::FinArgs f{};
-  f.rec = ctx->d_records;
-  f.nrec = ctx->grid;
-  f.rec_stride = ctx->rec_stride;
-  f.TM = ctx->TM;
-  f.M = ctx->M;
-  f.inv_lam = 1.0 / ctx->mppi.lambda_;
-  f.inv_sdt = 1.0 / std::sqrt(ctx->mppi.dt);
-  f.u_nom = ctx->d_loop_unom;
-  f.u_new = ctx->d_loop_unew;
-  f.loop = ctx->d_loop;
-  const int fgrid = (ctx->TM + jm::kFinCols - 1) / jm::kFinCols;
-  jm::finalize_kernel<<<fgrid, jm::kFinThreads, 0, ctx->stream>>>(f);
-  cudaError_t e2 = cudaGetLastError();
-  cudaError_t e3 = ctx->eng->plant(ctx, ctx->d_loop, ctx->d_loop_unew, ctx->d_loop_unom);
+  cudaError_t e1 = loop_step_launches(ctx, nullptr);
   cudaGraph_t g = nullptr;
   cudaError_t e4 = cudaStreamEndCapture(ctx->stream, &g);
   ctx->stream = saved;
   CK(e1);
-  CK(e2);
-  CK(e3);
   CK(e4);
   ctx->graph = g;
   CK(cudaGraphInstantiate(&ctx->graph_exec, g, 0));
@@ -248,6 +246,9 @@ int jm_create(const jm_model_desc* model, const jm_cost_desc* cost, const jm_mpp
   if (!(cost->lambda_ > 0)) return fail(nullptr, JM_ERR_CONFIG, "invalid configuration: cost lambda must be positive");
   if (!(cost->c >= 1.0)) return fail(nullptr, JM_ERR_CONFIG, "invalid configuration: cost c must be at least 1");
   const int m = model->control_dim, n = model->state_dim;
+  for (int i = 0; i < JM_MAX_STATE; ++i)
+    if (!(cost->weights[i] >= 0.0))  // nonnegative state costs (costs.py:37)
+      return fail(nullptr, JM_ERR_CONFIG, "invalid configuration: cost weights must be nonnegative");
   if (m != p.control_dim) return fail(nullptr, JM_ERR_CONFIG, "control_dim mismatch between model (%d) and config (%d)", m, p.control_dim);
   if (p.jump_enabled && !(p.nu * p.dt < 0.1))  // noise.py:148-149
     return fail(nullptr, JM_ERR_VALUE, "zero-one jump law violated (nu*dt = %g)", p.nu * p.dt);
@@ -337,6 +338,8 @@ int jm_create(const jm_model_desc* model, const jm_cost_desc* cost, const jm_mpp
   if (e == cudaSuccess) e = dalloc(&ctx->d_weights, (size_t)ctx->K);
   if (e == cudaSuccess) e = dalloc(&ctx->d_records, (size_t)ctx->grid * ctx->rec_stride);
   if (e == cudaSuccess) e = dalloc(&ctx->d_small, ctx->small_doubles());
+  if (e == cudaSuccess) e = dalloc(&ctx->d_counter, 1);
+  if (e == cudaSuccess) e = cudaMemsetAsync(ctx->d_counter, 0, sizeof(unsigned int), ctx->stream);
   if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_small, ctx->small_doubles() * sizeof(double));
   if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_big, 2 * (size_t)ctx->K * sizeof(double));
   if (e == cudaSuccess) e = cudaMemsetAsync(ctx->d_small, 0, ctx->small_doubles() * sizeof(double), ctx->stream);
@@ -363,6 +366,7 @@ int jm_destroy(jm_ctx* ctx) {
   dfree(ctx->d_weights);
   dfree(ctx->d_records);
   dfree(ctx->d_small);
+  dfree(ctx->d_counter);
   dfree(ctx->d_states);
   dfree(ctx->d_div);
   dfree(ctx->d_loop);
@@ -491,18 +495,9 @@ int jm_rollout_dev(jm_ctx* ctx, const double* x0_dev, const double* u_nom_dev, u
 int jm_reduce_dev(jm_ctx* ctx, double* record_dev) {
   if (!ctx || !record_dev) return fail(ctx, JM_ERR_VALUE, "null argument");
   CK(cudaSetDevice(ctx->device));
-  jm::FinArgs f{};
-  f.rec = ctx->d_records;
-  f.nrec = ctx->grid;
-  f.rec_stride = ctx->rec_stride;
-  f.TM = ctx->TM;
-  f.M = ctx->M;
-  f.inv_lam = 1.0 / ctx->mppi.lambda_;
-  f.inv_sdt = 1.0 / std::sqrt(ctx->mppi.dt);
+  jm::FinArgs f = fin_args(ctx, nullptr, 0);
   f.rec_out = record_dev;
-  const int fgrid = (ctx->TM + jm::kFinCols - 1) / jm::kFinCols;
-  jm::finalize_kernel<<<fgrid, jm::kFinThreads, 0, ctx->stream>>>(f);
-  CK(cudaGetLastError());
+  CK(ctx->eng->finalize(ctx, f, nullptr, nullptr));
   return JM_OK;
 }
 
@@ -510,24 +505,16 @@ int jm_finalize_dev(jm_ctx* ctx, const double* records_dev, int32_t nrec, const 
                     const double* mapping_dev, double* u_new_dev, double* step_norms_dev,
                     jm_diag* diag_dev, int32_t* status_dev) {
   if (!ctx || !u_nom_dev || !u_new_dev) return fail(ctx, JM_ERR_VALUE, "null argument");
+  if (records_dev && (nrec < 1 || nrec > jm::kMaxRecords)) return fail(ctx, JM_ERR_VALUE, "bad record count");
   CK(cudaSetDevice(ctx->device));
-  jm::FinArgs f{};
-  f.rec = records_dev ? records_dev : ctx->d_records;
-  f.nrec = records_dev ? nrec : ctx->grid;
-  f.rec_stride = ctx->rec_stride;
-  f.TM = ctx->TM;
-  f.M = ctx->M;
-  f.inv_lam = 1.0 / ctx->mppi.lambda_;
-  f.inv_sdt = 1.0 / std::sqrt(ctx->mppi.dt);
+  jm::FinArgs f = fin_args(ctx, records_dev, nrec);
   f.u_nom = u_nom_dev;
   f.mapping = mapping_dev;
   f.u_new = u_new_dev;
   f.norms = step_norms_dev;
   f.diag = reinterpret_cast<DiagOut*>(diag_dev);
   f.status = status_dev;
-  const int fgrid = (ctx->TM + jm::kFinCols - 1) / jm::kFinCols;
-  jm::finalize_kernel<<<fgrid, jm::kFinThreads, 0, ctx->stream>>>(f);
-  CK(cudaGetLastError());
+  CK(ctx->eng->finalize(ctx, f, nullptr, nullptr));
   return JM_OK;
 }
 
@@ -631,7 +618,6 @@ static jm::NoiseArgs noise_args(const jm_ctx* ctx, uint64_t seed, uint64_t itera
   na.K = ctx->K;
   na.T = ctx->T;
   na.q = ctx->Q;
-  na.jmode = ctx->model.jump_channel;
   na.jthr = ctx->jthr;
   na.jump_on = ctx->jthr != 0;
   na.sample_offset = ctx->mppi.sample_offset;
@@ -848,32 +834,9 @@ static int ensure_flush(jm_ctx* ctx, int64_t bytes) {
 }
 
 static int loop_direct(jm_ctx* ctx, cudaEvent_t mid) {
-  // the graph's three kernels, launched directly on the own stream
   cudaStream_t saved = ctx->stream;
   ctx->stream = ctx->own_stream;
-  jm::RolloutCall rc;
-  rc.u_nom = ctx->d_loop_unom;
-  rc.costs = ctx->d_costs;
-  rc.loop = ctx->d_loop;
-  cudaError_t e = ctx->eng->rollout(ctx, rc);
-  if (e == cudaSuccess && mid) e = cudaEventRecord(mid, ctx->stream);
-  if (e == cudaSuccess) {
-    jm::FinArgs f{};
-    f.rec = ctx->d_records;
-    f.nrec = ctx->grid;
-    f.rec_stride = ctx->rec_stride;
-    f.TM = ctx->TM;
-    f.M = ctx->M;
-    f.inv_lam = 1.0 / ctx->mppi.lambda_;
-    f.inv_sdt = 1.0 / std::sqrt(ctx->mppi.dt);
-    f.u_nom = ctx->d_loop_unom;
-    f.u_new = ctx->d_loop_unew;
-    f.loop = ctx->d_loop;
-    const int fgrid = (ctx->TM + jm::kFinCols - 1) / jm::kFinCols;
-    jm::finalize_kernel<<<fgrid, jm::kFinThreads, 0, ctx->stream>>>(f);
-    e = cudaGetLastError();
-  }
-  if (e == cudaSuccess) e = ctx->eng->plant(ctx, ctx->d_loop, ctx->d_loop_unew, ctx->d_loop_unom);
+  cudaError_t e = loop_step_launches(ctx, mid);
   ctx->stream = saved;
   CK(e);
   return JM_OK;
@@ -946,22 +909,13 @@ int jm_bench_iteration(jm_ctx* ctx, int32_t reps, int64_t flush_bytes, double* i
     CK(cudaEventRecord(ev[3 * i], s));
     CK(ctx->eng->rollout(ctx, rc));
     CK(cudaEventRecord(ev[3 * i + 1], s));
-    jm::FinArgs f{};
-    f.rec = ctx->d_records;
-    f.nrec = ctx->grid;
-    f.rec_stride = ctx->rec_stride;
-    f.TM = ctx->TM;
-    f.M = ctx->M;
-    f.inv_lam = 1.0 / ctx->mppi.lambda_;
-    f.inv_sdt = 1.0 / std::sqrt(ctx->mppi.dt);
+    jm::FinArgs f = fin_args(ctx, nullptr, 0);
     f.u_nom = rc.u_nom;
     f.u_new = ctx->d_small + ctx->off_unew();
     f.norms = ctx->d_small + ctx->off_norms();
     f.diag = ctx->d_diag();
     f.status = ctx->d_status();
-    const int fgrid = (ctx->TM + jm::kFinCols - 1) / jm::kFinCols;
-    jm::finalize_kernel<<<fgrid, jm::kFinThreads, 0, s>>>(f);
-    CK(cudaGetLastError());
+    CK(ctx->eng->finalize(ctx, f, nullptr, nullptr));
     CK(cudaEventRecord(ev[3 * i + 2], s));
   }
   CK(cudaStreamSynchronize(s));

@@ -1,6 +1,8 @@
 // engine.cuh -- per-(system, precision) launcher: packs the plugin
-// descriptors into kernel parameters and launches the templated kernels.
+// descriptors into kernel parameters, picks the launch shape and launches the
+// templated kernels.
 #pragma once
+#include <algorithm>
 #include <cmath>
 #include <type_traits>
 
@@ -32,6 +34,29 @@ void fill_quadrotor(const jm_model_desc& md, SysParams<Real>& sp) {
   sp.mp[7] = Real(1.0 / izz);
 }
 
+// cost weights enter as sqrt(w), sqrt(w) * target (systems.cuh)
+template <typename Real>
+void fill_cost(const jm_cost_desc& cd, int n, SysParams<Real>& sp) {
+  for (int i = 0; i < 12; ++i) {
+    sp.sw[i] = Real(0);
+    sp.swt[i] = Real(0);
+  }
+  if (cd.kind == JM_COST_DIAG_QUADRATIC) {
+    for (int i = 0; i < n; ++i) {
+      const double s = std::sqrt(cd.weights[i]);
+      sp.sw[i] = Real(s);
+      sp.swt[i] = Real(s * cd.target[i]);
+    }
+  } else {
+    for (int i = 0; i < 4; ++i) sp.sw[i] = Real(std::sqrt(cd.weights[i]));
+    if (cd.kind == JM_COST_QUADROTOR_HOVER) {
+      const double s = std::sqrt(cd.weights[0]);
+      for (int i = 0; i < 3; ++i) sp.swt[i] = Real(s * cd.target[i]);
+    }
+  }
+  sp.term_scale = Real(cd.terminal_scale);
+}
+
 template <class Dyn, class Cost, typename Real>
 class Engine final : public EngineBase {
   using Sys = System<Dyn, Cost>;
@@ -41,43 +66,65 @@ class Engine final : public EngineBase {
   template <typename R>
   static void fill_sys(const jm_ctx* c, SysParams<R>& sp) {
     for (auto& v : sp.mp) v = R(0);
-    for (auto& v : sp.w) v = R(0);
-    for (auto& v : sp.tgt) v = R(0);
     if constexpr (std::is_same<Dyn, Cartpole>::value) fill_cartpole<R>(c->model, sp);
     if constexpr (std::is_same<Dyn, Quadrotor>::value) fill_quadrotor<R>(c->model, sp);
-    for (int i = 0; i < 12; ++i) {
-      sp.w[i] = R(c->cost.weights[i]);
-      sp.tgt[i] = R(c->cost.target[i]);
-    }
-    sp.term_scale = R(c->cost.terminal_scale);
+    fill_cost<R>(c->cost, N, sp);
   }
 
   size_t smem_bytes(const jm_ctx* c, int block) const {
     return sizeof(double) * (size_t)c->TM + sizeof(Real) * ((size_t)c->T * (2 * M + 1) + block);
   }
 
-  template <bool PH, bool TR>
+  template <bool PH, bool TR, int JM>
   static const void* kfn() {
-    return reinterpret_cast<const void*>(&rollout_kernel<Sys, Real, PH, TR>);
+    return reinterpret_cast<const void*>(&rollout_kernel<Sys, Real, PH, TR, JM>);
   }
 
-  cudaError_t configure(jm_ctx* c) override {
-    const int block = c->block;
-    const size_t smem = smem_bytes(c, block);
-    const void* fns[4] = {kfn<true, false>(), kfn<true, true>(), kfn<false, false>(), kfn<false, true>()};
+  template <int JM>
+  cudaError_t set_attrs(size_t smem, const void** main_fn, bool philox) {
+    const void* fns[4] = {kfn<true, false, JM>(), kfn<true, true, JM>(), kfn<false, false, JM>(),
+                          kfn<false, true, JM>()};
     for (const void* f : fns) {
       cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
     }
-    const bool philox = c->mppi.noise_source == JM_NOISE_PHILOX;
-    int occ = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, philox ? fns[0] : fns[2], block, smem);
-    if (e != cudaSuccess) return e;
-    if (occ < 1) occ = 1;
-    c->smem = smem;
-    c->ntiles = (c->K + block - 1) / block;
-    c->grid = std::min(c->ntiles, occ * c->num_sms);
+    *main_fn = philox ? fns[0] : fns[2];
     return cudaSuccess;
+  }
+
+  // Launch shape.  K <= num_sms * 512: one CTA per SM, every SM gets the
+  // same sample count (a latency-bound horizon loop gains nothing from
+  // stacking CTAs on few SMs).  Larger K: 256-thread tiles, grid = SMs x
+  // occupancy, tiles grid-strided.
+  cudaError_t configure(jm_ctx* c) override {
+    const bool philox = c->mppi.noise_source == JM_NOISE_PHILOX;
+    int block = c->mppi.block_threads;
+    const int K = c->K, sms = c->num_sms;
+    if (block <= 0) {
+      if (K <= sms * kRolloutMaxThreads) {
+        const int per = (K + sms - 1) / sms;
+        block = std::max(32, ((per + 31) / 32) * 32);
+      } else {
+        block = 256;
+      }
+    }
+    c->block = block;
+    const size_t smem = smem_bytes(c, block);
+    const void* fn = nullptr;
+    cudaError_t e = (c->model.jump_channel == JM_JUMP_STATE) ? set_attrs<1>(smem, &fn, philox)
+                                                            : set_attrs<0>(smem, &fn, philox);
+    if (e != cudaSuccess) return e;
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, block, smem);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) return cudaErrorInvalidConfiguration;
+    c->smem = smem;
+    c->ntiles = (K + block - 1) / block;
+    c->grid = std::min(c->ntiles, occ * sms);
+    if (c->grid > kMaxRecords) c->grid = kMaxRecords;
+    const size_t fsm = finalize_smem_bytes(kMaxRecords);
+    return cudaFuncSetAttribute(reinterpret_cast<const void*>(&finalize_kernel<Dyn>),
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
   }
 
   RolloutArgs<Real> make_args(const jm_ctx* c, const RolloutCall& rc) const {
@@ -104,8 +151,6 @@ class Engine final : public EngineBase {
       a.mu_j[j] = Real(c->mppi.mark_mean[j]);
     }
     a.has_limits = c->model.has_limits;
-    a.q = c->Q;
-    a.jmode = c->model.jump_channel;
     a.jthr = c->jthr;
     a.jump_on = c->jthr != 0;
     a.jscale = Real(c->model.jump_scale_unit ? 1.0 : std::sqrt(dt));
@@ -127,30 +172,41 @@ class Engine final : public EngineBase {
     return a;
   }
 
+  template <int JM>
+  void launch(jm_ctx* c, const RolloutArgs<Real>& a, bool philox, bool trace) {
+    dim3 grid(c->grid), block(c->block);
+    if (philox && !trace)
+      rollout_kernel<Sys, Real, true, false, JM><<<grid, block, c->smem, c->stream>>>(a);
+    else if (philox)
+      rollout_kernel<Sys, Real, true, true, JM><<<grid, block, c->smem, c->stream>>>(a);
+    else if (!trace)
+      rollout_kernel<Sys, Real, false, false, JM><<<grid, block, c->smem, c->stream>>>(a);
+    else
+      rollout_kernel<Sys, Real, false, true, JM><<<grid, block, c->smem, c->stream>>>(a);
+  }
+
   cudaError_t rollout(jm_ctx* c, const RolloutCall& rc) override {
     const RolloutArgs<Real> a = make_args(c, rc);
     const bool philox = c->mppi.noise_source == JM_NOISE_PHILOX;
     const bool trace = rc.states != nullptr;
-    dim3 grid(c->grid), block(c->block);
-    if (philox && !trace)
-      rollout_kernel<Sys, Real, true, false><<<grid, block, c->smem, c->stream>>>(a);
-    else if (philox)
-      rollout_kernel<Sys, Real, true, true><<<grid, block, c->smem, c->stream>>>(a);
-    else if (!trace)
-      rollout_kernel<Sys, Real, false, false><<<grid, block, c->smem, c->stream>>>(a);
+    if (c->model.jump_channel == JM_JUMP_STATE)
+      launch<1>(c, a, philox, trace);
     else
-      rollout_kernel<Sys, Real, false, true><<<grid, block, c->smem, c->stream>>>(a);
+      launch<0>(c, a, philox, trace);
     return cudaGetLastError();
   }
 
   cudaError_t noise(jm_ctx* c, NoiseArgs& na) override {
     const int block = 128;
     const int grid = (c->K + block - 1) / block;
-    noise_kernel<M, Real><<<grid, block, 0, c->stream>>>(na);
+    if (c->model.jump_channel == JM_JUMP_STATE)
+      noise_kernel<M, 1, Dyn::QJ, Real><<<grid, block, 0, c->stream>>>(na);
+    else
+      noise_kernel<M, 0, Dyn::QJ, Real><<<grid, block, 0, c->stream>>>(na);
     return cudaGetLastError();
   }
 
-  cudaError_t plant(jm_ctx* c, LoopState* loop, const double* u_new, double* u_nom) override {
+  PlantArgs plant_args(const jm_ctx* c, LoopState* loop, const double* u_new, double* u_nom) const {
     PlantArgs p{};
     fill_sys<double>(c, p.sp);
     const double dt = c->mppi.dt;
@@ -175,7 +231,16 @@ class Engine final : public EngineBase {
     p.loop = loop;
     p.u_new = u_new;
     p.u_nom = u_nom;
-    plant_kernel<Dyn><<<1, 128, 0, c->stream>>>(p);
+    return p;
+  }
+
+  cudaError_t finalize(jm_ctx* c, FinArgs f, LoopState* loop, double* u_nom_next) override {
+    if (f.nrec > kMaxRecords) return cudaErrorInvalidValue;
+    f.loop = loop;
+    f.counter = c->d_counter;
+    const PlantArgs p = plant_args(c, loop, f.u_new, u_nom_next);
+    const int fgrid = (c->TM + kFinCols - 1) / kFinCols;
+    finalize_kernel<Dyn><<<fgrid, kFinThreads, finalize_smem_bytes(f.nrec), c->stream>>>(f, p);
     return cudaGetLastError();
   }
 

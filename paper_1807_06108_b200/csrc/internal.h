@@ -30,7 +30,9 @@ struct EngineBase {
   virtual cudaError_t configure(jm_ctx* c) = 0;
   virtual cudaError_t rollout(jm_ctx* c, const RolloutCall& rc) = 0;
   virtual cudaError_t noise(jm_ctx* c, NoiseArgs& na) = 0;
-  virtual cudaError_t plant(jm_ctx* c, LoopState* loop, const double* u_new, double* u_nom) = 0;
+  // combine records -> u_new (+ diagnostics); loop != null: the last CTA also
+  // runs the plant step and writes the shifted sequence to u_nom_next
+  virtual cudaError_t finalize(jm_ctx* c, FinArgs f, LoopState* loop, double* u_nom_next) = 0;
   virtual const char* kernel_name(bool trace) const = 0;
 };
 
@@ -80,6 +82,7 @@ struct jm_ctx {
   int64_t* d_hist_jumps = nullptr;
   uint64_t* d_hist_t = nullptr;   // t_start | t_end
   int loop_cap = 0;
+  unsigned int* d_counter = nullptr;  // finalize last-CTA counter
   void* d_flush = nullptr;         // L2 flush buffer (bench)
   size_t flush_cap = 0;
   cudaGraph_t graph = nullptr;

@@ -8,12 +8,11 @@
 //                    dynamics.py:87-135, costs.py:80-111.
 //   finalize_kernel  K3/K4/K5 across CTAs (or across GPUs): log-sum-exp merge
 //                    of the partial records, u_new = u_nom + N/(Z sqrt dt)
-//                    (@ mapping^T), diagnostics.  controller.py:62-78,
-//                    :157-169.
-//   weights_kernel   per-sample weights (controller.py:62-71) on demand.
-//   shift_kernel     K6 warm_start_shift (controller.py:96-100).
-//   plant_kernel     K7 closed-loop plant step + shift (harness.py:131-150).
+//                    (@ mapping^T), diagnostics (controller.py:62-78,
+//                    :157-169); in the closed loop its last CTA also runs K7,
+//                    the plant step + warm-start shift (harness.py:131-150).
 //   noise_kernel     K1 in write mode (sample_noise_batch on device).
+//   weights_kernel / shift_kernel (api.cu only): controller.py:62-71, :96-100.
 // All reductions are fixed-order (no float atomics): results are bitwise
 // reproducible run to run for a given launch configuration, and the noise is
 // independent of it.
@@ -28,8 +27,10 @@
 
 namespace jm {
 
-constexpr int kFinCols = 128;   // finalize: columns per CTA (multiple of m for m in {1,2,4})
-constexpr int kFinThreads = 256;
+constexpr int kFinCols = 128;      // finalize: columns per CTA (multiple of m for m in {1,2,4})
+constexpr int kFinThreads = 1024;  // finalize: 32 warps split the records
+constexpr int kMaxRecords = 4096;
+constexpr int kRolloutMaxThreads = 512;
 
 // Device-resident closed-loop controller state (ControllerState +
 // the plant state of run_trial).
@@ -98,13 +99,11 @@ struct RolloutArgs {
   Real R[16];
   Real u_lo[4], u_hi[4];
   int has_limits;
-  int q;            // jump mark dimension
-  int jmode;        // 0 control channel, 1 state selector
   int jump_on;      // sampler draws jumps (jump_sampling_enabled && nu > 0)
   uint32_t jthr;    // jump iff uniform word < jthr
   Real jscale;      // state-jump scale (1 or sqrt dt)
   Real Ld[16];      // chol(c * Sigma_D), m x m row-major
-  Real Lj[16];      // chol(Sigma_J), q x q
+  Real Lj[16];      // chol(Sigma_J), q x q row-major
   Real mu_j[4];     // mark mean
   SysParams<Real> sp;
   uint64_t seed, iteration;
@@ -113,7 +112,7 @@ struct RolloutArgs {
   const double* u_nom;
   const Real* eps_in;    // HBM mode: step-major eps_combined
   const Real* jump_in;   // HBM mode, state jumps: step-major ind*mark
-  Real* eps_out;         // Philox mode: per-CTA eps_combined scratch [cta][t*m+j][lane] (re-read by the epilogue)
+  Real* eps_out;         // Philox mode: per-CTA eps_combined scratch [cta][t*m+j][lane]
   double* costs;         // K
   double* states;        // trace: K*(T+1)*n
   int64_t* diverged;     // trace: K
@@ -123,7 +122,8 @@ struct RolloutArgs {
 };
 
 // ---------------------------------------------------------------- noise
-// Normals of one 4-step group for sample kg: z[s*MP + j] for step t0+s.
+// Diffusion normals of one 4-step group for sample kg: z[s*MP + j] for step
+// t0+s (normal index i = t*MP + j, Philox block i>>2, lane i&3).
 template <int MP>
 __device__ __forceinline__ void group_normals(const StreamKey& sk, uint32_t t0, uint32_t kg, float* z) {
 #pragma unroll
@@ -131,6 +131,25 @@ __device__ __forceinline__ void group_normals(const StreamKey& sk, uint32_t t0, 
     const P4 r = draw(sk, kSlotDiffusion, (t0 * MP >> 2) + b, kg);
     box_muller(r.x, r.y, z[4 * b + 0], z[4 * b + 1]);
     box_muller(r.z, r.w, z[4 * b + 2], z[4 * b + 3]);
+  }
+}
+
+// Jump-mark normals of the group, same indexing with QP per step (slot 2);
+// only the Philox blocks that hold a jump step are drawn.
+template <int QP>
+__device__ __forceinline__ void group_mark_normals(const StreamKey& sk, uint32_t t0, uint32_t kg,
+                                                   const bool* jf, float* zm) {
+#pragma unroll
+  for (int b = 0; b < QP; ++b) {
+    bool need = false;
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+      if ((s * QP) >> 2 == b) need = need || jf[s];
+    if (need) {
+      const P4 r = draw(sk, kSlotMark, (t0 * QP >> 2) + b, kg);
+      box_muller(r.x, r.y, zm[4 * b + 0], zm[4 * b + 1]);
+      box_muller(r.z, r.w, zm[4 * b + 2], zm[4 * b + 3]);
+    }
   }
 }
 
@@ -147,37 +166,32 @@ __device__ __forceinline__ void apply_chol(const Real* L, const float* z, Real* 
   }
 }
 
-// Jump marks for (kg, t): mk = mu + Lj z (q <= 4).
-template <typename Real>
-__device__ __forceinline__ void draw_marks(const StreamKey& sk, uint32_t t, uint32_t kg, const Real* Lj,
-                                        const Real* mu, int q, Real* mk) {
-  const P4 r = draw(sk, kSlotMark, t, kg);
-  float z[4];
-  box_muller(r.x, r.y, z[0], z[1]);
-  box_muller(r.z, r.w, z[2], z[3]);
+// marks = mu + Lj z
+template <int Q, typename Real>
+__device__ __forceinline__ void apply_marks(const Real* Lj, const Real* mu, const float* z, Real* mk) {
+  Real c[Q];
+  apply_chol<Q, Real>(Lj, z, c);
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    Real acc = Real(0);
-#pragma unroll
-    for (int l = 0; l < 4; ++l)
-      if (l <= i && i < q) acc = fma(Lj[i * q + l], Real(z[l]), acc);
-    mk[i] = (i < q) ? mu[i] + acc : Real(0);
-  }
+  for (int i = 0; i < Q; ++i) mk[i] = mu[i] + c[i];
 }
 
-__device__ __forceinline__ uint32_t word_of(const P4& w, int s) {
-  return s == 0 ? w.x : (s == 1 ? w.y : (s == 2 ? w.z : w.w));
-}
+template <int Q>
+struct Pad {
+  static constexpr int value = (Q == 3) ? 4 : Q;
+};
 
 // ---------------------------------------------------------------- rollout
-template <class Sys, typename Real, bool PHILOX, bool TRACE>
-__global__ void __launch_bounds__(256) rollout_kernel(const RolloutArgs<Real> a) {
+// JM = 0: control-channel jumps (marks folded into eps_combined, q = m);
+// JM = 1: state-space jumps on Dyn::jump_row (q = Dyn::QJ, eps_combined = eps_d).
+template <class Sys, typename Real, bool PHILOX, bool TRACE, int JM>
+__global__ void __launch_bounds__(kRolloutMaxThreads) rollout_kernel(const RolloutArgs<Real> a) {
   using Dyn = typename Sys::Dyn;
   using Cost = typename Sys::Cost;
   constexpr int N = Sys::N, M = Sys::M;
-  constexpr int MP = (M == 3) ? 4 : M;
+  constexpr int MP = Pad<M>::value;
+  constexpr int Q = (JM == 0) ? M : Dyn::QJ;
+  constexpr int QP = Pad<Q>::value;
   constexpr int TS = 2 * M + 1;
-  constexpr int QJ = Dyn::QJ;
 
   extern __shared__ double smem_d[];
   __shared__ double s_red[3][32];
@@ -226,14 +240,39 @@ __global__ void __launch_bounds__(256) rollout_kernel(const RolloutArgs<Real> a)
   }
   __syncthreads();
 
+  // loop-invariant parameters, pinned in registers
+  SysParams<Real> sp = a.sp;
+#pragma unroll
+  for (int i = 0; i < 10; ++i) pin(sp.mp[i]);
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    pin(sp.sw[i]);
+    pin(sp.swt[i]);
+  }
+  Real Ld[M * M], Lj[Q * Q], mu[Q];
+#pragma unroll
+  for (int i = 0; i < M * M; ++i) {
+    Ld[i] = a.Ld[i];
+    pin(Ld[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < Q * Q; ++i) Lj[i] = a.Lj[i];
+#pragma unroll
+  for (int i = 0; i < Q; ++i) mu[i] = a.mu_j[i];
+  Real dt = a.dt, sdt = a.sdt, cq = a.cq, jscale = a.jscale;
+  pin(dt);
+  pin(sdt);
+  pin(cq);
+  const uint32_t jthr = a.jthr;
+
   const StreamKey sk = make_stream_key(L ? L->seed : a.seed, iter);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  const Real dt = a.dt, sdt = a.sdt, cq = a.cq;
 
   for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
     const int kl = tile * blockDim.x + threadIdx.x;
     const bool active = kl < K;
     const uint32_t kg = (uint32_t)(a.sample_offset + kl);
+    Real* eout = PHILOX ? a.eps_out + (size_t)blockIdx.x * TM * blockDim.x + threadIdx.x : nullptr;
     Real S = Real(0);
     if (active) {
       Real x[N];
@@ -246,50 +285,60 @@ __global__ void __launch_bounds__(256) rollout_kernel(const RolloutArgs<Real> a)
       }
       for (int t0 = 0; t0 < T; t0 += 4) {
         float z[4 * MP];
-        P4 jw = P4{0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
+        float zm[4 * QP];
+        bool jf[4] = {false, false, false, false};
         if (PHILOX) {
           group_normals<MP>(sk, (uint32_t)t0, kg, z);
-          if (a.jump_on) jw = draw(sk, kSlotJumpUniform, (uint32_t)(t0 >> 2), kg);
+          if (a.jump_on) {  // zero-one law, noise.py:151
+            const P4 jw = draw(sk, kSlotJumpUniform, (uint32_t)(t0 >> 2), kg);
+            jf[0] = jw.x < jthr;
+            jf[1] = jw.y < jthr;
+            jf[2] = jw.z < jthr;
+            jf[3] = jw.w < jthr;
+            if (jf[0] | jf[1] | jf[2] | jf[3]) group_mark_normals<QP>(sk, (uint32_t)t0, kg, jf, zm);
+          }
         }
 #pragma unroll
         for (int s = 0; s < 4; ++s) {
           const int t = t0 + s;
           if (t >= T) break;
           Real eps[M];
-          Real sj[4] = {Real(0), Real(0), Real(0), Real(0)};  // state-space jump increment
+          Real sj[Q];
+#pragma unroll
+          for (int i = 0; i < Q; ++i) sj[i] = Real(0);
           bool has_sj = false;
           if (PHILOX) {
-            apply_chol<M, Real>(a.Ld, z + s * MP, eps);
-            if (word_of(jw, s) < a.jthr) {  // zero-one law, noise.py:151
-              Real mk[4];
-              draw_marks<Real>(sk, (uint32_t)t, kg, a.Lj, a.mu_j, a.q, mk);
-              if (a.jmode == 0) {
+            apply_chol<M, Real>(Ld, z + s * MP, eps);
+            if (jf[s]) {
+              Real mk[Q];
+              apply_marks<Q, Real>(Lj, mu, zm + s * QP, mk);
+              if (JM == 0) {
 #pragma unroll
-                for (int j = 0; j < M; ++j) eps[j] += mk[j];  // eps_c = eps_d + eps_j (noise.py:156-157)
+                for (int j = 0; j < M; ++j) eps[j] += mk[(j < Q) ? j : 0];  // eps_c = eps_d + eps_j (noise.py:156-157)
               } else {
 #pragma unroll
-                for (int i = 0; i < 4; ++i) sj[i] = a.jscale * mk[i];
+                for (int i = 0; i < Q; ++i) sj[i] = jscale * mk[i];
                 has_sj = true;
               }
             }
 #pragma unroll
-            for (int j = 0; j < M; ++j) a.eps_out[((size_t)blockIdx.x * TM + t * M + j) * blockDim.x + threadIdx.x] = eps[j];
+            for (int j = 0; j < M; ++j) eout[(size_t)(t * M + j) * blockDim.x] = eps[j];
           } else {
 #pragma unroll
             for (int j = 0; j < M; ++j) eps[j] = __ldg(a.eps_in + (size_t)(t * M + j) * K + kl);
-            if (a.jump_in != nullptr) {
+            if (JM == 1 && a.jump_in != nullptr) {
 #pragma unroll
-              for (int i = 0; i < QJ; ++i) sj[i] = a.jscale * __ldg(a.jump_in + (size_t)(t * QJ + i) * K + kl);
+              for (int i = 0; i < Q; ++i) sj[i] = jscale * __ldg(a.jump_in + (size_t)(t * Q + i) * K + kl);
               has_sj = true;
             }
           }
-          // modified running cost on x_t (controller.py:140-142)
-          const auto ax = Dyn::template aux<Real>(x, a.sp);
-          const Real qv = Cost::template q<Dyn, Real>(x, ax, a.sp);
-          const Real* st = tab + t * TS;
+          // modified running cost on x_t (controller.py:140-142):
           // q dt + 1/2 u'Ru dt + lambda sqrt(dt) u'eps + 1/2 lambda (1-1/c) eps'eps
-          // (the eps'eps sum is formed first, as costs.py:101/:514 does, so an
-          // overflowing eps gives NaN even when c = 1)
+          // (eps'eps formed first, as costs.py:101/:514, so an overflowing eps
+          // gives NaN even when c = 1)
+          const auto ax = Dyn::template aux<Real>(x, sp);
+          const Real qv = Cost::template q<Dyn, Real>(x, ax, sp);
+          const Real* st = tab + t * TS;
           Real inc = fma(qv, dt, st[M]);
           Real quad = eps[0] * eps[0];
 #pragma unroll
@@ -306,10 +355,10 @@ __global__ void __launch_bounds__(256) rollout_kernel(const RolloutArgs<Real> a)
           Real v[M];
 #pragma unroll
           for (int j = 0; j < M; ++j) v[j] = fma(eps[j], sdt, st[j]);
-          Dyn::template advance<Real>(x, ax, v, dt, a.sp);
-          if (has_sj) {
+          Dyn::template advance<Real>(x, ax, v, dt, sp);
+          if (JM == 1 && has_sj) {
 #pragma unroll
-            for (int i = 0; i < QJ; ++i) x[Dyn::jump_row(i)] += sj[i];
+            for (int i = 0; i < Q; ++i) x[Dyn::jump_row(i)] += sj[i];
           }
           if (TRACE) {
             // divergence mask, controller.py:144-151
@@ -336,8 +385,8 @@ __global__ void __launch_bounds__(256) rollout_kernel(const RolloutArgs<Real> a)
         a.diverged[kl] = dstep;
       }
       if (fin) {
-        const auto ax = Dyn::template aux<Real>(x, a.sp);
-        S += a.sp.term_scale * Cost::template q<Dyn, Real>(x, ax, a.sp);  // controller.py:155
+        const auto ax = Dyn::template aux<Real>(x, sp);
+        S += sp.term_scale * Cost::template q<Dyn, Real>(x, ax, sp);  // controller.py:155
       } else {
         S = r_inf<Real>();
       }
@@ -385,20 +434,18 @@ __global__ void __launch_bounds__(256) rollout_kernel(const RolloutArgs<Real> a)
       s_acc[2] = s_acc[2] * scale_old * scale_old + z2;
       s_acc[3] += nf;
     }
-    // N[r] += sum_k w_k eps[r, k] over the tile: warp-per-row, lanes over k
-    const int base = tile * blockDim.x;
-    const int nk = min((int)blockDim.x, K - base);
+    // N[r] += sum_k w_k eps[r, k] over the tile: warp-per-row, lanes over k.
     // Philox: this CTA's scratch slab (rows of blockDim.x, written above);
     // HBM: the input tensor itself (rows of K).
+    const int base = tile * blockDim.x;
+    const int nk = min((int)blockDim.x, K - base);
     const Real* src = PHILOX ? a.eps_out + (size_t)blockIdx.x * TM * blockDim.x : a.eps_in + base;
     const size_t rstride = PHILOX ? (size_t)blockDim.x : (size_t)K;
     for (int r = warp; r < TM; r += nwarps) {
       const Real* row = src + (size_t)r * rstride;
       Real acc = Real(0);
 #pragma unroll 4
-      for (int kk = lane; kk < nk; kk += 32) {
-        acc = fma(sw[kk], row[kk], acc);  // einsum semantics: 0 * inf = NaN like controller.py:78
-      }
+      for (int kk = lane; kk < nk; kk += 32) acc = fma(sw[kk], row[kk], acc);  // 0 * inf = NaN like controller.py:78
       acc = warp_sum(acc);
       if (lane == 0) Nacc[r] = Nacc[r] * scale_old + double(acc);
     }
@@ -415,6 +462,99 @@ __global__ void __launch_bounds__(256) rollout_kernel(const RolloutArgs<Real> a)
   for (int r = threadIdx.x; r < TM; r += blockDim.x) rec[4 + r] = Nacc[r];
 }
 
+// ---------------------------------------------------------------- plant + shift (closed loop)
+struct PlantArgs {
+  SysParams<double> sp;
+  double dt, sdt, jscale;
+  double Lp[16];   // chol(Sigma_D)  (plant: Sigma_D, not c*Sigma_D; harness.py:123)
+  double Lj[16];   // chol(Sigma_J)
+  double mu_j[4];
+  uint32_t jthr;   // plant always has jumps (harness.py:138)
+  int q, jmode, has_limits, T, M;
+  double u_lo[4], u_hi[4];
+  LoopState* loop;
+  const double* u_new;
+  double* u_nom;
+};
+
+// One plant step from u_new[0] and the warm-start shift; run by one CTA after
+// u_new is complete.
+template <class Dyn>
+__device__ void plant_and_shift(const PlantArgs& a) {
+  constexpr int N = Dyn::N, M = Dyn::M;
+  LoopState* L = a.loop;
+  __shared__ int s_ok;
+  if (threadIdx.x == 0) {
+    const int k = L->step;
+    L->t_end[k] = globaltimer();
+    double u0[M];
+    for (int j = 0; j < M; ++j) {
+      double v = __ldcg(a.u_new + j);
+      if (a.has_limits) v = fmin(fmax(v, a.u_lo[j]), a.u_hi[j]);  // harness.py:136
+      u0[j] = v;
+    }
+    const StreamKey sk = make_stream_key(L->seed, 0);
+    // eps_d = L_D N(0,I); has_jump = U < nu dt; eps_j = L_J N(0,I) drawn every step (:137-139)
+    P4 r = draw(sk, kSlotPlant, 3u * k + 0u, 0u);
+    float z[4];
+    box_muller(r.x, r.y, z[0], z[1]);
+    box_muller(r.z, r.w, z[2], z[3]);
+    double ed[M];
+    apply_chol<M, double>(a.Lp, z, ed);
+    const P4 ju = draw(sk, kSlotPlant, 3u * k + 1u, 0u);
+    const bool jump = ju.x < a.jthr;
+    r = draw(sk, kSlotPlant, 3u * k + 2u, 0u);
+    box_muller(r.x, r.y, z[0], z[1]);
+    box_muller(r.z, r.w, z[2], z[3]);
+    double mk[4];
+    for (int i = 0; i < 4; ++i) {
+      double acc = 0.0;
+      for (int l = 0; l <= i && i < a.q; ++l) acc = fma(a.Lj[i * a.q + l], double(z[l]), acc);
+      mk[i] = (i < a.q) ? a.mu_j[i] + acc : 0.0;
+    }
+    double x[N];
+    for (int i = 0; i < N; ++i) x[i] = L->x[i];
+    const auto ax = Dyn::template aux<double>(x, a.sp);
+    double v[M];
+    for (int j = 0; j < M; ++j) {
+      const double e = (jump && a.jmode == 0) ? ed[j] + mk[j] : ed[j];
+      v[j] = fma(e, a.sdt, u0[j] * a.dt);
+    }
+    Dyn::template advance<double>(x, ax, v, a.dt, a.sp);
+    if (jump && a.jmode == 1) {
+#pragma unroll
+      for (int i = 0; i < Dyn::QJ; ++i) x[Dyn::jump_row(i)] += a.jscale * mk[i];
+    }
+    bool fin = true;
+    for (int i = 0; i < N; ++i) fin = fin && isfinite(x[i]);
+    for (int j = 0; j < M; ++j) L->hist_controls[(size_t)k * M + j] = u0[j];
+    L->hist_jumps[k] = jump ? 1 : 0;
+    if (!fin) {  // StateDivergedError -> trial failure (harness.py:144-148)
+      L->halted = 1;
+      L->status = 7;
+      L->diverged_at = k;
+      s_ok = 0;
+    } else {
+      for (int i = 0; i < N; ++i) {
+        L->x[i] = x[i];
+        L->hist_states[(size_t)(k + 1) * N + i] = x[i];
+      }
+      s_ok = 1;
+    }
+  }
+  __syncthreads();
+  if (!s_ok) return;
+  const int TM = a.T * M;
+  for (int i = threadIdx.x; i < TM; i += blockDim.x)
+    a.u_nom[i] = (i < TM - M) ? __ldcg(a.u_new + i + M) : L->u_init[i - (TM - M)];  // warm_start_shift
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    L->iteration += 1;  // ControllerState(..., k+1, cfg) (harness.py:150)
+    L->step += 1;
+    if (L->step >= L->max_steps) L->halted = 1;
+  }
+}
+
 // ---------------------------------------------------------------- finalize
 struct FinArgs {
   const double* rec;
@@ -428,17 +568,26 @@ struct FinArgs {
   int32_t* status;        // or null
   double* rec_out;        // reduce mode: write the merged record instead of finalizing
   LoopState* loop;
+  unsigned int* counter;  // last-CTA-done counter (closed loop)
 };
 
-#ifdef JM_COMMON_KERNELS  // non-template kernels: defined in api.cu only
-__global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a) {
-  __shared__ double s_red[3][kFinThreads / 32];
-  __shared__ double s_part[kFinThreads / 32][kFinCols];
+inline size_t finalize_smem_bytes(int nrec) {
+  return sizeof(double) * ((size_t)nrec + (size_t)(kFinThreads / 32) * kFinCols);
+}
+
+template <class Dyn>
+__global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, const PlantArgs p) {
+  extern __shared__ double fsm[];
+  constexpr int NW = kFinThreads / 32;
+  double* se = fsm;                 // e_b = exp(-(rho_b - rho)/lambda), per record
+  double* part = fsm + a.nrec;      // [NW][kFinCols]
+  __shared__ double s_red[3][NW];
   __shared__ double s_delta[kFinCols];
   __shared__ double s_bc[4];
+  __shared__ int s_last;
   LoopState* L = a.loop;
   if (L != nullptr && L->halted) return;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = kFinThreads / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int rs = a.rec_stride;
   // global rho (controller.py:69: min over finite costs)
   double m = CUDART_INF;
@@ -448,20 +597,19 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a) 
   __syncthreads();
   if (tid == 0) {
     double mm = CUDART_INF;
-    for (int w = 0; w < nw; ++w) mm = fmin(mm, s_red[0][w]);
+    for (int w = 0; w < NW; ++w) mm = fmin(mm, s_red[0][w]);
     s_bc[0] = mm;
   }
   __syncthreads();
   const double rho = s_bc[0];
   double z = 0.0, w2 = 0.0, nf = 0.0;
-  if (rho != CUDART_INF) {
-    for (int b = tid; b < a.nrec; b += kFinThreads) {
-      const double* r = a.rec + (size_t)b * rs;
-      const double e = (r[0] == CUDART_INF) ? 0.0 : exp(-(r[0] - rho) * a.inv_lam);
-      z += r[1] * e;
-      w2 += r[2] * e * e;
-      nf += r[3];
-    }
+  for (int b = tid; b < a.nrec; b += kFinThreads) {
+    const double* r = a.rec + (size_t)b * rs;
+    const double e = (r[0] == CUDART_INF || rho == CUDART_INF) ? 0.0 : exp(-(r[0] - rho) * a.inv_lam);
+    se[b] = e;
+    z += r[1] * e;
+    w2 += r[2] * e * e;
+    nf += r[3];
   }
   z = warp_sum(z);
   w2 = warp_sum(w2);
@@ -475,7 +623,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a) 
   __syncthreads();
   if (tid == 0) {
     double zz = 0.0, ww = 0.0, nn = 0.0;
-    for (int w = 0; w < nw; ++w) {
+    for (int w = 0; w < NW; ++w) {
       zz += s_red[0][w];
       ww += s_red[1][w];
       nn += s_red[2][w];
@@ -511,28 +659,27 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a) 
     }
     return;
   }
-  // columns: warps split records, lanes split columns
+  // columns: warps split records (several in flight), lanes split columns
   constexpr int CPL = kFinCols / 32;
   double acc[CPL];
 #pragma unroll
   for (int i = 0; i < CPL; ++i) acc[i] = 0.0;
-  for (int b = warp; b < a.nrec; b += nw) {
-    const double* r = a.rec + (size_t)b * rs;
-    const double rb = r[0];
-    if (rb == CUDART_INF) continue;
-    const double e = exp(-(rb - rho) * a.inv_lam);
+#pragma unroll 4
+  for (int b = warp; b < a.nrec; b += NW) {
+    const double* r = a.rec + (size_t)b * rs + 4;
+    const double e = se[b];
 #pragma unroll
     for (int i = 0; i < CPL; ++i) {
       const int c = c0 + lane + 32 * i;
-      if (c < a.TM) acc[i] = fma(r[4 + c], e, acc[i]);
+      if (c < a.TM) acc[i] = fma(r[c], e, acc[i]);
     }
   }
 #pragma unroll
-  for (int i = 0; i < CPL; ++i) s_part[warp][lane + 32 * i] = acc[i];
+  for (int i = 0; i < CPL; ++i) part[warp * kFinCols + lane + 32 * i] = acc[i];
   __syncthreads();
   if (tid < kFinCols) {
     double n = 0.0;
-    for (int w = 0; w < nw; ++w) n += s_part[w][tid];
+    for (int w = 0; w < NW; ++w) n += part[w * kFinCols + tid];
     s_delta[tid] = n;
   }
   __syncthreads();
@@ -577,8 +724,106 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a) 
     if (a.status) *a.status = 0;
     if (a.diag) *a.diag = DiagOut{rho, Z * Z / W2, Z, (int64_t)NF};  // ESS = 1/sum w^2 (:167)
   }
+  if (L != nullptr) {
+    // closed loop: the last CTA to finish runs the plant step + shift
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = (atomicAdd(a.counter, 1u) == gridDim.x - 1) ? 1 : 0;
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      plant_and_shift<Dyn>(p);
+      if (tid == 0) *a.counter = 0u;
+    }
+  }
 }
 
+// ---------------------------------------------------------------- noise (write mode)
+struct NoiseArgs {
+  int K, T, q, jump_on;
+  uint32_t jthr;
+  long long sample_offset;
+  uint64_t seed, iteration;
+  double Ld[16], Lj[16], mu_j[4];
+  // sample-major float64 outputs (host API mirror of sample_noise_batch)
+  double* eps_d;
+  int64_t* ind;
+  double* eps_j;
+  double* eps_c;
+  // step-major Real outputs (HBM-mode inputs)
+  void* eps_c_sm;
+  void* jump_sm;
+};
+
+template <int M, int JM, int QJ, typename Real>
+__global__ void __launch_bounds__(256) noise_kernel(const NoiseArgs a) {
+  constexpr int MP = Pad<M>::value;
+  constexpr int Q = (JM == 0) ? M : QJ;
+  constexpr int QP = Pad<Q>::value;
+  const int kl = blockIdx.x * blockDim.x + threadIdx.x;
+  if (kl >= a.K) return;
+  const uint32_t kg = (uint32_t)(a.sample_offset + kl);
+  const StreamKey sk = make_stream_key(a.seed, a.iteration);
+  Real Ld[M * M], Lj[Q * Q], mu[Q];
+#pragma unroll
+  for (int i = 0; i < M * M; ++i) Ld[i] = Real(a.Ld[i]);
+#pragma unroll
+  for (int i = 0; i < Q * Q; ++i) Lj[i] = Real(a.Lj[i]);
+#pragma unroll
+  for (int i = 0; i < Q; ++i) mu[i] = Real(a.mu_j[i]);
+  const int T = a.T, K = a.K;
+  for (int t0 = 0; t0 < T; t0 += 4) {
+    float z[4 * MP];
+    float zm[4 * QP];
+    bool jf[4] = {false, false, false, false};
+    group_normals<MP>(sk, (uint32_t)t0, kg, z);
+    if (a.jump_on) {
+      const P4 jw = draw(sk, kSlotJumpUniform, (uint32_t)(t0 >> 2), kg);
+      jf[0] = jw.x < a.jthr;
+      jf[1] = jw.y < a.jthr;
+      jf[2] = jw.z < a.jthr;
+      jf[3] = jw.w < a.jthr;
+      if (jf[0] | jf[1] | jf[2] | jf[3]) group_mark_normals<QP>(sk, (uint32_t)t0, kg, jf, zm);
+    }
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const int t = t0 + s;
+      if (t >= T) break;
+      Real ed[M], ec[M], mk[Q];
+      apply_chol<M, Real>(Ld, z + s * MP, ed);
+      const bool jump = jf[s];
+#pragma unroll
+      for (int i = 0; i < Q; ++i) mk[i] = Real(0);
+      if (jump) apply_marks<Q, Real>(Lj, mu, zm + s * QP, mk);
+#pragma unroll
+      for (int j = 0; j < M; ++j) ec[j] = ed[j];
+      if (JM == 0 && jump) {
+#pragma unroll
+        for (int j = 0; j < M; ++j) ec[j] += mk[(j < Q) ? j : 0];
+      }
+      const size_t row = (size_t)kl * T + t;
+      if (a.eps_d)
+#pragma unroll
+        for (int j = 0; j < M; ++j) a.eps_d[row * M + j] = double(ed[j]);
+      if (a.ind) a.ind[row] = jump ? 1 : 0;
+      if (a.eps_j)
+#pragma unroll
+        for (int i = 0; i < Q; ++i) a.eps_j[row * Q + i] = jump ? double(mk[i]) : 0.0;
+      if (a.eps_c)
+#pragma unroll
+        for (int j = 0; j < M; ++j) a.eps_c[row * M + j] = double(ec[j]);
+      if (a.eps_c_sm)
+#pragma unroll
+        for (int j = 0; j < M; ++j) reinterpret_cast<Real*>(a.eps_c_sm)[(size_t)(t * M + j) * K + kl] = ec[j];
+      if (JM == 1 && a.jump_sm)
+#pragma unroll
+        for (int i = 0; i < Q; ++i)
+          reinterpret_cast<Real*>(a.jump_sm)[(size_t)(t * Q + i) * K + kl] = jump ? mk[i] : Real(0);
+    }
+  }
+}
+
+#ifdef JM_COMMON_KERNELS  // non-template kernels: defined in api.cu only
 // ---------------------------------------------------------------- weights
 __global__ void weights_kernel(const double* costs, const DiagOut* diag, double inv_lam, int K,
                                double* w) {
@@ -597,160 +842,6 @@ __global__ void shift_kernel(const double* u, const double* u_init, int T, int M
   out[i] = (i < TM - M) ? u[i + M] : u_init[i - (TM - M)];
 }
 
-#endif  // JM_COMMON_KERNELS
-
-// ---------------------------------------------------------------- noise (write mode)
-struct NoiseArgs {
-  int K, T, q, jmode, jump_on;
-  uint32_t jthr;
-  long long sample_offset;
-  uint64_t seed, iteration;
-  double Ld[16], Lj[16], mu_j[4];
-  // sample-major float64 outputs (host API mirror of sample_noise_batch)
-  double* eps_d;
-  int64_t* ind;
-  double* eps_j;
-  double* eps_c;
-  // step-major Real outputs (HBM-mode inputs)
-  void* eps_c_sm;
-  void* jump_sm;
-};
-
-template <int M, typename Real>
-__global__ void __launch_bounds__(256) noise_kernel(const NoiseArgs a) {
-  constexpr int MP = (M == 3) ? 4 : M;
-  const int kl = blockIdx.x * blockDim.x + threadIdx.x;
-  if (kl >= a.K) return;
-  const uint32_t kg = (uint32_t)(a.sample_offset + kl);
-  const StreamKey sk = make_stream_key(a.seed, a.iteration);
-  Real Ld[16], Lj[16], mu[4];
-  for (int i = 0; i < 16; ++i) {
-    Ld[i] = Real(a.Ld[i]);
-    Lj[i] = Real(a.Lj[i]);
-  }
-  for (int i = 0; i < 4; ++i) mu[i] = Real(a.mu_j[i]);
-  const int T = a.T, K = a.K;
-  for (int t0 = 0; t0 < T; t0 += 4) {
-    float z[4 * MP];
-    group_normals<MP>(sk, (uint32_t)t0, kg, z);
-    P4 jw = P4{0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
-    if (a.jump_on) jw = draw(sk, kSlotJumpUniform, (uint32_t)(t0 >> 2), kg);
-    for (int s = 0; s < 4 && t0 + s < T; ++s) {
-      const int t = t0 + s;
-      Real ed[M], ec[M], mk[4] = {Real(0), Real(0), Real(0), Real(0)};
-      apply_chol<M, Real>(Ld, z + s * MP, ed);
-      const bool jump = word_of(jw, s) < a.jthr;
-      if (jump) draw_marks<Real>(sk, (uint32_t)t, kg, Lj, mu, a.q, mk);
-      for (int j = 0; j < M; ++j) ec[j] = (jump && a.jmode == 0) ? ed[j] + mk[j] : ed[j];
-      const size_t row = (size_t)kl * T + t;
-      if (a.eps_d)
-        for (int j = 0; j < M; ++j) a.eps_d[row * M + j] = double(ed[j]);
-      if (a.ind) a.ind[row] = jump ? 1 : 0;
-      if (a.eps_j)
-        for (int i = 0; i < a.q; ++i) a.eps_j[row * a.q + i] = jump ? double(mk[i]) : 0.0;
-      if (a.eps_c)
-        for (int j = 0; j < M; ++j) a.eps_c[row * M + j] = double(ec[j]);
-      if (a.eps_c_sm)
-        for (int j = 0; j < M; ++j) reinterpret_cast<Real*>(a.eps_c_sm)[(size_t)(t * M + j) * K + kl] = ec[j];
-      if (a.jump_sm)
-        for (int i = 0; i < a.q; ++i)
-          reinterpret_cast<Real*>(a.jump_sm)[(size_t)(t * a.q + i) * K + kl] = jump ? mk[i] : Real(0);
-    }
-  }
-}
-
-// ---------------------------------------------------------------- plant + shift (closed loop)
-struct PlantArgs {
-  SysParams<double> sp;
-  double dt, sdt, jscale;
-  double Lp[16];   // chol(Sigma_D)  (plant: Sigma_D, not c*Sigma_D; harness.py:123)
-  double Lj[16];   // chol(Sigma_J)
-  double mu_j[4];
-  uint32_t jthr;   // plant always has jumps (harness.py:138)
-  int q, jmode, has_limits, T, M;
-  double u_lo[4], u_hi[4];
-  LoopState* loop;
-  const double* u_new;
-  double* u_nom;
-};
-
-template <class Dyn>
-__global__ void plant_kernel(const PlantArgs a) {
-  constexpr int N = Dyn::N, M = Dyn::M;
-  LoopState* L = a.loop;
-  __shared__ int s_ok;
-  if (L->halted) return;
-  if (threadIdx.x == 0) {
-    const int k = L->step;
-    L->t_end[k] = globaltimer();
-    double u0[M];
-    for (int j = 0; j < M; ++j) {
-      double v = a.u_new[j];
-      if (a.has_limits) v = fmin(fmax(v, a.u_lo[j]), a.u_hi[j]);  // harness.py:136
-      u0[j] = v;
-    }
-    const StreamKey sk = make_stream_key(L->seed, 0);
-    // eps_d = L_D N(0,I); has_jump = U < nu dt; eps_j = L_J N(0,I) drawn every step (:137-139)
-    P4 r = draw(sk, kSlotPlant, 3u * k + 0u, 0u);
-    float z[4];
-    box_muller(r.x, r.y, z[0], z[1]);
-    box_muller(r.z, r.w, z[2], z[3]);
-    double ed[M];
-    apply_chol<M, double>(a.Lp, z, ed);
-    const P4 ju = draw(sk, kSlotPlant, 3u * k + 1u, 0u);
-    const bool jump = ju.x < a.jthr;
-    r = draw(sk, kSlotPlant, 3u * k + 2u, 0u);
-    box_muller(r.x, r.y, z[0], z[1]);
-    box_muller(r.z, r.w, z[2], z[3]);
-    double mk[4];
-    for (int i = 0; i < 4; ++i) {
-      double acc = 0.0;
-      for (int l = 0; l <= i && i < a.q; ++l) acc = fma(a.Lj[i * a.q + l], double(z[l]), acc);
-      mk[i] = (i < a.q) ? a.mu_j[i] + acc : 0.0;
-    }
-    double x[N];
-    for (int i = 0; i < N; ++i) x[i] = L->x[i];
-    const auto ax = Dyn::template aux<double>(x, a.sp);
-    double v[M];
-    for (int j = 0; j < M; ++j) {
-      const double e = (jump && a.jmode == 0) ? ed[j] + mk[j] : ed[j];
-      v[j] = fma(e, a.sdt, u0[j] * a.dt);
-    }
-    Dyn::template advance<double>(x, ax, v, a.dt, a.sp);
-    if (jump && a.jmode == 1)
-#pragma unroll
-      for (int i = 0; i < Dyn::QJ; ++i) x[Dyn::jump_row(i)] += a.jscale * mk[i];
-    bool fin = true;
-    for (int i = 0; i < N; ++i) fin = fin && isfinite(x[i]);
-    for (int j = 0; j < M; ++j) L->hist_controls[(size_t)k * M + j] = u0[j];
-    L->hist_jumps[k] = jump ? 1 : 0;
-    if (!fin) {  // StateDivergedError -> trial failure (harness.py:144-148)
-      L->halted = 1;
-      L->status = 7;
-      L->diverged_at = k;
-      s_ok = 0;
-    } else {
-      for (int i = 0; i < N; ++i) {
-        L->x[i] = x[i];
-        L->hist_states[(size_t)(k + 1) * N + i] = x[i];
-      }
-      s_ok = 1;
-    }
-  }
-  __syncthreads();
-  if (!s_ok) return;
-  const int TM = a.T * M;
-  for (int i = threadIdx.x; i < TM; i += blockDim.x)
-    a.u_nom[i] = (i < TM - M) ? a.u_new[i + M] : L->u_init[i - (TM - M)];  // warm_start_shift
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    L->iteration += 1;  // ControllerState(..., k+1, cfg) (harness.py:150)
-    L->step += 1;
-    if (L->step >= L->max_steps) L->halted = 1;
-  }
-}
-
-#ifdef JM_COMMON_KERNELS
 // ---------------------------------------------------------------- microbenchmarks
 __global__ void mb_ffma_kernel(float* out, int iters, float b, float c) {
   float a0 = threadIdx.x * 1e-7f, a1 = a0 + 1e-7f, a2 = a0 + 2e-7f, a3 = a0 + 3e-7f;
@@ -792,7 +883,6 @@ __global__ void mb_dfma_kernel(double* out, int iters, double b, double c) {
   const double s = a0 + a1 + a2 + a3;
   if (s == 12345.678) out[blockIdx.x] = s;
 }
-
 #endif  // JM_COMMON_KERNELS
 
 }  // namespace jm

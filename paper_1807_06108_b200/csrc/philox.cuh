@@ -18,7 +18,8 @@
 //   ctr  = (block, sample, iteration lo32, slot<<24 | iteration hi32 & 0xffffff)
 //   slot 0: diffusion normals, normal index i = t*MP + j, block = i>>2, lane = i&3
 //   slot 1: jump uniforms, block = t>>2, word = t&3, jump iff word < thr<<8
-//   slot 2: marks, block = t, normals 0..q-1
+//   slot 2: marks, normal index t*QP + i (QP = q, 3 padded to 4), block = index>>2
+//           (drawn only for 4-step groups / blocks that hold a jump event)
 //   slot 3: closed-loop plant, block = 3*step + {0 diffusion, 1 uniform, 2 marks}
 // Normals: Box-Muller on pairs of words with 23-bit mantissa uniforms.
 // The CPU emulation of this exact mapping is oracle/philox_stream.py.
