@@ -283,96 +283,116 @@ __global__ void __launch_bounds__(kRolloutMaxThreads) rollout_kernel(const Rollo
 #pragma unroll
         for (int i = 0; i < N; ++i) a.states[((size_t)kl * (T + 1)) * N + i] = double(x[i]);
       }
-      for (int t0 = 0; t0 < T; t0 += 4) {
-        float z[4 * MP];
-        float zm[4 * QP];
-        bool jf[4] = {false, false, false, false};
+      Real* ep = eout;  // Philox scratch: row (t*M+j) of this thread's column
+      // one horizon step t (sub-step s of its 4-step group)
+      auto step = [&](const int t, const int s, const float* z, const float* zm, const bool* jf) {
+        Real eps[M];
+        Real sj[Q];
+#pragma unroll
+        for (int i = 0; i < Q; ++i) sj[i] = Real(0);
+        bool has_sj = false;
         if (PHILOX) {
-          group_normals<MP>(sk, (uint32_t)t0, kg, z);
-          if (a.jump_on) {  // zero-one law, noise.py:151
-            const P4 jw = draw(sk, kSlotJumpUniform, (uint32_t)(t0 >> 2), kg);
-            jf[0] = jw.x < jthr;
-            jf[1] = jw.y < jthr;
-            jf[2] = jw.z < jthr;
-            jf[3] = jw.w < jthr;
-            if (jf[0] | jf[1] | jf[2] | jf[3]) group_mark_normals<QP>(sk, (uint32_t)t0, kg, jf, zm);
-          }
-        }
+          apply_chol<M, Real>(Ld, z + s * MP, eps);
+          if (jf[s]) {
+            Real mk[Q];
+            apply_marks<Q, Real>(Lj, mu, zm + s * QP, mk);
+            if (JM == 0) {
 #pragma unroll
-        for (int s = 0; s < 4; ++s) {
-          const int t = t0 + s;
-          if (t >= T) break;
-          Real eps[M];
-          Real sj[Q];
+              for (int j = 0; j < M; ++j) eps[j] += mk[(j < Q) ? j : 0];  // eps_c = eps_d + eps_j (noise.py:156-157)
+            } else {
 #pragma unroll
-          for (int i = 0; i < Q; ++i) sj[i] = Real(0);
-          bool has_sj = false;
-          if (PHILOX) {
-            apply_chol<M, Real>(Ld, z + s * MP, eps);
-            if (jf[s]) {
-              Real mk[Q];
-              apply_marks<Q, Real>(Lj, mu, zm + s * QP, mk);
-              if (JM == 0) {
-#pragma unroll
-                for (int j = 0; j < M; ++j) eps[j] += mk[(j < Q) ? j : 0];  // eps_c = eps_d + eps_j (noise.py:156-157)
-              } else {
-#pragma unroll
-                for (int i = 0; i < Q; ++i) sj[i] = jscale * mk[i];
-                has_sj = true;
-              }
-            }
-#pragma unroll
-            for (int j = 0; j < M; ++j) eout[(size_t)(t * M + j) * blockDim.x] = eps[j];
-          } else {
-#pragma unroll
-            for (int j = 0; j < M; ++j) eps[j] = __ldg(a.eps_in + (size_t)(t * M + j) * K + kl);
-            if (JM == 1 && a.jump_in != nullptr) {
-#pragma unroll
-              for (int i = 0; i < Q; ++i) sj[i] = jscale * __ldg(a.jump_in + (size_t)(t * Q + i) * K + kl);
+              for (int i = 0; i < Q; ++i) sj[i] = jscale * mk[i];
               has_sj = true;
             }
           }
-          // modified running cost on x_t (controller.py:140-142):
-          // q dt + 1/2 u'Ru dt + lambda sqrt(dt) u'eps + 1/2 lambda (1-1/c) eps'eps
-          // (eps'eps formed first, as costs.py:101/:514, so an overflowing eps
-          // gives NaN even when c = 1)
-          const auto ax = Dyn::template aux<Real>(x, sp);
-          const Real qv = Cost::template q<Dyn, Real>(x, ax, sp);
-          const Real* st = tab + t * TS;
-          Real inc = fma(qv, dt, st[M]);
-          Real quad = eps[0] * eps[0];
 #pragma unroll
-          for (int j = 1; j < M; ++j) quad = fma(eps[j], eps[j], quad);
+          for (int j = 0; j < M; ++j) ep[(size_t)j * blockDim.x] = eps[j];
+          ep += (size_t)M * blockDim.x;
+        } else {
 #pragma unroll
-          for (int j = 0; j < M; ++j) inc = fma(st[M + 1 + j], eps[j], inc);
-          S += fma(cq, quad, inc);
-          // Euler step (dynamics.py:130-135 / :115-129 with B = G)
-          Real xold[N];
-          if (TRACE) {
+          for (int j = 0; j < M; ++j) eps[j] = __ldg(a.eps_in + (size_t)(t * M + j) * K + kl);
+          if (JM == 1 && a.jump_in != nullptr) {
 #pragma unroll
-            for (int i = 0; i < N; ++i) xold[i] = x[i];
+            for (int i = 0; i < Q; ++i) sj[i] = jscale * __ldg(a.jump_in + (size_t)(t * Q + i) * K + kl);
+            has_sj = true;
           }
-          Real v[M];
+        }
+        // modified running cost on x_t (controller.py:140-142):
+        // q dt + 1/2 u'Ru dt + lambda sqrt(dt) u'eps + 1/2 lambda (1-1/c) eps'eps
+        // (eps'eps formed first, as costs.py:101/:514, so an overflowing eps
+        // gives NaN even when c = 1)
+        const auto ax = Dyn::template aux<Real>(x, sp);
+        const Real qv = Cost::template q<Dyn, Real>(x, ax, sp);
+        const Real* st = tab + t * TS;
+        Real inc = fma(qv, dt, st[M]);
+        Real quad = eps[0] * eps[0];
 #pragma unroll
-          for (int j = 0; j < M; ++j) v[j] = fma(eps[j], sdt, st[j]);
-          Dyn::template advance<Real>(x, ax, v, dt, sp);
-          if (JM == 1 && has_sj) {
+        for (int j = 1; j < M; ++j) quad = fma(eps[j], eps[j], quad);
 #pragma unroll
-            for (int i = 0; i < Q; ++i) x[Dyn::jump_row(i)] += sj[i];
+        for (int j = 0; j < M; ++j) inc = fma(st[M + 1 + j], eps[j], inc);
+        S += fma(cq, quad, inc);
+        // Euler step (dynamics.py:130-135 / :115-129 with B = G)
+        Real xold[N];
+        if (TRACE) {
+#pragma unroll
+          for (int i = 0; i < N; ++i) xold[i] = x[i];
+        }
+        Real v[M];
+#pragma unroll
+        for (int j = 0; j < M; ++j) v[j] = fma(eps[j], sdt, st[j]);
+        Dyn::template advance<Real>(x, ax, v, dt, sp);
+        if (JM == 1 && has_sj) {
+#pragma unroll
+          for (int i = 0; i < Q; ++i) x[Dyn::jump_row(i)] += sj[i];
+        }
+        if (TRACE) {
+          // divergence mask, controller.py:144-151
+          bool fin = true;
+#pragma unroll
+          for (int i = 0; i < N; ++i) fin = fin && isfinite(x[i]);
+          if (dstep >= 0 || !fin) {
+            if (dstep < 0) dstep = t;
+#pragma unroll
+            for (int i = 0; i < N; ++i) x[i] = xold[i];
           }
-          if (TRACE) {
-            // divergence mask, controller.py:144-151
-            bool fin = true;
 #pragma unroll
-            for (int i = 0; i < N; ++i) fin = fin && isfinite(x[i]);
-            if (dstep >= 0 || !fin) {
-              if (dstep < 0) dstep = t;
-#pragma unroll
-              for (int i = 0; i < N; ++i) x[i] = xold[i];
-            }
-#pragma unroll
-            for (int i = 0; i < N; ++i) a.states[((size_t)kl * (T + 1) + t + 1) * N + i] = double(x[i]);
+          for (int i = 0; i < N; ++i) a.states[((size_t)kl * (T + 1) + t + 1) * N + i] = double(x[i]);
+        }
+      };
+      // Noise of group g+1 is drawn while group g steps (software pipeline:
+      // it is independent of the state, so it fills the dynamics chain's
+      // latency); full groups carry no per-step horizon checks.
+      float z[4 * MP];
+      P4 jw = P4{0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
+      if (PHILOX) {
+        group_normals<MP>(sk, 0u, kg, z);
+        if (a.jump_on) jw = draw(sk, kSlotJumpUniform, 0u, kg);
+      }
+      for (int t0 = 0; t0 < T; t0 += 4) {
+        float zm[4 * QP];
+        bool jf[4] = {jw.x < jthr, jw.y < jthr, jw.z < jthr, jw.w < jthr};
+        if (PHILOX && (jf[0] | jf[1] | jf[2] | jf[3]))  // zero-one law jump events (noise.py:151-155)
+          group_mark_normals<QP>(sk, (uint32_t)t0, kg, jf, zm);
+        if (t0 + 4 <= T) {
+          float zn[4 * MP];
+          P4 jwn = jw;
+          if (PHILOX) {
+            group_normals<MP>(sk, (uint32_t)(t0 + 4), kg, zn);
+            if (a.jump_on) jwn = draw(sk, kSlotJumpUniform, (uint32_t)((t0 + 4) >> 2), kg);
           }
+          step(t0 + 0, 0, z, zm, jf);
+          step(t0 + 1, 1, z, zm, jf);
+          step(t0 + 2, 2, z, zm, jf);
+          step(t0 + 3, 3, z, zm, jf);
+          if (PHILOX) {
+#pragma unroll
+            for (int i = 0; i < 4 * MP; ++i) z[i] = zn[i];
+            jw = jwn;
+          }
+        } else {
+#pragma unroll
+          for (int s = 0; s < 4; ++s)
+            if (t0 + s < T) step(t0 + s, s, z, zm, jf);
         }
       }
       // Once non-finite, an Euler state x += dx stays non-finite, so the
