@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <type_traits>
+#include <utility>
 
 #include "internal.h"
 
@@ -172,28 +173,37 @@ class Engine final : public EngineBase {
     return a;
   }
 
+  template <typename... KArgs, typename... Args>
+  static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  }
+
   template <int JM>
-  void launch(jm_ctx* c, const RolloutArgs<Real>& a, bool philox, bool trace) {
+  cudaError_t launch(jm_ctx* c, const RolloutArgs<Real>& a, bool philox, bool trace) {
     dim3 grid(c->grid), block(c->block);
-    if (philox && !trace)
-      rollout_kernel<Sys, Real, true, false, JM><<<grid, block, c->smem, c->stream>>>(a);
-    else if (philox)
-      rollout_kernel<Sys, Real, true, true, JM><<<grid, block, c->smem, c->stream>>>(a);
-    else if (!trace)
-      rollout_kernel<Sys, Real, false, false, JM><<<grid, block, c->smem, c->stream>>>(a);
-    else
-      rollout_kernel<Sys, Real, false, true, JM><<<grid, block, c->smem, c->stream>>>(a);
+    if (philox && !trace) return launch_pdl(rollout_kernel<Sys, Real, true, false, JM>, grid, block, c->smem, c->stream, a);
+    if (philox) return launch_pdl(rollout_kernel<Sys, Real, true, true, JM>, grid, block, c->smem, c->stream, a);
+    if (!trace) return launch_pdl(rollout_kernel<Sys, Real, false, false, JM>, grid, block, c->smem, c->stream, a);
+    return launch_pdl(rollout_kernel<Sys, Real, false, true, JM>, grid, block, c->smem, c->stream, a);
   }
 
   cudaError_t rollout(jm_ctx* c, const RolloutCall& rc) override {
     const RolloutArgs<Real> a = make_args(c, rc);
     const bool philox = c->mppi.noise_source == JM_NOISE_PHILOX;
     const bool trace = rc.states != nullptr;
-    if (c->model.jump_channel == JM_JUMP_STATE)
-      launch<1>(c, a, philox, trace);
-    else
-      launch<0>(c, a, philox, trace);
-    return cudaGetLastError();
+    if (c->model.jump_channel == JM_JUMP_STATE) return launch<1>(c, a, philox, trace);
+    return launch<0>(c, a, philox, trace);
   }
 
   cudaError_t noise(jm_ctx* c, NoiseArgs& na) override {
@@ -240,8 +250,8 @@ class Engine final : public EngineBase {
     f.counter = c->d_counter;
     const PlantArgs p = plant_args(c, loop, f.u_new, u_nom_next);
     const int fgrid = (c->TM + kFinCols - 1) / kFinCols;
-    finalize_kernel<Dyn><<<fgrid, kFinThreads, finalize_smem_bytes(f.nrec), c->stream>>>(f, p);
-    return cudaGetLastError();
+    return launch_pdl(finalize_kernel<Dyn>, dim3(fgrid), dim3(kFinThreads), finalize_smem_bytes(f.nrec), c->stream,
+                      f, p);
   }
 
   const char* kernel_name(bool trace) const override {

@@ -64,6 +64,13 @@ __device__ __forceinline__ uint64_t globaltimer() {
   return t;
 }
 
+// Programmatic dependent launch (sm_90+): a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may start while its
+// predecessor runs; grid_dep_wait() blocks until the predecessor grid has
+// completed and its writes are visible.
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll
@@ -203,6 +210,10 @@ __global__ void __launch_bounds__(kRolloutMaxThreads) rollout_kernel(const Rollo
   Real* tab = reinterpret_cast<Real*>(Nacc + TM);
   Real* sw = tab + T * TS;
 
+  grid_dep_wait();    // u_nom / x / iteration come from the previous control step
+  grid_dep_launch();  // (after the wait: the finalize's pre-wait prologue reads the
+                      // plant state the previous finalize wrote) let the finalize
+                      // grid get resident while the horizon runs
   LoopState* L = a.loop;
   if (L != nullptr && L->halted) return;
   const uint64_t iter = L ? L->iteration : (a.iteration_dev ? *a.iteration_dev : a.iteration);
@@ -497,15 +508,53 @@ struct PlantArgs {
   double* u_nom;
 };
 
+// The plant step, split so that everything that does not depend on u_new
+// (the LoopState fields, the plant noise draws) is done before the finalize
+// kernel waits for the rollout grid.
+struct PlantPre {
+  double x[12];
+  double ed[4];   // L_D z  (Sigma_D, harness.py:137)
+  double mk[4];   // mu + L_J z', drawn every step (harness.py:139)
+  int k;
+  int jump;       // U < nu dt (harness.py:138)
+};
+
+template <class Dyn>
+__device__ void plant_prepare(const PlantArgs& a, PlantPre& pre) {
+  constexpr int N = Dyn::N, M = Dyn::M;
+  const LoopState* L = a.loop;
+  const int k = L->step;
+  pre.k = k;
+  for (int i = 0; i < N; ++i) pre.x[i] = L->x[i];
+  const StreamKey sk = make_stream_key(L->seed, 0);
+  P4 r = draw(sk, kSlotPlant, 3u * k + 0u, 0u);
+  float z[4];
+  box_muller(r.x, r.y, z[0], z[1]);
+  box_muller(r.z, r.w, z[2], z[3]);
+  double ed[M];
+  apply_chol<M, double>(a.Lp, z, ed);
+  for (int j = 0; j < M; ++j) pre.ed[j] = ed[j];
+  const P4 ju = draw(sk, kSlotPlant, 3u * k + 1u, 0u);
+  pre.jump = ju.x < a.jthr ? 1 : 0;
+  r = draw(sk, kSlotPlant, 3u * k + 2u, 0u);
+  box_muller(r.x, r.y, z[0], z[1]);
+  box_muller(r.z, r.w, z[2], z[3]);
+  for (int i = 0; i < 4; ++i) {
+    double acc = 0.0;
+    for (int l = 0; l <= i && i < a.q; ++l) acc = fma(a.Lj[i * a.q + l], double(z[l]), acc);
+    pre.mk[i] = (i < a.q) ? a.mu_j[i] + acc : 0.0;
+  }
+}
+
 // One plant step from u_new[0] and the warm-start shift; run by one CTA after
 // u_new is complete.
 template <class Dyn>
-__device__ void plant_and_shift(const PlantArgs& a) {
+__device__ void plant_finish(const PlantArgs& a, const PlantPre& pre) {
   constexpr int N = Dyn::N, M = Dyn::M;
   LoopState* L = a.loop;
   __shared__ int s_ok;
   if (threadIdx.x == 0) {
-    const int k = L->step;
+    const int k = pre.k;
     L->t_end[k] = globaltimer();
     double u0[M];
     for (int j = 0; j < M; ++j) {
@@ -513,37 +562,19 @@ __device__ void plant_and_shift(const PlantArgs& a) {
       if (a.has_limits) v = fmin(fmax(v, a.u_lo[j]), a.u_hi[j]);  // harness.py:136
       u0[j] = v;
     }
-    const StreamKey sk = make_stream_key(L->seed, 0);
-    // eps_d = L_D N(0,I); has_jump = U < nu dt; eps_j = L_J N(0,I) drawn every step (:137-139)
-    P4 r = draw(sk, kSlotPlant, 3u * k + 0u, 0u);
-    float z[4];
-    box_muller(r.x, r.y, z[0], z[1]);
-    box_muller(r.z, r.w, z[2], z[3]);
-    double ed[M];
-    apply_chol<M, double>(a.Lp, z, ed);
-    const P4 ju = draw(sk, kSlotPlant, 3u * k + 1u, 0u);
-    const bool jump = ju.x < a.jthr;
-    r = draw(sk, kSlotPlant, 3u * k + 2u, 0u);
-    box_muller(r.x, r.y, z[0], z[1]);
-    box_muller(r.z, r.w, z[2], z[3]);
-    double mk[4];
-    for (int i = 0; i < 4; ++i) {
-      double acc = 0.0;
-      for (int l = 0; l <= i && i < a.q; ++l) acc = fma(a.Lj[i * a.q + l], double(z[l]), acc);
-      mk[i] = (i < a.q) ? a.mu_j[i] + acc : 0.0;
-    }
+    const bool jump = pre.jump != 0;
     double x[N];
-    for (int i = 0; i < N; ++i) x[i] = L->x[i];
+    for (int i = 0; i < N; ++i) x[i] = pre.x[i];
     const auto ax = Dyn::template aux<double>(x, a.sp);
     double v[M];
     for (int j = 0; j < M; ++j) {
-      const double e = (jump && a.jmode == 0) ? ed[j] + mk[j] : ed[j];
+      const double e = (jump && a.jmode == 0) ? pre.ed[j] + pre.mk[j] : pre.ed[j];
       v[j] = fma(e, a.sdt, u0[j] * a.dt);
     }
     Dyn::template advance<double>(x, ax, v, a.dt, a.sp);
     if (jump && a.jmode == 1) {
 #pragma unroll
-      for (int i = 0; i < Dyn::QJ; ++i) x[Dyn::jump_row(i)] += a.jscale * mk[i];
+      for (int i = 0; i < Dyn::QJ; ++i) x[Dyn::jump_row(i)] += a.jscale * pre.mk[i];
     }
     bool fin = true;
     for (int i = 0; i < N; ++i) fin = fin && isfinite(x[i]);
@@ -605,9 +636,14 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
   __shared__ double s_delta[kFinCols];
   __shared__ double s_bc[4];
   __shared__ int s_last;
+  __shared__ PlantPre s_pre;
   LoopState* L = a.loop;
-  if (L != nullptr && L->halted) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // closed loop: LoopState reads and the plant noise do not depend on the
+  // rollout, so they run before the grid dependency resolves
+  if (L != nullptr && tid == kFinThreads - 1) plant_prepare<Dyn>(p, s_pre);
+  grid_dep_wait();
+  if (L != nullptr && L->halted) return;
   const int rs = a.rec_stride;
   // global rho (controller.py:69: min over finite costs)
   double m = CUDART_INF;
@@ -745,14 +781,20 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
     if (a.diag) *a.diag = DiagOut{rho, Z * Z / W2, Z, (int64_t)NF};  // ESS = 1/sum w^2 (:167)
   }
   if (L != nullptr) {
-    // closed loop: the last CTA to finish runs the plant step + shift
+    grid_dep_launch();  // the next control step's rollout may become resident
+    if (gridDim.x == 1) {
+      __syncthreads();
+      plant_finish<Dyn>(p, s_pre);
+      return;
+    }
+    // several CTAs: the last one to finish runs the plant step + shift
     __threadfence();
     __syncthreads();
     if (tid == 0) s_last = (atomicAdd(a.counter, 1u) == gridDim.x - 1) ? 1 : 0;
     __syncthreads();
     if (s_last) {
       __threadfence();
-      plant_and_shift<Dyn>(p);
+      plant_finish<Dyn>(p, s_pre);
       if (tid == 0) *a.counter = 0u;
     }
   }
