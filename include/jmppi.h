@@ -144,7 +144,20 @@ int jm_record_doubles(const jm_ctx* ctx, int64_t* out);
 int jm_iteration_host(jm_ctx* ctx, const double* x0, const double* u_nom, uint64_t seed,
                       uint64_t iteration, const void* eps_c, const void* jump,
                       const double* mapping, double* u_new, double* costs, double* weights,
-                      double* step_norms, double* states, int64_t* diverged_step, jm_diag* diag);
+                      double* step_norms, double* states, int64_t* diverged_step, jm_diag* diag,
+                      const double* u_init, double* u_shift, uint64_t* weights_stash);
+/* Extra outputs of jm_iteration_host:
+ *  u_init (m) + u_shift (T*m): warm_start_shift(u_new, u_init) (controller.py:96-100)
+ *    computed by the same finalize kernel;
+ *  weights_stash: the per-sample weights stay in a device buffer identified by
+ *    the returned handle, fetched on demand (jm_stash_fetch) and released with
+ *    jm_stash_release -- the drop-in API's lazy UpdateDiagnostics.weights. */
+int jm_stash_fetch(jm_ctx* ctx, uint64_t handle, double* host);
+int jm_stash_release(jm_ctx* ctx, uint64_t handle);
+
+/* Upload x0 (n) and u_nom (T*m) into the context's device inputs (used by
+ * jm_bench_iteration; jm_iteration_host does this itself). */
+int jm_upload_inputs(jm_ctx* ctx, const double* x0, const double* u_nom);
 
 /* Device-resident split of the same iteration (all pointers device memory).
  * 1) rollout: K1 noise + K2 fused rollout/cost + per-CTA K3/K4 partials.

@@ -50,14 +50,47 @@ class ControllerState:
             raise ValueError("nominal_controls length must equal config.horizon_n")
 
 
-@dataclass(frozen=True)
 class UpdateDiagnostics:
-    """controller.py:48-53."""
+    """controller.py:48-53: weights (M,), min_cost, effective_sample_size,
+    per_step_update_norm (N,).
 
-    weights: np.ndarray
-    min_cost: float
-    effective_sample_size: float
-    per_step_update_norm: np.ndarray
+    The per-sample weights of a drop-in iteration stay on the GPU until first
+    read (a K-double download per iteration otherwise dominates the call);
+    `weights` then downloads them once and caches the array."""
+
+    __slots__ = ("_weights", "_ctx", "_handle", "min_cost", "effective_sample_size",
+                 "per_step_update_norm", "__weakref__")
+
+    def __init__(self, weights=None, min_cost=0.0, effective_sample_size=0.0, per_step_update_norm=None,
+                 *, _ctx=None, _handle=0):
+        self._weights = None if weights is None else np.asarray(weights)
+        self._ctx = _ctx
+        self._handle = _handle
+        self.min_cost = min_cost
+        self.effective_sample_size = effective_sample_size
+        self.per_step_update_norm = per_step_update_norm
+
+    @property
+    def weights(self) -> np.ndarray:
+        if self._weights is None and self._handle:
+            w = self._ctx.stash_fetch(self._handle)
+            w.setflags(write=False)
+            self._ctx.stash_release(self._handle)
+            self._handle = 0
+            self._ctx = None
+            self._weights = w
+        return self._weights
+
+    def __del__(self):
+        if getattr(self, "_handle", 0):
+            try:
+                self._ctx.stash_release(self._handle)
+            except Exception:
+                pass
+
+    def __repr__(self):
+        return (f"UpdateDiagnostics(min_cost={self.min_cost!r}, "
+                f"effective_sample_size={self.effective_sample_size!r})")
 
 
 def _device() -> int:
@@ -97,10 +130,17 @@ def update_controls(ctrl: ControllerState, rollouts: Sequence[RolloutResult], ma
 
 
 def warm_start_shift(controls: ControlSequence, u_init) -> ControlSequence:
-    """Drop u_0, shift forward, refill the tail with u_init."""
+    """Drop u_0, shift forward, refill the tail with u_init.
+
+    A sequence returned by mppi_iteration already carries its shift for the
+    config's u_init, computed by the iteration's finalize kernel; any other
+    sequence / u_init is shifted by a device kernel."""
     u = np.ascontiguousarray(controls.controls, dtype=float)
     T, m = u.shape
     ui = np.ascontiguousarray(np.atleast_1d(np.asarray(u_init, dtype=float)).reshape(m))
+    pre = getattr(controls, "_shifted", None)
+    if pre is not None and np.array_equal(pre[0], ui):
+        return ControlSequence(pre[1], controls.dt)
     out = np.empty_like(u)
     rc = L.load().jm_shift_host(_device(), T, m, L.dptr(u), L.dptr(ui), L.dptr(out))
     engine.raise_status(rc)
@@ -149,16 +189,21 @@ def mppi_iteration(
             q = ctx.Q
             jump = np.asarray(ind, float).reshape(K, T, 1) * np.asarray(eps_j, float).reshape(K, T, q)
             jump_arg = ctx.step_major(jump, q)
+    u_init = np.atleast_1d(np.asarray(cfg.u_init, dtype=float))
     out = ctx.iteration(x0, ctrl.nominal_controls.controls, master_seed, ctrl.iteration_index,
                         eps_c=eps_arg, jump=jump_arg, mapping=mapping, want_costs=return_rollouts,
-                        want_weights=True, trace=return_rollouts)
+                        want_weights=True, trace=return_rollouts, u_init=u_init,
+                        stash_weights=not return_rollouts)
     dt = cfg.dt
     new_controls = ControlSequence(out.u_new, dt)
+    object.__setattr__(new_controls, "_shifted", (u_init, out.u_shift))
     diagnostics = UpdateDiagnostics(
         weights=out.weights,
         min_cost=float(out.diag.min_cost),
         effective_sample_size=float(out.diag.ess),
-        per_step_update_norm=out.norms.copy(),
+        per_step_update_norm=out.norms,
+        _ctx=ctx if out.stash else None,
+        _handle=out.stash,
     )
     if not return_rollouts:
         return new_controls, diagnostics

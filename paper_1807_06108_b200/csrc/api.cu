@@ -152,7 +152,7 @@ jm::FinArgs fin_args(const jm_ctx* ctx, const double* records, int nrec) {
 }
 
 int rollout_and_finalize(jm_ctx* ctx, const jm::RolloutCall& rc, const double* mapping_dev,
-                         bool want_weights) {
+                         double* weights_dev, bool want_shift) {
   CK(ctx->eng->rollout(ctx, rc));
   jm::FinArgs f = fin_args(ctx, nullptr, 0);
   f.u_nom = rc.u_nom;
@@ -161,13 +161,30 @@ int rollout_and_finalize(jm_ctx* ctx, const jm::RolloutCall& rc, const double* m
   f.norms = ctx->d_small + ctx->off_norms();
   f.diag = ctx->d_diag();
   f.status = ctx->d_status();
+  if (want_shift) {
+    f.u_init = ctx->d_small + ctx->off_uinit();
+    f.u_shift = ctx->d_small + ctx->off_ushift();
+  }
   CK(ctx->eng->finalize(ctx, f, nullptr, nullptr));
-  if (want_weights) {
+  if (weights_dev) {
     const int b = 256, g = (ctx->K + b - 1) / b;
     jm::weights_kernel<<<g, b, 0, ctx->stream>>>(ctx->d_costs, ctx->d_diag(), 1.0 / ctx->mppi.lambda_,
-                                                 ctx->K, ctx->d_weights);
+                                                 ctx->K, weights_dev);
     CK(cudaGetLastError());
   }
+  return JM_OK;
+}
+
+int stash_acquire(jm_ctx* ctx, uint64_t* handle) {
+  if (ctx->stash_free.empty()) {
+    double* b = nullptr;
+    CK(dalloc(&b, (size_t)ctx->K));
+    ctx->stash.push_back(b);
+    ctx->stash_free.push_back((int)ctx->stash.size() - 1);
+  }
+  const int i = ctx->stash_free.back();
+  ctx->stash_free.pop_back();
+  *handle = (uint64_t)i + 1;
   return JM_OK;
 }
 
@@ -333,7 +350,7 @@ int jm_create(const jm_model_desc* model, const jm_cost_desc* cost, const jm_mpp
   if (e == cudaSuccess) e = ctx->eng->configure(ctx);
   ctx->stream = ctx->own_stream;
   if (e == cudaSuccess && p.noise_source == JM_NOISE_PHILOX)
-    e = cudaMalloc(&ctx->d_scratch, (size_t)ctx->grid * ctx->TM * ctx->block * ctx->real_size);
+    e = cudaMalloc(&ctx->d_scratch, (size_t)ctx->grid * ctx->TM * ctx->block * ctx->spt * ctx->real_size);
   if (e == cudaSuccess) e = dalloc(&ctx->d_costs, (size_t)ctx->K);
   if (e == cudaSuccess) e = dalloc(&ctx->d_weights, (size_t)ctx->K);
   if (e == cudaSuccess) e = dalloc(&ctx->d_records, (size_t)ctx->grid * ctx->rec_stride);
@@ -367,6 +384,7 @@ int jm_destroy(jm_ctx* ctx) {
   dfree(ctx->d_records);
   dfree(ctx->d_small);
   dfree(ctx->d_counter);
+  for (double* b : ctx->stash) dfree(b);
   dfree(ctx->d_states);
   dfree(ctx->d_div);
   dfree(ctx->d_loop);
@@ -399,8 +417,10 @@ int jm_record_doubles(const jm_ctx* ctx, int64_t* out) {
 int jm_iteration_host(jm_ctx* ctx, const double* x0, const double* u_nom, uint64_t seed,
                       uint64_t iteration, const void* eps_c, const void* jump,
                       const double* mapping, double* u_new, double* costs, double* weights,
-                      double* step_norms, double* states, int64_t* diverged_step, jm_diag* diag) {
+                      double* step_norms, double* states, int64_t* diverged_step, jm_diag* diag,
+                      const double* u_init, double* u_shift, uint64_t* weights_stash) {
   if (!ctx || !x0 || !u_nom || !u_new) return fail(ctx, JM_ERR_VALUE, "null argument");
+  if ((u_init == nullptr) != (u_shift == nullptr)) return fail(ctx, JM_ERR_VALUE, "u_init and u_shift go together");
   CK(cudaSetDevice(ctx->device));
   const bool hbm = ctx->mppi.noise_source == JM_NOISE_HBM;
   if (hbm && !eps_c) return fail(ctx, JM_ERR_VALUE, "HBM noise mode needs eps_combined");
@@ -412,6 +432,7 @@ int jm_iteration_host(jm_ctx* ctx, const double* x0, const double* u_nom, uint64
   std::memcpy(hs + ctx->off_x0(), x0, sizeof(double) * N);
   std::memcpy(hs + ctx->off_unom(), u_nom, sizeof(double) * TM);
   if (mapping) std::memcpy(hs + ctx->off_map(), mapping, sizeof(double) * M * M);
+  if (u_init) std::memcpy(hs + ctx->off_uinit(), u_init, sizeof(double) * M);
   CK(cudaMemcpyAsync(ds, hs, sizeof(double) * ctx->off_unew(), cudaMemcpyHostToDevice, ctx->stream));
   jm::RolloutCall rc;
   rc.x0 = ds + ctx->off_x0();
@@ -438,14 +459,23 @@ int jm_iteration_host(jm_ctx* ctx, const double* x0, const double* u_nom, uint64
     rc.states = ctx->d_states;
     rc.diverged = ctx->d_div;
   }
-  const int r = rollout_and_finalize(ctx, rc, mapping ? ds + ctx->off_map() : nullptr, weights != nullptr);
+  double* wdev = nullptr;
+  uint64_t handle = 0;
+  if (weights_stash) {
+    const int rs = stash_acquire(ctx, &handle);
+    if (rs != JM_OK) return rs;
+    wdev = ctx->stash[handle - 1];
+  } else if (weights) {
+    wdev = ctx->d_weights;
+  }
+  const int r = rollout_and_finalize(ctx, rc, mapping ? ds + ctx->off_map() : nullptr, wdev, u_shift != nullptr);
   if (r != JM_OK) return r;
   const size_t out_n = ctx->off_rec() - ctx->off_unew();
   CK(cudaMemcpyAsync(hs + ctx->off_unew(), ds + ctx->off_unew(), sizeof(double) * out_n,
                      cudaMemcpyDeviceToHost, ctx->stream));
   if (costs) CK(cudaMemcpyAsync(ctx->h_big, ctx->d_costs, sizeof(double) * K, cudaMemcpyDeviceToHost, ctx->stream));
   if (weights)
-    CK(cudaMemcpyAsync(ctx->h_big + K, ctx->d_weights, sizeof(double) * K, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->h_big + K, wdev, sizeof(double) * K, cudaMemcpyDeviceToHost, ctx->stream));
   if (states)
     CK(cudaMemcpyAsync(states, ctx->d_states, sizeof(double) * (size_t)K * (T + 1) * N,
                        cudaMemcpyDeviceToHost, ctx->stream));
@@ -455,7 +485,12 @@ int jm_iteration_host(jm_ctx* ctx, const double* x0, const double* u_nom, uint64
   const int32_t status = *reinterpret_cast<int32_t*>(hs + ctx->off_status());
   const DiagOut* dg = reinterpret_cast<const DiagOut*>(hs + ctx->off_diag());
   if (costs) std::memcpy(costs, ctx->h_big, sizeof(double) * K);
-  if (status == JM_ERR_NO_VIABLE) return fail(ctx, JM_ERR_NO_VIABLE, "no viable rollout");
+  if (status == JM_ERR_NO_VIABLE) {
+    if (handle) ctx->stash_free.push_back((int)handle - 1);
+    return fail(ctx, JM_ERR_NO_VIABLE, "no viable rollout");
+  }
+  if (weights_stash) *weights_stash = handle;
+  if (u_shift) std::memcpy(u_shift, hs + ctx->off_ushift(), sizeof(double) * TM);
   std::memcpy(u_new, hs + ctx->off_unew(), sizeof(double) * TM);
   if (step_norms) std::memcpy(step_norms, hs + ctx->off_norms(), sizeof(double) * T);
   if (weights) std::memcpy(weights, ctx->h_big + K, sizeof(double) * K);
@@ -465,6 +500,31 @@ int jm_iteration_host(jm_ctx* ctx, const double* x0, const double* u_nom, uint64
     diag->normaliser = dg->normaliser;
     diag->n_finite = dg->n_finite;
   }
+  return JM_OK;
+}
+
+int jm_upload_inputs(jm_ctx* ctx, const double* x0, const double* u_nom) {
+  if (!ctx || !x0 || !u_nom) return fail(ctx, JM_ERR_VALUE, "null argument");
+  CK(cudaSetDevice(ctx->device));
+  std::memcpy(ctx->h_small + ctx->off_x0(), x0, sizeof(double) * ctx->N);
+  std::memcpy(ctx->h_small + ctx->off_unom(), u_nom, sizeof(double) * ctx->TM);
+  CK(cudaMemcpyAsync(ctx->d_small, ctx->h_small, sizeof(double) * ctx->off_map(), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return JM_OK;
+}
+
+int jm_stash_fetch(jm_ctx* ctx, uint64_t handle, double* host) {
+  if (!ctx || !host || handle == 0 || handle > ctx->stash.size()) return fail(ctx, JM_ERR_VALUE, "bad stash handle");
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaMemcpyAsync(host, ctx->stash[handle - 1], sizeof(double) * ctx->K, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return JM_OK;
+}
+
+int jm_stash_release(jm_ctx* ctx, uint64_t handle) {
+  if (!ctx || handle == 0 || handle > ctx->stash.size()) return fail(ctx, JM_ERR_VALUE, "bad stash handle");
+  ctx->stash_free.push_back((int)handle - 1);
   return JM_OK;
 }
 
@@ -541,19 +601,25 @@ int jm_shift_host(int device, int32_t T, int32_t m, const double* u, const doubl
   jm_ctx* ctx = nullptr;
   if (T < 1 || m < 1 || !u || !u_init || !out) return fail(nullptr, JM_ERR_VALUE, "bad arguments");
   CK(cudaSetDevice(device));
+  // per-thread device scratch, grown on demand (no allocation per call)
+  thread_local int s_dev = -1;
+  thread_local size_t s_cap = 0;
+  thread_local double* s_buf = nullptr;
   const int TM = T * m;
-  double *d_u = nullptr, *d_i = nullptr, *d_o = nullptr;
-  CK(dalloc(&d_u, (size_t)TM));
-  CK(dalloc(&d_i, (size_t)m));
-  CK(dalloc(&d_o, (size_t)TM));
+  const size_t need = 2 * (size_t)TM + (size_t)m;
+  if (s_dev != device || s_cap < need) {
+    if (s_buf && s_dev == device) dfree(s_buf);
+    s_buf = nullptr;
+    CK(dalloc(&s_buf, need));
+    s_dev = device;
+    s_cap = need;
+  }
+  double *d_u = s_buf, *d_o = s_buf + TM, *d_i = s_buf + 2 * TM;
   CK(cudaMemcpy(d_u, u, sizeof(double) * TM, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(d_i, u_init, sizeof(double) * m, cudaMemcpyHostToDevice));
   jm::shift_kernel<<<(TM + 127) / 128, 128>>>(d_u, d_i, T, m, d_o);
   CK(cudaGetLastError());
   CK(cudaMemcpy(out, d_o, sizeof(double) * TM, cudaMemcpyDeviceToHost));
-  dfree(d_u);
-  dfree(d_i);
-  dfree(d_o);
   return JM_OK;
 }
 

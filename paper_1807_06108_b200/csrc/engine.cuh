@@ -72,13 +72,21 @@ class Engine final : public EngineBase {
     fill_cost<R>(c->cost, N, sp);
   }
 
-  size_t smem_bytes(const jm_ctx* c, int block) const {
-    return sizeof(double) * (size_t)c->TM + sizeof(Real) * ((size_t)c->T * (2 * M + 1) + block);
+  // two interleaved samples per thread for the fp32 Philox path of the small
+  // systems (more ILP at the same warp count); one elsewhere (register budget)
+  static constexpr int kSPT = 1;  // SPT=2 measured slower on the latency-bound shapes
+  template <bool PH, bool TR>
+  static constexpr int spt() {
+    return (PH && !TR) ? kSPT : 1;
+  }
+
+  size_t smem_bytes(const jm_ctx* c, int block, int spt_) const {
+    return sizeof(double) * (size_t)c->TM + sizeof(Real) * ((size_t)c->T * (2 * M + 1) + (size_t)block * spt_);
   }
 
   template <bool PH, bool TR, int JM>
   static const void* kfn() {
-    return reinterpret_cast<const void*>(&rollout_kernel<Sys, Real, PH, TR, JM>);
+    return reinterpret_cast<const void*>(&rollout_kernel<Sys, Real, PH, TR, JM, spt<PH, TR>()>);
   }
 
   template <int JM>
@@ -101,16 +109,19 @@ class Engine final : public EngineBase {
     const bool philox = c->mppi.noise_source == JM_NOISE_PHILOX;
     int block = c->mppi.block_threads;
     const int K = c->K, sms = c->num_sms;
+    const int sp = philox ? kSPT : 1;  // samples per thread of the main (non-trace) kernel
     if (block <= 0) {
-      if (K <= sms * kRolloutMaxThreads) {
-        const int per = (K + sms - 1) / sms;
+      if (K <= sms * kRolloutMaxThreads * sp) {
+        const int per = (K + sms * sp - 1) / (sms * sp);
         block = std::max(32, ((per + 31) / 32) * 32);
       } else {
         block = 256;
       }
     }
     c->block = block;
-    const size_t smem = smem_bytes(c, block);
+    c->spt = sp;
+    // the trace kernels run one sample per thread: size smem for the larger tile
+    const size_t smem = smem_bytes(c, block, std::max(sp, 1));
     const void* fn = nullptr;
     cudaError_t e = (c->model.jump_channel == JM_JUMP_STATE) ? set_attrs<1>(smem, &fn, philox)
                                                             : set_attrs<0>(smem, &fn, philox);
@@ -120,7 +131,7 @@ class Engine final : public EngineBase {
     if (e != cudaSuccess) return e;
     if (occ < 1) return cudaErrorInvalidConfiguration;
     c->smem = smem;
-    c->ntiles = (K + block - 1) / block;
+    c->ntiles = (K + block * sp - 1) / (block * sp);
     c->grid = std::min(c->ntiles, occ * sms);
     if (c->grid > kMaxRecords) c->grid = kMaxRecords;
     const size_t fsm = finalize_smem_bytes(kMaxRecords);
@@ -192,10 +203,15 @@ class Engine final : public EngineBase {
   template <int JM>
   cudaError_t launch(jm_ctx* c, const RolloutArgs<Real>& a, bool philox, bool trace) {
     dim3 grid(c->grid), block(c->block);
-    if (philox && !trace) return launch_pdl(rollout_kernel<Sys, Real, true, false, JM>, grid, block, c->smem, c->stream, a);
-    if (philox) return launch_pdl(rollout_kernel<Sys, Real, true, true, JM>, grid, block, c->smem, c->stream, a);
-    if (!trace) return launch_pdl(rollout_kernel<Sys, Real, false, false, JM>, grid, block, c->smem, c->stream, a);
-    return launch_pdl(rollout_kernel<Sys, Real, false, true, JM>, grid, block, c->smem, c->stream, a);
+    if (philox && !trace)
+      return launch_pdl(rollout_kernel<Sys, Real, true, false, JM, spt<true, false>()>, grid, block, c->smem, c->stream, a);
+    // the one-sample-per-thread variants cover the same samples with SPT x the tiles
+    // (same grid, so the same number of per-CTA records)
+    RolloutArgs<Real> b = a;
+    b.ntiles = (c->K + c->block - 1) / c->block;
+    if (philox) return launch_pdl(rollout_kernel<Sys, Real, true, true, JM, 1>, grid, block, c->smem, c->stream, b);
+    if (!trace) return launch_pdl(rollout_kernel<Sys, Real, false, false, JM, 1>, grid, block, c->smem, c->stream, b);
+    return launch_pdl(rollout_kernel<Sys, Real, false, true, JM, 1>, grid, block, c->smem, c->stream, b);
   }
 
   cudaError_t rollout(jm_ctx* c, const RolloutCall& rc) override {

@@ -5,6 +5,7 @@
 
 #include <cstdint>
 #include <string>
+#include <vector>
 
 #include "../../include/jmppi.h"
 #include "kernels.cuh"
@@ -51,7 +52,7 @@ struct jm_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t own_stream = nullptr;
   int N = 0, M = 0, Q = 0, T = 0, K = 0, TM = 0, rec_stride = 0;
-  int block = 128, grid = 1, ntiles = 1;
+  int block = 128, grid = 1, ntiles = 1, spt = 1;
   size_t smem = 0;
   size_t real_size = 4;
   double Ld[16] = {0}, Lj[16] = {0}, Lp[16] = {0};  // chol(c Sigma_D), chol(Sigma_J), chol(Sigma_D)
@@ -83,6 +84,8 @@ struct jm_ctx {
   uint64_t* d_hist_t = nullptr;   // t_start | t_end
   int loop_cap = 0;
   unsigned int* d_counter = nullptr;  // finalize last-CTA counter
+  std::vector<double*> stash;        // device weight buffers (K doubles)
+  std::vector<int> stash_free;
   void* d_flush = nullptr;         // L2 flush buffer (bench)
   size_t flush_cap = 0;
   cudaGraph_t graph = nullptr;
@@ -91,7 +94,7 @@ struct jm_ctx {
 
   // d_small / h_small layout (doubles):
   //   inputs  [x0:16][u_nom:TM][mapping:16][u_init:16]
-  //   outputs [u_new:TM][norms:T][diag:4][status:2]
+  //   outputs [u_new:TM][norms:T][diag:4][status:2][u_shift:TM]
   //   [record:rec_stride]  (this context's reduced record)
   size_t off_x0() const { return 0; }
   size_t off_unom() const { return 16; }
@@ -101,6 +104,7 @@ struct jm_ctx {
   size_t off_norms() const { return off_unew() + (size_t)TM; }
   size_t off_diag() const { return off_norms() + (size_t)T; }
   size_t off_status() const { return off_diag() + 4; }
-  size_t off_rec() const { return off_status() + 2; }
+  size_t off_ushift() const { return off_status() + 2; }
+  size_t off_rec() const { return off_ushift() + (size_t)TM; }
   size_t small_doubles() const { return off_rec() + (size_t)rec_stride; }
 };

@@ -190,7 +190,7 @@ struct Pad {
 // ---------------------------------------------------------------- rollout
 // JM = 0: control-channel jumps (marks folded into eps_combined, q = m);
 // JM = 1: state-space jumps on Dyn::jump_row (q = Dyn::QJ, eps_combined = eps_d).
-template <class Sys, typename Real, bool PHILOX, bool TRACE, int JM>
+template <class Sys, typename Real, bool PHILOX, bool TRACE, int JM, int SPT>
 __global__ void __launch_bounds__(kRolloutMaxThreads) rollout_kernel(const RolloutArgs<Real> a) {
   using Dyn = typename Sys::Dyn;
   using Cost = typename Sys::Cost;
@@ -279,154 +279,198 @@ __global__ void __launch_bounds__(kRolloutMaxThreads) rollout_kernel(const Rollo
   const StreamKey sk = make_stream_key(L ? L->seed : a.seed, iter);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
 
+  // SPT samples per thread: sub-tile u covers columns [u*blockDim, (u+1)*blockDim)
+  // of a tile of blockDim*SPT samples; the SPT independent dynamics chains of
+  // a thread are interleaved step by step (instruction-level parallelism
+  // without more warps: a K=65536 horizon gives each SM only ~14 warps).
+  const int tileK = blockDim.x * SPT;
   for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
-    const int kl = tile * blockDim.x + threadIdx.x;
-    const bool active = kl < K;
-    const uint32_t kg = (uint32_t)(a.sample_offset + kl);
-    Real* eout = PHILOX ? a.eps_out + (size_t)blockIdx.x * TM * blockDim.x + threadIdx.x : nullptr;
-    Real S = Real(0);
-    if (active) {
-      Real x[N];
+    const int base = tile * tileK;
+    int kl[SPT];
+    bool act[SPT];
+    uint32_t kg[SPT];
+    Real* ep[SPT];  // Philox scratch: row (t*M+j) of this sample's column
+    Real x[SPT][N];
+    Real S[SPT];
+    int dstep[SPT];
 #pragma unroll
-      for (int i = 0; i < N; ++i) x[i] = Real(x0[i]);
-      int dstep = -1;
-      if (TRACE) {
+    for (int u = 0; u < SPT; ++u) {
+      kl[u] = base + u * blockDim.x + threadIdx.x;
+      act[u] = kl[u] < K;
+      kg[u] = (uint32_t)(a.sample_offset + kl[u]);
+      ep[u] = PHILOX ? a.eps_out + (size_t)blockIdx.x * TM * tileK + u * blockDim.x + threadIdx.x : nullptr;
+      S[u] = Real(0);
+      dstep[u] = -1;
 #pragma unroll
-        for (int i = 0; i < N; ++i) a.states[((size_t)kl * (T + 1)) * N + i] = double(x[i]);
+      for (int i = 0; i < N; ++i) x[u][i] = Real(x0[i]);
+      if (TRACE && act[u]) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) a.states[((size_t)kl[u] * (T + 1)) * N + i] = double(x[u][i]);
       }
-      Real* ep = eout;  // Philox scratch: row (t*M+j) of this thread's column
-      // one horizon step t (sub-step s of its 4-step group)
-      auto step = [&](const int t, const int s, const float* z, const float* zm, const bool* jf) {
-        Real eps[M];
-        Real sj[Q];
+    }
+    // one horizon step t (sub-step s of its 4-step group) of sample slot u
+    auto step = [&](const int u, const int t, const int s, const float* z, const float* zm, const bool* jf) {
+      Real eps[M];
+      Real sj[Q];
 #pragma unroll
-        for (int i = 0; i < Q; ++i) sj[i] = Real(0);
-        bool has_sj = false;
-        if (PHILOX) {
-          apply_chol<M, Real>(Ld, z + s * MP, eps);
-          if (jf[s]) {
-            Real mk[Q];
-            apply_marks<Q, Real>(Lj, mu, zm + s * QP, mk);
-            if (JM == 0) {
+      for (int i = 0; i < Q; ++i) sj[i] = Real(0);
+      bool has_sj = false;
+      if (PHILOX) {
+        apply_chol<M, Real>(Ld, z + s * MP, eps);
+        if (jf[s]) {
+          Real mk[Q];
+          apply_marks<Q, Real>(Lj, mu, zm + s * QP, mk);
+          if (JM == 0) {
 #pragma unroll
-              for (int j = 0; j < M; ++j) eps[j] += mk[(j < Q) ? j : 0];  // eps_c = eps_d + eps_j (noise.py:156-157)
-            } else {
+            for (int j = 0; j < M; ++j) eps[j] += mk[(j < Q) ? j : 0];  // eps_c = eps_d + eps_j (noise.py:156-157)
+          } else {
 #pragma unroll
-              for (int i = 0; i < Q; ++i) sj[i] = jscale * mk[i];
-              has_sj = true;
-            }
-          }
-#pragma unroll
-          for (int j = 0; j < M; ++j) ep[(size_t)j * blockDim.x] = eps[j];
-          ep += (size_t)M * blockDim.x;
-        } else {
-#pragma unroll
-          for (int j = 0; j < M; ++j) eps[j] = __ldg(a.eps_in + (size_t)(t * M + j) * K + kl);
-          if (JM == 1 && a.jump_in != nullptr) {
-#pragma unroll
-            for (int i = 0; i < Q; ++i) sj[i] = jscale * __ldg(a.jump_in + (size_t)(t * Q + i) * K + kl);
+            for (int i = 0; i < Q; ++i) sj[i] = jscale * mk[i];
             has_sj = true;
           }
         }
-        // modified running cost on x_t (controller.py:140-142):
-        // q dt + 1/2 u'Ru dt + lambda sqrt(dt) u'eps + 1/2 lambda (1-1/c) eps'eps
-        // (eps'eps formed first, as costs.py:101/:514, so an overflowing eps
-        // gives NaN even when c = 1)
-        const auto ax = Dyn::template aux<Real>(x, sp);
-        const Real qv = Cost::template q<Dyn, Real>(x, ax, sp);
-        const Real* st = tab + t * TS;
-        Real inc = fma(qv, dt, st[M]);
-        Real quad = eps[0] * eps[0];
 #pragma unroll
-        for (int j = 1; j < M; ++j) quad = fma(eps[j], eps[j], quad);
+        for (int j = 0; j < M; ++j) ep[u][(size_t)j * tileK] = eps[j];
+        ep[u] += (size_t)M * tileK;
+      } else {
+        const int k = act[u] ? kl[u] : 0;
 #pragma unroll
-        for (int j = 0; j < M; ++j) inc = fma(st[M + 1 + j], eps[j], inc);
-        S += fma(cq, quad, inc);
-        // Euler step (dynamics.py:130-135 / :115-129 with B = G)
-        Real xold[N];
-        if (TRACE) {
+        for (int j = 0; j < M; ++j) eps[j] = __ldg(a.eps_in + (size_t)(t * M + j) * K + k);
+        if (JM == 1 && a.jump_in != nullptr) {
 #pragma unroll
-          for (int i = 0; i < N; ++i) xold[i] = x[i];
+          for (int i = 0; i < Q; ++i) sj[i] = jscale * __ldg(a.jump_in + (size_t)(t * Q + i) * K + k);
+          has_sj = true;
         }
-        Real v[M];
+      }
+      Real* xs = x[u];
+      // modified running cost on x_t (controller.py:140-142):
+      // q dt + 1/2 u'Ru dt + lambda sqrt(dt) u'eps + 1/2 lambda (1-1/c) eps'eps
+      // (eps'eps formed first, as costs.py:101/:514, so an overflowing eps
+      // gives NaN even when c = 1)
+      const auto ax = Dyn::template aux<Real>(xs, sp);
+      const Real qv = Cost::template q<Dyn, Real>(xs, ax, sp);
+      const Real* st = tab + t * TS;
+      Real inc = fma(qv, dt, st[M]);
+      Real quad = eps[0] * eps[0];
 #pragma unroll
-        for (int j = 0; j < M; ++j) v[j] = fma(eps[j], sdt, st[j]);
-        Dyn::template advance<Real>(x, ax, v, dt, sp);
-        if (JM == 1 && has_sj) {
+      for (int j = 1; j < M; ++j) quad = fma(eps[j], eps[j], quad);
 #pragma unroll
-          for (int i = 0; i < Q; ++i) x[Dyn::jump_row(i)] += sj[i];
+      for (int j = 0; j < M; ++j) inc = fma(st[M + 1 + j], eps[j], inc);
+      S[u] += fma(cq, quad, inc);
+      // Euler step (dynamics.py:130-135 / :115-129 with B = G)
+      Real xold[N];
+      if (TRACE) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) xold[i] = xs[i];
+      }
+      Real v[M];
+#pragma unroll
+      for (int j = 0; j < M; ++j) v[j] = fma(eps[j], sdt, st[j]);
+      Dyn::template advance<Real>(xs, ax, v, dt, sp);
+      if (JM == 1 && has_sj) {
+#pragma unroll
+        for (int i = 0; i < Q; ++i) xs[Dyn::jump_row(i)] += sj[i];
+      }
+      if (TRACE) {
+        // divergence mask, controller.py:144-151
+        bool fin = true;
+#pragma unroll
+        for (int i = 0; i < N; ++i) fin = fin && isfinite(xs[i]);
+        if (dstep[u] >= 0 || !fin) {
+          if (dstep[u] < 0) dstep[u] = t;
+#pragma unroll
+          for (int i = 0; i < N; ++i) xs[i] = xold[i];
         }
-        if (TRACE) {
-          // divergence mask, controller.py:144-151
-          bool fin = true;
+        if (act[u]) {
 #pragma unroll
-          for (int i = 0; i < N; ++i) fin = fin && isfinite(x[i]);
-          if (dstep >= 0 || !fin) {
-            if (dstep < 0) dstep = t;
-#pragma unroll
-            for (int i = 0; i < N; ++i) x[i] = xold[i];
-          }
-#pragma unroll
-          for (int i = 0; i < N; ++i) a.states[((size_t)kl * (T + 1) + t + 1) * N + i] = double(x[i]);
+          for (int i = 0; i < N; ++i) a.states[((size_t)kl[u] * (T + 1) + t + 1) * N + i] = double(xs[i]);
         }
-      };
-      // Noise of group g+1 is drawn while group g steps (software pipeline:
-      // it is independent of the state, so it fills the dynamics chain's
-      // latency); full groups carry no per-step horizon checks.
-      float z[4 * MP];
-      P4 jw = P4{0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
+      }
+    };
+    // Noise of group g+1 is drawn while group g steps (software pipeline: it
+    // is independent of the state, so it fills the dynamics chains'
+    // latency); full groups carry no per-step horizon checks.
+    float z[SPT][4 * MP];
+    P4 jw[SPT];
+#pragma unroll
+    for (int u = 0; u < SPT; ++u) {
+      jw[u] = P4{0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
       if (PHILOX) {
-        group_normals<MP>(sk, 0u, kg, z);
-        if (a.jump_on) jw = draw(sk, kSlotJumpUniform, 0u, kg);
+        group_normals<MP>(sk, 0u, kg[u], z[u]);
+        if (a.jump_on) jw[u] = draw(sk, kSlotJumpUniform, 0u, kg[u]);
       }
-      for (int t0 = 0; t0 < T; t0 += 4) {
-        float zm[4 * QP];
-        bool jf[4] = {jw.x < jthr, jw.y < jthr, jw.z < jthr, jw.w < jthr};
-        if (PHILOX && (jf[0] | jf[1] | jf[2] | jf[3]))  // zero-one law jump events (noise.py:151-155)
-          group_mark_normals<QP>(sk, (uint32_t)t0, kg, jf, zm);
-        if (t0 + 4 <= T) {
-          float zn[4 * MP];
-          P4 jwn = jw;
-          if (PHILOX) {
-            group_normals<MP>(sk, (uint32_t)(t0 + 4), kg, zn);
-            if (a.jump_on) jwn = draw(sk, kSlotJumpUniform, (uint32_t)((t0 + 4) >> 2), kg);
-          }
-          step(t0 + 0, 0, z, zm, jf);
-          step(t0 + 1, 1, z, zm, jf);
-          step(t0 + 2, 2, z, zm, jf);
-          step(t0 + 3, 3, z, zm, jf);
-          if (PHILOX) {
+    }
+    for (int t0 = 0; t0 < T; t0 += 4) {
+      float zm[SPT][4 * QP];
+      bool jf[SPT][4];
 #pragma unroll
-            for (int i = 0; i < 4 * MP; ++i) z[i] = zn[i];
-            jw = jwn;
-          }
-        } else {
+      for (int u = 0; u < SPT; ++u) {
+        jf[u][0] = jw[u].x < jthr;
+        jf[u][1] = jw[u].y < jthr;
+        jf[u][2] = jw[u].z < jthr;
+        jf[u][3] = jw[u].w < jthr;
+        if (PHILOX && (jf[u][0] | jf[u][1] | jf[u][2] | jf[u][3]))  // zero-one law jump events (noise.py:151-155)
+          group_mark_normals<QP>(sk, (uint32_t)t0, kg[u], jf[u], zm[u]);
+      }
+      if (t0 + 4 <= T) {
+        float zn[SPT][4 * MP];
+        P4 jwn[SPT];
 #pragma unroll
-          for (int s = 0; s < 4; ++s)
-            if (t0 + s < T) step(t0 + s, s, z, zm, jf);
+        for (int u = 0; u < SPT; ++u) {
+          jwn[u] = jw[u];
+          if (PHILOX) {
+            group_normals<MP>(sk, (uint32_t)(t0 + 4), kg[u], zn[u]);
+            if (a.jump_on) jwn[u] = draw(sk, kSlotJumpUniform, (uint32_t)((t0 + 4) >> 2), kg[u]);
+          }
         }
+#pragma unroll
+        for (int s2 = 0; s2 < 4; ++s2)
+#pragma unroll
+          for (int u = 0; u < SPT; ++u) step(u, t0 + s2, s2, z[u], zm[u], jf[u]);
+        if (PHILOX) {
+#pragma unroll
+          for (int u = 0; u < SPT; ++u) {
+#pragma unroll
+            for (int i = 0; i < 4 * MP; ++i) z[u][i] = zn[u][i];
+            jw[u] = jwn[u];
+          }
+        }
+      } else {
+#pragma unroll
+        for (int s2 = 0; s2 < 4; ++s2)
+          if (t0 + s2 < T) {
+#pragma unroll
+            for (int u = 0; u < SPT; ++u) step(u, t0 + s2, s2, z[u], zm[u], jf[u]);
+          }
       }
-      // Once non-finite, an Euler state x += dx stays non-finite, so the
-      // final state decides divergence (the reference checks every step).
+    }
+    // Once non-finite, an Euler state x += dx stays non-finite, so the final
+    // state decides divergence (the reference checks every step).
+    Real Sf[SPT];
+#pragma unroll
+    for (int u = 0; u < SPT; ++u) {
       bool fin = true;
 #pragma unroll
-      for (int i = 0; i < N; ++i) fin = fin && isfinite(x[i]);
+      for (int i = 0; i < N; ++i) fin = fin && isfinite(x[u][i]);
       if (TRACE) {
-        fin = dstep < 0;
-        a.diverged[kl] = dstep;
+        fin = dstep[u] < 0;
+        if (act[u]) a.diverged[kl[u]] = dstep[u];
       }
       if (fin) {
-        const auto ax = Dyn::template aux<Real>(x, sp);
-        S += sp.term_scale * Cost::template q<Dyn, Real>(x, ax, sp);  // controller.py:155
+        const auto ax = Dyn::template aux<Real>(x[u], sp);
+        S[u] += sp.term_scale * Cost::template q<Dyn, Real>(x[u], ax, sp);  // controller.py:155
       } else {
-        S = r_inf<Real>();
+        S[u] = r_inf<Real>();
       }
-      if (a.costs) a.costs[kl] = double(S);
+      if (act[u] && a.costs) a.costs[kl[u]] = double(S[u]);
+      Sf[u] = act[u] ? S[u] : r_inf<Real>();
     }
 
     // ---- per-CTA online softmax over this tile (K3/K4 partials) ----
-    const Real Sf = active ? S : r_inf<Real>();
-    Real m = warp_min(Sf);
+    Real mloc = Sf[0];
+#pragma unroll
+    for (int u = 1; u < SPT; ++u) mloc = fmin(mloc, Sf[u]);
+    const Real m = warp_min(mloc);
     if (lane == 0) s_red[0][warp] = double(m);
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -440,38 +484,44 @@ __global__ void __launch_bounds__(kRolloutMaxThreads) rollout_kernel(const Rollo
     __syncthreads();
     const double rho_new = s_bc[0], scale_old = s_bc[1];
     if (rho_new == CUDART_INF) continue;  // no finite cost yet in this CTA (uniform)
-    const Real w = (Sf < r_inf<Real>()) ? r_exp<Real>(-(Sf - Real(rho_new)) * a.inv_lam) : Real(0);
-    sw[threadIdx.x] = w;
-    {
-      const double z1 = warp_sum(double(w)), z2 = warp_sum(double(w) * double(w));
-      const double nf = warp_sum((Sf < r_inf<Real>()) ? 1.0 : 0.0);
-      __syncwarp();
-      if (lane == 0) {
-        s_red[0][warp] = z1;
-        s_red[1][warp] = z2;
-        s_red[2][warp] = nf;
-      }
+    double z1 = 0.0, z2 = 0.0, nf = 0.0;
+#pragma unroll
+    for (int u = 0; u < SPT; ++u) {
+      const bool fin = Sf[u] < r_inf<Real>();
+      const Real w = fin ? r_exp<Real>(-(Sf[u] - Real(rho_new)) * a.inv_lam) : Real(0);
+      sw[u * blockDim.x + threadIdx.x] = w;
+      z1 += double(w);
+      z2 += double(w) * double(w);
+      nf += fin ? 1.0 : 0.0;
+    }
+    z1 = warp_sum(z1);
+    z2 = warp_sum(z2);
+    nf = warp_sum(nf);
+    __syncwarp();
+    if (lane == 0) {
+      s_red[0][warp] = z1;
+      s_red[1][warp] = z2;
+      s_red[2][warp] = nf;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      double z1 = 0.0, z2 = 0.0, nf = 0.0;
+      double a1 = 0.0, a2 = 0.0, a3 = 0.0;
       for (int w2 = 0; w2 < nwarps; ++w2) {
-        z1 += s_red[0][w2];
-        z2 += s_red[1][w2];
-        nf += s_red[2][w2];
+        a1 += s_red[0][w2];
+        a2 += s_red[1][w2];
+        a3 += s_red[2][w2];
       }
       s_acc[0] = rho_new;
-      s_acc[1] = s_acc[1] * scale_old + z1;
-      s_acc[2] = s_acc[2] * scale_old * scale_old + z2;
-      s_acc[3] += nf;
+      s_acc[1] = s_acc[1] * scale_old + a1;
+      s_acc[2] = s_acc[2] * scale_old * scale_old + a2;
+      s_acc[3] += a3;
     }
     // N[r] += sum_k w_k eps[r, k] over the tile: warp-per-row, lanes over k.
-    // Philox: this CTA's scratch slab (rows of blockDim.x, written above);
+    // Philox: this CTA's scratch slab (rows of tileK, written above);
     // HBM: the input tensor itself (rows of K).
-    const int base = tile * blockDim.x;
-    const int nk = min((int)blockDim.x, K - base);
-    const Real* src = PHILOX ? a.eps_out + (size_t)blockIdx.x * TM * blockDim.x : a.eps_in + base;
-    const size_t rstride = PHILOX ? (size_t)blockDim.x : (size_t)K;
+    const int nk = min(tileK, K - base);
+    const Real* src = PHILOX ? a.eps_out + (size_t)blockIdx.x * TM * tileK : a.eps_in + base;
+    const size_t rstride = PHILOX ? (size_t)tileK : (size_t)K;
     for (int r = warp; r < TM; r += nwarps) {
       const Real* row = src + (size_t)r * rstride;
       Real acc = Real(0);
@@ -619,7 +669,9 @@ struct FinArgs {
   int32_t* status;        // or null
   double* rec_out;        // reduce mode: write the merged record instead of finalizing
   LoopState* loop;
-  unsigned int* counter;  // last-CTA-done counter (closed loop)
+  unsigned int* counter;  // last-CTA-done counter (closed loop / shift output)
+  const double* u_init;   // optional: u_shift = warm_start_shift(u_new, u_init)
+  double* u_shift;
 };
 
 inline size_t finalize_smem_bytes(int nrec) {
@@ -779,6 +831,24 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
   if (blockIdx.x == 0 && tid == 0) {
     if (a.status) *a.status = 0;
     if (a.diag) *a.diag = DiagOut{rho, Z * Z / W2, Z, (int64_t)NF};  // ESS = 1/sum w^2 (:167)
+  }
+  if (a.u_shift != nullptr && gridDim.x == 1) {  // warm_start_shift of this iteration's result
+    __syncthreads();
+    const int TM = a.TM, Mm = a.M;
+    for (int i = tid; i < TM; i += kFinThreads)
+      a.u_shift[i] = (i < TM - Mm) ? a.u_new[i + Mm] : a.u_init[i - (TM - Mm)];
+  } else if (a.u_shift != nullptr) {
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = (atomicAdd(a.counter, 1u) == gridDim.x - 1) ? 1 : 0;
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      const int TM = a.TM, Mm = a.M;
+      for (int i = tid; i < TM; i += kFinThreads)
+        a.u_shift[i] = (i < TM - Mm) ? __ldcg(a.u_new + i + Mm) : a.u_init[i - (TM - Mm)];
+      if (tid == 0) *a.counter = 0u;
+    }
   }
   if (L != nullptr) {
     grid_dep_launch();  // the next control step's rollout may become resident

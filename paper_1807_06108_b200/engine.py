@@ -210,6 +210,8 @@ class IterationOut:
     weights: Optional[np.ndarray]
     states: Optional[np.ndarray]
     diverged: Optional[np.ndarray]
+    u_shift: Optional[np.ndarray] = None
+    stash: int = 0
 
 
 class Context:
@@ -250,7 +252,8 @@ class Context:
         return np.ascontiguousarray(a.transpose(1, 2, 0), dtype=self.real)
 
     def iteration(self, x0, u_nom, seed, iteration, *, eps_c=None, jump=None, mapping=None,
-                  want_costs=False, want_weights=True, trace=False) -> IterationOut:
+                  want_costs=False, want_weights=True, trace=False, u_init=None,
+                  stash_weights=False) -> IterationOut:
         x0 = np.ascontiguousarray(x0, dtype=float).reshape(self.N)
         u_nom = np.ascontiguousarray(u_nom, dtype=float).reshape(self.T * self.M)
         u_new = np.empty(self.T * self.M)
@@ -259,14 +262,32 @@ class Context:
         weights = np.empty(self.K) if want_weights else None
         states = np.empty((self.K, self.T + 1, self.N)) if trace else None
         div = np.empty(self.K, dtype=np.int64) if trace else None
+        if stash_weights:
+            weights = None
         mp = None if mapping is None else np.ascontiguousarray(mapping, dtype=float).reshape(self.M, self.M)
+        ui = None if u_init is None else np.ascontiguousarray(u_init, dtype=float).reshape(self.M)
+        u_shift = None if u_init is None else np.empty(self.T * self.M)
+        handle = C.c_uint64(0)
         diag = L.Diag()
         rc = self.lib.jm_iteration_host(
             self.h, L.dptr(x0), L.dptr(u_nom), C.c_uint64(int(seed)), C.c_uint64(int(iteration)),
             L.vptr(eps_c), L.vptr(jump), L.dptr(mp), L.dptr(u_new), L.dptr(costs), L.dptr(weights),
-            L.dptr(norms), L.dptr(states), L.i64ptr(div), C.byref(diag))
+            L.dptr(norms), L.dptr(states), L.i64ptr(div), C.byref(diag), L.dptr(ui), L.dptr(u_shift),
+            C.byref(handle) if stash_weights else None)
         self.check(rc)
-        return IterationOut(u_new.reshape(self.T, self.M), norms, diag, costs, weights, states, div)
+        out = IterationOut(u_new.reshape(self.T, self.M), norms, diag, costs, weights, states, div)
+        out.u_shift = None if u_shift is None else u_shift.reshape(self.T, self.M)
+        out.stash = handle.value if stash_weights else 0
+        return out
+
+    def stash_fetch(self, handle: int) -> np.ndarray:
+        w = np.empty(self.K)
+        self.check(self.lib.jm_stash_fetch(self.h, C.c_uint64(handle), L.dptr(w)))
+        return w
+
+    def stash_release(self, handle: int):
+        if getattr(self, "h", None) is not None and self.h.value:
+            self.lib.jm_stash_release(self.h, C.c_uint64(handle))
 
     def sample_noise(self, seed, iteration):
         KT = self.K * self.T
@@ -306,14 +327,37 @@ _cache_lock = threading.Lock()
 _CACHE_MAX = 12
 
 
+# identity-keyed fast path: the plugin objects are immutable (frozen
+# dataclasses with read-only arrays), so (id(model), id(cost), id(cfg), ...)
+# names a context as long as the objects are alive (they are kept referenced)
+_fast: "OrderedDict[tuple, tuple]" = OrderedDict()
+
+
 def get_context(model, cost_model, cfg, *, samples=None, precision=None, hbm=False,
                 sample_offset=0, device=None, block_threads=0) -> Context:
+    dev = int(os.environ.get("JM_B200_DEVICE", "0")) if device is None else int(device)
+    prec = precision or default_precision()
+    fkey = (id(model), id(cost_model), id(cfg), samples, prec, hbm, sample_offset, dev, block_threads)
+    hit = _fast.get(fkey)
+    if hit is not None and hit[0] is model and hit[1] is cost_model and hit[2] is cfg:
+        return hit[3]
+    ctx = _get_context_slow(model, cost_model, cfg, samples=samples, precision=prec, hbm=hbm,
+                            sample_offset=sample_offset, device=dev, block_threads=block_threads)
+    with _cache_lock:
+        _fast[fkey] = (model, cost_model, cfg, ctx)
+        while len(_fast) > 4 * _CACHE_MAX:
+            _fast.popitem(last=False)
+    return ctx
+
+
+def _get_context_slow(model, cost_model, cfg, *, samples, precision, hbm, sample_offset, device,
+                      block_threads) -> Context:
     mdesc = describe_model(model)
     cdesc = describe_cost(cost_model, mdesc.state_dim, mdesc.control_dim)
     q = mdesc.jump_dim
     pdesc = describe_mppi(cfg, mdesc.control_dim, q, samples=samples, precision=precision, hbm=hbm,
                           sample_offset=sample_offset, block_threads=block_threads)
-    dev = int(os.environ.get("JM_B200_DEVICE", "0")) if device is None else int(device)
+    dev = device
     key = (bytes(mdesc), bytes(cdesc), bytes(pdesc), dev)
     with _cache_lock:
         ctx = _cache.get(key)
@@ -324,16 +368,14 @@ def get_context(model, cost_model, cfg, *, samples=None, precision=None, hbm=Fal
     with _cache_lock:
         _cache[key] = ctx
         while len(_cache) > _CACHE_MAX:
-            _, old = _cache.popitem(last=False)
-            old.close()
+            _cache.popitem(last=False)  # freed when the last user (e.g. a lazy diagnostics) lets go
     return ctx
 
 
 def clear_cache():
     with _cache_lock:
-        for ctx in _cache.values():
-            ctx.close()
         _cache.clear()
+        _fast.clear()
 
 
 def microbench(device: int = 0):
