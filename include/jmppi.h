@@ -130,6 +130,8 @@ int jm_device_count(int* out);
 int jm_create(const jm_model_desc* model, const jm_cost_desc* cost, const jm_mppi_desc* mppi,
               int device, jm_ctx** out);
 int jm_destroy(jm_ctx* ctx);
+/* stream: a cudaStream_t; NULL = the context's own non-blocking stream (the
+ * legacy default stream 0 cannot be selected: pass an explicit stream). */
 int jm_set_stream(jm_ctx* ctx, void* stream);
 /* size in doubles of one weighting record: 4 + T*m (rho, Z, sum w^2, n_finite, N[T*m]) */
 int jm_record_doubles(const jm_ctx* ctx, int64_t* out);
@@ -225,6 +227,17 @@ int jm_loop_init(jm_ctx* ctx, const double* x0, const double* u_init, uint64_t s
 int jm_loop_step(jm_ctx* ctx);
 int jm_loop_read(jm_ctx* ctx, double* x_out, uint64_t* iteration_out, int32_t* step_out,
                  int32_t* halted_out, int32_t* status_out);
+/* Raw loop histories of the first `steps` control steps: states ((steps+1)*n),
+ * controls (steps*m), jumps (steps); synchronises the context's stream. */
+int jm_loop_history(jm_ctx* ctx, int32_t steps, double* states, double* controls, int64_t* jumps);
+
+/* Closed-loop control step split around a cross-GPU exchange (one process per
+ * GPU, samples sharded by mppi.sample_offset): stage 1 = rollout of the local
+ * shard + reduction into one weighting record; stage 2 = merge nrec gathered
+ * records (rank order), update, plant step, shift.  Both enqueue on the
+ * context's stream (jm_set_stream: share it with the collective). */
+int jm_loop_rollout(jm_ctx* ctx, double* record_dev);
+int jm_loop_finish(jm_ctx* ctx, const double* records_dev, int32_t nrec);
 
 /* ---- measurement helpers ---- */
 /* Time `steps` closed-loop control steps (jm_loop_init first) with CUDA events

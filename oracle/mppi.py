@@ -379,3 +379,35 @@ def warm_start_shift(u, u_init):
     """jm/controller.py:96-100."""
     u = np.asarray(u, float)
     return np.vstack([u[1:], np.atleast_1d(np.asarray(u_init, float))[None, :]])
+
+
+# ---------------------------------------------------------------- shard records (multi-GPU merge)
+def partial_record(costs, eps_c, lam):
+    """One shard's weighting record [rho, Z, sum w^2, n_finite, N[T*m]] relative
+    to the shard's own minimum (the format libjmppi exchanges between ranks)."""
+    costs = np.asarray(costs, float)
+    fin = np.isfinite(costs)
+    K, T, m = eps_c.shape
+    rec = np.zeros(4 + T * m)
+    if not fin.any():
+        rec[0] = np.inf
+        return rec
+    rho = costs[fin].min()
+    w = np.where(fin, np.exp(-(np.where(fin, costs, rho) - rho) / lam), 0.0)
+    rec[0], rec[1], rec[2], rec[3] = rho, w.sum(), (w * w).sum(), fin.sum()
+    rec[4:] = np.einsum("k,ktj->tj", w, eps_c).reshape(-1)
+    return rec
+
+
+def combine_records(records, lam, dt, u_nom):
+    """Log-sum-exp merge of shard records in order; returns (u_new, rho, ess)."""
+    records = np.asarray(records, float)
+    rho = records[:, 0].min()
+    if not np.isfinite(rho):
+        raise OracleNoViable("no viable rollout")
+    e = np.where(np.isfinite(records[:, 0]), np.exp(-(records[:, 0] - rho) / lam), 0.0)
+    Z = (records[:, 1] * e).sum()
+    W2 = (records[:, 2] * e * e).sum()
+    N = (records[:, 4:] * e[:, None]).sum(axis=0)
+    u_nom = np.asarray(u_nom, float)
+    return u_nom + (N / (Z * np.sqrt(dt))).reshape(u_nom.shape), rho, Z * Z / W2

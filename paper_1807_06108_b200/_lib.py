@@ -99,6 +99,9 @@ SIGNATURES = {
     "jm_closed_loop_host": (C.c_int, [_vp, _pd, _pd, _u64, _i32, _pd, _pd, _pi64, _pd, _pi32, _pi32]),
     "jm_loop_init": (C.c_int, [_vp, _pd, _pd, _u64, _u64, _i32]),
     "jm_loop_step": (C.c_int, [_vp]),
+    "jm_loop_history": (C.c_int, [_vp, _i32, _pd, _pd, _pi64]),
+    "jm_loop_rollout": (C.c_int, [_vp, _vp]),
+    "jm_loop_finish": (C.c_int, [_vp, _vp, _i32]),
     "jm_loop_read": (C.c_int, [_vp, _pd, _pu64, _pi32, _pi32, _pi32]),
     "jm_microbench": (C.c_int, [C.c_int, _pd, _pd, _pd]),
     "jm_bench_loop": (C.c_int, [_vp, _i32, _i64, _i32, _pd, _pd]),

@@ -784,6 +784,31 @@ int jm_loop_init(jm_ctx* ctx, const double* x0, const double* u_init, uint64_t s
   return capture_loop_graph(ctx);
 }
 
+int jm_loop_rollout(jm_ctx* ctx, double* record_dev) {
+  if (!ctx || !ctx->d_loop || !record_dev) return fail(ctx, JM_ERR_VALUE, "loop not initialised");
+  CK(cudaSetDevice(ctx->device));
+  jm::RolloutCall rc;
+  rc.u_nom = ctx->d_loop_unom;
+  rc.costs = ctx->d_costs;
+  rc.loop = ctx->d_loop;
+  CK(ctx->eng->rollout(ctx, rc));
+  jm::FinArgs f = fin_args(ctx, nullptr, 0);
+  f.rec_out = record_dev;
+  CK(ctx->eng->finalize(ctx, f, nullptr, nullptr));
+  return JM_OK;
+}
+
+int jm_loop_finish(jm_ctx* ctx, const double* records_dev, int32_t nrec) {
+  if (!ctx || !ctx->d_loop || !records_dev || nrec < 1 || nrec > jm::kMaxRecords)
+    return fail(ctx, JM_ERR_VALUE, "bad arguments");
+  CK(cudaSetDevice(ctx->device));
+  jm::FinArgs f = fin_args(ctx, records_dev, nrec);
+  f.u_nom = ctx->d_loop_unom;
+  f.u_new = ctx->d_loop_unew;
+  CK(ctx->eng->finalize(ctx, f, ctx->d_loop, ctx->d_loop_unom));
+  return JM_OK;
+}
+
 int jm_loop_step(jm_ctx* ctx) {
   if (!ctx || !ctx->graph_exec) return fail(ctx, JM_ERR_VALUE, "loop not initialised");
   CK(cudaGraphLaunch(ctx->graph_exec, ctx->own_stream));
@@ -802,6 +827,20 @@ int jm_loop_read(jm_ctx* ctx, double* x_out, uint64_t* iteration_out, int32_t* s
   if (step_out) *step_out = h.step;
   if (halted_out) *halted_out = h.halted;
   if (status_out) *status_out = h.status;
+  return JM_OK;
+}
+
+int jm_loop_history(jm_ctx* ctx, int32_t steps, double* states, double* controls, int64_t* jumps) {
+  if (!ctx || !ctx->d_loop || steps < 0 || steps > ctx->loop_cap) return fail(ctx, JM_ERR_VALUE, "bad arguments");
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaStreamSynchronize(ctx->own_stream));
+  const int N = ctx->N, M = ctx->M;
+  if (states) CK(cudaMemcpy(states, ctx->d_hist, sizeof(double) * (size_t)(steps + 1) * N, cudaMemcpyDeviceToHost));
+  if (controls)
+    CK(cudaMemcpy(controls, ctx->d_hist + (size_t)(ctx->loop_cap + 1) * N, sizeof(double) * (size_t)steps * M,
+                  cudaMemcpyDeviceToHost));
+  if (jumps) CK(cudaMemcpy(jumps, ctx->d_hist_jumps, sizeof(int64_t) * (size_t)steps, cudaMemcpyDeviceToHost));
   return JM_OK;
 }
 

@@ -1,0 +1,190 @@
+"""Multi-GPU sharding of the sampled-trajectory core: one process per GPU.
+
+Samples shard naturally: rank r rolls out its own K_local
+samples with GLOBAL sample indices in the Philox counter
+(sample_offset = r * K_local), so the noise of a sharded run is exactly the
+noise of one big run.  Per MPC iteration the only exchange is one all_gather
+of each rank's weighting record (rho_r, Z_r, sum w^2_r, n_finite_r,
+N_r[T*m]; 4 + T*m doubles, 3.2 KB at config 3) over NCCL; every rank then
+merges the records in rank order with the same log-sum-exp rescale
+exp(-(rho_r - rho)/lambda) (the finalize kernel) and applies the identical
+update, plant step and shift -- one collective instead of a MIN all-reduce
+followed by a SUM all-reduce.
+
+torch.distributed is the plumbing (process group, NCCL over NVLink/NVSwitch,
+streams); all arithmetic is in libjmppi.so.  The host-side logic here
+(shard ranges, record exchange, rank-order merge) is covered on CPU by
+tests/test_distributed.py with world_size 2 over gloo.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from typing import Tuple
+
+import numpy as np
+
+from . import _lib as L
+from . import engine
+
+
+def shard(k_per_rank: int, rank: int) -> Tuple[int, int]:
+    """(sample_offset, count) of a rank under weak scaling (K_local fixed per GPU)."""
+    return rank * k_per_rank, k_per_rank
+
+
+def shard_strong(k_total: int, rank: int, world: int) -> Tuple[int, int]:
+    """(sample_offset, count) when a fixed global K is split over `world` ranks."""
+    base, rem = divmod(k_total, world)
+    count = base + (1 if rank < rem else 0)
+    offset = rank * base + min(rank, rem)
+    return offset, count
+
+
+def exchange_records(local, group=None):
+    """All-gather one record per rank into a (world, rec) tensor, rank order.
+
+    Uses all_gather_into_tensor where the backend has it (NCCL) and the list
+    form otherwise (gloo on CPU)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    out = torch.empty((world,) + tuple(local.shape), dtype=local.dtype, device=local.device)
+    if local.is_cuda:
+        dist.all_gather_into_tensor(out, local.contiguous(), group=group)
+    else:
+        parts = [torch.empty_like(local) for _ in range(world)]
+        dist.all_gather(parts, local.contiguous(), group=group)
+        out = torch.stack(parts)
+    return out
+
+
+@dataclass
+class ShardedLoop:
+    """Closed-loop MPC with the sample set sharded over the ranks of a process group.
+
+    Every rank holds an identical plant state (same seed, same merged update),
+    so the trajectory equals a single-GPU run over rank-count x K_local samples
+    up to the reduction order of the merge."""
+
+    ctx: object
+    world: int
+    rank: int
+    group: object = None
+
+    @classmethod
+    def create(cls, task, cfg, rank: int, world: int, device: int, precision=None, group=None):
+        off, _ = shard(cfg.samples_m, rank)
+        ctx = engine.get_context(task.model, task.cost_model, cfg, precision=precision, sample_offset=off,
+                                 device=device)
+        return cls(ctx, world, rank, group)
+
+    def init(self, x0, u_init, seed: int, max_steps: int):
+        import torch
+
+        lib, h = self.ctx.lib, self.ctx.h
+        x0 = np.ascontiguousarray(x0, float)
+        ui = np.ascontiguousarray(u_init, float)
+        self.ctx.check(lib.jm_loop_init(h, L.dptr(x0), L.dptr(ui), C.c_uint64(seed), C.c_uint64(0), max_steps))
+        rs = C.c_int64()
+        self.ctx.check(lib.jm_record_doubles(h, C.byref(rs)))
+        dev = torch.device("cuda", self.ctx.device)
+        # one explicit (non-legacy) stream carries the kernels AND the collective:
+        # torch's default stream is the legacy stream 0, which jm_set_stream
+        # would read as "the context's own non-blocking stream"
+        self.stream = torch.cuda.Stream(device=dev)
+        with torch.cuda.stream(self.stream):
+            self.record = torch.zeros(rs.value, dtype=torch.float64, device=dev)
+        self.ctx.check(lib.jm_set_stream(h, C.c_void_p(self.stream.cuda_stream)))
+        torch.cuda.synchronize(dev)
+
+    def step(self):
+        """One control step: local rollout + record, all_gather, merge/update/plant/shift."""
+        import torch
+
+        lib, h = self.ctx.lib, self.ctx.h
+        with torch.cuda.stream(self.stream):
+            self.ctx.check(lib.jm_loop_rollout(h, C.c_void_p(self.record.data_ptr())))
+            gathered = exchange_records(self.record, self.group)
+            self.ctx.check(lib.jm_loop_finish(h, C.c_void_p(gathered.data_ptr()), self.world))
+        self._keep = gathered  # alive until the stream consumed it
+
+    def history(self, steps: int):
+        """(states (steps+1, n), controls (steps, m), jumps (steps,)) of the loop so far."""
+        import torch
+
+        torch.cuda.synchronize(self.ctx.device)
+        st = np.empty((steps + 1, self.ctx.N))
+        co = np.empty((steps, self.ctx.M))
+        ju = np.empty(steps, dtype=np.int64)
+        self.ctx.check(self.ctx.lib.jm_loop_history(self.ctx.h, steps, L.dptr(st), L.dptr(co), L.i64ptr(ju)))
+        return st, co, ju
+
+    def read(self):
+        import torch
+
+        torch.cuda.synchronize(self.ctx.device)  # the steps ran on torch's stream
+        lib, h = self.ctx.lib, self.ctx.h
+        x = np.zeros(self.ctx.N)
+        it, st, hal, status = C.c_uint64(), C.c_int32(), C.c_int32(), C.c_int32()
+        self.ctx.check(lib.jm_loop_read(h, L.dptr(x), C.byref(it), C.byref(st), C.byref(hal), C.byref(status)))
+        return x, it.value, st.value, hal.value, status.value
+
+
+def bench_sharded(a, world: int, rank: int, local: int):
+    """bench.py entry for N > 1 (torchrun): weak scaling, K samples per GPU."""
+    import json
+    import time
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1807_06108_b200 as jb
+
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    idx = {"cfg0": 0, "cfg1": 1, "cfg2": 2, "cfg3": 3}[a.workload]
+    task, cfg = jb.baseline_config(idx, K=a.samples, T=a.horizon)
+    K, T = cfg.samples_m, cfg.horizon_n
+    loop = ShardedLoop.create(task, cfg, rank, world, local, precision=a.precision)
+    n_total = a.warmup + a.steps
+    loop.init(task.x0, cfg.u_init, 0, 2 * n_total + 64)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for _ in range(a.warmup):
+        loop.step()
+    torch.cuda.synchronize()
+    times = []
+    for i in range(a.steps):
+        with torch.cuda.stream(loop.stream):
+            flush.fill_(i & 0xFF)  # evict L2 between timed steps
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(loop.stream)  # events on the stream the kernels run on
+        loop.step()
+        e1.record(loop.stream)
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+    t = torch.tensor([float(np.mean(times))], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)  # max over ranks
+    ms = float(t.item())
+    x, it, st, halted, status = loop.read()
+    if halted:
+        raise RuntimeError(f"sharded loop halted (status {status})")
+    if rank == 0:
+        value = world * K * T / (ms * 1e-3)
+        line = {"metric": "rollout state-steps/sec (K*T/s)", "value": value, "unit": "state-steps/s",
+                "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": a.precision,
+                "data": "synthetic",
+                "config": {"workload": f"{a.workload}: BASELINE config {idx} closed-loop control step, "
+                                       f"K={K} per GPU (global {world * K}), T={T}, one NCCL all_gather "
+                                       "of the weighting records per step",
+                           "K_per_gpu": K, "T": T, "parallelism": f"dp{world}",
+                           "l2": "flushed (256 MiB fill) before each timed step"},
+                "mpc_iteration_latency_ms": ms, "gpu_launches": 3 * a.steps}
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()

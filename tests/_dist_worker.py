@@ -1,0 +1,45 @@
+"""One rank of tests/test_distributed.py (gloo, CPU).  Prints a JSON line."""
+import json
+import os
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from oracle import mppi as om  # noqa: E402
+from oracle import philox_stream as ps  # noqa: E402
+from paper_1807_06108_b200 import distributed as jd  # noqa: E402
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from conftest import load_golden, oracle_spec
+
+    g = load_golden(os.environ["JM_CASE"])
+    spec = oracle_spec(g["spec"])
+    k_local = int(os.environ["JM_K_LOCAL"])
+    off, cnt = jd.shard(k_local, rank)
+    Ld = np.linalg.cholesky(spec.c * spec.sigma_d)
+    Lj = np.linalg.cholesky(spec.sigma_j)
+    jthr = ps.jump_threshold(spec.nu * spec.dt) if spec.jump_enabled else 0
+    noise = ps.device_noise(7, 3, cnt, spec.T, spec.m, spec.q, Ld, Lj, spec.mark_mean, jthr,
+                            jump_channel=spec.jump_channel, sample_offset=off)
+    spec.K = cnt
+    out = om.mppi_iteration_oracle(spec, g["x0"], g["u_nom"], noise)
+    rec = torch.from_numpy(om.partial_record(out["costs"], noise[3], spec.lam))
+    gathered = jd.exchange_records(rec).numpy()
+    u_new, rho, ess = om.combine_records(gathered, spec.lam, spec.dt, g["u_nom"])
+    print(json.dumps({"rank": rank, "u_new": u_new.tolist(), "rho": rho, "ess": ess,
+                      "gathered_rho": gathered[:, 0].tolist()}))
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

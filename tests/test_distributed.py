@@ -1,0 +1,86 @@
+"""Multi-GPU host logic on CPU (gloo, world_size 2): shard ranges, the record
+exchange in rank order and the log-sum-exp merge reproduce the unsharded
+iteration.  The per-shard arithmetic here is the oracle's; on
+GPUs the same exchange_records() feeds libjmppi's finalize kernel."""
+
+from __future__ import annotations
+
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, load_golden, oracle_spec
+from oracle import mppi as om
+from oracle import philox_stream as ps
+from paper_1807_06108_b200 import distributed as jd
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_shard_ranges_partition():
+    for k, w in [(65536, 8), (1000, 3), (7, 4)]:
+        spans = [jd.shard_strong(k, r, w) for r in range(w)]
+        assert spans[0][0] == 0 and sum(c for _, c in spans) == k
+        for (o0, c0), (o1, _) in zip(spans, spans[1:]):
+            assert o0 + c0 == o1
+    assert jd.shard(4096, 3) == (3 * 4096, 4096)
+
+
+def test_record_merge_matches_unsharded_oracle():
+    g = load_golden("b_cartpole")
+    spec = oracle_spec(g["spec"])
+    Ld = np.linalg.cholesky(spec.c * spec.sigma_d)
+    Lj = np.linalg.cholesky(spec.sigma_j)
+    jthr = ps.jump_threshold(spec.nu * spec.dt)
+    full = ps.device_noise(1, 0, 96, spec.T, 1, 1, Ld, Lj, spec.mark_mean, jthr, jump_channel="state")
+    spec.K = 96
+    ref = om.mppi_iteration_oracle(spec, g["x0"], g["u_nom"], full)
+    recs = []
+    for off, cnt in [(0, 40), (40, 56)]:
+        part = tuple(a[off:off + cnt] for a in full)
+        spec.K = cnt
+        o = om.mppi_iteration_oracle(spec, g["x0"], g["u_nom"], part)
+        recs.append(om.partial_record(o["costs"], part[3], spec.lam))
+    u_new, rho, ess = om.combine_records(recs, spec.lam, spec.dt, g["u_nom"])
+    assert rho == ref["min_cost"]
+    assert np.allclose(u_new, ref["u_new"], rtol=1e-12, atol=1e-12)
+    assert ess == pytest.approx(ref["ess"], rel=1e-12)
+
+
+@pytest.mark.parametrize("case", ["b_cartpole", "r_quadrotor_task"])
+def test_gloo_world2_exchange(case):
+    port = _free_port()
+    k_local = 48
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), WORLD_SIZE="2",
+               JM_CASE=case, JM_K_LOCAL=str(k_local), CUDA_VISIBLE_DEVICES="")
+    procs = [subprocess.Popen([sys.executable, str(ROOT / "tests" / "_dist_worker.py")],
+                              env=dict(env, RANK=str(r), LOCAL_RANK=str(r)), stdout=subprocess.PIPE,
+                              stderr=subprocess.PIPE, text=True) for r in range(2)]
+    outs = []
+    for p in procs:
+        o, e = p.communicate(timeout=300)
+        assert p.returncode == 0, e[-3000:]
+        outs.append(json.loads(o.strip().splitlines()[-1]))
+    # every rank merged the same records into the same update
+    assert outs[0]["u_new"] == outs[1]["u_new"]
+    # ... equal to one unsharded iteration over the 2*k_local global samples
+    g = load_golden(case)
+    spec = oracle_spec(g["spec"])
+    Ld = np.linalg.cholesky(spec.c * spec.sigma_d)
+    Lj = np.linalg.cholesky(spec.sigma_j)
+    jthr = ps.jump_threshold(spec.nu * spec.dt) if spec.jump_enabled else 0
+    full = ps.device_noise(7, 3, 2 * k_local, spec.T, spec.m, spec.q, Ld, Lj, spec.mark_mean, jthr,
+                           jump_channel=spec.jump_channel)
+    spec.K = 2 * k_local
+    ref = om.mppi_iteration_oracle(spec, g["x0"], g["u_nom"], full)
+    assert np.allclose(np.array(outs[0]["u_new"]), ref["u_new"], rtol=1e-11, atol=1e-11)
+    assert outs[0]["rho"] == pytest.approx(ref["min_cost"], rel=1e-13)

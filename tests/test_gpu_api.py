@@ -274,3 +274,34 @@ def test_closed_loop_f32_runs_and_stays_finite(gpu_device):
     rec = jb.run_trial(task, cfg, seed=3)
     assert np.isfinite(rec.states).all()
     assert rec.wall_time_per_iteration.shape == (30,)
+
+
+def test_sharded_loop_world1_matches_graph_loop(gpu_device):
+    """The multi-GPU stage split (rollout+record, all_gather, merge/plant) over a
+    one-rank NCCL group reproduces the single-GPU graph loop."""
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1807_06108_b200 import distributed as jd
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        task, cfg = jb.baseline_config(0, K=2048, T=60, steps=12)
+        rec = jb.run_trial(task, cfg, seed=5, precision="f64")
+        loop = jd.ShardedLoop.create(task, cfg, 0, 1, 0, precision="f64")
+        loop.init(task.x0, cfg.u_init, 5, 64)
+        for _ in range(12):
+            loop.step()
+        x, it, st, halted, status = loop.read()
+        assert st == 12 and it == 12 and not halted
+        assert np.allclose(x, rec.states[-1], rtol=1e-9, atol=1e-12)
+    finally:
+        dist.destroy_process_group()
