@@ -333,12 +333,12 @@ __global__ void __launch_bounds__(kRolloutMaxThreads) rollout_kernel(const Rollo
         for (int j = 0; j < M; ++j) ep[u][(size_t)j * tileK] = eps[j];
         ep[u] += (size_t)M * tileK;
       } else {
-        const int k = act[u] ? kl[u] : 0;
+        // HBM wire format, prefetched one group ahead into z / zm (see below)
 #pragma unroll
-        for (int j = 0; j < M; ++j) eps[j] = __ldg(a.eps_in + (size_t)(t * M + j) * K + k);
+        for (int j = 0; j < M; ++j) eps[j] = Real(reinterpret_cast<const Real*>(z)[s * M + j]);
         if (JM == 1 && a.jump_in != nullptr) {
 #pragma unroll
-          for (int i = 0; i < Q; ++i) sj[i] = jscale * __ldg(a.jump_in + (size_t)(t * Q + i) * K + k);
+          for (int i = 0; i < Q; ++i) sj[i] = jscale * reinterpret_cast<const Real*>(zm)[s * Q + i];
           has_sj = true;
         }
       }
@@ -390,7 +390,27 @@ __global__ void __launch_bounds__(kRolloutMaxThreads) rollout_kernel(const Rollo
     // Noise of group g+1 is drawn while group g steps (software pipeline: it
     // is independent of the state, so it fills the dynamics chains'
     // latency); full groups carry no per-step horizon checks.
-    float z[SPT][4 * MP];
+    // HBM mode reuses the same group buffers as raw storage for the loaded
+    // noise: z holds 4 steps x M Reals of eps, zm 4 x Q Reals of jumps
+    constexpr int ZW = PHILOX ? 4 * MP : (4 * M * (int)sizeof(Real) + 3) / 4;
+    constexpr int ZMW = PHILOX ? 4 * QP : (4 * Q * (int)sizeof(Real) + 3) / 4;
+    auto load_group = [&](const int u, const int g0, float* zz, float* zzm) {
+      Real* ze = reinterpret_cast<Real*>(zz);
+      Real* zj = reinterpret_cast<Real*>(zzm);
+      const int k = act[u] ? kl[u] : 0;
+#pragma unroll
+      for (int s2 = 0; s2 < 4; ++s2) {
+        const int t = min(g0 + s2, T - 1);
+#pragma unroll
+        for (int j = 0; j < M; ++j) ze[s2 * M + j] = __ldg(a.eps_in + (size_t)(t * M + j) * K + k);
+        if (JM == 1 && a.jump_in != nullptr) {
+#pragma unroll
+          for (int i = 0; i < Q; ++i) zj[s2 * Q + i] = __ldg(a.jump_in + (size_t)(t * Q + i) * K + k);
+        }
+      }
+    };
+    float z[SPT][ZW];
+    float zmh[SPT][ZMW];  // HBM mode: jump rows of the current group
     P4 jw[SPT];
 #pragma unroll
     for (int u = 0; u < SPT; ++u) {
@@ -398,10 +418,12 @@ __global__ void __launch_bounds__(kRolloutMaxThreads) rollout_kernel(const Rollo
       if (PHILOX) {
         group_normals<MP>(sk, 0u, kg[u], z[u]);
         if (a.jump_on) jw[u] = draw(sk, kSlotJumpUniform, 0u, kg[u]);
+      } else {
+        load_group(u, 0, z[u], zmh[u]);
       }
     }
     for (int t0 = 0; t0 < T; t0 += 4) {
-      float zm[SPT][4 * QP];
+      float zm[SPT][ZMW];
       bool jf[SPT][4];
 #pragma unroll
       for (int u = 0; u < SPT; ++u) {
@@ -409,11 +431,16 @@ __global__ void __launch_bounds__(kRolloutMaxThreads) rollout_kernel(const Rollo
         jf[u][1] = jw[u].y < jthr;
         jf[u][2] = jw[u].z < jthr;
         jf[u][3] = jw[u].w < jthr;
-        if (PHILOX && (jf[u][0] | jf[u][1] | jf[u][2] | jf[u][3]))  // zero-one law jump events (noise.py:151-155)
-          group_mark_normals<QP>(sk, (uint32_t)t0, kg[u], jf[u], zm[u]);
+        if (PHILOX) {
+          if (jf[u][0] | jf[u][1] | jf[u][2] | jf[u][3])  // zero-one law jump events (noise.py:151-155)
+            group_mark_normals<QP>(sk, (uint32_t)t0, kg[u], jf[u], zm[u]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < ZMW; ++i) zm[u][i] = zmh[u][i];
+        }
       }
       if (t0 + 4 <= T) {
-        float zn[SPT][4 * MP];
+        float zn[SPT][ZW];
         P4 jwn[SPT];
 #pragma unroll
         for (int u = 0; u < SPT; ++u) {
@@ -421,19 +448,19 @@ __global__ void __launch_bounds__(kRolloutMaxThreads) rollout_kernel(const Rollo
           if (PHILOX) {
             group_normals<MP>(sk, (uint32_t)(t0 + 4), kg[u], zn[u]);
             if (a.jump_on) jwn[u] = draw(sk, kSlotJumpUniform, (uint32_t)((t0 + 4) >> 2), kg[u]);
+          } else {
+            load_group(u, t0 + 4, zn[u], zmh[u]);
           }
         }
 #pragma unroll
         for (int s2 = 0; s2 < 4; ++s2)
 #pragma unroll
           for (int u = 0; u < SPT; ++u) step(u, t0 + s2, s2, z[u], zm[u], jf[u]);
-        if (PHILOX) {
 #pragma unroll
-          for (int u = 0; u < SPT; ++u) {
+        for (int u = 0; u < SPT; ++u) {
 #pragma unroll
-            for (int i = 0; i < 4 * MP; ++i) z[u][i] = zn[u][i];
-            jw[u] = jwn[u];
-          }
+          for (int i = 0; i < ZW; ++i) z[u][i] = zn[u][i];
+          jw[u] = jwn[u];
         }
       } else {
 #pragma unroll
@@ -522,13 +549,25 @@ __global__ void __launch_bounds__(kRolloutMaxThreads) rollout_kernel(const Rollo
     const int nk = min(tileK, K - base);
     const Real* src = PHILOX ? a.eps_out + (size_t)blockIdx.x * TM * tileK : a.eps_in + base;
     const size_t rstride = PHILOX ? (size_t)tileK : (size_t)K;
-    for (int r = warp; r < TM; r += nwarps) {
-      const Real* row = src + (size_t)r * rstride;
-      Real acc = Real(0);
-#pragma unroll 4
-      for (int kk = lane; kk < nk; kk += 32) acc = fma(sw[kk], row[kk], acc);  // 0 * inf = NaN like controller.py:78
-      acc = warp_sum(acc);
-      if (lane == 0) Nacc[r] = Nacc[r] * scale_old + double(acc);
+    // 4 rows per warp pass so each lane keeps ~4x(nk/32) loads in flight
+    // (the scratch / HBM rows are cold for large T*m; one row at a time was
+    // latency-bound)
+    constexpr int RPW = 4;
+    for (int r0 = warp * RPW; r0 < TM; r0 += nwarps * RPW) {
+      Real acc[RPW];
+#pragma unroll
+      for (int i = 0; i < RPW; ++i) acc[i] = Real(0);
+      for (int kk = lane; kk < nk; kk += 32) {
+        const Real wk = sw[kk];
+#pragma unroll
+        for (int i = 0; i < RPW; ++i)
+          if (r0 + i < TM) acc[i] = fma(wk, src[(size_t)(r0 + i) * rstride + kk], acc[i]);  // 0 * inf = NaN like controller.py:78
+      }
+#pragma unroll
+      for (int i = 0; i < RPW; ++i) {
+        const Real v = warp_sum(acc[i]);
+        if (lane == 0 && r0 + i < TM) Nacc[r0 + i] = Nacc[r0 + i] * scale_old + double(v);
+      }
     }
     __syncthreads();
   }

@@ -28,7 +28,7 @@ def summary(rep):
             seen.add(n)
             out.append(f"{n:32s} {d['Metric Value']} {d['Metric Unit']}")
     raw = list(csv.reader(io.StringIO(ncu([rep, "--page", "raw", "--csv"]))))
-    rh, rv = raw[0], raw[2]
+    rh, ru, rv = raw[0], raw[1], raw[2]
     stalls = []
     for k, v in zip(rh, rv):
         if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued"):
@@ -38,10 +38,12 @@ def summary(rep):
                 pass
     tot = sum(s for s, _ in stalls) or 1
     out.append("stalls: " + ", ".join(f"{n} {100*s/tot:.0f}%" for s, n in sorted(stalls, reverse=True)[:8]))
-    for k, v in zip(rh, rv):
+    for k, u, v in zip(rh, ru, rv):
         if k in ("dram__bytes_read.sum", "dram__bytes_write.sum", "smsp__inst_executed.sum",
-                 "gpu__time_duration.sum", "sm__inst_executed_pipe_fma.sum", "sm__inst_executed_pipe_xu.sum"):
-            out.append(f"{k:40s} {v}")
+                 "gpu__time_duration.sum", "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+                 "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+                 "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"):
+            out.append(f"{k:48s} {v} {u}")
     return "\n".join(out)
 
 
