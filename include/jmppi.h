@@ -151,10 +151,12 @@ int jm_iteration_host(jm_ctx* ctx, const double* x0, const double* u_nom, uint64
 /* Extra outputs of jm_iteration_host:
  *  u_init (m) + u_shift (T*m): warm_start_shift(u_new, u_init) (controller.py:96-100)
  *    computed by the same finalize kernel;
- *  weights_stash: the per-sample weights stay in a device buffer identified by
- *    the returned handle, fetched on demand (jm_stash_fetch) and released with
- *    jm_stash_release -- the drop-in API's lazy UpdateDiagnostics.weights. */
-int jm_stash_fetch(jm_ctx* ctx, uint64_t handle, double* host);
+ *  weights_stash: the per-sample costs stay in a device buffer identified by
+ *    the returned handle; jm_stash_fetch forms the weights from them with the
+ *    iteration's min_cost and normaliser (jm_diag) and downloads them;
+ *    jm_stash_release frees the slot -- the drop-in API's lazy
+ *    UpdateDiagnostics.weights. */
+int jm_stash_fetch(jm_ctx* ctx, uint64_t handle, double min_cost, double normaliser, double* host);
 int jm_stash_release(jm_ctx* ctx, uint64_t handle);
 
 /* Upload x0 (n) and u_nom (T*m) into the context's device inputs (used by

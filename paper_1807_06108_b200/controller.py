@@ -58,14 +58,15 @@ class UpdateDiagnostics:
     read (a K-double download per iteration otherwise dominates the call);
     `weights` then downloads them once and caches the array."""
 
-    __slots__ = ("_weights", "_ctx", "_handle", "min_cost", "effective_sample_size",
+    __slots__ = ("_weights", "_ctx", "_handle", "_z", "min_cost", "effective_sample_size",
                  "per_step_update_norm", "__weakref__")
 
     def __init__(self, weights=None, min_cost=0.0, effective_sample_size=0.0, per_step_update_norm=None,
-                 *, _ctx=None, _handle=0):
+                 *, _ctx=None, _handle=0, _z=0.0):
         self._weights = None if weights is None else np.asarray(weights)
         self._ctx = _ctx
         self._handle = _handle
+        self._z = _z
         self.min_cost = min_cost
         self.effective_sample_size = effective_sample_size
         self.per_step_update_norm = per_step_update_norm
@@ -73,7 +74,7 @@ class UpdateDiagnostics:
     @property
     def weights(self) -> np.ndarray:
         if self._weights is None and self._handle:
-            w = self._ctx.stash_fetch(self._handle)
+            w = self._ctx.stash_fetch(self._handle, self.min_cost, self._z)
             w.setflags(write=False)
             self._ctx.stash_release(self._handle)
             self._handle = 0
@@ -204,6 +205,7 @@ def mppi_iteration(
         per_step_update_norm=out.norms,
         _ctx=ctx if out.stash else None,
         _handle=out.stash,
+        _z=float(out.diag.normaliser),
     )
     if not return_rollouts:
         return new_controls, diagnostics

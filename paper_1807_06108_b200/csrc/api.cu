@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -151,6 +152,14 @@ jm::FinArgs fin_args(const jm_ctx* ctx, const double* records, int nrec) {
   return f;
 }
 
+// weights of `costs` into `w` (2 launches; scratch = ctx->d_wsum)
+cudaError_t launch_weights(jm_ctx* ctx, const double* costs, const DiagOut* diag, double* w) {
+  const int b = jm::kWThreads, g = (ctx->K + b - 1) / b;
+  jm::weights_exp_kernel<<<g, b, 0, ctx->stream>>>(costs, diag, 1.0 / ctx->mppi.lambda_, ctx->K, w, ctx->d_wsum);
+  jm::weights_norm_kernel<<<g, b, 0, ctx->stream>>>(ctx->d_wsum, g, ctx->K, w);
+  return cudaGetLastError();
+}
+
 int rollout_and_finalize(jm_ctx* ctx, const jm::RolloutCall& rc, const double* mapping_dev,
                          double* weights_dev, bool want_shift) {
   CK(ctx->eng->rollout(ctx, rc));
@@ -166,12 +175,7 @@ int rollout_and_finalize(jm_ctx* ctx, const jm::RolloutCall& rc, const double* m
     f.u_shift = ctx->d_small + ctx->off_ushift();
   }
   CK(ctx->eng->finalize(ctx, f, nullptr, nullptr));
-  if (weights_dev) {
-    const int b = 256, g = (ctx->K + b - 1) / b;
-    jm::weights_kernel<<<g, b, 0, ctx->stream>>>(ctx->d_costs, ctx->d_diag(), 1.0 / ctx->mppi.lambda_,
-                                                 ctx->K, weights_dev);
-    CK(cudaGetLastError());
-  }
+  if (weights_dev) CK(launch_weights(ctx, ctx->d_costs, ctx->d_diag(), weights_dev));
   return JM_OK;
 }
 
@@ -185,6 +189,64 @@ int stash_acquire(jm_ctx* ctx, uint64_t* handle) {
   const int i = ctx->stash_free.back();
   ctx->stash_free.pop_back();
   *handle = (uint64_t)i + 1;
+  return JM_OK;
+}
+
+// One drop-in iteration as a static CUDA graph: staged H2D of the input block,
+// rollout (per-sample costs into the stash buffer named in the block), finalize
+// (+shift), D2H of the output block; weights are formed from the stashed costs
+// when first read (jm_stash_fetch).  seed / iteration / stash pointer travel in
+// the staged block (x0 slots 13..15), so replays need no parameter updates.
+int capture_iteration_graph(jm_ctx* ctx) {
+  if (ctx->iter_exec) return JM_OK;
+  cudaStream_t saved = ctx->stream;
+  ctx->stream = ctx->own_stream;
+  double* ds = ctx->d_small;
+  double* hs = ctx->h_small;
+  uint64_t* words = reinterpret_cast<uint64_t*>(ds + ctx->off_x0());
+  static const bool dma = std::getenv("JM_ITER_GRAPH_DMA") != nullptr;  // experiment switch
+  CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  cudaError_t e = cudaSuccess;
+  if (dma) {
+    e = cudaMemcpyAsync(ds, hs, sizeof(double) * ctx->off_unew(), cudaMemcpyHostToDevice, ctx->stream);
+  } else {
+    jm::copy_block_kernel<<<1, 256, 0, ctx->stream>>>(hs, ds, (int)ctx->off_unew());
+    e = cudaGetLastError();
+  }
+  jm::RolloutCall rc;
+  rc.x0 = ds + ctx->off_x0();
+  rc.u_nom = ds + ctx->off_unom();
+  rc.seed_dev = words + 14;
+  rc.iteration_dev = words + 15;
+  rc.costs_dev = reinterpret_cast<double* const*>(words + 13);  // costs straight into the stash buffer
+  if (e == cudaSuccess) e = ctx->eng->rollout(ctx, rc);
+  if (e == cudaSuccess) {
+    jm::FinArgs f = fin_args(ctx, nullptr, 0);
+    f.u_nom = rc.u_nom;
+    f.u_new = ds + ctx->off_unew();
+    f.norms = ds + ctx->off_norms();
+    f.diag = ctx->d_diag();
+    f.status = ctx->d_status();
+    f.u_init = ds + ctx->off_uinit();
+    f.u_shift = ds + ctx->off_ushift();
+    e = ctx->eng->finalize(ctx, f, nullptr, nullptr);
+  }
+  if (e == cudaSuccess && dma) {
+    e = cudaMemcpyAsync(hs + ctx->off_unew(), ds + ctx->off_unew(), sizeof(double) * (ctx->off_rec() - ctx->off_unew()),
+                        cudaMemcpyDeviceToHost, ctx->stream);
+  } else if (e == cudaSuccess) {
+    jm::copy_block_kernel<<<1, 256, 0, ctx->stream>>>(ds + ctx->off_unew(), hs + ctx->off_unew(),
+                                                      (int)(ctx->off_rec() - ctx->off_unew()));
+    e = cudaGetLastError();
+  }
+  cudaGraph_t g = nullptr;
+  cudaError_t e2 = cudaStreamEndCapture(ctx->stream, &g);
+  ctx->stream = saved;
+  CK(e);
+  CK(e2);
+  cudaError_t e3 = cudaGraphInstantiate(&ctx->iter_exec, g, 0);
+  cudaGraphDestroy(g);
+  CK(e3);
   return JM_OK;
 }
 
@@ -353,6 +415,7 @@ int jm_create(const jm_model_desc* model, const jm_cost_desc* cost, const jm_mpp
     e = cudaMalloc(&ctx->d_scratch, (size_t)ctx->grid * ctx->TM * ctx->block * ctx->spt * ctx->real_size);
   if (e == cudaSuccess) e = dalloc(&ctx->d_costs, (size_t)ctx->K);
   if (e == cudaSuccess) e = dalloc(&ctx->d_weights, (size_t)ctx->K);
+  if (e == cudaSuccess) e = dalloc(&ctx->d_wsum, (size_t)(ctx->K + jm::kWThreads - 1) / jm::kWThreads);
   if (e == cudaSuccess) e = dalloc(&ctx->d_records, (size_t)ctx->grid * ctx->rec_stride);
   if (e == cudaSuccess) e = dalloc(&ctx->d_small, ctx->small_doubles());
   if (e == cudaSuccess) e = dalloc(&ctx->d_counter, 1);
@@ -376,11 +439,13 @@ int jm_destroy(jm_ctx* ctx) {
   if (ctx->own_stream) cudaStreamSynchronize(ctx->own_stream);
   if (ctx->graph_exec) cudaGraphExecDestroy(ctx->graph_exec);
   if (ctx->graph) cudaGraphDestroy(ctx->graph);
+  if (ctx->iter_exec) cudaGraphExecDestroy(ctx->iter_exec);
   dfree(ctx->d_scratch);
   dfree(ctx->d_hbm_eps);
   dfree(ctx->d_hbm_jump);
   dfree(ctx->d_costs);
   dfree(ctx->d_weights);
+  dfree(ctx->d_wsum);
   dfree(ctx->d_records);
   dfree(ctx->d_small);
   dfree(ctx->d_counter);
@@ -429,6 +494,41 @@ int jm_iteration_host(jm_ctx* ctx, const double* x0, const double* u_nom, uint64
   const int N = ctx->N, M = ctx->M, TM = ctx->TM, T = ctx->T, K = ctx->K;
   double* hs = ctx->h_small;
   double* ds = ctx->d_small;
+  static const bool iter_graph = std::getenv("JM_NO_ITER_GRAPH") == nullptr;
+  if (iter_graph && !hbm && !mapping && !costs && !weights && !states && !diverged_step && u_shift && weights_stash) {
+    // the drop-in fast path: one graph launch
+    int r = capture_iteration_graph(ctx);
+    if (r != JM_OK) return r;
+    uint64_t handle = 0;
+    r = stash_acquire(ctx, &handle);
+    if (r != JM_OK) return r;
+    std::memcpy(hs + ctx->off_x0(), x0, sizeof(double) * N);
+    std::memcpy(hs + ctx->off_unom(), u_nom, sizeof(double) * TM);
+    std::memcpy(hs + ctx->off_uinit(), u_init, sizeof(double) * M);
+    uint64_t* words = reinterpret_cast<uint64_t*>(hs + ctx->off_x0());
+    words[13] = reinterpret_cast<uint64_t>(ctx->stash[handle - 1]);
+    words[14] = seed;
+    words[15] = iteration;
+    CK(cudaGraphLaunch(ctx->iter_exec, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    const int32_t status = *reinterpret_cast<int32_t*>(hs + ctx->off_status());
+    if (status == JM_ERR_NO_VIABLE) {
+      ctx->stash_free.push_back((int)handle - 1);
+      return fail(ctx, JM_ERR_NO_VIABLE, "no viable rollout");
+    }
+    const DiagOut* dg = reinterpret_cast<const DiagOut*>(hs + ctx->off_diag());
+    std::memcpy(u_new, hs + ctx->off_unew(), sizeof(double) * TM);
+    std::memcpy(u_shift, hs + ctx->off_ushift(), sizeof(double) * TM);
+    if (step_norms) std::memcpy(step_norms, hs + ctx->off_norms(), sizeof(double) * T);
+    if (diag) {
+      diag->min_cost = dg->min_cost;
+      diag->ess = dg->ess;
+      diag->normaliser = dg->normaliser;
+      diag->n_finite = dg->n_finite;
+    }
+    *weights_stash = handle;
+    return JM_OK;
+  }
   std::memcpy(hs + ctx->off_x0(), x0, sizeof(double) * N);
   std::memcpy(hs + ctx->off_unom(), u_nom, sizeof(double) * TM);
   if (mapping) std::memcpy(hs + ctx->off_map(), mapping, sizeof(double) * M * M);
@@ -459,17 +559,21 @@ int jm_iteration_host(jm_ctx* ctx, const double* x0, const double* u_nom, uint64
     rc.states = ctx->d_states;
     rc.diverged = ctx->d_div;
   }
-  double* wdev = nullptr;
+  double* wdev = weights ? ctx->d_weights : nullptr;
   uint64_t handle = 0;
-  if (weights_stash) {
+  if (weights_stash && !costs && !weights) {  // keep this iteration's costs; weights are formed on fetch
     const int rs = stash_acquire(ctx, &handle);
     if (rs != JM_OK) return rs;
-    wdev = ctx->stash[handle - 1];
-  } else if (weights) {
-    wdev = ctx->d_weights;
+    rc.costs = ctx->stash[handle - 1];
   }
   const int r = rollout_and_finalize(ctx, rc, mapping ? ds + ctx->off_map() : nullptr, wdev, u_shift != nullptr);
   if (r != JM_OK) return r;
+  if (weights_stash && !handle) {
+    const int rs = stash_acquire(ctx, &handle);
+    if (rs != JM_OK) return rs;
+    CK(cudaMemcpyAsync(ctx->stash[handle - 1], ctx->d_costs, sizeof(double) * K, cudaMemcpyDeviceToDevice,
+                       ctx->stream));
+  }
   const size_t out_n = ctx->off_rec() - ctx->off_unew();
   CK(cudaMemcpyAsync(hs + ctx->off_unew(), ds + ctx->off_unew(), sizeof(double) * out_n,
                      cudaMemcpyDeviceToHost, ctx->stream));
@@ -514,10 +618,15 @@ int jm_upload_inputs(jm_ctx* ctx, const double* x0, const double* u_nom) {
   return JM_OK;
 }
 
-int jm_stash_fetch(jm_ctx* ctx, uint64_t handle, double* host) {
+int jm_stash_fetch(jm_ctx* ctx, uint64_t handle, double min_cost, double normaliser, double* host) {
   if (!ctx || !host || handle == 0 || handle > ctx->stash.size()) return fail(ctx, JM_ERR_VALUE, "bad stash handle");
   CK(cudaSetDevice(ctx->device));
-  CK(cudaMemcpyAsync(host, ctx->stash[handle - 1], sizeof(double) * ctx->K, cudaMemcpyDeviceToHost, ctx->stream));
+  // weights of the stashed costs (controller.py:62-71) with that iteration's rho and Z
+  DiagOut* dd = reinterpret_cast<DiagOut*>(ctx->d_small + ctx->off_rec());  // scratch slot
+  DiagOut hd{min_cost, 0.0, normaliser, 0};
+  CK(cudaMemcpyAsync(dd, &hd, sizeof(hd), cudaMemcpyHostToDevice, ctx->stream));
+  CK(launch_weights(ctx, ctx->stash[handle - 1], dd, ctx->d_weights));
+  CK(cudaMemcpyAsync(host, ctx->d_weights, sizeof(double) * ctx->K, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   return JM_OK;
 }
@@ -581,10 +690,7 @@ int jm_finalize_dev(jm_ctx* ctx, const double* records_dev, int32_t nrec, const 
 int jm_weights_dev(jm_ctx* ctx, const double* costs_dev, const jm_diag* diag_dev, double* weights_dev) {
   if (!ctx || !costs_dev || !diag_dev || !weights_dev) return fail(ctx, JM_ERR_VALUE, "null argument");
   CK(cudaSetDevice(ctx->device));
-  const int b = 256, g = (ctx->K + b - 1) / b;
-  jm::weights_kernel<<<g, b, 0, ctx->stream>>>(costs_dev, reinterpret_cast<const DiagOut*>(diag_dev),
-                                               1.0 / ctx->mppi.lambda_, ctx->K, weights_dev);
-  CK(cudaGetLastError());
+  CK(launch_weights(ctx, costs_dev, reinterpret_cast<const DiagOut*>(diag_dev), weights_dev));
   return JM_OK;
 }
 

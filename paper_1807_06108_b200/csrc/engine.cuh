@@ -171,12 +171,14 @@ class Engine final : public EngineBase {
     a.seed = rc.seed;
     a.iteration = rc.iteration;
     a.iteration_dev = rc.iteration_dev;
+    a.seed_dev = rc.seed_dev;
     a.x0 = rc.x0;
     a.u_nom = rc.u_nom;
     a.eps_in = reinterpret_cast<const Real*>(rc.eps_in);
     a.jump_in = reinterpret_cast<const Real*>(rc.jump_in);
     a.eps_out = reinterpret_cast<Real*>(c->d_scratch);
     a.costs = rc.costs;
+    a.costs_dev = rc.costs_dev;
     a.states = rc.states;
     a.diverged = rc.diverged;
     a.records = c->d_records;

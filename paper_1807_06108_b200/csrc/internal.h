@@ -17,6 +17,8 @@ struct RolloutCall {
   const double* u_nom = nullptr;
   uint64_t seed = 0, iteration = 0;
   const uint64_t* iteration_dev = nullptr;
+  const uint64_t* seed_dev = nullptr;
+  double* const* costs_dev = nullptr;
   const void* eps_in = nullptr;
   const void* jump_in = nullptr;
   double* costs = nullptr;
@@ -65,6 +67,7 @@ struct jm_ctx {
   void* d_hbm_jump = nullptr;
   double* d_costs = nullptr;      // K
   double* d_weights = nullptr;    // K
+  double* d_wsum = nullptr;       // weight normaliser block sums
   double* d_records = nullptr;    // grid * rec_stride
   double* d_small = nullptr;      // x0 | u_nom | u_new | norms | mapping | u_init | record
   double* h_big = nullptr;        // pinned 2K doubles: costs | weights
@@ -89,11 +92,13 @@ struct jm_ctx {
   void* d_flush = nullptr;         // L2 flush buffer (bench)
   size_t flush_cap = 0;
   cudaGraph_t graph = nullptr;
+  cudaGraphExec_t iter_exec = nullptr;  // graph of one drop-in iteration (H2D..D2H)
   cudaGraphExec_t graph_exec = nullptr;
   std::string err;
 
   // d_small / h_small layout (doubles):
-  //   inputs  [x0:16][u_nom:TM][mapping:16][u_init:16]
+  //   inputs  [x0:16][u_nom:TM][mapping:16][u_init:16]   (x0 slots 13..15 of
+  //           the graph path: stash pointer, seed, iteration as raw 64-bit words)
   //   outputs [u_new:TM][norms:T][diag:4][status:2][u_shift:TM]
   //   [record:rec_stride]  (this context's reduced record)
   size_t off_x0() const { return 0; }

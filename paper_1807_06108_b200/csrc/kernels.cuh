@@ -12,7 +12,7 @@
 //                    :157-169); in the closed loop its last CTA also runs K7,
 //                    the plant step + warm-start shift (harness.py:131-150).
 //   noise_kernel     K1 in write mode (sample_noise_batch on device).
-//   weights_kernel / shift_kernel (api.cu only): controller.py:62-71, :96-100.
+//   weights_*_kernel / shift_kernel (api.cu only): controller.py:62-71, :96-100.
 // All reductions are fixed-order (no float atomics): results are bitwise
 // reproducible run to run for a given launch configuration, and the noise is
 // independent of it.
@@ -115,12 +115,14 @@ struct RolloutArgs {
   SysParams<Real> sp;
   uint64_t seed, iteration;
   const uint64_t* iteration_dev;
+  const uint64_t* seed_dev;  // graph-replayed drop-in call: seed staged in device memory
   const double* x0;
   const double* u_nom;
   const Real* eps_in;    // HBM mode: step-major eps_combined
   const Real* jump_in;   // HBM mode, state jumps: step-major ind*mark
   Real* eps_out;         // Philox mode: per-CTA eps_combined scratch [cta][t*m+j][lane]
   double* costs;         // K
+  double* const* costs_dev;  // graph-replayed drop-in call: costs go to the buffer named in device memory
   double* states;        // trace: K*(T+1)*n
   int64_t* diverged;     // trace: K
   double* records;       // gridDim.x * rec_stride
@@ -276,7 +278,8 @@ __global__ void __launch_bounds__(kRolloutMaxThreads) rollout_kernel(const Rollo
   pin(cq);
   const uint32_t jthr = a.jthr;
 
-  const StreamKey sk = make_stream_key(L ? L->seed : a.seed, iter);
+  const StreamKey sk = make_stream_key(L ? L->seed : (a.seed_dev ? *a.seed_dev : a.seed), iter);
+  double* const costs_out = a.costs_dev ? *a.costs_dev : a.costs;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
 
   // SPT samples per thread: sub-tile u covers columns [u*blockDim, (u+1)*blockDim)
@@ -489,7 +492,7 @@ __global__ void __launch_bounds__(kRolloutMaxThreads) rollout_kernel(const Rollo
       } else {
         S[u] = r_inf<Real>();
       }
-      if (act[u] && a.costs) a.costs[kl[u]] = double(S[u]);
+      if (act[u] && costs_out) costs_out[kl[u]] = double(S[u]);
       Sf[u] = act[u] ? S[u] : r_inf<Real>();
     }
 
@@ -721,6 +724,7 @@ template <class Dyn>
 __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, const PlantArgs p) {
   extern __shared__ double fsm[];
   constexpr int NW = kFinThreads / 32;
+  static_assert(NW == 32, "warp-0 reductions assume 32 warps");
   double* se = fsm;                 // e_b = exp(-(rho_b - rho)/lambda), per record
   double* part = fsm + a.nrec;      // [NW][kFinCols]
   __shared__ double s_red[3][NW];
@@ -736,16 +740,16 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
   grid_dep_wait();
   if (L != nullptr && L->halted) return;
   const int rs = a.rec_stride;
-  // global rho (controller.py:69: min over finite costs)
+  // global rho (controller.py:69: min over finite costs); block reductions
+  // finish in warp 0 with shuffles (fixed order), not serial thread-0 loops
   double m = CUDART_INF;
   for (int b = tid; b < a.nrec; b += kFinThreads) m = fmin(m, a.rec[(size_t)b * rs]);
   m = warp_min(m);
   if (lane == 0) s_red[0][warp] = m;
   __syncthreads();
-  if (tid == 0) {
-    double mm = CUDART_INF;
-    for (int w = 0; w < NW; ++w) mm = fmin(mm, s_red[0][w]);
-    s_bc[0] = mm;
+  if (warp == 0) {
+    double mm = warp_min(s_red[0][lane]);
+    if (lane == 0) s_bc[0] = mm;
   }
   __syncthreads();
   const double rho = s_bc[0];
@@ -761,23 +765,19 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
   z = warp_sum(z);
   w2 = warp_sum(w2);
   nf = warp_sum(nf);
-  __syncthreads();
   if (lane == 0) {
     s_red[0][warp] = z;
     s_red[1][warp] = w2;
     s_red[2][warp] = nf;
   }
   __syncthreads();
-  if (tid == 0) {
-    double zz = 0.0, ww = 0.0, nn = 0.0;
-    for (int w = 0; w < NW; ++w) {
-      zz += s_red[0][w];
-      ww += s_red[1][w];
-      nn += s_red[2][w];
+  if (warp == 0) {
+    const double zz = warp_sum(s_red[0][lane]), ww = warp_sum(s_red[1][lane]), nn = warp_sum(s_red[2][lane]);
+    if (lane == 0) {
+      s_bc[1] = zz;
+      s_bc[2] = ww;
+      s_bc[3] = nn;
     }
-    s_bc[1] = zz;
-    s_bc[2] = ww;
-    s_bc[3] = nn;
   }
   __syncthreads();
   const double Z = s_bc[1], W2 = s_bc[2], NF = s_bc[3];
@@ -824,10 +824,11 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
 #pragma unroll
   for (int i = 0; i < CPL; ++i) part[warp * kFinCols + lane + 32 * i] = acc[i];
   __syncthreads();
-  if (tid < kFinCols) {
-    double n = 0.0;
-    for (int w = 0; w < NW; ++w) n += part[w * kFinCols + tid];
-    s_delta[tid] = n;
+  // cross-warp column sums: warp w reduces columns w, w+32, ... over the 32
+  // warp partials with a shuffle tree (fixed order)
+  for (int col = warp; col < kFinCols; col += NW) {
+    const double v = warp_sum(part[lane * kFinCols + col]);
+    if (lane == 0) s_delta[col] = v;
   }
   __syncthreads();
   if (reduce_mode) {
@@ -996,13 +997,49 @@ __global__ void __launch_bounds__(256) noise_kernel(const NoiseArgs a) {
 
 #ifdef JM_COMMON_KERNELS  // non-template kernels: defined in api.cu only
 // ---------------------------------------------------------------- weights
-__global__ void weights_kernel(const double* costs, const DiagOut* diag, double inv_lam, int K,
-                               double* w) {
+// Output weights = compute_weights (controller.py:62-71) of the returned
+// float64 costs: w = exp(-(S - rho)/lambda) normalised by its own float64 sum
+// (fixed-order: per-block shuffle trees, then the block sums in order), so they
+// sum to 1 to rounding in both compute precisions.
+constexpr int kWThreads = 256;
+__global__ void weights_exp_kernel(const double* costs, const DiagOut* diag, double inv_lam, int K, double* w,
+                                   double* block_sums) {
+  __shared__ double s[kWThreads / 32];
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= K) return;
-  const double rho = diag->min_cost, Z = diag->normaliser;
-  const double s = costs[k];
-  w[k] = (isfinite(s) && Z > 0.0) ? exp(-(s - rho) * inv_lam) / Z : 0.0;
+  double e = 0.0;
+  if (k < K) {
+    const double c = costs[k];
+    e = isfinite(c) ? exp(-(c - diag->min_cost) * inv_lam) : 0.0;
+    w[k] = e;
+  }
+  e = warp_sum(e);
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = e;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (kWThreads / 32) ? s[threadIdx.x] : 0.0;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) block_sums[blockIdx.x] = v;
+  }
+}
+
+__global__ void weights_norm_kernel(const double* block_sums, int nblocks, int K, double* w) {
+  __shared__ double s_z;
+  if (threadIdx.x < 32) {
+    double z = 0.0;
+    for (int b = threadIdx.x; b < nblocks; b += 32) z += block_sums[b];
+    z = warp_sum(z);
+    if (threadIdx.x == 0) s_z = z;
+  }
+  __syncthreads();
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < K && s_z > 0.0) w[k] /= s_z;
+}
+
+// ---------------------------------------------------------------- zero-copy staging
+// The drop-in graph moves its ~1-2 KB input/output blocks with one CTA reading /
+// writing pinned host memory directly (UVA) instead of DMA memcpy nodes.
+__global__ void copy_block_kernel(const double* __restrict__ src, double* __restrict__ dst, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
 }
 
 // ---------------------------------------------------------------- shift

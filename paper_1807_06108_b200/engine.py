@@ -280,9 +280,10 @@ class Context:
         out.stash = handle.value if stash_weights else 0
         return out
 
-    def stash_fetch(self, handle: int) -> np.ndarray:
+    def stash_fetch(self, handle: int, min_cost: float, normaliser: float) -> np.ndarray:
         w = np.empty(self.K)
-        self.check(self.lib.jm_stash_fetch(self.h, C.c_uint64(handle), L.dptr(w)))
+        self.check(self.lib.jm_stash_fetch(self.h, C.c_uint64(handle), float(min_cost), float(normaliser),
+                                           L.dptr(w)))
         return w
 
     def stash_release(self, handle: int):

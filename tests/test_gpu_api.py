@@ -305,3 +305,20 @@ def test_sharded_loop_world1_matches_graph_loop(gpu_device):
         assert np.allclose(x, rec.states[-1], rtol=1e-9, atol=1e-12)
     finally:
         dist.destroy_process_group()
+
+
+def test_lazy_weights_match_eager_and_survive_later_iterations(gpu_device):
+    task, cfg = jb.baseline_config(0, K=4096, T=40)
+    c0 = jb.initial_controller_state(cfg)
+    s0, d0 = jb.mppi_iteration(c0, task.model, task.cost_model, task.x0, 3)        # graph fast path, lazy
+    c1 = jb.ControllerState(jb.warm_start_shift(s0, cfg.u_init), 1, cfg)
+    s1, d1 = jb.mppi_iteration(c1, task.model, task.cost_model, task.x0, 3)
+    _, e0, ro = jb.mppi_iteration(c0, task.model, task.cost_model, task.x0, 3, return_rollouts=True)  # eager
+    assert np.array_equal(d0.weights, e0.weights)  # fetched after a later iteration ran
+    assert d0.weights.sum() == pytest.approx(1.0, abs=1e-12)
+    costs = np.array([r.cost for r in ro])
+    assert np.allclose(d0.weights, jb.compute_weights(costs, cfg.lambda_), rtol=1e-6, atol=1e-300)
+    assert not np.array_equal(d0.weights, d1.weights)
+    # the GPU-precomputed shift equals the device shift kernel
+    assert np.array_equal(jb.warm_start_shift(s1, cfg.u_init).controls,
+                          jb.warm_start_shift(jb.ControlSequence(s1.controls, cfg.dt), cfg.u_init).controls)
