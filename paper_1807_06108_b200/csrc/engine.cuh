@@ -102,12 +102,40 @@ class Engine final : public EngineBase {
     return cudaSuccess;
   }
 
-  // Launch shape.  K <= num_sms * 512: one CTA per SM, every SM gets the
+  // warp-specialised kernel (Philox, non-trace): block = 2 x tile
+  static constexpr int kWsMaxThreads = (N <= 4) ? 1024 : 512;
+  static int ws_buf() {
+    static const int b = std::getenv("JM_WS_BUF") ? std::atoi(std::getenv("JM_WS_BUF")) : 4;
+    return b;
+  }
+  template <int JM, int B>
+  static auto ws_kern() {
+    return &rollout_kernel_ws<Sys, Real, JM, kWsMaxThreads, B>;
+  }
+  template <int JM>
+  static const void* ws_fn() {
+    const int b = ws_buf();
+    if (b == 2) return reinterpret_cast<const void*>(ws_kern<JM, 2>());
+    if (b == 7) return reinterpret_cast<const void*>(ws_kern<JM, 7>());
+    return reinterpret_cast<const void*>(ws_kern<JM, 4>());
+  }
+  size_t ws_smem_bytes(const jm_ctx* c, int tile) const {
+    const int gw = (c->model.jump_channel == JM_JUMP_STATE) ? WsShape<Sys, 1>::GW : WsShape<Sys, 0>::GW;
+    return smem_bytes(c, tile, 1) + sizeof(Real) * (size_t)ws_buf() * gw * tile;
+  }
+
+  // Launch shape.  K <= num_sms * tile_max: one CTA per SM, every SM gets the
   // same sample count (a latency-bound horizon loop gains nothing from
-  // stacking CTAs on few SMs).  Larger K: 256-thread tiles, grid = SMs x
-  // occupancy, tiles grid-strided.
+  // stacking CTAs on few SMs).  Larger K: 256-sample tiles, grid = SMs x
+  // occupancy, tiles grid-strided.  Philox path, single wave: the per-CTA
+  // eps scratch the epilogue reads is kept in shared memory when it fits, and
+  // tiles of <= kWsMaxTile samples run the warp-specialised kernel (measured:
+  // it wins only where a few warps per SM leave the issue slots idle).
+  static constexpr int kWsMaxTile = 128;
   cudaError_t configure(jm_ctx* c) override {
     const bool philox = c->mppi.noise_source == JM_NOISE_PHILOX;
+    static const int ws_env = std::getenv("JM_WS") ? std::atoi(std::getenv("JM_WS")) : -1;  // A/B: 0 off, 1 on
+    static const bool no_eps_smem = std::getenv("JM_NO_EPS_SMEM") != nullptr;
     int block = c->mppi.block_threads;
     const int K = c->K, sms = c->num_sms;
     const int sp = philox ? kSPT : 1;  // samples per thread of the main (non-trace) kernel
@@ -119,20 +147,39 @@ class Engine final : public EngineBase {
         block = 256;
       }
     }
+    bool ws = philox && 2 * block <= kWsMaxThreads && (ws_env < 0 ? block <= kWsMaxTile : ws_env == 1);
     c->block = block;
-    c->spt = sp;
-    // the trace kernels run one sample per thread: size smem for the larger tile
-    const size_t smem = smem_bytes(c, block, std::max(sp, 1));
+    c->spt = ws ? 1 : sp;
+    c->ws = ws;
+    // the trace / HBM kernels run one sample per thread
+    const size_t smem = smem_bytes(c, block, std::max(c->spt, 1));
     const void* fn = nullptr;
-    cudaError_t e = (c->model.jump_channel == JM_JUMP_STATE) ? set_attrs<1>(smem, &fn, philox)
-                                                            : set_attrs<0>(smem, &fn, philox);
+    const bool sj = c->model.jump_channel == JM_JUMP_STATE;
+    cudaError_t e = sj ? set_attrs<1>(smem, &fn, philox) : set_attrs<0>(smem, &fn, philox);
+    if (e != cudaSuccess) return e;
+    int threads = block;
+    size_t msmem = smem;
+    if (ws) {
+      fn = sj ? ws_fn<1>() : ws_fn<0>();
+      threads = 2 * block;
+      msmem = ws_smem_bytes(c, block);
+    }
+    const int tile = block * c->spt;
+    c->ntiles = (K + tile - 1) / tile;
+    int optin = 0;
+    e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device);
+    if (e != cudaSuccess) return e;
+    const size_t scr = sizeof(Real) * (size_t)c->TM * tile;
+    c->eps_smem = philox && !no_eps_smem && c->ntiles <= sms && msmem + scr + 1024 <= (size_t)optin;
+    if (c->eps_smem) msmem += scr;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem);
     if (e != cudaSuccess) return e;
     int occ = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, block, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, msmem);
     if (e != cudaSuccess) return e;
     if (occ < 1) return cudaErrorInvalidConfiguration;
     c->smem = smem;
-    c->ntiles = (K + block * sp - 1) / (block * sp);
+    c->main_smem = msmem;
     c->grid = std::min(c->ntiles, occ * sms);
     if (c->grid > kMaxRecords) c->grid = kMaxRecords;
     const size_t fsm = finalize_smem_bytes(kMaxRecords);
@@ -177,6 +224,7 @@ class Engine final : public EngineBase {
     a.eps_in = reinterpret_cast<const Real*>(rc.eps_in);
     a.jump_in = reinterpret_cast<const Real*>(rc.jump_in);
     a.eps_out = reinterpret_cast<Real*>(c->d_scratch);
+    a.eps_smem = c->eps_smem;
     a.costs = rc.costs;
     a.costs_dev = rc.costs_dev;
     a.states = rc.states;
@@ -207,11 +255,19 @@ class Engine final : public EngineBase {
   template <int JM>
   cudaError_t launch(jm_ctx* c, const RolloutArgs<Real>& a, bool philox, bool trace) {
     dim3 grid(c->grid), block(c->block);
+    if (philox && !trace && c->ws)
+    {
+      const int b = ws_buf();
+      auto k = b == 2 ? ws_kern<JM, 2>() : b == 7 ? ws_kern<JM, 7>() : ws_kern<JM, 4>();
+      return launch_pdl(k, grid, dim3(2 * c->block), c->main_smem, c->stream, a);
+    }
     if (philox && !trace)
-      return launch_pdl(rollout_kernel<Sys, Real, true, false, JM, spt<true, false>()>, grid, block, c->smem, c->stream, a);
+      return launch_pdl(rollout_kernel<Sys, Real, true, false, JM, spt<true, false>()>, grid, block, c->main_smem,
+                        c->stream, a);
     // the one-sample-per-thread variants cover the same samples with SPT x the tiles
     // (same grid, so the same number of per-CTA records)
     RolloutArgs<Real> b = a;
+    b.eps_smem = 0;
     b.ntiles = (c->K + c->block - 1) / c->block;
     if (philox) return launch_pdl(rollout_kernel<Sys, Real, true, true, JM, 1>, grid, block, c->smem, c->stream, b);
     if (!trace) return launch_pdl(rollout_kernel<Sys, Real, false, false, JM, 1>, grid, block, c->smem, c->stream, b);

@@ -121,6 +121,7 @@ struct RolloutArgs {
   const Real* eps_in;    // HBM mode: step-major eps_combined
   const Real* jump_in;   // HBM mode, state jumps: step-major ind*mark
   Real* eps_out;         // Philox mode: per-CTA eps_combined scratch [cta][t*m+j][lane]
+  int eps_smem;          // Philox, single wave: the scratch lives in shared memory instead
   double* costs;         // K
   double* const* costs_dev;  // graph-replayed drop-in call: costs go to the buffer named in device memory
   double* states;        // trace: K*(T+1)*n
@@ -188,6 +189,88 @@ template <int Q>
 struct Pad {
   static constexpr int value = (Q == 3) ? 4 : Q;
 };
+
+// ---------------------------------------------------------------- per-tile weighting
+// Online softmax of one tile into the CTA accumulator (K3/K4 partials):
+// rho_new = min(rho_acc, min_tile S); w_k = exp(-(S_k - rho_new)/lambda);
+// Z, sum w^2, n_finite and N[r] += sum_k w_k eps[r,k] (rescaled by
+// exp(-(rho_new - rho_acc)/lambda)).  Every thread of the CTA calls it; Sf holds
+// the thread's SPT costs (+inf for none), cols their tile columns.
+template <typename Real, int SPT>
+__device__ __forceinline__ void tile_epilogue(const Real* Sf, const int* cols, int nk, const Real* src,
+                                              size_t rstride, int TM, Real inv_lam, Real* sw, double* Nacc,
+                                              double (*s_red)[32], double* s_acc, double* s_bc) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  Real mloc = Sf[0];
+#pragma unroll
+  for (int u = 1; u < SPT; ++u) mloc = fmin(mloc, Sf[u]);
+  const Real m = warp_min(mloc);
+  if (lane == 0) s_red[0][warp] = double(m);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double mm = CUDART_INF;
+    for (int w = 0; w < nwarps; ++w) mm = fmin(mm, s_red[0][w]);
+    const double rho_prev = s_acc[0];
+    const double rho_new = fmin(rho_prev, mm);
+    s_bc[0] = rho_new;
+    s_bc[1] = (rho_prev == CUDART_INF) ? 0.0 : exp((rho_new - rho_prev) * double(inv_lam));
+  }
+  __syncthreads();
+  const double rho_new = s_bc[0], scale_old = s_bc[1];
+  if (rho_new == CUDART_INF) return;  // no finite cost yet in this CTA (uniform)
+  double z1 = 0.0, z2 = 0.0, nf = 0.0;
+#pragma unroll
+  for (int u = 0; u < SPT; ++u) {
+    const bool fin = Sf[u] < r_inf<Real>();
+    const Real w = fin ? r_exp<Real>(-(Sf[u] - Real(rho_new)) * inv_lam) : Real(0);
+    if (cols[u] >= 0) sw[cols[u]] = w;
+    z1 += double(w);
+    z2 += double(w) * double(w);
+    nf += fin ? 1.0 : 0.0;
+  }
+  z1 = warp_sum(z1);
+  z2 = warp_sum(z2);
+  nf = warp_sum(nf);
+  __syncwarp();
+  if (lane == 0) {
+    s_red[0][warp] = z1;
+    s_red[1][warp] = z2;
+    s_red[2][warp] = nf;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    for (int w2 = 0; w2 < nwarps; ++w2) {
+      a1 += s_red[0][w2];
+      a2 += s_red[1][w2];
+      a3 += s_red[2][w2];
+    }
+    s_acc[0] = rho_new;
+    s_acc[1] = s_acc[1] * scale_old + a1;
+    s_acc[2] = s_acc[2] * scale_old * scale_old + a2;
+    s_acc[3] += a3;
+  }
+  // N[r] += sum_k w_k eps[r, k] over the tile: warp-per-row, lanes over k;
+  // 4 rows per warp pass so each lane keeps ~4x(nk/32) loads in flight
+  constexpr int RPW = 4;
+  for (int r0 = warp * RPW; r0 < TM; r0 += nwarps * RPW) {
+    Real acc[RPW];
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) acc[i] = Real(0);
+    for (int kk = lane; kk < nk; kk += 32) {
+      const Real wk = sw[kk];
+#pragma unroll
+      for (int i = 0; i < RPW; ++i)
+        if (r0 + i < TM) acc[i] = fma(wk, src[(size_t)(r0 + i) * rstride + kk], acc[i]);  // 0 * inf = NaN like controller.py:78
+    }
+#pragma unroll
+    for (int i = 0; i < RPW; ++i) {
+      const Real v = warp_sum(acc[i]);
+      if (lane == 0 && r0 + i < TM) Nacc[r0 + i] = Nacc[r0 + i] * scale_old + double(v);
+    }
+  }
+  __syncthreads();
+}
 
 // ---------------------------------------------------------------- rollout
 // JM = 0: control-channel jumps (marks folded into eps_combined, q = m);
@@ -287,6 +370,7 @@ __global__ void __launch_bounds__(kRolloutMaxThreads) rollout_kernel(const Rollo
   // a thread are interleaved step by step (instruction-level parallelism
   // without more warps: a K=65536 horizon gives each SM only ~14 warps).
   const int tileK = blockDim.x * SPT;
+  Real* const scr = (PHILOX && !TRACE && a.eps_smem) ? sw + tileK : a.eps_out + (size_t)blockIdx.x * TM * tileK;
   for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
     const int base = tile * tileK;
     int kl[SPT];
@@ -301,7 +385,7 @@ __global__ void __launch_bounds__(kRolloutMaxThreads) rollout_kernel(const Rollo
       kl[u] = base + u * blockDim.x + threadIdx.x;
       act[u] = kl[u] < K;
       kg[u] = (uint32_t)(a.sample_offset + kl[u]);
-      ep[u] = PHILOX ? a.eps_out + (size_t)blockIdx.x * TM * tileK + u * blockDim.x + threadIdx.x : nullptr;
+      ep[u] = PHILOX ? scr + u * blockDim.x + threadIdx.x : nullptr;
       S[u] = Real(0);
       dstep[u] = -1;
 #pragma unroll
@@ -497,82 +581,259 @@ __global__ void __launch_bounds__(kRolloutMaxThreads) rollout_kernel(const Rollo
     }
 
     // ---- per-CTA online softmax over this tile (K3/K4 partials) ----
-    Real mloc = Sf[0];
+    int cols[SPT];
 #pragma unroll
-    for (int u = 1; u < SPT; ++u) mloc = fmin(mloc, Sf[u]);
-    const Real m = warp_min(mloc);
-    if (lane == 0) s_red[0][warp] = double(m);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double mm = CUDART_INF;
-      for (int w = 0; w < nwarps; ++w) mm = fmin(mm, s_red[0][w]);
-      const double rho_prev = s_acc[0];
-      const double rho_new = fmin(rho_prev, mm);
-      s_bc[0] = rho_new;
-      s_bc[1] = (rho_prev == CUDART_INF) ? 0.0 : exp((rho_new - rho_prev) * double(a.inv_lam));
-    }
-    __syncthreads();
-    const double rho_new = s_bc[0], scale_old = s_bc[1];
-    if (rho_new == CUDART_INF) continue;  // no finite cost yet in this CTA (uniform)
-    double z1 = 0.0, z2 = 0.0, nf = 0.0;
+    for (int u = 0; u < SPT; ++u) cols[u] = u * blockDim.x + threadIdx.x;
+    tile_epilogue<Real, SPT>(Sf, cols, min(tileK, K - base),
+                             PHILOX ? scr : a.eps_in + base,
+                             PHILOX ? (size_t)tileK : (size_t)K, TM, a.inv_lam, sw, Nacc, s_red, s_acc, s_bc);
+  }
+  __syncthreads();
+  double* rec = a.records + (size_t)blockIdx.x * a.rec_stride;
+  if (threadIdx.x == 0) {
+    rec[0] = s_acc[0];
+    rec[1] = s_acc[1];
+    rec[2] = s_acc[2];
+    rec[3] = s_acc[3];
+  }
+  for (int r = threadIdx.x; r < TM; r += blockDim.x) rec[4 + r] = Nacc[r];
+}
+
+// ---------------------------------------------------------------- rollout, warp-specialised
+// Philox, non-trace.  The block is 2C threads: warps [0, C/32) are consumers
+// (one sample each: dynamics + modified cost), warps [C/32, 2C/32) producers
+// (thread C+c draws the noise of consumer c's sample).  Per 4-step group a
+// producer writes eps_combined (and the state-jump increments, JM = 1) into
+// a shared-memory ring of NBUF slots and the eps rows into the per-CTA
+// scratch the epilogue reads; full/empty handshakes are named barriers
+// (bar.arrive / bar.sync over all 2C threads).  The split takes the ~60
+// Philox/Box-Muller/Cholesky instructions per state-step off the dynamics
+// warps, so the latency-bound horizon chains issue back to back while the
+// noise is produced in parallel on the SM's other schedulers' idle slots.
+// Same noise bits, same tiles and records as rollout_kernel<..., PHILOX, !TRACE, .., 1>.
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void named_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+template <class Sys, int JM>
+struct WsShape {
+  static constexpr int M = Sys::M;
+  static constexpr int Q = (JM == 0) ? M : Sys::Dyn::QJ;
+  static constexpr int GW = 4 * M + (JM == 1 ? 4 * Q : 0);  // Reals per sample per group
+};
+
+template <class Sys, typename Real, int JM, int MAXT, int kWsBuf>
+__global__ void __launch_bounds__(MAXT) rollout_kernel_ws(const RolloutArgs<Real> a) {
+  using Dyn = typename Sys::Dyn;
+  using Cost = typename Sys::Cost;
+  constexpr int N = Sys::N, M = Sys::M;
+  constexpr int MP = Pad<M>::value;
+  constexpr int Q = (JM == 0) ? M : Dyn::QJ;
+  constexpr int QP = Pad<Q>::value;
+  constexpr int TS = 2 * M + 1;
+  constexpr int GW = WsShape<Sys, JM>::GW;
+
+  extern __shared__ double smem_d[];
+  __shared__ double s_red[3][32];
+  __shared__ double s_acc[4];
+  __shared__ double s_bc[2];
+
+  const int TM = a.TM, T = a.T, K = a.K;
+  const int C = blockDim.x >> 1;  // samples per tile
+  double* Nacc = smem_d;
+  Real* tab = reinterpret_cast<Real*>(Nacc + TM);
+  Real* sw = tab + T * TS;
+  Real* ring = sw + C;  // [slot][w][c]
+  Real* const scr = a.eps_smem ? ring + (size_t)kWsBuf * GW * C : a.eps_out + (size_t)blockIdx.x * TM * C;
+
+  grid_dep_wait();
+  grid_dep_launch();
+  LoopState* L = a.loop;
+  if (L != nullptr && L->halted) return;
+  const uint64_t iter = L ? L->iteration : (a.iteration_dev ? *a.iteration_dev : a.iteration);
+  const double* x0 = L ? L->x : a.x0;
+  if (L != nullptr && blockIdx.x == 0 && threadIdx.x == 0) L->t_start[L->step] = globaltimer();
+
+  for (int t = threadIdx.x; t < T; t += blockDim.x) {  // per-step table, as rollout_kernel
+    Real u[M];
 #pragma unroll
-    for (int u = 0; u < SPT; ++u) {
-      const bool fin = Sf[u] < r_inf<Real>();
-      const Real w = fin ? r_exp<Real>(-(Sf[u] - Real(rho_new)) * a.inv_lam) : Real(0);
-      sw[u * blockDim.x + threadIdx.x] = w;
-      z1 += double(w);
-      z2 += double(w) * double(w);
-      nf += fin ? 1.0 : 0.0;
+    for (int j = 0; j < M; ++j) {
+      Real v = Real(a.u_nom[t * M + j]);
+      if (a.has_limits) v = fmin(fmax(v, a.u_lo[j]), a.u_hi[j]);
+      u[j] = v;
     }
-    z1 = warp_sum(z1);
-    z2 = warp_sum(z2);
-    nf = warp_sum(nf);
-    __syncwarp();
-    if (lane == 0) {
-      s_red[0][warp] = z1;
-      s_red[1][warp] = z2;
-      s_red[2][warp] = nf;
+    Real uru = Real(0);
+#pragma unroll
+    for (int j = 0; j < M; ++j)
+#pragma unroll
+      for (int l = 0; l < M; ++l) uru += u[j] * a.R[j * M + l] * u[l];
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      tab[t * TS + j] = u[j] * a.dt;
+      tab[t * TS + M + 1 + j] = a.lam_sdt * u[j];
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      for (int w2 = 0; w2 < nwarps; ++w2) {
-        a1 += s_red[0][w2];
-        a2 += s_red[1][w2];
-        a3 += s_red[2][w2];
+    tab[t * TS + M] = Real(0.5) * uru * a.dt;
+  }
+  for (int r = threadIdx.x; r < TM; r += blockDim.x) Nacc[r] = 0.0;
+  if (threadIdx.x == 0) {
+    s_acc[0] = CUDART_INF;
+    s_acc[1] = 0.0;
+    s_acc[2] = 0.0;
+    s_acc[3] = 0.0;
+  }
+  __syncthreads();
+
+  const bool producer = (int)threadIdx.x >= C;
+  const int c = producer ? (int)threadIdx.x - C : (int)threadIdx.x;
+  const int G = (T + 3) >> 2;
+  const int nb = 2 * C;
+  double* const costs_out = a.costs_dev ? *a.costs_dev : a.costs;
+
+  for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+    const int base = tile * C;
+    const int kl = base + c;
+    const bool act = kl < K;
+    Real Sf = r_inf<Real>();
+    if (producer) {
+      const StreamKey sk = make_stream_key(L ? L->seed : (a.seed_dev ? *a.seed_dev : a.seed), iter);
+      const uint32_t kg = (uint32_t)(a.sample_offset + kl);
+      Real Ld[M * M], Lj[Q * Q], mu[Q];
+#pragma unroll
+      for (int i = 0; i < M * M; ++i) Ld[i] = a.Ld[i];
+#pragma unroll
+      for (int i = 0; i < Q * Q; ++i) Lj[i] = a.Lj[i];
+#pragma unroll
+      for (int i = 0; i < Q; ++i) mu[i] = a.mu_j[i];
+      const uint32_t jthr = a.jthr;
+      const Real jscale = a.jscale;
+      Real* ep = scr + c;
+      for (int g = 0; g < G; ++g) {
+        const int slot = g % kWsBuf;
+        const uint32_t t0 = (uint32_t)(4 * g);
+        float z[4 * MP], zm[4 * QP];
+        group_normals<MP>(sk, t0, kg, z);
+        bool jf[4] = {false, false, false, false};
+        if (a.jump_on) {
+          const P4 jw = draw(sk, kSlotJumpUniform, t0 >> 2, kg);
+          jf[0] = jw.x < jthr;
+          jf[1] = jw.y < jthr;
+          jf[2] = jw.z < jthr;
+          jf[3] = jw.w < jthr;
+          if (jf[0] | jf[1] | jf[2] | jf[3]) group_mark_normals<QP>(sk, t0, kg, jf, zm);  // noise.py:151-155
+        }
+        Real eps[4][M], sj[4][Q];
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+          apply_chol<M, Real>(Ld, z + s * MP, eps[s]);
+#pragma unroll
+          for (int i = 0; i < Q; ++i) sj[s][i] = Real(0);
+          if (jf[s]) {
+            Real mk[Q];
+            apply_marks<Q, Real>(Lj, mu, zm + s * QP, mk);
+            if (JM == 0) {
+#pragma unroll
+              for (int j = 0; j < M; ++j) eps[s][j] += mk[(j < Q) ? j : 0];  // noise.py:156-157
+            } else {
+#pragma unroll
+              for (int i = 0; i < Q; ++i) sj[s][i] = jscale * mk[i];
+            }
+          }
+        }
+        if (g >= kWsBuf) named_sync(1 + kWsBuf + slot, nb);  // slot drained by the consumers
+        Real* rs = ring + (size_t)slot * GW * C + c;
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+#pragma unroll
+          for (int j = 0; j < M; ++j) rs[(s * M + j) * C] = eps[s][j];
+          if (JM == 1) {
+#pragma unroll
+            for (int i = 0; i < Q; ++i) rs[(4 * M + s * Q + i) * C] = sj[s][i];
+          }
+        }
+        named_arrive(1 + slot, nb);  // slot full
+#pragma unroll
+        for (int s = 0; s < 4; ++s)
+          if ((int)t0 + s < T) {
+#pragma unroll
+            for (int j = 0; j < M; ++j) ep[(size_t)j * C] = eps[s][j];
+            ep += (size_t)M * C;
+          }
       }
-      s_acc[0] = rho_new;
-      s_acc[1] = s_acc[1] * scale_old + a1;
-      s_acc[2] = s_acc[2] * scale_old * scale_old + a2;
-      s_acc[3] += a3;
-    }
-    // N[r] += sum_k w_k eps[r, k] over the tile: warp-per-row, lanes over k.
-    // Philox: this CTA's scratch slab (rows of tileK, written above);
-    // HBM: the input tensor itself (rows of K).
-    const int nk = min(tileK, K - base);
-    const Real* src = PHILOX ? a.eps_out + (size_t)blockIdx.x * TM * tileK : a.eps_in + base;
-    const size_t rstride = PHILOX ? (size_t)tileK : (size_t)K;
-    // 4 rows per warp pass so each lane keeps ~4x(nk/32) loads in flight
-    // (the scratch / HBM rows are cold for large T*m; one row at a time was
-    // latency-bound)
-    constexpr int RPW = 4;
-    for (int r0 = warp * RPW; r0 < TM; r0 += nwarps * RPW) {
-      Real acc[RPW];
+    } else {
+      SysParams<Real> sp = a.sp;
 #pragma unroll
-      for (int i = 0; i < RPW; ++i) acc[i] = Real(0);
-      for (int kk = lane; kk < nk; kk += 32) {
-        const Real wk = sw[kk];
+      for (int i = 0; i < 10; ++i) pin(sp.mp[i]);
 #pragma unroll
-        for (int i = 0; i < RPW; ++i)
-          if (r0 + i < TM) acc[i] = fma(wk, src[(size_t)(r0 + i) * rstride + kk], acc[i]);  // 0 * inf = NaN like controller.py:78
+      for (int i = 0; i < N; ++i) {
+        pin(sp.sw[i]);
+        pin(sp.swt[i]);
       }
+      Real dt = a.dt, sdt = a.sdt, cq = a.cq;
+      pin(dt);
+      pin(sdt);
+      pin(cq);
+      Real x[N];
 #pragma unroll
-      for (int i = 0; i < RPW; ++i) {
-        const Real v = warp_sum(acc[i]);
-        if (lane == 0 && r0 + i < TM) Nacc[r0 + i] = Nacc[r0 + i] * scale_old + double(v);
+      for (int i = 0; i < N; ++i) x[i] = Real(x0[i]);
+      Real S = Real(0);
+      auto step = [&](const int t, const Real* eps, const Real* sj) {
+        const auto ax = Dyn::template aux<Real>(x, sp);
+        const Real qv = Cost::template q<Dyn, Real>(x, ax, sp);
+        const Real* st = tab + t * TS;
+        Real inc = fma(qv, dt, st[M]);
+        Real quad = eps[0] * eps[0];
+#pragma unroll
+        for (int j = 1; j < M; ++j) quad = fma(eps[j], eps[j], quad);
+#pragma unroll
+        for (int j = 0; j < M; ++j) inc = fma(st[M + 1 + j], eps[j], inc);
+        S += fma(cq, quad, inc);  // costs.py:98-111 times dt
+        Real v[M];
+#pragma unroll
+        for (int j = 0; j < M; ++j) v[j] = fma(eps[j], sdt, st[j]);
+        Dyn::template advance<Real>(x, ax, v, dt, sp);  // dynamics.py:130-135
+        if (JM == 1) {
+#pragma unroll
+          for (int i = 0; i < Q; ++i) x[Dyn::jump_row(i)] += sj[i];  // x + H (ind * mark)
+        }
+      };
+      for (int g = 0; g < G; ++g) {
+        const int slot = g % kWsBuf;
+        named_sync(1 + slot, nb);
+        const Real* rs = ring + (size_t)slot * GW * C + c;
+        Real e[4 * M], jv[(JM == 1) ? 4 * Q : 1];
+#pragma unroll
+        for (int i = 0; i < 4 * M; ++i) e[i] = rs[i * C];
+        if (JM == 1) {
+#pragma unroll
+          for (int i = 0; i < 4 * Q; ++i) jv[i] = rs[(4 * M + i) * C];
+        }
+        if (g < G - kWsBuf) named_arrive(1 + kWsBuf + slot, nb);
+        const int t0 = 4 * g;
+        if (t0 + 4 <= T) {
+#pragma unroll
+          for (int s = 0; s < 4; ++s) step(t0 + s, e + s * M, jv + (JM == 1 ? s * Q : 0));
+        } else {
+#pragma unroll
+          for (int s = 0; s < 4; ++s)
+            if (t0 + s < T) step(t0 + s, e + s * M, jv + (JM == 1 ? s * Q : 0));
+        }
       }
+      bool fin = true;
+#pragma unroll
+      for (int i = 0; i < N; ++i) fin = fin && isfinite(x[i]);
+      if (fin) {
+        const auto ax = Dyn::template aux<Real>(x, sp);
+        S += sp.term_scale * Cost::template q<Dyn, Real>(x, ax, sp);  // controller.py:155
+      } else {
+        S = r_inf<Real>();
+      }
+      if (act && costs_out) costs_out[kl] = double(S);
+      Sf = act ? S : r_inf<Real>();
     }
-    __syncthreads();
+    const int col = producer ? -1 : c;
+    tile_epilogue<Real, 1>(&Sf, &col, min(C, K - base), scr, (size_t)C, TM,
+                           a.inv_lam, sw, Nacc, s_red, s_acc, s_bc);
   }
   __syncthreads();
   double* rec = a.records + (size_t)blockIdx.x * a.rec_stride;
