@@ -28,6 +28,7 @@ import json
 import os
 import statistics
 import subprocess
+import tempfile
 import sys
 import time
 from pathlib import Path
@@ -194,7 +195,7 @@ class ClockSampler:
     def __init__(self, device):
         self.device = device
         self.proc = None
-        self.path = ROOT / "gpurun_out" / f"clocks_{os.getpid()}.csv"
+        self.path = Path(tempfile.gettempdir()) / f"jm_clocks_{os.getpid()}.csv"
 
     def __enter__(self):
         try:
@@ -233,6 +234,7 @@ class ClockSampler:
         busy = [r for r in rows if r[3] > 0] or rows
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in busy for i, v in enumerate(r[4]) if v.lower() == "active"})
+        self.path.unlink(missing_ok=True)
         return {"sm_mhz": statistics.median(r[0] for r in busy), "sm_max_mhz": max(r[1] for r in rows),
                 "reasons": reasons, "samples": len(busy), "power_w_max": max(r[2] for r in rows)}
 

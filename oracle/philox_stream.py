@@ -61,7 +61,42 @@ def box_muller(a, b):
     f = _f32_from_bits(one | (np.asarray(b, np.uint32) >> np.uint32(9))).astype(np.float64)
     ang = np.float32(f * np.float64(np.float32(6.2831853071795865)) + np.float64(np.float32(-9.4247779607693797)))
     r = np.sqrt(-2.0 * np.log(u1))
-    return r * np.cos(np.float64(ang)), r * np.sin(np.float64(ang))
+    ang = np.asarray(ang, dtype=np.float64)
+    return r * np.cos(ang), r * np.sin(ang)
+
+
+def gap_table(p: float, T: int):
+    """Survival table of the geometric jump gaps (csrc/philox.cuh slot 1, api.cu gap_table):
+    S[0] = 2^24, S[g] = floor(S[g-1] (2^24 - q) / 2^24), q = ceil(p 2^24); exact integers."""
+    q = min(int(np.ceil(p * 16777216.0)), 16777216) if p > 0 else 0
+    S = [1 << 24]
+    for _ in range(T):
+        S.append((S[-1] * ((1 << 24) - q)) >> 24)
+    return np.array(S, dtype=np.int64)
+
+
+def jump_gap(S, u24):
+    """G = max{g in [0, T] : u < S[g]} (S decreasing, S[0] = 2^24 > u)."""
+    return np.sum(np.asarray(u24, np.int64)[..., None] < S[None, 1:], axis=-1)
+
+
+def jump_events(key, k, T, p):
+    """Per-sample jump steps from the renewal clock: list over events e of
+    (event index e, step array (K,), alive mask (K,) where step < T)."""
+    S = gap_table(p, T)
+    K = k.shape[0]
+    t = np.full(K, -1, dtype=np.int64)
+    out = []
+    e = 0
+    while True:
+        w = draw(key, SLOT_JUMP_UNIFORM, np.uint32(e >> 2), k[:, 0])
+        u24 = (w[e & 3] >> np.uint32(8)).astype(np.int64)
+        t = t + 1 + jump_gap(S, u24)
+        alive = t < T
+        if not alive.any():
+            return out
+        out.append((e, t.copy(), alive))
+        e += 1
 
 
 def jump_threshold(p: float) -> int:
@@ -76,7 +111,8 @@ def device_noise(seed, iteration, K, T, m, q, Ld, Lj, mark_mean, jthr, jump_chan
     """(eps_d, ind, eps_j, eps_c) as the device sampler draws them (float64).
 
     Ld (m x m) = chol(c Sigma_D), Lj (q x q) = chol(Sigma_J), jthr from
-    jump_threshold(nu dt) (0 = no jumps)."""
+    jump_threshold(nu dt) (0 = no jumps; the renewal clock's per-step
+    probability is its quantised ceil(nu dt 2^24) / 2^24)."""
     key = stream_key(seed, iteration)
     MP = 4 if m == 3 else m
     k = (np.arange(K, dtype=np.int64) + sample_offset).astype(np.uint32)[:, None]
@@ -92,21 +128,20 @@ def device_noise(seed, iteration, K, T, m, q, Ld, Lj, mark_mean, jthr, jump_chan
     ind = np.zeros((K, T), dtype=np.int64)
     eps_j = np.zeros((K, T, q))
     if jthr:
-        ublk = np.arange((T + 3) // 4, dtype=np.uint32)[None, :]
-        uw = draw(key, SLOT_JUMP_UNIFORM, ublk, k)
-        words = np.stack(uw, axis=-1).reshape(K, -1)[:, :T]
-        ind = (words < np.uint32(jthr)).astype(np.int64)
-        rows, cols = np.nonzero(ind)
-        if rows.size:
-            # mark normals: index t*QP + i, Philox block index>>2, lane index&3
-            QP = 4 if q == 3 else q
-            idx = cols[:, None].astype(np.int64) * QP + np.arange(q)[None, :]
-            blk = (idx >> 2).astype(np.uint32)
+        # jump steps from the renewal clock; marks of event e: normals e*QP + i (slot 2)
+        p = (jthr >> 8) / 16777216.0  # the quantised per-step probability the table is built from
+        QP = 4 if q == 3 else q
+        for e, t, alive in jump_events(key, k, T, p):
+            rows = np.nonzero(alive)[0]
+            cols = t[rows]
+            ind[rows, cols] = 1
+            idx = np.int64(e * QP) + np.arange(q)[None, :]
+            blk = np.broadcast_to((idx >> 2).astype(np.uint32), (rows.size, q))
             mw = draw(key, SLOT_MARK, blk, k[rows, 0][:, None])
             a01 = box_muller(mw[0], mw[1])
             a23 = box_muller(mw[2], mw[3])
             allz = np.stack([a01[0], a01[1], a23[0], a23[1]], axis=-1)  # (events, q, 4)
-            zz = np.take_along_axis(allz, (idx & 3)[..., None], axis=-1)[..., 0]
+            zz = np.take_along_axis(allz, np.broadcast_to((idx & 3)[..., None], (rows.size, q, 1)), axis=-1)[..., 0]
             eps_j[rows, cols] = np.asarray(mark_mean, float)[:q] + zz @ np.tril(Lj).T
     eps_c = eps_d + eps_j if jump_channel == "control" else eps_d.copy()
     return eps_d, ind, eps_j, eps_c

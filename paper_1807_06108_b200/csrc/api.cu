@@ -65,6 +65,19 @@ uint32_t jump_threshold(double p) {
   return ((uint32_t)thr) << 8;
 }
 
+// Survival table of the geometric jump gaps (philox.cuh, slot 1):
+// S[0] = 2^24, S[g] = floor(S[g-1] (2^24 - q) / 2^24), q = ceil(p 2^24), g <= T;
+// *inv = 1 / log2((2^24 - q) / 2^24) for the sampler's first guess.
+std::vector<uint32_t> gap_table(double p, int T, float* inv) {
+  const double qd = p > 0.0 ? std::min(std::ceil(p * 16777216.0), 16777216.0) : 0.0;
+  const uint64_t keep = (1ull << 24) - (uint64_t)qd;
+  std::vector<uint32_t> S((size_t)T + 1, 0u);
+  S[0] = 1u << 24;
+  for (int g = 1; g <= T; ++g) S[g] = (uint32_t)(((uint64_t)S[g - 1] * keep) >> 24);
+  *inv = (float)(1.0 / std::log2((double)keep / 16777216.0));
+  return S;
+}
+
 template <typename T>
 cudaError_t dalloc(T** p, size_t count) {
   *p = nullptr;
@@ -408,11 +421,17 @@ int jm_create(const jm_model_desc* model, const jm_cost_desc* cost, const jm_mpp
 
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (e == cudaSuccess && ctx->jthr) {
+    const std::vector<uint32_t> S = gap_table(p.nu * p.dt, ctx->T, &ctx->gap_inv);
+    ctx->gap_n = (int)S.size();
+    e = cudaMalloc(&ctx->d_gap, S.size() * sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMemcpy(ctx->d_gap, S.data(), S.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
+  }
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = ctx->eng->configure(ctx);
   ctx->stream = ctx->own_stream;
   if (e == cudaSuccess && p.noise_source == JM_NOISE_PHILOX)
-    e = cudaMalloc(&ctx->d_scratch, (size_t)ctx->grid * ctx->TM * ctx->block * ctx->spt * ctx->real_size);
+    e = cudaMalloc(&ctx->d_scratch, (size_t)ctx->grid * ctx->TM * ctx->block * ctx->real_size);
   if (e == cudaSuccess) e = dalloc(&ctx->d_costs, (size_t)ctx->K);
   if (e == cudaSuccess) e = dalloc(&ctx->d_weights, (size_t)ctx->K);
   if (e == cudaSuccess) e = dalloc(&ctx->d_wsum, (size_t)(ctx->K + jm::kWThreads - 1) / jm::kWThreads);
@@ -441,6 +460,7 @@ int jm_destroy(jm_ctx* ctx) {
   if (ctx->graph) cudaGraphDestroy(ctx->graph);
   if (ctx->iter_exec) cudaGraphExecDestroy(ctx->iter_exec);
   dfree(ctx->d_scratch);
+  dfree(ctx->d_gap);
   dfree(ctx->d_hbm_eps);
   dfree(ctx->d_hbm_jump);
   dfree(ctx->d_costs);
@@ -790,8 +810,9 @@ static jm::NoiseArgs noise_args(const jm_ctx* ctx, uint64_t seed, uint64_t itera
   na.K = ctx->K;
   na.T = ctx->T;
   na.q = ctx->Q;
-  na.jthr = ctx->jthr;
   na.jump_on = ctx->jthr != 0;
+  na.gap_thr = ctx->d_gap;
+  na.gap_inv = ctx->gap_inv;
   na.sample_offset = ctx->mppi.sample_offset;
   na.seed = seed;
   na.iteration = iteration;

@@ -73,21 +73,19 @@ class Engine final : public EngineBase {
     fill_cost<R>(c->cost, N, sp);
   }
 
-  // two interleaved samples per thread for the fp32 Philox path of the small
-  // systems (more ILP at the same warp count); one elsewhere (register budget)
-  static constexpr int kSPT = 1;  // SPT=2 measured slower on the latency-bound shapes
-  template <bool PH, bool TR>
-  static constexpr int spt() {
-    return (PH && !TR) ? kSPT : 1;
-  }
-
-  size_t smem_bytes(const jm_ctx* c, int block, int spt_) const {
-    return sizeof(double) * (size_t)c->TM + sizeof(Real) * ((size_t)c->T * (2 * M + 1) + (size_t)block * spt_);
+  int q_of(const jm_ctx* c) const { return c->model.jump_channel == JM_JUMP_STATE ? Dyn::QJ : M; }
+  // dynamic smem of a rollout launch (kernels.cuh smem_plan)
+  // (jump-mark staging: 32 lanes x W steps x q per warp; marks_warps = the warps running jump windows)
+  size_t plan_bytes(const jm_ctx* c, int tile, int marks_warps, int W, int nring, bool scr) const {
+    const int nmarks = c->jthr ? marks_warps * 32 * W * q_of(c) : 0;
+    return smem_plan(c->TM, c->T * (2 * M + 1), tile, nmarks, nring, scr ? c->TM * tile : 0, c->gap_n,
+                     (int)sizeof(Real))
+        .total;
   }
 
   template <bool PH, bool TR, int JM>
   static const void* kfn() {
-    return reinterpret_cast<const void*>(&rollout_kernel<Sys, Real, PH, TR, JM, spt<PH, TR>()>);
+    return reinterpret_cast<const void*>(&rollout_kernel<Sys, Real, PH, TR, JM>);
   }
 
   template <int JM>
@@ -104,27 +102,17 @@ class Engine final : public EngineBase {
 
   // warp-specialised kernel (Philox, non-trace): block = 2 x tile
   static constexpr int kWsMaxThreads = (N <= 4) ? 1024 : 512;
-  static int ws_buf() {
-    static const int b = std::getenv("JM_WS_BUF") ? std::atoi(std::getenv("JM_WS_BUF")) : 4;
-    return b;
-  }
-  template <int JM, int B>
-  static auto ws_kern() {
-    return &rollout_kernel_ws<Sys, Real, JM, kWsMaxThreads, B>;
-  }
+  static constexpr int kWsBufs = 2;
   template <int JM>
-  static const void* ws_fn() {
-    const int b = ws_buf();
-    if (b == 2) return reinterpret_cast<const void*>(ws_kern<JM, 2>());
-    if (b == 7) return reinterpret_cast<const void*>(ws_kern<JM, 7>());
-    return reinterpret_cast<const void*>(ws_kern<JM, 4>());
+  static auto ws_kern() {
+    return &rollout_kernel_ws<Sys, Real, JM, kWsMaxThreads, kWsBufs>;
   }
-  size_t ws_smem_bytes(const jm_ctx* c, int tile) const {
+  int ws_ring(const jm_ctx* c, int tile) const {
     const int gw = (c->model.jump_channel == JM_JUMP_STATE) ? WsShape<Sys, 1>::GW : WsShape<Sys, 0>::GW;
-    return smem_bytes(c, tile, 1) + sizeof(Real) * (size_t)ws_buf() * gw * tile;
+    return kWsBufs * gw * tile;
   }
 
-  // Launch shape.  K <= num_sms * tile_max: one CTA per SM, every SM gets the
+  // Launch shape.  K <= num_sms * 512: one CTA per SM, every SM gets the
   // same sample count (a latency-bound horizon loop gains nothing from
   // stacking CTAs on few SMs).  Larger K: 256-sample tiles, grid = SMs x
   // occupancy, tiles grid-strided.  Philox path, single wave: the per-CTA
@@ -138,40 +126,41 @@ class Engine final : public EngineBase {
     static const bool no_eps_smem = std::getenv("JM_NO_EPS_SMEM") != nullptr;
     int block = c->mppi.block_threads;
     const int K = c->K, sms = c->num_sms;
-    const int sp = philox ? kSPT : 1;  // samples per thread of the main (non-trace) kernel
     if (block <= 0) {
-      if (K <= sms * kRolloutMaxThreads * sp) {
-        const int per = (K + sms * sp - 1) / (sms * sp);
+      if (K <= sms * kRolloutMaxThreads) {
+        const int per = (K + sms - 1) / sms;
         block = std::max(32, ((per + 31) / 32) * 32);
       } else {
         block = 256;
       }
     }
-    bool ws = philox && 2 * block <= kWsMaxThreads && (ws_env < 0 ? block <= kWsMaxTile : ws_env == 1);
+    const bool ws = philox && 2 * block <= kWsMaxThreads && (ws_env < 0 ? block <= kWsMaxTile : ws_env == 1);
     c->block = block;
-    c->spt = ws ? 1 : sp;
+    c->spt = 1;
     c->ws = ws;
-    // the trace / HBM kernels run one sample per thread
-    const size_t smem = smem_bytes(c, block, std::max(c->spt, 1));
+    const int threads = ws ? 2 * block : block;
+    const int nring = ws ? ws_ring(c, block) : 0;
+    const int mwarps = block / 32;  // warps running jump windows (the producers under WS)
+    int optin = 0;
+    cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device);
+    if (e != cudaSuccess) return e;
+    c->ntiles = (K + block - 1) / block;
+    // jump window: the longest (fewer window passes) whose staging fits; single
+    // wave: also keep the eps scratch in shared memory if possible
+    const size_t cap = (size_t)optin - 1024;
+    const bool single = philox && !no_eps_smem && c->ntiles <= sms;
+    const size_t budget = single ? cap : std::min(cap, (size_t)64 * 1024);
+    int W = 32;
+    while (W > 8 && plan_bytes(c, block, mwarps, W, nring, single) > budget) W >>= 1;
+    c->jw_len = W;
+    c->eps_smem = single && plan_bytes(c, block, mwarps, W, nring, true) <= cap;
+    const size_t msmem = plan_bytes(c, block, mwarps, W, nring, c->eps_smem);
+    const size_t smem = plan_bytes(c, block, mwarps, W, 0, false);  // trace / HBM kernels
     const void* fn = nullptr;
     const bool sj = c->model.jump_channel == JM_JUMP_STATE;
-    cudaError_t e = sj ? set_attrs<1>(smem, &fn, philox) : set_attrs<0>(smem, &fn, philox);
+    e = sj ? set_attrs<1>(smem, &fn, philox) : set_attrs<0>(smem, &fn, philox);
     if (e != cudaSuccess) return e;
-    int threads = block;
-    size_t msmem = smem;
-    if (ws) {
-      fn = sj ? ws_fn<1>() : ws_fn<0>();
-      threads = 2 * block;
-      msmem = ws_smem_bytes(c, block);
-    }
-    const int tile = block * c->spt;
-    c->ntiles = (K + tile - 1) / tile;
-    int optin = 0;
-    e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device);
-    if (e != cudaSuccess) return e;
-    const size_t scr = sizeof(Real) * (size_t)c->TM * tile;
-    c->eps_smem = philox && !no_eps_smem && c->ntiles <= sms && msmem + scr + 1024 <= (size_t)optin;
-    if (c->eps_smem) msmem += scr;
+    if (ws) fn = sj ? reinterpret_cast<const void*>(ws_kern<1>()) : reinterpret_cast<const void*>(ws_kern<0>());
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem);
     if (e != cudaSuccess) return e;
     int occ = 0;
@@ -211,8 +200,11 @@ class Engine final : public EngineBase {
       a.mu_j[j] = Real(c->mppi.mark_mean[j]);
     }
     a.has_limits = c->model.has_limits;
-    a.jthr = c->jthr;
     a.jump_on = c->jthr != 0;
+    a.gap_thr = c->d_gap;
+    a.gap_n = c->gap_n;
+    a.gap_inv = c->gap_inv;
+    a.jw_len = c->jw_len;
     a.jscale = Real(c->model.jump_scale_unit ? 1.0 : std::sqrt(dt));
     fill_sys<Real>(c, a.sp);
     a.seed = rc.seed;
@@ -255,23 +247,14 @@ class Engine final : public EngineBase {
   template <int JM>
   cudaError_t launch(jm_ctx* c, const RolloutArgs<Real>& a, bool philox, bool trace) {
     dim3 grid(c->grid), block(c->block);
-    if (philox && !trace && c->ws)
-    {
-      const int b = ws_buf();
-      auto k = b == 2 ? ws_kern<JM, 2>() : b == 7 ? ws_kern<JM, 7>() : ws_kern<JM, 4>();
-      return launch_pdl(k, grid, dim3(2 * c->block), c->main_smem, c->stream, a);
-    }
+    if (philox && !trace && c->ws) return launch_pdl(ws_kern<JM>(), grid, dim3(2 * c->block), c->main_smem, c->stream, a);
     if (philox && !trace)
-      return launch_pdl(rollout_kernel<Sys, Real, true, false, JM, spt<true, false>()>, grid, block, c->main_smem,
-                        c->stream, a);
-    // the one-sample-per-thread variants cover the same samples with SPT x the tiles
-    // (same grid, so the same number of per-CTA records)
+      return launch_pdl(rollout_kernel<Sys, Real, true, false, JM>, grid, block, c->main_smem, c->stream, a);
     RolloutArgs<Real> b = a;
     b.eps_smem = 0;
-    b.ntiles = (c->K + c->block - 1) / c->block;
-    if (philox) return launch_pdl(rollout_kernel<Sys, Real, true, true, JM, 1>, grid, block, c->smem, c->stream, b);
-    if (!trace) return launch_pdl(rollout_kernel<Sys, Real, false, false, JM, 1>, grid, block, c->smem, c->stream, b);
-    return launch_pdl(rollout_kernel<Sys, Real, false, true, JM, 1>, grid, block, c->smem, c->stream, b);
+    if (philox) return launch_pdl(rollout_kernel<Sys, Real, true, true, JM>, grid, block, c->smem, c->stream, b);
+    if (!trace) return launch_pdl(rollout_kernel<Sys, Real, false, false, JM>, grid, block, c->smem, c->stream, b);
+    return launch_pdl(rollout_kernel<Sys, Real, false, true, JM>, grid, block, c->smem, c->stream, b);
   }
 
   cudaError_t rollout(jm_ctx* c, const RolloutCall& rc) override {

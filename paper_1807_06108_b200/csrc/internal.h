@@ -63,6 +63,10 @@ struct jm_ctx {
   double Ld[16] = {0}, Lj[16] = {0}, Lp[16] = {0};  // chol(c Sigma_D), chol(Sigma_J), chol(Sigma_D)
   uint32_t jthr = 0;      // sampler jump threshold (0 = no jumps)
   uint32_t jthr_plant = 0;
+  uint32_t* d_gap = nullptr;  // jump-gap survival table (philox.cuh), gap_n = T + 1 entries
+  int gap_n = 0;
+  float gap_inv = 0.f;        // 1 / log2(1 - p)
+  int jw_len = 32;            // jump window of the rollout kernels (steps)
   jm::EngineBase* eng = nullptr;
   // device workspace
   void* d_scratch = nullptr;      // per-CTA eps_combined slabs (Philox mode)

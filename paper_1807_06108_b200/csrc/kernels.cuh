@@ -107,7 +107,10 @@ struct RolloutArgs {
   Real u_lo[4], u_hi[4];
   int has_limits;
   int jump_on;      // sampler draws jumps (jump_sampling_enabled && nu > 0)
-  uint32_t jthr;    // jump iff uniform word < jthr
+  const uint32_t* gap_thr;  // jump-gap survival table (philox.cuh), gap_n = T + 1 entries
+  int gap_n;
+  float gap_inv;    // 1 / log2(1 - p)
+  int jw_len;       // jump window (steps, power of two <= 32)
   Real jscale;      // state-jump scale (1 or sqrt dt)
   Real Ld[16];      // chol(c * Sigma_D), m x m row-major
   Real Lj[16];      // chol(Sigma_J), q x q row-major
@@ -141,25 +144,6 @@ __device__ __forceinline__ void group_normals(const StreamKey& sk, uint32_t t0, 
     const P4 r = draw(sk, kSlotDiffusion, (t0 * MP >> 2) + b, kg);
     box_muller(r.x, r.y, z[4 * b + 0], z[4 * b + 1]);
     box_muller(r.z, r.w, z[4 * b + 2], z[4 * b + 3]);
-  }
-}
-
-// Jump-mark normals of the group, same indexing with QP per step (slot 2);
-// only the Philox blocks that hold a jump step are drawn.
-template <int QP>
-__device__ __forceinline__ void group_mark_normals(const StreamKey& sk, uint32_t t0, uint32_t kg,
-                                                   const bool* jf, float* zm) {
-#pragma unroll
-  for (int b = 0; b < QP; ++b) {
-    bool need = false;
-#pragma unroll
-    for (int s = 0; s < 4; ++s)
-      if ((s * QP) >> 2 == b) need = need || jf[s];
-    if (need) {
-      const P4 r = draw(sk, kSlotMark, (t0 * QP >> 2) + b, kg);
-      box_muller(r.x, r.y, zm[4 * b + 0], zm[4 * b + 1]);
-      box_muller(r.z, r.w, zm[4 * b + 2], zm[4 * b + 3]);
-    }
   }
 }
 
@@ -272,41 +256,127 @@ __device__ __forceinline__ void tile_epilogue(const Real* Sf, const int* cols, i
   __syncthreads();
 }
 
+// ---------------------------------------------------------------- shared memory plan
+// One layout for both rollout kernels and the host launcher (engine.cuh):
+//   Nacc (TM doubles) | marks (nmarks Real) | step table (T*(2m+1) Real) |
+//   sw (tile Real) | ring (WS only) | eps scratch (single wave) | gap table (uint32)
+struct SmemPlan {
+  size_t nacc, marks, tab, sw, ring, scr, gap, total;
+};
+__host__ __device__ __forceinline__ size_t al16(size_t x) { return (x + 15) & ~(size_t)15; }
+__host__ __device__ __forceinline__ SmemPlan smem_plan(int TM, int tabn, int tile, int nmarks, int nring, int nscr,
+                                                       int ngap, int rs) {
+  SmemPlan p;
+  size_t o = 0;
+  p.nacc = o;
+  o = al16(o + sizeof(double) * (size_t)TM);
+  p.marks = o;
+  o = al16(o + (size_t)rs * nmarks);
+  p.tab = o;
+  o = al16(o + (size_t)rs * tabn);
+  p.sw = o;
+  o = al16(o + (size_t)rs * tile);
+  p.ring = o;
+  o = al16(o + (size_t)rs * nring);
+  p.scr = o;
+  o = al16(o + (size_t)rs * nscr);
+  p.gap = o;
+  o = al16(o + sizeof(uint32_t) * (size_t)ngap);
+  p.total = o;
+  return p;
+}
+
+// ---------------------------------------------------------------- jump windows
+// Jump events come from each sample's JumpClock (philox.cuh).  Per window of
+// W <= 32 steps a warp (a) advances every lane's clock through the window
+// (one uniform per event) into a bit mask, and (b) generates the marks of all
+// its events cooperatively: the warp's events form one list (lane-major,
+// then time order) and lane j produces entries j, j+32, ... -- the
+// Philox + Box-Muller + Cholesky work of a mark is done once, by one lane,
+// instead of by the whole warp every time any lane jumps.  Marks land in a
+// dense per-warp buffer wd[(s*Q + i)*32 + lane] (zero where no event), so a
+// step adds its staged value with one conflict-free shared-memory load and
+// no branch.  State jumps (JM = 1) are staged pre-scaled (jscale * mark).
+template <typename Real>
+__device__ __forceinline__ Real radd(Real a, Real b);  // uncontracted add / mul: every kernel
+template <>                                            // (and the oracle) rounds them alike
+__device__ __forceinline__ float radd<float>(float a, float b) { return __fadd_rn(a, b); }
+template <>
+__device__ __forceinline__ double radd<double>(double a, double b) { return __dadd_rn(a, b); }
+template <typename Real>
+__device__ __forceinline__ Real rmul(Real a, Real b);
+template <>
+__device__ __forceinline__ float rmul<float>(float a, float b) { return __fmul_rn(a, b); }
+template <>
+__device__ __forceinline__ double rmul<double>(double a, double b) { return __dmul_rn(a, b); }
+
+template <int Q, int QP, typename Real>
+__device__ __forceinline__ void mark_of(const StreamKey& sk, uint32_t kg, uint32_t e, const Real* Lj, const Real* mu,
+                                        Real* mk) {
+  float z[QP];
+  event_mark_normals<QP>(sk, kg, e, z);
+  apply_marks<Q, Real>(Lj, mu, z, mk);
+}
+
+// Called by all 32 lanes of a warp whose samples kg are consecutive by lane.
+template <int Q, int QP, int JM, typename Real>
+__device__ __forceinline__ void jump_window(JumpClock& c, int w0, int wend, int W, const StreamKey& sk, uint32_t kg,
+                                            const GapSampler& gs, const Real* Lj, const Real* mu, Real jscale,
+                                            Real* wd) {
+  const int lane = threadIdx.x & 31;
+  uint32_t mask = 0u;
+  const uint32_t e0 = c.e;
+  int n = 0;
+  while (__any_sync(0xFFFFFFFFu, c.tj < wend)) {
+    if (c.tj < wend) {
+      mask |= 1u << (c.tj - w0);
+      ++n;
+      clock_next(c, sk, kg, gs);
+    }
+  }
+  int inc = n;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+    if (lane >= o) inc += v;
+  }
+  const int off = inc - n;
+  const int tot = __shfl_sync(0xFFFFFFFFu, inc, 31);
+  __syncwarp();  // the previous window's marks have been read
+  for (int i = 0; i < W * Q; ++i) wd[i * 32 + lane] = Real(0);
+  __syncwarp();
+  for (int j0 = 0; j0 < tot; j0 += 32) {
+    const int j = j0 + lane;
+    int L = 0;  // owner lane of entry j: the last lane with off <= j
+#pragma unroll
+    for (int bb = 16; bb > 0; bb >>= 1) {
+      const int oc = __shfl_sync(0xFFFFFFFFu, off, L + bb);
+      if (oc <= j) L += bb;
+    }
+    const int k = j - __shfl_sync(0xFFFFFFFFu, off, L);
+    const uint32_t eL = __shfl_sync(0xFFFFFFFFu, e0, L) + (uint32_t)k;
+    uint32_t mL = __shfl_sync(0xFFFFFFFFu, mask, L);
+    if (j < tot) {
+      for (int r = 0; r < k; ++r) mL &= mL - 1u;  // the owner's k-th event step
+      const int s = __ffs(mL) - 1;
+      Real mk[Q];
+      mark_of<Q, QP, Real>(sk, kg - (uint32_t)lane + (uint32_t)L, eL, Lj, mu, mk);
+#pragma unroll
+      for (int i = 0; i < Q; ++i) wd[(s * Q + i) * 32 + L] = (JM == 1) ? rmul<Real>(jscale, mk[i]) : mk[i];
+    }
+  }
+  __syncwarp();
+}
+
 // ---------------------------------------------------------------- rollout
-// JM = 0: control-channel jumps (marks folded into eps_combined, q = m);
-// JM = 1: state-space jumps on Dyn::jump_row (q = Dyn::QJ, eps_combined = eps_d).
-template <class Sys, typename Real, bool PHILOX, bool TRACE, int JM, int SPT>
-__global__ void __launch_bounds__(kRolloutMaxThreads) rollout_kernel(const RolloutArgs<Real> a) {
-  using Dyn = typename Sys::Dyn;
-  using Cost = typename Sys::Cost;
-  constexpr int N = Sys::N, M = Sys::M;
-  constexpr int MP = Pad<M>::value;
-  constexpr int Q = (JM == 0) ? M : Dyn::QJ;
-  constexpr int QP = Pad<Q>::value;
+// Common prologue: per-step table (clamped u, controller.py:128, hoisted into
+//   udt = u dt, a_t = 1/2 u'Ru dt, b_t = lambda u sqrt(dt)   (costs.py:98-111 times dt)),
+// accumulator reset and the gap table copy.
+template <int M, typename Real>
+__device__ __forceinline__ void rollout_prologue(const RolloutArgs<Real>& a, Real* tab, double* Nacc, double* s_acc,
+                                                 uint32_t* S) {
   constexpr int TS = 2 * M + 1;
-
-  extern __shared__ double smem_d[];
-  __shared__ double s_red[3][32];
-  __shared__ double s_acc[4];  // rho, Z, W2, nfinite of this CTA
-  __shared__ double s_bc[2];
-
-  const int TM = a.TM, T = a.T, K = a.K;
-  double* Nacc = smem_d;
-  Real* tab = reinterpret_cast<Real*>(Nacc + TM);
-  Real* sw = tab + T * TS;
-
-  grid_dep_wait();    // u_nom / x / iteration come from the previous control step
-  grid_dep_launch();  // (after the wait: the finalize's pre-wait prologue reads the
-                      // plant state the previous finalize wrote) let the finalize
-                      // grid get resident while the horizon runs
-  LoopState* L = a.loop;
-  if (L != nullptr && L->halted) return;
-  const uint64_t iter = L ? L->iteration : (a.iteration_dev ? *a.iteration_dev : a.iteration);
-  const double* x0 = L ? L->x : a.x0;
-  if (L != nullptr && blockIdx.x == 0 && threadIdx.x == 0) L->t_start[L->step] = globaltimer();
-
-  // per-step table: clamped u (controller.py:128) hoisted into
-  //   udt = u dt, a_t = 1/2 u'Ru dt, b_t = lambda u sqrt(dt)   (costs.py:98-111 times dt)
+  const int T = a.T;
   for (int t = threadIdx.x; t < T; t += blockDim.x) {
     Real u[M];
 #pragma unroll
@@ -327,13 +397,78 @@ __global__ void __launch_bounds__(kRolloutMaxThreads) rollout_kernel(const Rollo
     }
     tab[t * TS + M] = Real(0.5) * uru * a.dt;
   }
-  for (int r = threadIdx.x; r < TM; r += blockDim.x) Nacc[r] = 0.0;
+  for (int r = threadIdx.x; r < a.TM; r += blockDim.x) Nacc[r] = 0.0;
+  for (int i = threadIdx.x; i < a.gap_n; i += blockDim.x) S[i] = a.gap_thr[i];
   if (threadIdx.x == 0) {
     s_acc[0] = CUDART_INF;
     s_acc[1] = 0.0;
     s_acc[2] = 0.0;
     s_acc[3] = 0.0;
   }
+}
+
+template <typename Real>
+__device__ __forceinline__ void write_record(const RolloutArgs<Real>& a, const double* s_acc, const double* Nacc) {
+  double* rec = a.records + (size_t)blockIdx.x * a.rec_stride;
+  if (threadIdx.x == 0) {
+    rec[0] = s_acc[0];
+    rec[1] = s_acc[1];
+    rec[2] = s_acc[2];
+    rec[3] = s_acc[3];
+  }
+  for (int r = threadIdx.x; r < a.TM; r += blockDim.x) rec[4 + r] = Nacc[r];
+}
+
+// One sample per thread.  JM = 0: control-channel jumps (marks folded into
+// eps_combined, q = m); JM = 1: state-space jumps on Dyn::jump_row (q =
+// Dyn::QJ, eps_combined = eps_d).  PHILOX: noise drawn in registers (else the
+// HBM wire format); TRACE: per-step states + divergence steps (host API).
+// (a 64-register cap via 2 blocks/SM measured slower: parameter reloads)
+template <class Sys, typename Real>
+struct RolloutMinBlocks {
+  static constexpr int value = 1;
+};
+
+template <class Sys, typename Real, bool PHILOX, bool TRACE, int JM>
+__global__ void __launch_bounds__(kRolloutMaxThreads, (RolloutMinBlocks<Sys, Real>::value))
+    rollout_kernel(const RolloutArgs<Real> a) {
+  using Dyn = typename Sys::Dyn;
+  using Cost = typename Sys::Cost;
+  constexpr int N = Sys::N, M = Sys::M;
+  constexpr int MP = Pad<M>::value;
+  constexpr int Q = (JM == 0) ? M : Dyn::QJ;
+  constexpr int QP = Pad<Q>::value;
+  constexpr int TS = 2 * M + 1;
+
+  extern __shared__ double smem_d[];
+  __shared__ double s_red[3][32];
+  __shared__ double s_acc[4];  // rho, Z, W2, nfinite of this CTA
+  __shared__ double s_bc[2];
+
+  const int TM = a.TM, T = a.T, K = a.K;
+  const int tileK = blockDim.x, nwarps = blockDim.x >> 5;
+  const bool in_smem = PHILOX && !TRACE && a.eps_smem;
+  const SmemPlan sp_ = smem_plan(TM, T * TS, tileK, a.jump_on ? nwarps * 32 * a.jw_len * Q : 0, 0,
+                                 in_smem ? TM * tileK : 0, a.gap_n, (int)sizeof(Real));
+  (void)nwarps;
+  char* const sb = reinterpret_cast<char*>(smem_d);
+  double* Nacc = reinterpret_cast<double*>(sb + sp_.nacc);
+  Real* tab = reinterpret_cast<Real*>(sb + sp_.tab);
+  Real* sw = reinterpret_cast<Real*>(sb + sp_.sw);
+  uint32_t* Sg = reinterpret_cast<uint32_t*>(sb + sp_.gap);
+  Real* const wd = reinterpret_cast<Real*>(sb + sp_.marks) + (threadIdx.x >> 5) * 32 * a.jw_len * Q;
+  Real* const scr = in_smem ? reinterpret_cast<Real*>(sb + sp_.scr) : a.eps_out + (size_t)blockIdx.x * TM * tileK;
+
+  grid_dep_wait();    // u_nom / x / iteration come from the previous control step
+  grid_dep_launch();  // (after the wait: the finalize's pre-wait prologue reads the
+                      // plant state the previous finalize wrote) let the finalize
+                      // grid get resident while the horizon runs
+  LoopState* L = a.loop;
+  if (L != nullptr && L->halted) return;
+  const uint64_t iter = L ? L->iteration : (a.iteration_dev ? *a.iteration_dev : a.iteration);
+  const double* x0 = L ? L->x : a.x0;
+  if (L != nullptr && blockIdx.x == 0 && threadIdx.x == 0) L->t_start[L->step] = globaltimer();
+  rollout_prologue<M, Real>(a, tab, Nacc, s_acc, Sg);
   __syncthreads();
 
   // loop-invariant parameters, pinned in registers
@@ -359,83 +494,40 @@ __global__ void __launch_bounds__(kRolloutMaxThreads) rollout_kernel(const Rollo
   pin(dt);
   pin(sdt);
   pin(cq);
-  const uint32_t jthr = a.jthr;
+  const GapSampler gs{Sg, T, a.gap_inv};
+  const int JW = a.jw_len;
+  const bool jumps = PHILOX && a.jump_on;
 
   const StreamKey sk = make_stream_key(L ? L->seed : (a.seed_dev ? *a.seed_dev : a.seed), iter);
   double* const costs_out = a.costs_dev ? *a.costs_dev : a.costs;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
 
-  // SPT samples per thread: sub-tile u covers columns [u*blockDim, (u+1)*blockDim)
-  // of a tile of blockDim*SPT samples; the SPT independent dynamics chains of
-  // a thread are interleaved step by step (instruction-level parallelism
-  // without more warps: a K=65536 horizon gives each SM only ~14 warps).
-  const int tileK = blockDim.x * SPT;
-  Real* const scr = (PHILOX && !TRACE && a.eps_smem) ? sw + tileK : a.eps_out + (size_t)blockIdx.x * TM * tileK;
   for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
     const int base = tile * tileK;
-    int kl[SPT];
-    bool act[SPT];
-    uint32_t kg[SPT];
-    Real* ep[SPT];  // Philox scratch: row (t*M+j) of this sample's column
-    Real x[SPT][N];
-    Real S[SPT];
-    int dstep[SPT];
+    const int kl = base + threadIdx.x;
+    const bool act = kl < K;
+    const uint32_t kg = (uint32_t)(a.sample_offset + kl);
+    Real* ep = scr + threadIdx.x;  // Philox scratch: row (t*M+j) of this sample's column
+    Real x[N];
+    Real S = Real(0);
+    int dstep = -1;
 #pragma unroll
-    for (int u = 0; u < SPT; ++u) {
-      kl[u] = base + u * blockDim.x + threadIdx.x;
-      act[u] = kl[u] < K;
-      kg[u] = (uint32_t)(a.sample_offset + kl[u]);
-      ep[u] = PHILOX ? scr + u * blockDim.x + threadIdx.x : nullptr;
-      S[u] = Real(0);
-      dstep[u] = -1;
+    for (int i = 0; i < N; ++i) x[i] = Real(x0[i]);
+    if (TRACE && act) {
 #pragma unroll
-      for (int i = 0; i < N; ++i) x[u][i] = Real(x0[i]);
-      if (TRACE && act[u]) {
-#pragma unroll
-        for (int i = 0; i < N; ++i) a.states[((size_t)kl[u] * (T + 1)) * N + i] = double(x[u][i]);
-      }
+      for (int i = 0; i < N; ++i) a.states[((size_t)kl * (T + 1)) * N + i] = double(x[i]);
     }
-    // one horizon step t (sub-step s of its 4-step group) of sample slot u
-    auto step = [&](const int u, const int t, const int s, const float* z, const float* zm, const bool* jf) {
-      Real eps[M];
-      Real sj[Q];
-#pragma unroll
-      for (int i = 0; i < Q; ++i) sj[i] = Real(0);
-      bool has_sj = false;
-      if (PHILOX) {
-        apply_chol<M, Real>(Ld, z + s * MP, eps);
-        if (jf[s]) {
-          Real mk[Q];
-          apply_marks<Q, Real>(Lj, mu, zm + s * QP, mk);
-          if (JM == 0) {
-#pragma unroll
-            for (int j = 0; j < M; ++j) eps[j] += mk[(j < Q) ? j : 0];  // eps_c = eps_d + eps_j (noise.py:156-157)
-          } else {
-#pragma unroll
-            for (int i = 0; i < Q; ++i) sj[i] = jscale * mk[i];
-            has_sj = true;
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < M; ++j) ep[u][(size_t)j * tileK] = eps[j];
-        ep[u] += (size_t)M * tileK;
-      } else {
-        // HBM wire format, prefetched one group ahead into z / zm (see below)
-#pragma unroll
-        for (int j = 0; j < M; ++j) eps[j] = Real(reinterpret_cast<const Real*>(z)[s * M + j]);
-        if (JM == 1 && a.jump_in != nullptr) {
-#pragma unroll
-          for (int i = 0; i < Q; ++i) sj[i] = jscale * reinterpret_cast<const Real*>(zm)[s * Q + i];
-          has_sj = true;
-        }
-      }
-      Real* xs = x[u];
+    JumpClock clk;
+    const Real* wl = wd + (threadIdx.x & 31);  // this lane's staged marks, advanced per step
+    if (jumps) clock_start(clk, sk, kg, gs);
+
+    // one horizon step t with its final eps_combined and state jump
+    auto step = [&](const int t, const Real* eps, const Real* sj, const bool has_sj) {
       // modified running cost on x_t (controller.py:140-142):
       // q dt + 1/2 u'Ru dt + lambda sqrt(dt) u'eps + 1/2 lambda (1-1/c) eps'eps
       // (eps'eps formed first, as costs.py:101/:514, so an overflowing eps
       // gives NaN even when c = 1)
-      const auto ax = Dyn::template aux<Real>(xs, sp);
-      const Real qv = Cost::template q<Dyn, Real>(xs, ax, sp);
+      const auto ax = Dyn::template aux<Real>(x, sp);
+      const Real qv = Cost::template q<Dyn, Real>(x, ax, sp);
       const Real* st = tab + t * TS;
       Real inc = fma(qv, dt, st[M]);
       Real quad = eps[0] * eps[0];
@@ -443,48 +535,80 @@ __global__ void __launch_bounds__(kRolloutMaxThreads) rollout_kernel(const Rollo
       for (int j = 1; j < M; ++j) quad = fma(eps[j], eps[j], quad);
 #pragma unroll
       for (int j = 0; j < M; ++j) inc = fma(st[M + 1 + j], eps[j], inc);
-      S[u] += fma(cq, quad, inc);
+      S += fma(cq, quad, inc);
       // Euler step (dynamics.py:130-135 / :115-129 with B = G)
       Real xold[N];
       if (TRACE) {
 #pragma unroll
-        for (int i = 0; i < N; ++i) xold[i] = xs[i];
+        for (int i = 0; i < N; ++i) xold[i] = x[i];
       }
       Real v[M];
 #pragma unroll
       for (int j = 0; j < M; ++j) v[j] = fma(eps[j], sdt, st[j]);
-      Dyn::template advance<Real>(xs, ax, v, dt, sp);
+      Dyn::template advance<Real>(x, ax, v, dt, sp);
       if (JM == 1 && has_sj) {
 #pragma unroll
-        for (int i = 0; i < Q; ++i) xs[Dyn::jump_row(i)] += sj[i];
+        for (int i = 0; i < Q; ++i) x[Dyn::jump_row(i)] = radd<Real>(x[Dyn::jump_row(i)], sj[i]);  // x + H (ind * mark)
       }
       if (TRACE) {
         // divergence mask, controller.py:144-151
         bool fin = true;
 #pragma unroll
-        for (int i = 0; i < N; ++i) fin = fin && isfinite(xs[i]);
-        if (dstep[u] >= 0 || !fin) {
-          if (dstep[u] < 0) dstep[u] = t;
+        for (int i = 0; i < N; ++i) fin = fin && isfinite(x[i]);
+        if (dstep >= 0 || !fin) {
+          if (dstep < 0) dstep = t;
 #pragma unroll
-          for (int i = 0; i < N; ++i) xs[i] = xold[i];
+          for (int i = 0; i < N; ++i) x[i] = xold[i];
         }
-        if (act[u]) {
+        if (act) {
 #pragma unroll
-          for (int i = 0; i < N; ++i) a.states[((size_t)kl[u] * (T + 1) + t + 1) * N + i] = double(xs[i]);
+          for (int i = 0; i < N; ++i) a.states[((size_t)kl * (T + 1) + t + 1) * N + i] = double(x[i]);
         }
       }
     };
-    // Noise of group g+1 is drawn while group g steps (software pipeline: it
-    // is independent of the state, so it fills the dynamics chains'
-    // latency); full groups carry no per-step horizon checks.
-    // HBM mode reuses the same group buffers as raw storage for the loaded
-    // noise: z holds 4 steps x M Reals of eps, zm 4 x Q Reals of jumps
+    // noise of step t (sub-step s2 of its group) from the group buffers, then the step
+    auto noisy_step = [&](const int t, const int s2, const float* zz, const float* zzm) {
+      Real eps[M];
+      Real sj[Q];
+      bool has_sj = false;
+      if (PHILOX) {
+        apply_chol<M, Real>(Ld, zz + s2 * MP, eps);
+        if (jumps) {
+          if (JM == 0) {
+#pragma unroll
+            for (int j = 0; j < M; ++j) eps[j] = radd<Real>(eps[j], wl[j * 32]);  // eps_c = eps_d + eps_j (noise.py:156-157)
+          } else {
+#pragma unroll
+            for (int i = 0; i < Q; ++i) sj[i] = wl[i * 32];  // jscale * ind * mark
+            has_sj = true;
+          }
+          wl += Q * 32;
+        }
+#pragma unroll
+        for (int j = 0; j < M; ++j) ep[(size_t)j * tileK] = eps[j];
+        ep += (size_t)M * tileK;
+      } else {
+        // HBM wire format, prefetched one group ahead into zz / zzm
+#pragma unroll
+        for (int j = 0; j < M; ++j) eps[j] = reinterpret_cast<const Real*>(zz)[s2 * M + j];
+        if (JM == 1 && a.jump_in != nullptr) {
+#pragma unroll
+          for (int i = 0; i < Q; ++i) sj[i] = jscale * reinterpret_cast<const Real*>(zzm)[s2 * Q + i];
+          has_sj = true;
+        }
+      }
+      step(t, eps, sj, has_sj);
+    };
+    // Diffusion noise of group g+1 is drawn while group g steps (software
+    // pipeline: it is independent of the state, so it fills the dynamics
+    // chain's latency); full groups carry no per-step horizon checks.  HBM
+    // mode reuses the group buffers as raw storage for the loaded noise.
     constexpr int ZW = PHILOX ? 4 * MP : (4 * M * (int)sizeof(Real) + 3) / 4;
-    constexpr int ZMW = PHILOX ? 4 * QP : (4 * Q * (int)sizeof(Real) + 3) / 4;
-    auto load_group = [&](const int u, const int g0, float* zz, float* zzm) {
+    constexpr int ZMW = (4 * Q * (int)sizeof(Real) + 3) / 4;
+    auto load_group = [&](const int g0, float* zz, float* zzm) {
       Real* ze = reinterpret_cast<Real*>(zz);
       Real* zj = reinterpret_cast<Real*>(zzm);
-      const int k = act[u] ? kl[u] : 0;
+      const int k = act ? kl : 0;
 #pragma unroll
       for (int s2 = 0; s2 < 4; ++s2) {
         const int t = min(g0 + s2, T - 1);
@@ -496,107 +620,61 @@ __global__ void __launch_bounds__(kRolloutMaxThreads) rollout_kernel(const Rollo
         }
       }
     };
-    float z[SPT][ZW];
-    float zmh[SPT][ZMW];  // HBM mode: jump rows of the current group
-    P4 jw[SPT];
-#pragma unroll
-    for (int u = 0; u < SPT; ++u) {
-      jw[u] = P4{0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
-      if (PHILOX) {
-        group_normals<MP>(sk, 0u, kg[u], z[u]);
-        if (a.jump_on) jw[u] = draw(sk, kSlotJumpUniform, 0u, kg[u]);
-      } else {
-        load_group(u, 0, z[u], zmh[u]);
-      }
-    }
+    float z[ZW];
+    float zm[ZMW];  // HBM mode: jump rows of the current group
+    if (PHILOX)
+      group_normals<MP>(sk, 0u, kg, z);
+    else
+      load_group(0, z, zm);
     for (int t0 = 0; t0 < T; t0 += 4) {
-      float zm[SPT][ZMW];
-      bool jf[SPT][4];
-#pragma unroll
-      for (int u = 0; u < SPT; ++u) {
-        jf[u][0] = jw[u].x < jthr;
-        jf[u][1] = jw[u].y < jthr;
-        jf[u][2] = jw[u].z < jthr;
-        jf[u][3] = jw[u].w < jthr;
-        if (PHILOX) {
-          if (jf[u][0] | jf[u][1] | jf[u][2] | jf[u][3])  // zero-one law jump events (noise.py:151-155)
-            group_mark_normals<QP>(sk, (uint32_t)t0, kg[u], jf[u], zm[u]);
-        } else {
-#pragma unroll
-          for (int i = 0; i < ZMW; ++i) zm[u][i] = zmh[u][i];
-        }
+      if (jumps && (t0 & (JW - 1)) == 0) {
+        jump_window<Q, QP, JM, Real>(clk, t0, min(t0 + JW, T), JW, sk, kg, gs, Lj, mu, jscale, wd);
+        wl = wd + (threadIdx.x & 31);
       }
       if (t0 + 4 <= T) {
-        float zn[SPT][ZW];
-        P4 jwn[SPT];
+        float zn[ZW], zmn[ZMW];
+        if (PHILOX)
+          group_normals<MP>(sk, (uint32_t)(t0 + 4), kg, zn);
+        else
+          load_group(t0 + 4, zn, zmn);
 #pragma unroll
-        for (int u = 0; u < SPT; ++u) {
-          jwn[u] = jw[u];
-          if (PHILOX) {
-            group_normals<MP>(sk, (uint32_t)(t0 + 4), kg[u], zn[u]);
-            if (a.jump_on) jwn[u] = draw(sk, kSlotJumpUniform, (uint32_t)((t0 + 4) >> 2), kg[u]);
-          } else {
-            load_group(u, t0 + 4, zn[u], zmh[u]);
-          }
-        }
+        for (int s2 = 0; s2 < 4; ++s2) noisy_step(t0 + s2, s2, z, zm);
 #pragma unroll
-        for (int s2 = 0; s2 < 4; ++s2)
+        for (int i = 0; i < ZW; ++i) z[i] = zn[i];
+        if (!PHILOX) {
 #pragma unroll
-          for (int u = 0; u < SPT; ++u) step(u, t0 + s2, s2, z[u], zm[u], jf[u]);
-#pragma unroll
-        for (int u = 0; u < SPT; ++u) {
-#pragma unroll
-          for (int i = 0; i < ZW; ++i) z[u][i] = zn[u][i];
-          jw[u] = jwn[u];
+          for (int i = 0; i < ZMW; ++i) zm[i] = zmn[i];
         }
       } else {
 #pragma unroll
         for (int s2 = 0; s2 < 4; ++s2)
-          if (t0 + s2 < T) {
-#pragma unroll
-            for (int u = 0; u < SPT; ++u) step(u, t0 + s2, s2, z[u], zm[u], jf[u]);
-          }
+          if (t0 + s2 < T) noisy_step(t0 + s2, s2, z, zm);
       }
     }
     // Once non-finite, an Euler state x += dx stays non-finite, so the final
     // state decides divergence (the reference checks every step).
-    Real Sf[SPT];
+    bool fin = true;
 #pragma unroll
-    for (int u = 0; u < SPT; ++u) {
-      bool fin = true;
-#pragma unroll
-      for (int i = 0; i < N; ++i) fin = fin && isfinite(x[u][i]);
-      if (TRACE) {
-        fin = dstep[u] < 0;
-        if (act[u]) a.diverged[kl[u]] = dstep[u];
-      }
-      if (fin) {
-        const auto ax = Dyn::template aux<Real>(x[u], sp);
-        S[u] += sp.term_scale * Cost::template q<Dyn, Real>(x[u], ax, sp);  // controller.py:155
-      } else {
-        S[u] = r_inf<Real>();
-      }
-      if (act[u] && costs_out) costs_out[kl[u]] = double(S[u]);
-      Sf[u] = act[u] ? S[u] : r_inf<Real>();
+    for (int i = 0; i < N; ++i) fin = fin && isfinite(x[i]);
+    if (TRACE) {
+      fin = dstep < 0;
+      if (act) a.diverged[kl] = dstep;
     }
-
+    if (fin) {
+      const auto ax = Dyn::template aux<Real>(x, sp);
+      S += sp.term_scale * Cost::template q<Dyn, Real>(x, ax, sp);  // controller.py:155
+    } else {
+      S = r_inf<Real>();
+    }
+    if (act && costs_out) costs_out[kl] = double(S);
+    const Real Sf = act ? S : r_inf<Real>();
+    const int col = threadIdx.x;
     // ---- per-CTA online softmax over this tile (K3/K4 partials) ----
-    int cols[SPT];
-#pragma unroll
-    for (int u = 0; u < SPT; ++u) cols[u] = u * blockDim.x + threadIdx.x;
-    tile_epilogue<Real, SPT>(Sf, cols, min(tileK, K - base),
-                             PHILOX ? scr : a.eps_in + base,
-                             PHILOX ? (size_t)tileK : (size_t)K, TM, a.inv_lam, sw, Nacc, s_red, s_acc, s_bc);
+    tile_epilogue<Real, 1>(&Sf, &col, min(tileK, K - base), PHILOX ? scr : a.eps_in + base,
+                           PHILOX ? (size_t)tileK : (size_t)K, TM, a.inv_lam, sw, Nacc, s_red, s_acc, s_bc);
   }
   __syncthreads();
-  double* rec = a.records + (size_t)blockIdx.x * a.rec_stride;
-  if (threadIdx.x == 0) {
-    rec[0] = s_acc[0];
-    rec[1] = s_acc[1];
-    rec[2] = s_acc[2];
-    rec[3] = s_acc[3];
-  }
-  for (int r = threadIdx.x; r < TM; r += blockDim.x) rec[4 + r] = Nacc[r];
+  write_record(a, s_acc, Nacc);
 }
 
 // ---------------------------------------------------------------- rollout, warp-specialised
@@ -606,11 +684,12 @@ __global__ void __launch_bounds__(kRolloutMaxThreads) rollout_kernel(const Rollo
 // producer writes eps_combined (and the state-jump increments, JM = 1) into
 // a shared-memory ring of NBUF slots and the eps rows into the per-CTA
 // scratch the epilogue reads; full/empty handshakes are named barriers
-// (bar.arrive / bar.sync over all 2C threads).  The split takes the ~60
-// Philox/Box-Muller/Cholesky instructions per state-step off the dynamics
-// warps, so the latency-bound horizon chains issue back to back while the
-// noise is produced in parallel on the SM's other schedulers' idle slots.
-// Same noise bits, same tiles and records as rollout_kernel<..., PHILOX, !TRACE, .., 1>.
+// (bar.arrive / bar.sync over all 2C threads).  Used for small tiles, where
+// a few warps per SM cannot hide the dynamics chain's latency: moving the
+// noise to other warps roughly doubles the warps in flight (measured: a win
+// up to ~128 samples per SM, a loss above, where the +30% instructions of
+// the hand-off dominate).  Same noise bits, same tiles and records
+// as rollout_kernel<..., PHILOX, !TRACE, ..>.
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void named_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -641,11 +720,15 @@ __global__ void __launch_bounds__(MAXT) rollout_kernel_ws(const RolloutArgs<Real
 
   const int TM = a.TM, T = a.T, K = a.K;
   const int C = blockDim.x >> 1;  // samples per tile
-  double* Nacc = smem_d;
-  Real* tab = reinterpret_cast<Real*>(Nacc + TM);
-  Real* sw = tab + T * TS;
-  Real* ring = sw + C;  // [slot][w][c]
-  Real* const scr = a.eps_smem ? ring + (size_t)kWsBuf * GW * C : a.eps_out + (size_t)blockIdx.x * TM * C;
+  const SmemPlan sp_ = smem_plan(TM, T * TS, C, a.jump_on ? (C >> 5) * 32 * a.jw_len * Q : 0, kWsBuf * GW * C,
+                                 a.eps_smem ? TM * C : 0, a.gap_n, (int)sizeof(Real));
+  char* const sb = reinterpret_cast<char*>(smem_d);
+  double* Nacc = reinterpret_cast<double*>(sb + sp_.nacc);
+  Real* tab = reinterpret_cast<Real*>(sb + sp_.tab);
+  Real* sw = reinterpret_cast<Real*>(sb + sp_.sw);
+  Real* ring = reinterpret_cast<Real*>(sb + sp_.ring);  // [slot][w][c]
+  uint32_t* Sg = reinterpret_cast<uint32_t*>(sb + sp_.gap);
+  Real* const scr = a.eps_smem ? reinterpret_cast<Real*>(sb + sp_.scr) : a.eps_out + (size_t)blockIdx.x * TM * C;
 
   grid_dep_wait();
   grid_dep_launch();
@@ -654,34 +737,7 @@ __global__ void __launch_bounds__(MAXT) rollout_kernel_ws(const RolloutArgs<Real
   const uint64_t iter = L ? L->iteration : (a.iteration_dev ? *a.iteration_dev : a.iteration);
   const double* x0 = L ? L->x : a.x0;
   if (L != nullptr && blockIdx.x == 0 && threadIdx.x == 0) L->t_start[L->step] = globaltimer();
-
-  for (int t = threadIdx.x; t < T; t += blockDim.x) {  // per-step table, as rollout_kernel
-    Real u[M];
-#pragma unroll
-    for (int j = 0; j < M; ++j) {
-      Real v = Real(a.u_nom[t * M + j]);
-      if (a.has_limits) v = fmin(fmax(v, a.u_lo[j]), a.u_hi[j]);
-      u[j] = v;
-    }
-    Real uru = Real(0);
-#pragma unroll
-    for (int j = 0; j < M; ++j)
-#pragma unroll
-      for (int l = 0; l < M; ++l) uru += u[j] * a.R[j * M + l] * u[l];
-#pragma unroll
-    for (int j = 0; j < M; ++j) {
-      tab[t * TS + j] = u[j] * a.dt;
-      tab[t * TS + M + 1 + j] = a.lam_sdt * u[j];
-    }
-    tab[t * TS + M] = Real(0.5) * uru * a.dt;
-  }
-  for (int r = threadIdx.x; r < TM; r += blockDim.x) Nacc[r] = 0.0;
-  if (threadIdx.x == 0) {
-    s_acc[0] = CUDART_INF;
-    s_acc[1] = 0.0;
-    s_acc[2] = 0.0;
-    s_acc[3] = 0.0;
-  }
+  rollout_prologue<M, Real>(a, tab, Nacc, s_acc, Sg);
   __syncthreads();
 
   const bool producer = (int)threadIdx.x >= C;
@@ -705,39 +761,39 @@ __global__ void __launch_bounds__(MAXT) rollout_kernel_ws(const RolloutArgs<Real
       for (int i = 0; i < Q * Q; ++i) Lj[i] = a.Lj[i];
 #pragma unroll
       for (int i = 0; i < Q; ++i) mu[i] = a.mu_j[i];
-      const uint32_t jthr = a.jthr;
       const Real jscale = a.jscale;
+      const GapSampler gs{Sg, T, a.gap_inv};
+      const int JW = a.jw_len;
+      const bool jumps = a.jump_on;
+      Real* const wd = reinterpret_cast<Real*>(sb + sp_.marks) + (c >> 5) * 32 * JW * Q;
       Real* ep = scr + c;
+      JumpClock clk;
+      const Real* wl = wd + (c & 31);
+      if (jumps) clock_start(clk, sk, kg, gs);
       for (int g = 0; g < G; ++g) {
         const int slot = g % kWsBuf;
-        const uint32_t t0 = (uint32_t)(4 * g);
-        float z[4 * MP], zm[4 * QP];
-        group_normals<MP>(sk, t0, kg, z);
-        bool jf[4] = {false, false, false, false};
-        if (a.jump_on) {
-          const P4 jw = draw(sk, kSlotJumpUniform, t0 >> 2, kg);
-          jf[0] = jw.x < jthr;
-          jf[1] = jw.y < jthr;
-          jf[2] = jw.z < jthr;
-          jf[3] = jw.w < jthr;
-          if (jf[0] | jf[1] | jf[2] | jf[3]) group_mark_normals<QP>(sk, t0, kg, jf, zm);  // noise.py:151-155
+        const int t0 = 4 * g;
+        if (jumps && (t0 & (JW - 1)) == 0) {
+          jump_window<Q, QP, JM, Real>(clk, t0, min(t0 + JW, T), JW, sk, kg, gs, Lj, mu, jscale, wd);
+          wl = wd + (c & 31);
         }
+        float z[4 * MP];
+        group_normals<MP>(sk, (uint32_t)t0, kg, z);
         Real eps[4][M], sj[4][Q];
 #pragma unroll
         for (int s = 0; s < 4; ++s) {
           apply_chol<M, Real>(Ld, z + s * MP, eps[s]);
 #pragma unroll
           for (int i = 0; i < Q; ++i) sj[s][i] = Real(0);
-          if (jf[s]) {
-            Real mk[Q];
-            apply_marks<Q, Real>(Lj, mu, zm + s * QP, mk);
+          if (jumps) {  // staged marks (zero where no event, and past T)
             if (JM == 0) {
 #pragma unroll
-              for (int j = 0; j < M; ++j) eps[s][j] += mk[(j < Q) ? j : 0];  // noise.py:156-157
+              for (int j = 0; j < M; ++j) eps[s][j] = radd<Real>(eps[s][j], wl[j * 32]);  // noise.py:156-157
             } else {
 #pragma unroll
-              for (int i = 0; i < Q; ++i) sj[s][i] = jscale * mk[i];
+              for (int i = 0; i < Q; ++i) sj[s][i] = wl[i * 32];
             }
+            wl += Q * 32;
           }
         }
         if (g >= kWsBuf) named_sync(1 + kWsBuf + slot, nb);  // slot drained by the consumers
@@ -754,7 +810,7 @@ __global__ void __launch_bounds__(MAXT) rollout_kernel_ws(const RolloutArgs<Real
         named_arrive(1 + slot, nb);  // slot full
 #pragma unroll
         for (int s = 0; s < 4; ++s)
-          if ((int)t0 + s < T) {
+          if (t0 + s < T) {
 #pragma unroll
             for (int j = 0; j < M; ++j) ep[(size_t)j * C] = eps[s][j];
             ep += (size_t)M * C;
@@ -794,7 +850,7 @@ __global__ void __launch_bounds__(MAXT) rollout_kernel_ws(const RolloutArgs<Real
         Dyn::template advance<Real>(x, ax, v, dt, sp);  // dynamics.py:130-135
         if (JM == 1) {
 #pragma unroll
-          for (int i = 0; i < Q; ++i) x[Dyn::jump_row(i)] += sj[i];  // x + H (ind * mark)
+          for (int i = 0; i < Q; ++i) x[Dyn::jump_row(i)] = radd<Real>(x[Dyn::jump_row(i)], sj[i]);  // x + H (ind * mark)
         }
       };
       for (int g = 0; g < G; ++g) {
@@ -832,18 +888,10 @@ __global__ void __launch_bounds__(MAXT) rollout_kernel_ws(const RolloutArgs<Real
       Sf = act ? S : r_inf<Real>();
     }
     const int col = producer ? -1 : c;
-    tile_epilogue<Real, 1>(&Sf, &col, min(C, K - base), scr, (size_t)C, TM,
-                           a.inv_lam, sw, Nacc, s_red, s_acc, s_bc);
+    tile_epilogue<Real, 1>(&Sf, &col, min(C, K - base), scr, (size_t)C, TM, a.inv_lam, sw, Nacc, s_red, s_acc, s_bc);
   }
   __syncthreads();
-  double* rec = a.records + (size_t)blockIdx.x * a.rec_stride;
-  if (threadIdx.x == 0) {
-    rec[0] = s_acc[0];
-    rec[1] = s_acc[1];
-    rec[2] = s_acc[2];
-    rec[3] = s_acc[3];
-  }
-  for (int r = threadIdx.x; r < TM; r += blockDim.x) rec[4 + r] = Nacc[r];
+  write_record(a, s_acc, Nacc);
 }
 
 // ---------------------------------------------------------------- plant + shift (closed loop)
@@ -1174,7 +1222,8 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
 // ---------------------------------------------------------------- noise (write mode)
 struct NoiseArgs {
   int K, T, q, jump_on;
-  uint32_t jthr;
+  const uint32_t* gap_thr;  // jump-gap survival table (device), T + 1 entries
+  float gap_inv;
   long long sample_offset;
   uint64_t seed, iteration;
   double Ld[16], Lj[16], mu_j[4];
@@ -1188,6 +1237,9 @@ struct NoiseArgs {
   void* jump_sm;
 };
 
+// One thread per sample, its jump clock advanced step by step (a utility
+// path: the rollout kernels use the cooperative windows instead; both give
+// the same events and marks).
 template <int M, int JM, int QJ, typename Real>
 __global__ void __launch_bounds__(256) noise_kernel(const NoiseArgs a) {
   constexpr int MP = Pad<M>::value;
@@ -1205,34 +1257,30 @@ __global__ void __launch_bounds__(256) noise_kernel(const NoiseArgs a) {
 #pragma unroll
   for (int i = 0; i < Q; ++i) mu[i] = Real(a.mu_j[i]);
   const int T = a.T, K = a.K;
+  JumpClock clk;
+  const GapSampler gs{a.gap_thr, T, a.gap_inv};
+  if (a.jump_on) clock_start(clk, sk, kg, gs);
   for (int t0 = 0; t0 < T; t0 += 4) {
     float z[4 * MP];
-    float zm[4 * QP];
-    bool jf[4] = {false, false, false, false};
     group_normals<MP>(sk, (uint32_t)t0, kg, z);
-    if (a.jump_on) {
-      const P4 jw = draw(sk, kSlotJumpUniform, (uint32_t)(t0 >> 2), kg);
-      jf[0] = jw.x < a.jthr;
-      jf[1] = jw.y < a.jthr;
-      jf[2] = jw.z < a.jthr;
-      jf[3] = jw.w < a.jthr;
-      if (jf[0] | jf[1] | jf[2] | jf[3]) group_mark_normals<QP>(sk, (uint32_t)t0, kg, jf, zm);
-    }
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
       const int t = t0 + s;
       if (t >= T) break;
       Real ed[M], ec[M], mk[Q];
       apply_chol<M, Real>(Ld, z + s * MP, ed);
-      const bool jump = jf[s];
+      const bool jump = a.jump_on && t == clk.tj;
 #pragma unroll
       for (int i = 0; i < Q; ++i) mk[i] = Real(0);
-      if (jump) apply_marks<Q, Real>(Lj, mu, zm + s * QP, mk);
+      if (jump) {
+        mark_of<Q, QP, Real>(sk, kg, clk.e, Lj, mu, mk);
+        clock_next(clk, sk, kg, gs);
+      }
 #pragma unroll
       for (int j = 0; j < M; ++j) ec[j] = ed[j];
       if (JM == 0 && jump) {
 #pragma unroll
-        for (int j = 0; j < M; ++j) ec[j] += mk[(j < Q) ? j : 0];
+        for (int j = 0; j < M; ++j) ec[j] = radd<Real>(ec[j], mk[(j < Q) ? j : 0]);
       }
       const size_t row = (size_t)kl * T + t;
       if (a.eps_d)

@@ -10,20 +10,28 @@
 //   * Gaussian draws use counter slots independent of the jump draws, so
 //     jump_sampling_enabled=False and nu=0 give bit-identical eps_d
 //     (noise.py:114-115, tests/test_noise.py:149-154, acceptance P2);
-//   * zero-one jump law: one uniform per (sample, step) vs nu*dt
-//     (noise.py:151); marks drawn only for jump events (noise.py:152-155).
+//   * zero-one jump law per (sample, step) with probability nu*dt
+//     (noise.py:151), realised as the equivalent renewal process: the gaps
+//     between jump steps are geometric, so one uniform is drawn per EVENT
+//     instead of per step (nu*dt ~ 0.01 in every BASELINE config); marks are
+//     drawn only for events (noise.py:152-155).
 //
 // Counter layout (Philox4x32-10, Salmon et al. SC'11):
 //   key  = (seed lo32, seed hi32)
 //   ctr  = (block, sample, iteration lo32, slot<<24 | iteration hi32 & 0xffffff)
 //   slot 0: diffusion normals, normal index i = t*MP + j, block = i>>2, lane = i&3
-//   slot 1: jump uniforms, block = t>>2, word = t&3, jump iff word < thr<<8
-//   slot 2: marks, normal index t*QP + i (QP = q, 3 padded to 4), block = index>>2
-//           (drawn only for 4-step groups / blocks that hold a jump event)
+//   slot 1: jump gaps, event e: word e&3 of block e>>2, u = word>>8 (24 bits);
+//           gap G_e = max{g in [0,T] : u < S[g]} with the integer survival
+//           table S[0] = 2^24, S[g] = floor(S[g-1] * (2^24 - q) / 2^24),
+//           q = ceil(nu dt 2^24) (so P(G >= g) = S[g]/2^24 = (1-p)^g up to
+//           2^-24 roundings); event steps t_0 = G_0, t_e = t_{e-1} + 1 + G_e
+//   slot 2: marks of event e, normal index e*QP + i (QP = q, 3 padded to 4),
+//           block = index>>2, lane = index&3
 //   slot 3: closed-loop plant, block = 3*step + {0 diffusion, 1 uniform, 2 marks}
 // Normals: Box-Muller on pairs of words with 23-bit mantissa uniforms.
 // The CPU emulation of this exact mapping is oracle/philox_stream.py.
 #pragma once
+#include <cmath>
 #include <cstdint>
 
 namespace jm {
@@ -72,6 +80,55 @@ __host__ __device__ __forceinline__ P4 draw(const StreamKey& s, uint32_t slot, u
   return philox4x32_10(P4{block, sample, s.c2, s.c3 | (slot << 24)}, s.k0, s.k1);
 }
 
+// Jump clock of one sample: step and index of its next jump event.
+struct JumpClock {
+  int tj;      // step of the next event (>= T: none left in the horizon)
+  uint32_t e;  // index of that event
+  P4 w;        // gap words of block e >> 2
+};
+
+__host__ __device__ __forceinline__ uint32_t p4_word(const P4& w, uint32_t i) {
+  return i == 0 ? w.x : (i == 1 ? w.y : (i == 2 ? w.z : w.w));
+}
+
+// Geometric gap G = max{g in [0, T] : u < S[g]} over the survival table
+// S[0..T].  A float estimate log2(u / 2^24) / log2(1 - p) lands on G or next
+// to it; the integer comparisons against S make the result exact (and
+// identical to the oracle's count), whatever the estimate's rounding.
+struct GapSampler {
+  const uint32_t* S;  // survival table, T + 1 entries
+  int T;
+  float inv_l2keep;   // 1 / log2(1 - p) (< 0; -0 when p = 1)
+};
+
+__host__ __device__ __forceinline__ int jump_gap(const GapSampler& gs, uint32_t u24) {
+#ifdef __CUDA_ARCH__
+  float l;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"((float)u24 + 0.5f));
+  int g = __float2int_rz((l - 24.0f) * gs.inv_l2keep);  // saturating
+#else
+  int g = (int)std::fmin((std::log2((double)u24 + 0.5) - 24.0) * gs.inv_l2keep, (double)gs.T);
+#endif
+  g = g < 0 ? 0 : (g > gs.T ? gs.T : g);
+  while (g > 0 && u24 >= gs.S[g]) --g;
+  while (g < gs.T && u24 < gs.S[g + 1]) ++g;
+  return g;
+}
+
+__host__ __device__ __forceinline__ void clock_start(JumpClock& c, const StreamKey& sk, uint32_t kg,
+                                                     const GapSampler& gs) {
+  c.e = 0;
+  c.w = draw(sk, kSlotJumpUniform, 0u, kg);
+  c.tj = jump_gap(gs, c.w.x >> 8);
+}
+
+__host__ __device__ __forceinline__ void clock_next(JumpClock& c, const StreamKey& sk, uint32_t kg,
+                                                    const GapSampler& gs) {
+  c.e += 1;
+  if ((c.e & 3u) == 0u) c.w = draw(sk, kSlotJumpUniform, c.e >> 2, kg);
+  c.tj += 1 + jump_gap(gs, p4_word(c.w, c.e & 3u) >> 8);
+}
+
 #ifdef __CUDACC__
 // Box-Muller on two words.  u1 in (0,1], angle uniform in [-pi, pi).
 // MUFU lg2/sqrt/sin/cos: noise quality only needs ~1e-6 relative accuracy;
@@ -81,13 +138,38 @@ __device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, float& z0, fl
   const float u1 = 2.0f - __uint_as_float(0x3F800000u | (a >> 9));        // (0, 1]
   const float ang = __fmaf_rn(__uint_as_float(0x3F800000u | (b >> 9)),     // [1,2) -> [-pi,pi)
                               6.2831853071795865f, -9.4247779607693797f);
-  const float rr = __fmul_rn(-1.3862943611198906f, __log2f(u1));          // -2 ln u1
-  float r;
-  asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(rr));
+  // u1 >= 2^-23 and -2 ln u1 is 0 or >= ~2e-7: no subnormal operands, so the
+  // .ftz forms are exact equivalents without the subnormal fix-up instructions
+  float l2, r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l2) : "f"(u1));
+  const float rr = __fmul_rn(-1.3862943611198906f, l2);  // -2 ln u1
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(rr));
   float sn, cs;
   __sincosf(ang, &sn, &cs);
   z0 = __fmul_rn(r, cs);
   z1 = __fmul_rn(r, sn);
+}
+
+// Mark normals of event e (QP of them, QP in {1, 2, 4}: never straddles a
+// Philox block); only the Box-Muller pair(s) holding them are evaluated.
+template <int QP>
+__device__ __forceinline__ void event_mark_normals(const StreamKey& sk, uint32_t kg, uint32_t e, float* z) {
+  const uint32_t i0 = e * QP;
+  const P4 r = draw(sk, kSlotMark, i0 >> 2, kg);
+  if (QP == 4) {
+    box_muller(r.x, r.y, z[0], z[1]);
+    box_muller(r.z, r.w, z[2], z[3]);
+  } else {
+    const bool hi = (i0 & 2u) != 0u;
+    float a, b;
+    box_muller(hi ? r.z : r.x, hi ? r.w : r.y, a, b);
+    if (QP == 2) {
+      z[0] = a;
+      z[1] = b;
+    } else {
+      z[0] = (i0 & 1u) ? b : a;
+    }
+  }
 }
 #endif
 
