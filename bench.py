@@ -315,10 +315,10 @@ def ours_arm(a):
         init()
         wbuf = np.zeros(max(1, a.warmup))
         if a.warmup:
-            ck(lib.jm_bench_loop(ctx.h, a.warmup, FLUSH_BYTES, 1, L.dptr(wbuf), None))
+            ck(lib.jm_bench_loop(ctx.h, a.warmup, FLUSH_BYTES, 2, L.dptr(wbuf), None))
         with ClockSampler(local) as clk:
             settle()
-            ck(lib.jm_bench_loop(ctx.h, a.steps, FLUSH_BYTES, 1, L.dptr(step_ms), None))
+            ck(lib.jm_bench_loop(ctx.h, a.steps, FLUSH_BYTES, 2, L.dptr(step_ms), None))
         check_running()
         # kernel-level pass: the same control steps with direct launches, events around the rollout kernel
         init()
@@ -362,7 +362,7 @@ def ours_arm(a):
                                f"{'closed-loop control step' if use_loop else 'single MPC iteration'}, "
                                f"state-space jumps, {a.noise} noise)",
                    "K": K, "T": T, "system": system, "noise": a.noise, "l2": "flushed (256 MiB memset) before each timed step",
-                   "step": "rollout+weighting/update+plant+shift (CUDA graph)" if use_loop else "rollout+weighting/update"},
+                   "step": "rollout+weighting/update+plant+shift; the K timed steps are one CUDA graph (per step: L2 flush, event, 2 kernels, event)" if use_loop else "rollout+weighting/update"},
         "mpc_iteration_latency_ms": ms,
         "roofline": roof,
         "gpu_launches": launches,

@@ -244,7 +244,9 @@ int jm_loop_finish(jm_ctx* ctx, const double* records_dev, int32_t nrec);
 /* ---- measurement helpers ---- */
 /* Time `steps` closed-loop control steps (jm_loop_init first) with CUDA events
  * on the context's stream; before each step a cudaMemsetAsync of flush_bytes
- * (> L2) evicts the L2.  use_graph=1: one graph launch per step (step_ms);
+ * (> L2) evicts the L2.  use_graph=2: all steps captured into ONE graph
+ * (flush, event, step kernels, event per step -- the device-resident loop
+ * without per-step host launches); use_graph=1: one graph launch per step;
  * use_graph=0: direct launches, step_ms and rollout_ms (the rollout kernel
  * alone).  Either output may be NULL. */
 int jm_bench_loop(jm_ctx* ctx, int32_t steps, int64_t flush_bytes, int32_t use_graph, double* step_ms,

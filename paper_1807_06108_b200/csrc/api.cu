@@ -1083,6 +1083,39 @@ int jm_bench_loop(jm_ctx* ctx, int32_t steps, int64_t flush_bytes, int32_t use_g
   cudaStream_t s = ctx->own_stream;
   std::vector<cudaEvent_t> ev(3 * (size_t)steps);
   for (auto& e : ev) CK(cudaEventCreate(&e));
+  if (use_graph == 2) {
+    // the whole timed run as ONE graph (the device-resident loop as deployed:
+    // no host launch per control step); per step: L2 flush, event, the two
+    // step kernels, event -- the flush stays outside each step's event pair
+    cudaStream_t saved = ctx->stream;
+    ctx->stream = s;
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ge = nullptr;
+    cudaError_t e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+    for (int i = 0; e == cudaSuccess && i < steps; ++i) {
+      if (flush_bytes > 0) e = cudaMemsetAsync(ctx->d_flush, i & 0xFF, (size_t)flush_bytes, s);
+      if (e == cudaSuccess) e = cudaEventRecordWithFlags(ev[3 * i], s, cudaEventRecordExternal);
+      if (e == cudaSuccess) e = loop_step_launches(ctx, nullptr);
+      if (e == cudaSuccess) e = cudaEventRecordWithFlags(ev[3 * i + 2], s, cudaEventRecordExternal);
+    }
+    const cudaError_t e2 = cudaStreamEndCapture(s, &g);
+    ctx->stream = saved;
+    if (e == cudaSuccess) e = e2;
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&ge, g, 0);
+    if (e == cudaSuccess) e = cudaGraphLaunch(ge, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (ge) cudaGraphExecDestroy(ge);
+    if (g) cudaGraphDestroy(g);
+    CK(e);
+    for (int i = 0; i < steps; ++i) {
+      float a = 0.f;
+      CK(cudaEventElapsedTime(&a, ev[3 * i], ev[3 * i + 2]));
+      if (step_ms) step_ms[i] = a;
+      if (rollout_ms) rollout_ms[i] = 0.0;
+    }
+    for (auto& ee : ev) cudaEventDestroy(ee);
+    return JM_OK;
+  }
   for (int i = 0; i < steps; ++i) {
     if (flush_bytes > 0) CK(cudaMemsetAsync(ctx->d_flush, i & 0xFF, (size_t)flush_bytes, s));
     CK(cudaEventRecord(ev[3 * i], s));

@@ -89,23 +89,29 @@ class Engine final : public EngineBase {
   }
 
   template <int JM>
-  cudaError_t set_attrs(size_t smem, const void** main_fn, bool philox) {
+  cudaError_t set_attrs(size_t smem, const void** main_fn, bool philox, bool scr_smem) {
     const void* fns[4] = {kfn<true, false, JM>(), kfn<true, true, JM>(), kfn<false, false, JM>(),
                           kfn<false, true, JM>()};
     for (const void* f : fns) {
       cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
     }
-    *main_fn = philox ? fns[0] : fns[2];
+    *main_fn = philox ? (scr_smem ? reinterpret_cast<const void*>(&rollout_kernel<Sys, Real, true, false, JM, true>)
+                                  : fns[0])
+                      : fns[2];
     return cudaSuccess;
   }
 
   // warp-specialised kernel (Philox, non-trace): block = 2 x tile
   static constexpr int kWsMaxThreads = (N <= 4) ? 1024 : 512;
   static constexpr int kWsBufs = 2;
-  template <int JM>
+  template <int JM, bool SS>
   static auto ws_kern() {
-    return &rollout_kernel_ws<Sys, Real, JM, kWsMaxThreads, kWsBufs>;
+    return &rollout_kernel_ws<Sys, Real, JM, kWsMaxThreads, kWsBufs, SS>;
+  }
+  template <int JM>
+  static const void* ws_fn(bool ss) {
+    return ss ? reinterpret_cast<const void*>(ws_kern<JM, true>()) : reinterpret_cast<const void*>(ws_kern<JM, false>());
   }
   int ws_ring(const jm_ctx* c, int tile) const {
     const int gw = (c->model.jump_channel == JM_JUMP_STATE) ? WsShape<Sys, 1>::GW : WsShape<Sys, 0>::GW;
@@ -158,9 +164,9 @@ class Engine final : public EngineBase {
     const size_t smem = plan_bytes(c, block, mwarps, W, 0, false);  // trace / HBM kernels
     const void* fn = nullptr;
     const bool sj = c->model.jump_channel == JM_JUMP_STATE;
-    e = sj ? set_attrs<1>(smem, &fn, philox) : set_attrs<0>(smem, &fn, philox);
+    e = sj ? set_attrs<1>(smem, &fn, philox, c->eps_smem) : set_attrs<0>(smem, &fn, philox, c->eps_smem);
     if (e != cudaSuccess) return e;
-    if (ws) fn = sj ? reinterpret_cast<const void*>(ws_kern<1>()) : reinterpret_cast<const void*>(ws_kern<0>());
+    if (ws) fn = sj ? ws_fn<1>(c->eps_smem) : ws_fn<0>(c->eps_smem);
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem);
     if (e != cudaSuccess) return e;
     int occ = 0;
@@ -247,7 +253,11 @@ class Engine final : public EngineBase {
   template <int JM>
   cudaError_t launch(jm_ctx* c, const RolloutArgs<Real>& a, bool philox, bool trace) {
     dim3 grid(c->grid), block(c->block);
-    if (philox && !trace && c->ws) return launch_pdl(ws_kern<JM>(), grid, dim3(2 * c->block), c->main_smem, c->stream, a);
+    if (philox && !trace && c->ws)
+      return c->eps_smem ? launch_pdl(ws_kern<JM, true>(), grid, dim3(2 * c->block), c->main_smem, c->stream, a)
+                         : launch_pdl(ws_kern<JM, false>(), grid, dim3(2 * c->block), c->main_smem, c->stream, a);
+    if (philox && !trace && c->eps_smem)
+      return launch_pdl(rollout_kernel<Sys, Real, true, false, JM, true>, grid, block, c->main_smem, c->stream, a);
     if (philox && !trace)
       return launch_pdl(rollout_kernel<Sys, Real, true, false, JM>, grid, block, c->main_smem, c->stream, a);
     RolloutArgs<Real> b = a;

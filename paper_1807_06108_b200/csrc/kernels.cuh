@@ -241,6 +241,7 @@ __device__ __forceinline__ void tile_epilogue(const Real* Sf, const int* cols, i
     Real acc[RPW];
 #pragma unroll
     for (int i = 0; i < RPW; ++i) acc[i] = Real(0);
+#pragma unroll 4
     for (int kk = lane; kk < nk; kk += 32) {
       const Real wk = sw[kk];
 #pragma unroll
@@ -429,7 +430,10 @@ struct RolloutMinBlocks {
   static constexpr int value = 1;
 };
 
-template <class Sys, typename Real, bool PHILOX, bool TRACE, int JM>
+// SCR_SMEM (Philox, non-trace, single wave): the eps scratch is a
+// shared-memory array (compile-time, so its stores / epilogue loads are
+// STS / LDS with 32-bit addresses).
+template <class Sys, typename Real, bool PHILOX, bool TRACE, int JM, bool SCR_SMEM = false>
 __global__ void __launch_bounds__(kRolloutMaxThreads, (RolloutMinBlocks<Sys, Real>::value))
     rollout_kernel(const RolloutArgs<Real> a) {
   using Dyn = typename Sys::Dyn;
@@ -447,7 +451,8 @@ __global__ void __launch_bounds__(kRolloutMaxThreads, (RolloutMinBlocks<Sys, Rea
 
   const int TM = a.TM, T = a.T, K = a.K;
   const int tileK = blockDim.x, nwarps = blockDim.x >> 5;
-  const bool in_smem = PHILOX && !TRACE && a.eps_smem;
+  static_assert(!SCR_SMEM || (PHILOX && !TRACE), "shared-memory scratch: Philox main kernel only");
+  constexpr bool in_smem = SCR_SMEM;
   const SmemPlan sp_ = smem_plan(TM, T * TS, tileK, a.jump_on ? nwarps * 32 * a.jw_len * Q : 0, 0,
                                  in_smem ? TM * tileK : 0, a.gap_n, (int)sizeof(Real));
   (void)nwarps;
@@ -702,7 +707,7 @@ struct WsShape {
   static constexpr int GW = 4 * M + (JM == 1 ? 4 * Q : 0);  // Reals per sample per group
 };
 
-template <class Sys, typename Real, int JM, int MAXT, int kWsBuf>
+template <class Sys, typename Real, int JM, int MAXT, int kWsBuf, bool SCR_SMEM>
 __global__ void __launch_bounds__(MAXT) rollout_kernel_ws(const RolloutArgs<Real> a) {
   using Dyn = typename Sys::Dyn;
   using Cost = typename Sys::Cost;
@@ -721,14 +726,14 @@ __global__ void __launch_bounds__(MAXT) rollout_kernel_ws(const RolloutArgs<Real
   const int TM = a.TM, T = a.T, K = a.K;
   const int C = blockDim.x >> 1;  // samples per tile
   const SmemPlan sp_ = smem_plan(TM, T * TS, C, a.jump_on ? (C >> 5) * 32 * a.jw_len * Q : 0, kWsBuf * GW * C,
-                                 a.eps_smem ? TM * C : 0, a.gap_n, (int)sizeof(Real));
+                                 SCR_SMEM ? TM * C : 0, a.gap_n, (int)sizeof(Real));
   char* const sb = reinterpret_cast<char*>(smem_d);
   double* Nacc = reinterpret_cast<double*>(sb + sp_.nacc);
   Real* tab = reinterpret_cast<Real*>(sb + sp_.tab);
   Real* sw = reinterpret_cast<Real*>(sb + sp_.sw);
   Real* ring = reinterpret_cast<Real*>(sb + sp_.ring);  // [slot][w][c]
   uint32_t* Sg = reinterpret_cast<uint32_t*>(sb + sp_.gap);
-  Real* const scr = a.eps_smem ? reinterpret_cast<Real*>(sb + sp_.scr) : a.eps_out + (size_t)blockIdx.x * TM * C;
+  Real* const scr = SCR_SMEM ? reinterpret_cast<Real*>(sb + sp_.scr) : a.eps_out + (size_t)blockIdx.x * TM * C;
 
   grid_dep_wait();
   grid_dep_launch();
