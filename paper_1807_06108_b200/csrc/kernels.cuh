@@ -234,9 +234,11 @@ __device__ __forceinline__ void tile_epilogue(const Real* Sf, const int* cols, i
     s_acc[2] = s_acc[2] * scale_old * scale_old + a2;
     s_acc[3] += a3;
   }
-  // N[r] += sum_k w_k eps[r, k] over the tile: warp-per-row, lanes over k;
-  // 4 rows per warp pass so each lane keeps ~4x(nk/32) loads in flight
-  constexpr int RPW = 4;
+  // N[r] += sum_k w_k eps[r, k] over the tile: a warp takes RPW rows, lanes
+  // over k (RPW x 4 independent loads in flight per lane), then one
+  // transposing butterfly reduces the RPW row partials across the lanes
+  // (9 shuffles for 8 rows instead of 40) -- fixed order, deterministic
+  constexpr int RPW = 8;
   for (int r0 = warp * RPW; r0 < TM; r0 += nwarps * RPW) {
     Real acc[RPW];
 #pragma unroll
@@ -248,11 +250,22 @@ __device__ __forceinline__ void tile_epilogue(const Real* Sf, const int* cols, i
       for (int i = 0; i < RPW; ++i)
         if (r0 + i < TM) acc[i] = fma(wk, src[(size_t)(r0 + i) * rstride + kk], acc[i]);  // 0 * inf = NaN like controller.py:78
     }
+    // stage off = 16, 8, 4: lanes split the rows (upper half of the lane bit keeps the upper rows)
 #pragma unroll
-    for (int i = 0; i < RPW; ++i) {
-      const Real v = warp_sum(acc[i]);
-      if (lane == 0 && r0 + i < TM) Nacc[r0 + i] = Nacc[r0 + i] * scale_old + double(v);
+    for (int n = RPW / 2, off = 16; n >= 1; n >>= 1, off >>= 1) {
+      const bool up = (lane & off) != 0;
+#pragma unroll
+      for (int i = 0; i < n; ++i) {
+        const Real send = up ? acc[i] : acc[i + n];
+        const Real keep = up ? acc[i + n] : acc[i];
+        acc[i] = keep + __shfl_xor_sync(0xFFFFFFFFu, send, off);
+      }
     }
+    // lanes sharing lane >> 2 now hold partials of row (lane >> 2) & 7; finish across them
+    acc[0] += __shfl_xor_sync(0xFFFFFFFFu, acc[0], 2);
+    acc[0] += __shfl_xor_sync(0xFFFFFFFFu, acc[0], 1);
+    const int row = r0 + ((lane >> 2) & (RPW - 1));
+    if ((lane & 3) == 0 && row < TM) Nacc[row] = Nacc[row] * scale_old + double(acc[0]);
   }
   __syncthreads();
 }
