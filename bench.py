@@ -61,6 +61,7 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--samples", type=int, default=None, help="override K per GPU")
     p.add_argument("--horizon", type=int, default=None, help="override T")
+    p.add_argument("--block", type=int, default=0, help="override the rollout tile (block_threads, tuning)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--profile", action="store_true", help="ncu mode: no clock settle, e2e or CPU legs")
@@ -275,7 +276,8 @@ def ours_arm(a):
     K, T = cfg.samples_m, cfg.horizon_n
     hbm = a.noise == "hbm"
     use_loop = w["loop"] and not hbm
-    ctx = engine.get_context(task.model, task.cost_model, cfg, precision=a.precision, hbm=hbm, device=local)
+    ctx = engine.get_context(task.model, task.cost_model, cfg, precision=a.precision, hbm=hbm, device=local,
+                             block_threads=a.block)
     lib = ctx.lib
     peaks = engine.microbench(local)
 

@@ -104,7 +104,7 @@ class Engine final : public EngineBase {
 
   // warp-specialised kernel (Philox, non-trace): block = 2 x tile
   static constexpr int kWsMaxThreads = (N <= 4) ? 1024 : 512;
-  static constexpr int kWsBufs = 2;
+  static constexpr int kWsBufs = 6;  // ring depth: slack for the producers' jump-window bursts
   template <int JM, bool SS>
   static auto ws_kern() {
     return &rollout_kernel_ws<Sys, Real, JM, kWsMaxThreads, kWsBufs, SS>;

@@ -180,7 +180,7 @@ struct Pad {
 // Z, sum w^2, n_finite and N[r] += sum_k w_k eps[r,k] (rescaled by
 // exp(-(rho_new - rho_acc)/lambda)).  Every thread of the CTA calls it; Sf holds
 // the thread's SPT costs (+inf for none), cols their tile columns.
-template <typename Real, int SPT>
+template <typename Real, int SPT, int RPW>
 __device__ __forceinline__ void tile_epilogue(const Real* Sf, const int* cols, int nk, const Real* src,
                                               size_t rstride, int TM, Real inv_lam, Real* sw, double* Nacc,
                                               double (*s_red)[32], double* s_acc, double* s_bc) {
@@ -235,10 +235,11 @@ __device__ __forceinline__ void tile_epilogue(const Real* Sf, const int* cols, i
     s_acc[3] += a3;
   }
   // N[r] += sum_k w_k eps[r, k] over the tile: a warp takes RPW rows, lanes
-  // over k (RPW x 4 independent loads in flight per lane), then one
+  // over k (RPW x 4 independent loads in flight per lane: 16 rows for the
+  // small systems' global scratch, whose loads are L2/HBM latency-bound; the
+  // quadrotor keeps 8, 16 spills its horizon loop), then one
   // transposing butterfly reduces the RPW row partials across the lanes
   // (9 shuffles for 8 rows instead of 40) -- fixed order, deterministic
-  constexpr int RPW = 8;
   for (int r0 = warp * RPW; r0 < TM; r0 += nwarps * RPW) {
     Real acc[RPW];
 #pragma unroll
@@ -250,7 +251,7 @@ __device__ __forceinline__ void tile_epilogue(const Real* Sf, const int* cols, i
       for (int i = 0; i < RPW; ++i)
         if (r0 + i < TM) acc[i] = fma(wk, src[(size_t)(r0 + i) * rstride + kk], acc[i]);  // 0 * inf = NaN like controller.py:78
     }
-    // stage off = 16, 8, 4: lanes split the rows (upper half of the lane bit keeps the upper rows)
+    // stages off = 16, 8, ...: lanes split the rows (the upper half of the lane bit keeps the upper rows)
 #pragma unroll
     for (int n = RPW / 2, off = 16; n >= 1; n >>= 1, off >>= 1) {
       const bool up = (lane & off) != 0;
@@ -261,11 +262,12 @@ __device__ __forceinline__ void tile_epilogue(const Real* Sf, const int* cols, i
         acc[i] = keep + __shfl_xor_sync(0xFFFFFFFFu, send, off);
       }
     }
-    // lanes sharing lane >> 2 now hold partials of row (lane >> 2) & 7; finish across them
-    acc[0] += __shfl_xor_sync(0xFFFFFFFFu, acc[0], 2);
-    acc[0] += __shfl_xor_sync(0xFFFFFFFFu, acc[0], 1);
-    const int row = r0 + ((lane >> 2) & (RPW - 1));
-    if ((lane & 3) == 0 && row < TM) Nacc[row] = Nacc[row] * scale_old + double(acc[0]);
+    // the G = 32/RPW lanes sharing lane / G hold partials of row (lane / G) % RPW; finish across them
+    constexpr int G = 32 / RPW;
+#pragma unroll
+    for (int off = G / 2; off >= 1; off >>= 1) acc[0] += __shfl_xor_sync(0xFFFFFFFFu, acc[0], off);
+    const int row = r0 + ((lane / G) & (RPW - 1));
+    if ((lane & (G - 1)) == 0 && row < TM) Nacc[row] = Nacc[row] * scale_old + double(acc[0]);
   }
   __syncthreads();
 }
@@ -688,7 +690,7 @@ __global__ void __launch_bounds__(kRolloutMaxThreads, (RolloutMinBlocks<Sys, Rea
     const Real Sf = act ? S : r_inf<Real>();
     const int col = threadIdx.x;
     // ---- per-CTA online softmax over this tile (K3/K4 partials) ----
-    tile_epilogue<Real, 1>(&Sf, &col, min(tileK, K - base), PHILOX ? scr : a.eps_in + base,
+    tile_epilogue<Real, 1, (SCR_SMEM || N > 4) ? 8 : 16>(&Sf, &col, min(tileK, K - base), PHILOX ? scr : a.eps_in + base,
                            PHILOX ? (size_t)tileK : (size_t)K, TM, a.inv_lam, sw, Nacc, s_red, s_acc, s_bc);
   }
   __syncthreads();
@@ -906,7 +908,8 @@ __global__ void __launch_bounds__(MAXT) rollout_kernel_ws(const RolloutArgs<Real
       Sf = act ? S : r_inf<Real>();
     }
     const int col = producer ? -1 : c;
-    tile_epilogue<Real, 1>(&Sf, &col, min(C, K - base), scr, (size_t)C, TM, a.inv_lam, sw, Nacc, s_red, s_acc, s_bc);
+    tile_epilogue<Real, 1, (SCR_SMEM || N > 4) ? 8 : 16>(&Sf, &col, min(C, K - base), scr, (size_t)C, TM, a.inv_lam, sw, Nacc,
+                                              s_red, s_acc, s_bc);
   }
   __syncthreads();
   write_record(a, s_acc, Nacc);
