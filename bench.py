@@ -328,14 +328,16 @@ def ours_arm(a):
             ck(lib.jm_bench_loop(ctx.h, a.warmup, FLUSH_BYTES, 0, L.dptr(wbuf), None))
         ck(lib.jm_bench_loop(ctx.h, a.steps, FLUSH_BYTES, 0, L.dptr(np.zeros(a.steps)), L.dptr(roll_ms)))
         check_running()
-        launches = 3 * a.steps
+        launches = 2 * a.steps
     else:
         wbuf = np.zeros(max(1, a.warmup))
         if a.warmup:
             ck(lib.jm_bench_iteration(ctx.h, a.warmup, FLUSH_BYTES, L.dptr(wbuf), None))
         with ClockSampler(local) as clk:
             settle()
-            ck(lib.jm_bench_iteration(ctx.h, a.steps, FLUSH_BYTES, L.dptr(step_ms), L.dptr(roll_ms)))
+            ck(lib.jm_bench_iteration(ctx.h, a.steps, FLUSH_BYTES, L.dptr(step_ms), None))
+        # kernel-level pass: events around the rollout kernel alone
+        ck(lib.jm_bench_iteration(ctx.h, a.steps, FLUSH_BYTES, L.dptr(np.zeros(a.steps)), L.dptr(roll_ms)))
         launches = 2 * a.steps
     ms = float(np.mean(step_ms))
     rms = float(np.mean(roll_ms))

@@ -253,7 +253,9 @@ int jm_bench_loop(jm_ctx* ctx, int32_t steps, int64_t flush_bytes, int32_t use_g
                   double* rollout_ms);
 /* Time `reps` device-resident iterations (rollout + finalize, no host copies)
  * from the context's current x0/u_nom; HBM mode first fills device noise
- * tensors from the Philox sampler.  iter_ms / rollout_ms per rep. */
+ * tensors from the Philox sampler.  iter_ms / rollout_ms per rep; with
+ * rollout_ms NULL no event separates the two kernels (the timed path keeps
+ * the programmatic-dependent-launch overlap). */
 int jm_bench_iteration(jm_ctx* ctx, int32_t reps, int64_t flush_bytes, double* iter_ms, double* rollout_ms);
 /* FP32 FFMA and MUFU throughput microbenchmarks (the roofline denominators
  * SURVEY 8(d) asks to measure): returns TFLOP/s and Tops/s. */

@@ -970,8 +970,10 @@ __device__ void plant_prepare(const PlantArgs& a, PlantPre& pre) {
 
 // One plant step from u_new[0] and the warm-start shift; run by one CTA after
 // u_new is complete.
+// u_src: the finished control sequence (shared memory when the finalize is a
+// single CTA, else a.u_new in global memory, read past L1).
 template <class Dyn>
-__device__ void plant_finish(const PlantArgs& a, const PlantPre& pre) {
+__device__ void plant_finish(const PlantArgs& a, const PlantPre& pre, const double* u_src, bool u_src_global) {
   constexpr int N = Dyn::N, M = Dyn::M;
   LoopState* L = a.loop;
   __shared__ int s_ok;
@@ -980,7 +982,7 @@ __device__ void plant_finish(const PlantArgs& a, const PlantPre& pre) {
     L->t_end[k] = globaltimer();
     double u0[M];
     for (int j = 0; j < M; ++j) {
-      double v = __ldcg(a.u_new + j);
+      double v = u_src_global ? __ldcg(u_src + j) : u_src[j];
       if (a.has_limits) v = fmin(fmax(v, a.u_lo[j]), a.u_hi[j]);  // harness.py:136
       u0[j] = v;
     }
@@ -1019,7 +1021,8 @@ __device__ void plant_finish(const PlantArgs& a, const PlantPre& pre) {
   if (!s_ok) return;
   const int TM = a.T * M;
   for (int i = threadIdx.x; i < TM; i += blockDim.x)
-    a.u_nom[i] = (i < TM - M) ? __ldcg(a.u_new + i + M) : L->u_init[i - (TM - M)];  // warm_start_shift
+    a.u_nom[i] = (i < TM - M) ? (u_src_global ? __ldcg(u_src + i + M) : u_src[i + M])
+                              : L->u_init[i - (TM - M)];  // warm_start_shift
   __syncthreads();
   if (threadIdx.x == 0) {
     L->iteration += 1;  // ControllerState(..., k+1, cfg) (harness.py:150)
@@ -1059,21 +1062,56 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
   double* part = fsm + a.nrec;      // [NW][kFinCols]
   __shared__ double s_red[3][NW];
   __shared__ double s_delta[kFinCols];
+  __shared__ double s_unew[kFinCols];  // this CTA's u_new columns (single CTA: the whole sequence)
   __shared__ double s_bc[4];
   __shared__ int s_last;
   __shared__ PlantPre s_pre;
   LoopState* L = a.loop;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // closed loop: LoopState reads and the plant noise do not depend on the
-  // rollout, so they run before the grid dependency resolves
+  // rollout, so they run before the grid dependency resolves; so do the
+  // nominal controls (written by the previous step's shift / the input copy,
+  // both complete before this step's rollout released us) and `halted`
   if (L != nullptr && tid == kFinThreads - 1) plant_prepare<Dyn>(p, s_pre);
+  const bool halted = L != nullptr && L->halted;
+  const int c0 = blockIdx.x * kFinCols;
+  const bool reduce_mode = a.rec_out != nullptr;
+  const double unom_c = (!reduce_mode && tid < kFinCols && c0 + tid < a.TM) ? a.u_nom[c0 + tid] : 0.0;
   grid_dep_wait();
-  if (L != nullptr && L->halted) return;
+  if (halted) return;
   const int rs = a.rec_stride;
-  // global rho (controller.py:69: min over finite costs); block reductions
-  // finish in warp 0 with shuffles (fixed order), not serial thread-0 loops
+  // the column pass below reads every record's N block: start those lines
+  // towards L1 now, under the head reductions
+  {
+    constexpr int CPL = kFinCols / 32;
+    for (int b = warp; b < a.nrec; b += NW) {
+      const double* r = a.rec + (size_t)b * rs + 4;
+#pragma unroll
+      for (int i = 0; i < CPL; ++i) {
+        const int c = c0 + lane + 32 * i;
+        if (c < a.TM && ((c & 15) == 0 || c == c0 + lane)) asm volatile("prefetch.global.L1 [%0];" ::"l"(r + c));
+      }
+    }
+  }
+  // global rho (controller.py:69: min over finite costs) and the rescaled
+  // sums in one pass over the record heads (<= 1024 records: one per thread,
+  // held in registers); block reductions finish in warp 0 with shuffles
+  // (fixed order), not serial thread-0 loops
+  double h0 = CUDART_INF, h1 = 0.0, h2 = 0.0, h3 = 0.0;
+  const bool one_pass = a.nrec <= kFinThreads;
   double m = CUDART_INF;
-  for (int b = tid; b < a.nrec; b += kFinThreads) m = fmin(m, a.rec[(size_t)b * rs]);
+  if (one_pass) {
+    if (tid < a.nrec) {
+      const double* r = a.rec + (size_t)tid * rs;
+      h0 = r[0];
+      h1 = r[1];
+      h2 = r[2];
+      h3 = r[3];
+    }
+    m = h0;
+  } else {
+    for (int b = tid; b < a.nrec; b += kFinThreads) m = fmin(m, a.rec[(size_t)b * rs]);
+  }
   m = warp_min(m);
   if (lane == 0) s_red[0][warp] = m;
   __syncthreads();
@@ -1084,13 +1122,23 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
   __syncthreads();
   const double rho = s_bc[0];
   double z = 0.0, w2 = 0.0, nf = 0.0;
-  for (int b = tid; b < a.nrec; b += kFinThreads) {
-    const double* r = a.rec + (size_t)b * rs;
-    const double e = (r[0] == CUDART_INF || rho == CUDART_INF) ? 0.0 : exp(-(r[0] - rho) * a.inv_lam);
-    se[b] = e;
-    z += r[1] * e;
-    w2 += r[2] * e * e;
-    nf += r[3];
+  if (one_pass) {
+    if (tid < a.nrec) {
+      const double e = (h0 == CUDART_INF || rho == CUDART_INF) ? 0.0 : exp(-(h0 - rho) * a.inv_lam);
+      se[tid] = e;
+      z = h1 * e;
+      w2 = h2 * e * e;
+      nf = h3;
+    }
+  } else {
+    for (int b = tid; b < a.nrec; b += kFinThreads) {
+      const double* r = a.rec + (size_t)b * rs;
+      const double e = (r[0] == CUDART_INF || rho == CUDART_INF) ? 0.0 : exp(-(r[0] - rho) * a.inv_lam);
+      se[b] = e;
+      z += r[1] * e;
+      w2 += r[2] * e * e;
+      nf += r[3];
+    }
   }
   z = warp_sum(z);
   w2 = warp_sum(w2);
@@ -1111,8 +1159,6 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
   }
   __syncthreads();
   const double Z = s_bc[1], W2 = s_bc[2], NF = s_bc[3];
-  const int c0 = blockIdx.x * kFinCols;
-  const bool reduce_mode = a.rec_out != nullptr;
   if (rho == CUDART_INF) {  // controller.py:66-67
     if (blockIdx.x == 0 && tid == 0) {
       if (a.status) *a.status = 3;  // JM_ERR_NO_VIABLE
@@ -1187,7 +1233,9 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
   __syncthreads();
   if (tid < kFinCols && c < a.TM) {
     s_delta[tid] = out;
-    a.u_new[c] = a.u_nom[c] + out;  // u_nom + delta, unclamped (controller.py:161)
+    const double un = unom_c + out;  // u_nom + delta, unclamped (controller.py:161)
+    s_unew[tid] = un;
+    a.u_new[c] = un;
   }
   __syncthreads();
   if (a.norms) {  // per_step_update_norm (controller.py:168)
@@ -1203,10 +1251,9 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
     if (a.diag) *a.diag = DiagOut{rho, Z * Z / W2, Z, (int64_t)NF};  // ESS = 1/sum w^2 (:167)
   }
   if (a.u_shift != nullptr && gridDim.x == 1) {  // warm_start_shift of this iteration's result
-    __syncthreads();
     const int TM = a.TM, Mm = a.M;
     for (int i = tid; i < TM; i += kFinThreads)
-      a.u_shift[i] = (i < TM - Mm) ? a.u_new[i + Mm] : a.u_init[i - (TM - Mm)];
+      a.u_shift[i] = (i < TM - Mm) ? s_unew[i + Mm] : a.u_init[i - (TM - Mm)];
   } else if (a.u_shift != nullptr) {
     __threadfence();
     __syncthreads();
@@ -1223,8 +1270,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
   if (L != nullptr) {
     grid_dep_launch();  // the next control step's rollout may become resident
     if (gridDim.x == 1) {
-      __syncthreads();
-      plant_finish<Dyn>(p, s_pre);
+      plant_finish<Dyn>(p, s_pre, s_unew, false);
       return;
     }
     // several CTAs: the last one to finish runs the plant step + shift
@@ -1234,7 +1280,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
     __syncthreads();
     if (s_last) {
       __threadfence();
-      plant_finish<Dyn>(p, s_pre);
+      plant_finish<Dyn>(p, s_pre, a.u_new, true);
       if (tid == 0) *a.counter = 0u;
     }
   }
