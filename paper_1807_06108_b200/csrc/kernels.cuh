@@ -393,11 +393,14 @@ __device__ __forceinline__ void rollout_prologue(const RolloutArgs<Real>& a, Rea
                                                  uint32_t* S) {
   constexpr int TS = 2 * M + 1;
   const int T = a.T;
+  // read-only (.nc) loads, unrolled: the loop's global reads are issued
+  // together instead of one round trip per iteration
+#pragma unroll 4
   for (int t = threadIdx.x; t < T; t += blockDim.x) {
     Real u[M];
 #pragma unroll
     for (int j = 0; j < M; ++j) {
-      Real v = Real(a.u_nom[t * M + j]);
+      Real v = Real(__ldg(a.u_nom + t * M + j));
       if (a.has_limits) v = fmin(fmax(v, a.u_lo[j]), a.u_hi[j]);
       u[j] = v;
     }
@@ -414,7 +417,8 @@ __device__ __forceinline__ void rollout_prologue(const RolloutArgs<Real>& a, Rea
     tab[t * TS + M] = Real(0.5) * uru * a.dt;
   }
   for (int r = threadIdx.x; r < a.TM; r += blockDim.x) Nacc[r] = 0.0;
-  for (int i = threadIdx.x; i < a.gap_n; i += blockDim.x) S[i] = a.gap_thr[i];
+#pragma unroll 4
+  for (int i = threadIdx.x; i < a.gap_n; i += blockDim.x) S[i] = __ldg(a.gap_thr + i);
   if (threadIdx.x == 0) {
     s_acc[0] = CUDART_INF;
     s_acc[1] = 0.0;
