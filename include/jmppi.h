@@ -159,6 +159,17 @@ int jm_iteration_host(jm_ctx* ctx, const double* x0, const double* u_nom, uint64
 int jm_stash_fetch(jm_ctx* ctx, uint64_t handle, double min_cost, double normaliser, double* host);
 int jm_stash_release(jm_ctx* ctx, uint64_t handle);
 
+/* The drop-in call in its compact form (jump_mppi.mppi_iteration followed by
+ * warm_start_shift, controller.py:103-181 + :96-100, Philox noise, no
+ * mapping): the same work as jm_iteration_host(..., u_init, u_shift,
+ * weights_stash) with one output block
+ *   out = [u_new (T*m) | step_norms (T) | min_cost, ess, normaliser, n_finite
+ *          (int64 bits) | status, pad (2 words) | u_shift (T*m)]
+ * (jm_dropin_doubles() doubles), so a binding passes 4 pointers. */
+int jm_iteration_dropin(jm_ctx* ctx, const double* x0, const double* u_nom, const double* u_init,
+                        uint64_t seed, uint64_t iteration, double* out, uint64_t* weights_stash);
+int64_t jm_dropin_doubles(const jm_ctx* ctx);
+
 /* Upload x0 (n) and u_nom (T*m) into the context's device inputs (used by
  * jm_bench_iteration; jm_iteration_host does this itself). */
 int jm_upload_inputs(jm_ctx* ctx, const double* x0, const double* u_nom);

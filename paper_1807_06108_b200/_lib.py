@@ -84,6 +84,8 @@ SIGNATURES = {
     "jm_iteration_host": (C.c_int, [_vp, _pd, _pd, _u64, _u64, _vp, _vp, _pd, _pd, _pd, _pd, _pd, _pd,
                                     _pi64, C.POINTER(Diag), _pd, _pd, _pu64]),
     "jm_stash_fetch": (C.c_int, [_vp, _u64, _d, _d, _pd]),
+    "jm_iteration_dropin": (C.c_int, [_vp, _vp, _vp, _vp, _u64, _u64, _vp, _vp]),
+    "jm_dropin_doubles": (C.c_int64, [_vp]),
     "jm_stash_release": (C.c_int, [_vp, _u64]),
     "jm_upload_inputs": (C.c_int, [_vp, _pd, _pd]),
     "jm_rollout_dev": (C.c_int, [_vp, _vp, _vp, _u64, _u64, _vp, _vp, _vp, _vp, _vp, _vp]),

@@ -191,6 +191,14 @@ def mppi_iteration(
             jump = np.asarray(ind, float).reshape(K, T, 1) * np.asarray(eps_j, float).reshape(K, T, q)
             jump_arg = ctx.step_major(jump, q)
     u_init = np.atleast_1d(np.asarray(cfg.u_init, dtype=float))
+    if noise is None and mapping is None and not return_rollouts:
+        # the drop-in fast path: one compact C call (jm_iteration_dropin)
+        u_new, norms, (mc, ess, z, _), u_shift, handle = ctx.iteration_dropin(
+            x0, ctrl.nominal_controls.controls, master_seed, ctrl.iteration_index, u_init)
+        new_controls = ControlSequence(u_new, cfg.dt)
+        object.__setattr__(new_controls, "_shifted", (u_init, u_shift))
+        return new_controls, UpdateDiagnostics(weights=None, min_cost=mc, effective_sample_size=ess,
+                                               per_step_update_norm=norms, _ctx=ctx, _handle=handle, _z=z)
     out = ctx.iteration(x0, ctrl.nominal_controls.controls, master_seed, ctrl.iteration_index,
                         eps_c=eps_arg, jump=jump_arg, mapping=mapping, want_costs=return_rollouts,
                         want_weights=True, trace=return_rollouts, u_init=u_init,

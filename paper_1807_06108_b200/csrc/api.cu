@@ -8,6 +8,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <vector>
+#include <atomic>
+#include <chrono>
 
 #define JM_COMMON_KERNELS
 #include "internal.h"
@@ -205,11 +207,14 @@ int stash_acquire(jm_ctx* ctx, uint64_t* handle) {
   return JM_OK;
 }
 
-// One drop-in iteration as a static CUDA graph: staged H2D of the input block,
-// rollout (per-sample costs into the stash buffer named in the block), finalize
-// (+shift), D2H of the output block; weights are formed from the stashed costs
-// when first read (jm_stash_fetch).  seed / iteration / stash pointer travel in
-// the staged block (x0 slots 13..15), so replays need no parameter updates.
+// One drop-in iteration as a static CUDA graph: a one-CTA copy of the staged
+// input block from pinned host memory (zero-copy reads), the rollout (costs
+// straight into the stash buffer named in the block), and the finalize
+// (+shift), which writes its outputs straight into the pinned host block and
+// raises a done word there last -- the host spins on that word instead of a
+// stream synchronisation.  Weights are formed from the stashed costs when
+// first read (jm_stash_fetch).  seed / iteration / stash pointer travel in the
+// staged block (x0 slots 13..15), so replays need no parameter updates.
 int capture_iteration_graph(jm_ctx* ctx) {
   if (ctx->iter_exec) return JM_OK;
   cudaStream_t saved = ctx->stream;
@@ -217,15 +222,9 @@ int capture_iteration_graph(jm_ctx* ctx) {
   double* ds = ctx->d_small;
   double* hs = ctx->h_small;
   uint64_t* words = reinterpret_cast<uint64_t*>(ds + ctx->off_x0());
-  static const bool dma = std::getenv("JM_ITER_GRAPH_DMA") != nullptr;  // experiment switch
   CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-  cudaError_t e = cudaSuccess;
-  if (dma) {
-    e = cudaMemcpyAsync(ds, hs, sizeof(double) * ctx->off_unew(), cudaMemcpyHostToDevice, ctx->stream);
-  } else {
-    jm::copy_block_kernel<<<1, 256, 0, ctx->stream>>>(hs, ds, (int)ctx->off_unew());
-    e = cudaGetLastError();
-  }
+  jm::copy_block_kernel<<<1, 256, 0, ctx->stream>>>(hs, ds, (int)ctx->off_unew());
+  cudaError_t e = cudaGetLastError();
   jm::RolloutCall rc;
   rc.x0 = ds + ctx->off_x0();
   rc.u_nom = ds + ctx->off_unom();
@@ -236,21 +235,14 @@ int capture_iteration_graph(jm_ctx* ctx) {
   if (e == cudaSuccess) {
     jm::FinArgs f = fin_args(ctx, nullptr, 0);
     f.u_nom = rc.u_nom;
-    f.u_new = ds + ctx->off_unew();
-    f.norms = ds + ctx->off_norms();
-    f.diag = ctx->d_diag();
-    f.status = ctx->d_status();
+    f.u_new = hs + ctx->off_unew();  // zero-copy outputs (UVA: pinned host memory is device-addressable)
+    f.norms = hs + ctx->off_norms();
+    f.diag = reinterpret_cast<jm::DiagOut*>(hs + ctx->off_diag());
+    f.status = reinterpret_cast<int32_t*>(hs + ctx->off_status());
     f.u_init = ds + ctx->off_uinit();
-    f.u_shift = ds + ctx->off_ushift();
+    f.u_shift = hs + ctx->off_ushift();
+    f.done = reinterpret_cast<int32_t*>(hs + ctx->off_status()) + 1;
     e = ctx->eng->finalize(ctx, f, nullptr, nullptr);
-  }
-  if (e == cudaSuccess && dma) {
-    e = cudaMemcpyAsync(hs + ctx->off_unew(), ds + ctx->off_unew(), sizeof(double) * (ctx->off_rec() - ctx->off_unew()),
-                        cudaMemcpyDeviceToHost, ctx->stream);
-  } else if (e == cudaSuccess) {
-    jm::copy_block_kernel<<<1, 256, 0, ctx->stream>>>(ds + ctx->off_unew(), hs + ctx->off_unew(),
-                                                      (int)(ctx->off_rec() - ctx->off_unew()));
-    e = cudaGetLastError();
   }
   cudaGraph_t g = nullptr;
   cudaError_t e2 = cudaStreamEndCapture(ctx->stream, &g);
@@ -260,6 +252,48 @@ int capture_iteration_graph(jm_ctx* ctx) {
   cudaError_t e3 = cudaGraphInstantiate(&ctx->iter_exec, g, 0);
   cudaGraphDestroy(g);
   CK(e3);
+  return JM_OK;
+}
+
+// The drop-in graph launch: stage the inputs in the pinned block, replay the
+// iteration graph, spin on the done word; outputs are left in the pinned block
+// (h_small from off_unew on).
+int dropin_launch(jm_ctx* ctx, const double* x0, const double* u_nom, const double* u_init, uint64_t seed,
+                  uint64_t iteration, uint64_t* weights_stash) {
+  int r = capture_iteration_graph(ctx);
+  if (r != JM_OK) return r;
+  uint64_t handle = 0;
+  r = stash_acquire(ctx, &handle);
+  if (r != JM_OK) return r;
+  double* hs = ctx->h_small;
+  std::memcpy(hs + ctx->off_x0(), x0, sizeof(double) * ctx->N);
+  std::memcpy(hs + ctx->off_unom(), u_nom, sizeof(double) * ctx->TM);
+  std::memcpy(hs + ctx->off_uinit(), u_init, sizeof(double) * ctx->M);
+  uint64_t* words = reinterpret_cast<uint64_t*>(hs + ctx->off_x0());
+  words[13] = reinterpret_cast<uint64_t>(ctx->stash[handle - 1]);
+  words[14] = seed;
+  words[15] = iteration;
+  volatile int32_t* st = reinterpret_cast<volatile int32_t*>(hs + ctx->off_status());
+  st[0] = 0;
+  st[1] = 0;  // done word, raised by the finalize after its last output
+  CK(cudaGraphLaunch(ctx->iter_exec, ctx->stream));
+  // spin on the done word (a stream synchronisation wakes the host several
+  // microseconds later); fall back to the synchronisation after 2 s so a
+  // faulting launch still reports its error
+  const auto t_spin = std::chrono::steady_clock::now();
+  while (st[1] == 0) {
+    if (std::chrono::steady_clock::now() - t_spin > std::chrono::seconds(2)) {
+      CK(cudaStreamSynchronize(ctx->stream));
+      if (st[1] == 0) return fail(ctx, JM_ERR_CUDA, "drop-in iteration graph finished without its done word");
+      break;
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+  if (st[0] == JM_ERR_NO_VIABLE) {
+    ctx->stash_free.push_back((int)handle - 1);
+    return fail(ctx, JM_ERR_NO_VIABLE, "no viable rollout");
+  }
+  *weights_stash = handle;
   return JM_OK;
 }
 
@@ -517,25 +551,8 @@ int jm_iteration_host(jm_ctx* ctx, const double* x0, const double* u_nom, uint64
   static const bool iter_graph = std::getenv("JM_NO_ITER_GRAPH") == nullptr;
   if (iter_graph && !hbm && !mapping && !costs && !weights && !states && !diverged_step && u_shift && weights_stash) {
     // the drop-in fast path: one graph launch
-    int r = capture_iteration_graph(ctx);
+    const int r = dropin_launch(ctx, x0, u_nom, u_init, seed, iteration, weights_stash);
     if (r != JM_OK) return r;
-    uint64_t handle = 0;
-    r = stash_acquire(ctx, &handle);
-    if (r != JM_OK) return r;
-    std::memcpy(hs + ctx->off_x0(), x0, sizeof(double) * N);
-    std::memcpy(hs + ctx->off_unom(), u_nom, sizeof(double) * TM);
-    std::memcpy(hs + ctx->off_uinit(), u_init, sizeof(double) * M);
-    uint64_t* words = reinterpret_cast<uint64_t*>(hs + ctx->off_x0());
-    words[13] = reinterpret_cast<uint64_t>(ctx->stash[handle - 1]);
-    words[14] = seed;
-    words[15] = iteration;
-    CK(cudaGraphLaunch(ctx->iter_exec, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-    const int32_t status = *reinterpret_cast<int32_t*>(hs + ctx->off_status());
-    if (status == JM_ERR_NO_VIABLE) {
-      ctx->stash_free.push_back((int)handle - 1);
-      return fail(ctx, JM_ERR_NO_VIABLE, "no viable rollout");
-    }
     const DiagOut* dg = reinterpret_cast<const DiagOut*>(hs + ctx->off_diag());
     std::memcpy(u_new, hs + ctx->off_unew(), sizeof(double) * TM);
     std::memcpy(u_shift, hs + ctx->off_ushift(), sizeof(double) * TM);
@@ -546,7 +563,6 @@ int jm_iteration_host(jm_ctx* ctx, const double* x0, const double* u_nom, uint64
       diag->normaliser = dg->normaliser;
       diag->n_finite = dg->n_finite;
     }
-    *weights_stash = handle;
     return JM_OK;
   }
   std::memcpy(hs + ctx->off_x0(), x0, sizeof(double) * N);
@@ -637,6 +653,19 @@ int jm_upload_inputs(jm_ctx* ctx, const double* x0, const double* u_nom) {
   CK(cudaStreamSynchronize(ctx->stream));
   return JM_OK;
 }
+
+int jm_iteration_dropin(jm_ctx* ctx, const double* x0, const double* u_nom, const double* u_init,
+                        uint64_t seed, uint64_t iteration, double* out, uint64_t* weights_stash) {
+  if (!ctx || !x0 || !u_nom || !u_init || !out || !weights_stash) return fail(ctx, JM_ERR_VALUE, "null argument");
+  if (ctx->mppi.noise_source == JM_NOISE_HBM) return fail(ctx, JM_ERR_VALUE, "HBM noise mode needs jm_iteration_host");
+  CK(cudaSetDevice(ctx->device));
+  const int r = dropin_launch(ctx, x0, u_nom, u_init, seed, iteration, weights_stash);
+  if (r != JM_OK) return r;
+  std::memcpy(out, ctx->h_small + ctx->off_unew(), sizeof(double) * (size_t)jm_dropin_doubles(ctx));
+  return JM_OK;
+}
+
+int64_t jm_dropin_doubles(const jm_ctx* ctx) { return ctx ? (int64_t)(ctx->off_rec() - ctx->off_unew()) : 0; }
 
 int jm_stash_fetch(jm_ctx* ctx, uint64_t handle, double min_cost, double normaliser, double* host) {
   if (!ctx || !host || handle == 0 || handle > ctx->stash.size()) return fail(ctx, JM_ERR_VALUE, "bad stash handle");

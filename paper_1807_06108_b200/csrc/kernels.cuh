@@ -1051,6 +1051,7 @@ struct FinArgs {
   unsigned int* counter;  // last-CTA-done counter (closed loop / shift output)
   const double* u_init;   // optional: u_shift = warm_start_shift(u_new, u_init)
   double* u_shift;
+  volatile int32_t* done; // optional: set to 1 (system-scope fence first) once every output is written
 };
 
 inline size_t finalize_smem_bytes(int nrec) {
@@ -1177,6 +1178,10 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
         a.rec_out[2] = 0.0;
         a.rec_out[3] = 0.0;
       }
+      if (a.done != nullptr) {  // the caller only reads the status in this case
+        __threadfence_system();
+        *a.done = 1;
+      }
     }
     for (int c = c0 + tid; c < min(c0 + kFinCols, a.TM); c += kFinThreads) {
       if (reduce_mode)
@@ -1258,6 +1263,13 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
     const int TM = a.TM, Mm = a.M;
     for (int i = tid; i < TM; i += kFinThreads)
       a.u_shift[i] = (i < TM - Mm) ? s_unew[i + Mm] : a.u_init[i - (TM - Mm)];
+    if (a.done != nullptr) {
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence_system();
+        *a.done = 1;
+      }
+    }
   } else if (a.u_shift != nullptr) {
     __threadfence();
     __syncthreads();
@@ -1269,6 +1281,13 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
       for (int i = tid; i < TM; i += kFinThreads)
         a.u_shift[i] = (i < TM - Mm) ? __ldcg(a.u_new + i + Mm) : a.u_init[i - (TM - Mm)];
       if (tid == 0) *a.counter = 0u;
+      if (a.done != nullptr) {
+        __syncthreads();
+        if (tid == 0) {
+          __threadfence_system();
+          *a.done = 1;
+        }
+      }
     }
   }
   if (L != nullptr) {
@@ -1419,6 +1438,7 @@ __global__ void weights_norm_kernel(const double* block_sums, int nblocks, int K
 // The drop-in graph moves its ~1-2 KB input/output blocks with one CTA reading /
 // writing pinned host memory directly (UVA) instead of DMA memcpy nodes.
 __global__ void copy_block_kernel(const double* __restrict__ src, double* __restrict__ dst, int n) {
+  grid_dep_launch();  // the rollout may launch and wait in griddepcontrol.wait meanwhile
   for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
 }
 

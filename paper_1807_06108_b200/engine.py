@@ -25,6 +25,8 @@ import numpy as np
 from . import _lib as L
 from .errors import ConfigError, ControllerError, DeviceError, NoiseError, StateDivergedError
 
+_U64 = (1 << 64) - 1
+
 _PRECISIONS = {"f32": L.JM_F32, "fp32": L.JM_F32, "float32": L.JM_F32,
                "f64": L.JM_F64, "fp64": L.JM_F64, "float64": L.JM_F64}
 
@@ -230,6 +232,11 @@ class Context:
         self.T, self.K = pdesc.horizon, pdesc.samples
         self.real = np.float64 if pdesc.precision == L.JM_F64 else np.float32
         self.hbm = pdesc.noise_source == L.JM_NOISE_HBM
+        # drop-in fast path (iteration_dropin): bound function, output size, reusable handle slot
+        self._dropin = self.lib.jm_iteration_dropin
+        self._dropin_n = int(self.lib.jm_dropin_doubles(h))
+        self._handle = C.c_uint64(0)
+        self._handle_ref = C.byref(self._handle)
 
     def close(self):
         if getattr(self, "h", None) is not None and self.h.value:
@@ -279,6 +286,23 @@ class Context:
         out.u_shift = None if u_shift is None else u_shift.reshape(self.T, self.M)
         out.stash = handle.value if stash_weights else 0
         return out
+
+    def iteration_dropin(self, x0, u_nom, seed, iteration, u_init):
+        """The drop-in call (mppi_iteration + warm_start_shift) through jm_iteration_dropin:
+        returns (u_new (T, m), norms (T,), (min_cost, ess, normaliser, n_finite), u_shift (T, m), stash)."""
+        x0 = np.ascontiguousarray(x0, dtype=float)
+        u_nom = np.ascontiguousarray(u_nom, dtype=float)
+        if x0.size != self.N or u_nom.size != self.T * self.M or u_init.size != self.M:
+            raise ValueError("x0 / u_nom / u_init shapes do not match the context")
+        TM, T = self.T * self.M, self.T
+        out = np.empty(self._dropin_n)
+        rc = self._dropin(self.h, x0.ctypes.data, u_nom.ctypes.data, u_init.ctypes.data, int(seed) & _U64,
+                          int(iteration) & _U64, out.ctypes.data, self._handle_ref)
+        self.check(rc)
+        d = out[TM + T:TM + T + 4]
+        diag = (float(d[0]), float(d[1]), float(d[2]), int(d[3:4].view(np.int64)[0]))
+        return (out[:TM].reshape(T, self.M), out[TM:TM + T], diag, out[TM + T + 6:].reshape(T, self.M),
+                self._handle.value)
 
     def stash_fetch(self, handle: int, min_cost: float, normaliser: float) -> np.ndarray:
         w = np.empty(self.K)
