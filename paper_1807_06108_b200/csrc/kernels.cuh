@@ -646,10 +646,13 @@ __global__ void __launch_bounds__(kRolloutMaxThreads, (RolloutMinBlocks<Sys, Rea
     };
     float z[ZW];
     float zm[ZMW];  // HBM mode: jump rows of the current group
-    if (PHILOX)
+    float z1[PHILOX ? 1 : ZW], zm1[PHILOX ? 1 : ZMW];  // HBM mode: the next group (loads run two groups ahead)
+    if (PHILOX) {
       group_normals<MP>(sk, 0u, kg, z);
-    else
+    } else {
       load_group(0, z, zm);
+      load_group(4, z1, zm1);
+    }
     for (int t0 = 0; t0 < T; t0 += 4) {
       if (jumps && (t0 & (JW - 1)) == 0) {
         jump_window<Q, QP, JM, Real>(clk, t0, min(t0 + JW, T), JW, sk, kg, gs, Lj, mu, jscale, wd);
@@ -660,14 +663,23 @@ __global__ void __launch_bounds__(kRolloutMaxThreads, (RolloutMinBlocks<Sys, Rea
         if (PHILOX)
           group_normals<MP>(sk, (uint32_t)(t0 + 4), kg, zn);
         else
-          load_group(t0 + 4, zn, zmn);
+          load_group(t0 + 8, zn, zmn);  // (clamped inside the horizon)
 #pragma unroll
         for (int s2 = 0; s2 < 4; ++s2) noisy_step(t0 + s2, s2, z, zm);
+        if (PHILOX) {
 #pragma unroll
-        for (int i = 0; i < ZW; ++i) z[i] = zn[i];
-        if (!PHILOX) {
+          for (int i = 0; i < ZW; ++i) z[i] = zn[i];
+        } else {
 #pragma unroll
-          for (int i = 0; i < ZMW; ++i) zm[i] = zmn[i];
+          for (int i = 0; i < ZW; ++i) {
+            z[i] = z1[i];
+            z1[i] = zn[i];
+          }
+#pragma unroll
+          for (int i = 0; i < ZMW; ++i) {
+            zm[i] = zm1[i];
+            zm1[i] = zmn[i];
+          }
         }
       } else {
 #pragma unroll
