@@ -157,7 +157,7 @@ class Engine final : public EngineBase {
     const bool single = philox && !no_eps_smem && c->ntiles <= sms;
     const size_t budget = single ? cap : std::min(cap, (size_t)64 * 1024);
     int W = 32;
-    while (W > 8 && plan_bytes(c, block, mwarps, W, nring, single) > budget) W >>= 1;
+    while (W > 8 && plan_bytes(c, block, mwarps, W, nring, single) > budget) W -= 4;
     c->jw_len = W;
     c->eps_smem = single && plan_bytes(c, block, mwarps, W, nring, true) <= cap;
     const size_t msmem = plan_bytes(c, block, mwarps, W, nring, c->eps_smem);

@@ -110,7 +110,7 @@ struct RolloutArgs {
   const uint32_t* gap_thr;  // jump-gap survival table (philox.cuh), gap_n = T + 1 entries
   int gap_n;
   float gap_inv;    // 1 / log2(1 - p)
-  int jw_len;       // jump window (steps, power of two <= 32)
+  int jw_len;       // jump window (steps, multiple of 4 in [8, 32])
   Real jscale;      // state-jump scale (1 or sqrt dt)
   Real Ld[16];      // chol(c * Sigma_D), m x m row-major
   Real Lj[16];      // chol(Sigma_J), q x q row-major
@@ -542,6 +542,7 @@ __global__ void __launch_bounds__(kRolloutMaxThreads, (RolloutMinBlocks<Sys, Rea
     }
     JumpClock clk;
     const Real* wl = wd + (threadIdx.x & 31);  // this lane's staged marks, advanced per step
+    int wnext = 0;                             // first step of the next jump window
     if (jumps) clock_start(clk, sk, kg, gs);
 
     // one horizon step t with its final eps_combined and state jump
@@ -654,8 +655,9 @@ __global__ void __launch_bounds__(kRolloutMaxThreads, (RolloutMinBlocks<Sys, Rea
       load_group(4, z1, zm1);
     }
     for (int t0 = 0; t0 < T; t0 += 4) {
-      if (jumps && (t0 & (JW - 1)) == 0) {
-        jump_window<Q, QP, JM, Real>(clk, t0, min(t0 + JW, T), JW, sk, kg, gs, Lj, mu, jscale, wd);
+      if (jumps && t0 == wnext) {
+        wnext = t0 + JW;
+        jump_window<Q, QP, JM, Real>(clk, t0, min(wnext, T), JW, sk, kg, gs, Lj, mu, jscale, wd);
         wl = wd + (threadIdx.x & 31);
       }
       if (t0 + 4 <= T) {
@@ -805,12 +807,14 @@ __global__ void __launch_bounds__(MAXT) rollout_kernel_ws(const RolloutArgs<Real
       Real* ep = scr + c;
       JumpClock clk;
       const Real* wl = wd + (c & 31);
+      int wnext = 0;
       if (jumps) clock_start(clk, sk, kg, gs);
       for (int g = 0; g < G; ++g) {
         const int slot = g % kWsBuf;
         const int t0 = 4 * g;
-        if (jumps && (t0 & (JW - 1)) == 0) {
-          jump_window<Q, QP, JM, Real>(clk, t0, min(t0 + JW, T), JW, sk, kg, gs, Lj, mu, jscale, wd);
+        if (jumps && t0 == wnext) {
+          wnext = t0 + JW;
+          jump_window<Q, QP, JM, Real>(clk, t0, min(wnext, T), JW, sk, kg, gs, Lj, mu, jscale, wd);
           wl = wd + (c & 31);
         }
         float z[4 * MP];
