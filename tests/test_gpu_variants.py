@@ -30,6 +30,6 @@ VARIANTS = {
 def test_parity_suite_under_variant(variant, gpu_device):
     env = dict(os.environ, **VARIANTS[variant])
     r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-m", "gpu", "-p", "no:cacheprovider",
-                        "tests/test_gpu_parity.py", "tests/test_gpu_api.py"],
+                        "tests/test_gpu_parity.py", "tests/test_gpu_api.py", "tests/test_gpu_edges.py"],
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
