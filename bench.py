@@ -252,6 +252,14 @@ def traffic_from_profiles(workload, precision, noise):
         return None
 
 
+def instructions_from_profiles(workload, precision, noise):
+    f = ROOT / "profiles" / "instructions.json"
+    try:
+        return json.loads(f.read_text()).get(f"{workload}/{precision}/{noise}")
+    except (ValueError, OSError):
+        return None
+
+
 def ours_arm(a):
     import ctypes as C
 
@@ -341,6 +349,7 @@ def ours_arm(a):
         launches = 2 * a.steps
     ms = float(np.mean(step_ms))
     rms = float(np.mean(roll_ms))
+    clocks = clk.summary()
     value = K * T / (ms * 1e-3)
     flops = FLOPS_PER_STATE_STEP[system] * K * T
     achieved = flops / (rms * 1e-3) / 1e12
@@ -351,6 +360,20 @@ def ours_arm(a):
             "flops_per_state_step": FLOPS_PER_STATE_STEP[system],
             "peak_source": "live FFMA microbenchmark (jm_microbench), no FP32 entry in MEASURED_PEAKS.json",
             "mufu_peak_tops": peaks["mufu_tops"], "fp64_peak_tflops": peaks["fp64_tflops"]}
+    # issue-slot view of the same kernel: warp-instructions per state-step from the
+    # committed ncu capture, and the rate at which 4 schedulers/SM issuing every
+    # cycle would retire them -- what bounds this FP32-light, latency-bound loop
+    ninst = instructions_from_profiles(a.workload, a.precision, a.noise) if a.samples is None else None
+    if ninst:
+        ips = ninst / (K * T / 32.0)
+        import torch
+        sms = torch.cuda.get_device_properties(local).multi_processor_count
+        mhz = (clocks or {}).get("sm_mhz") or 1965.0
+        ceil = sms * 4 * mhz * 1e6 * 32 / ips
+        roof["issue_slots"] = {"warp_instructions_per_state_step": ips, "ceiling_state_steps_per_s": ceil,
+                               "achieved_state_steps_per_s": K * T / (rms * 1e-3),
+                               "frac": K * T / (rms * 1e-3) / ceil,
+                               "source": "smsp__inst_executed of profiles/r1 capture; 4 issue slots/SM/cycle"}
     if hbm:
         bpss = HBM_BYTES_PER_STATE_STEP[system] * (2 if a.precision == "f64" else 1)
         gbs = bpss * K * T / (rms * 1e-3) / 1e9
@@ -371,7 +394,6 @@ def ours_arm(a):
         "roofline": roof,
         "gpu_launches": launches,
     }
-    clocks = clk.summary()
     if clocks:
         line["clocks"] = clocks
 
