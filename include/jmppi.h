@@ -252,6 +252,20 @@ int jm_loop_history(jm_ctx* ctx, int32_t steps, double* states, double* controls
 int jm_loop_rollout(jm_ctx* ctx, double* record_dev);
 int jm_loop_finish(jm_ctx* ctx, const double* records_dev, int32_t nrec);
 
+/* Batched closed-loop trials (run_batch, harness.py:197-233, with the process
+ * pool replaced by a trial dimension on the GPU): `trials` independent
+ * run_trial loops of `steps` control steps, trial b from x0[b*n..] with
+ * master seed seeds[b], all advanced by the same two launches per control
+ * step (grid.y = trial).  Each trial's outputs equal a jm_closed_loop_host
+ * run with its seed, bit for bit.  Outputs are trial-major:
+ * states (trials, steps+1, n), controls (trials, steps, m), jumps (trials,
+ * steps), step_ns (trials, steps), diverged_at / status (trials); any may be
+ * NULL.  A trial halts on its own (divergence, no viable rollout) without
+ * stopping the others. */
+int jm_batch_loop_host(jm_ctx* ctx, int32_t trials, const double* x0, const double* u_init,
+                       const uint64_t* seeds, int32_t steps, double* states, double* controls, int64_t* jumps,
+                       double* step_ns, int32_t* diverged_at, int32_t* status);
+
 /* ---- measurement helpers ---- */
 /* Time `steps` closed-loop control steps (jm_loop_init first) with CUDA events
  * on the context's stream; before each step a cudaMemsetAsync of flush_bytes

@@ -1043,6 +1043,134 @@ int jm_closed_loop_host(jm_ctx* ctx, const double* x0, const double* u_init, uin
   return JM_OK;
 }
 
+int jm_batch_loop_host(jm_ctx* ctx, int32_t trials, const double* x0, const double* u_init,
+                       const uint64_t* seeds, int32_t steps, double* states, double* controls, int64_t* jumps,
+                       double* step_ns, int32_t* diverged_at, int32_t* status) {
+  if (!ctx || !x0 || !u_init || !seeds || trials < 1 || steps < 1) return fail(ctx, JM_ERR_VALUE, "bad arguments");
+  if (ctx->mppi.noise_source != JM_NOISE_PHILOX)
+    return fail(ctx, JM_ERR_UNSUPPORTED, "the device closed loop samples its own (Philox) noise");
+  if (trials > 65535) return fail(ctx, JM_ERR_VALUE, "at most 65535 trials per batch");
+  CK(cudaSetDevice(ctx->device));
+  const int N = ctx->N, M = ctx->M, TM = ctx->TM, B = trials;
+  const size_t S = (size_t)steps;
+  // trial-major device buffers for this run
+  jm::LoopState* d_loop = nullptr;
+  double *d_unom = nullptr, *d_unew = nullptr, *d_hs = nullptr, *d_hc = nullptr, *d_rec = nullptr;
+  double* d_scr = nullptr;
+  int64_t* d_hj = nullptr;
+  uint64_t* d_ht = nullptr;
+  unsigned int* d_cnt = nullptr;
+  cudaError_t e = dalloc(reinterpret_cast<char**>(&d_loop), sizeof(jm::LoopState) * (size_t)B);
+  if (e == cudaSuccess) e = dalloc(&d_unom, (size_t)B * TM);
+  if (e == cudaSuccess) e = dalloc(&d_unew, (size_t)B * TM);
+  if (e == cudaSuccess) e = dalloc(&d_hs, (size_t)B * (S + 1) * N);
+  if (e == cudaSuccess) e = dalloc(&d_hc, (size_t)B * S * M);
+  if (e == cudaSuccess) e = dalloc(&d_hj, (size_t)B * S);
+  if (e == cudaSuccess) e = dalloc(&d_ht, (size_t)B * 2 * S);
+  if (e == cudaSuccess) e = dalloc(&d_rec, (size_t)B * ctx->grid * ctx->rec_stride);
+  if (e == cudaSuccess) e = dalloc(&d_cnt, (size_t)B);
+  if (e == cudaSuccess) e = cudaMemset(d_cnt, 0, sizeof(unsigned int) * B);
+  if (e == cudaSuccess && !ctx->eps_smem)  // global eps slabs: one set per trial
+    e = cudaMalloc(&d_scr, (size_t)B * ctx->grid * TM * ctx->block * ctx->real_size);
+  std::vector<jm::LoopState> hl((size_t)B);
+  std::vector<double> unom((size_t)B * TM), hs0((size_t)B * (S + 1) * N, 0.0);
+  for (int b = 0; b < B && e == cudaSuccess; ++b) {
+    jm::LoopState& h = hl[b];
+    h = jm::LoopState{};
+    for (int i = 0; i < N; ++i) h.x[i] = x0[(size_t)b * N + i];
+    for (int j = 0; j < M; ++j) h.u_init[j] = u_init[j];
+    h.seed = seeds[b];
+    h.iteration = 0;
+    h.max_steps = steps;
+    h.diverged_at = -1;
+    h.hist_states = d_hs + (size_t)b * (S + 1) * N;
+    h.hist_controls = d_hc + (size_t)b * S * M;
+    h.hist_jumps = d_hj + (size_t)b * S;
+    h.t_start = d_ht + (size_t)b * 2 * S;
+    h.t_end = h.t_start + S;
+    for (int t = 0; t < ctx->T; ++t)
+      for (int j = 0; j < M; ++j) unom[(size_t)b * TM + (size_t)t * M + j] = u_init[j];  // controller.py:56-59
+    for (int i = 0; i < N; ++i) hs0[(size_t)b * (S + 1) * N + i] = x0[(size_t)b * N + i];
+  }
+  cudaStream_t s = ctx->own_stream;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_loop, hl.data(), sizeof(jm::LoopState) * B, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_unom, unom.data(), sizeof(double) * unom.size(), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_hs, hs0.data(), sizeof(double) * hs0.size(), cudaMemcpyHostToDevice, s);
+  // one control step of every trial = the two loop kernels with grid.y = B, captured once
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ge = nullptr;
+  if (e == cudaSuccess) {
+    cudaStream_t saved_stream = ctx->stream;
+    double* saved_rec = ctx->d_records;
+    void* saved_scr = ctx->d_scratch;
+    ctx->stream = s;
+    ctx->d_records = d_rec;
+    if (d_scr) ctx->d_scratch = d_scr;
+    ctx->launch_trials = B;
+    e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+      jm::RolloutCall rc;
+      rc.u_nom = d_unom;
+      rc.loop = d_loop;
+      cudaError_t e1 = ctx->eng->rollout(ctx, rc);
+      if (e1 == cudaSuccess) {
+        jm::FinArgs f = fin_args(ctx, nullptr, 0);
+        f.u_nom = d_unom;
+        f.u_new = d_unew;
+        f.counter = d_cnt;
+        e1 = ctx->eng->finalize(ctx, f, d_loop, d_unom);
+      }
+      const cudaError_t e2 = cudaStreamEndCapture(s, &g);
+      e = e1 != cudaSuccess ? e1 : e2;
+    }
+    ctx->launch_trials = 1;
+    ctx->d_records = saved_rec;
+    ctx->d_scratch = saved_scr;
+    ctx->stream = saved_stream;
+  }
+  if (e == cudaSuccess) e = cudaGraphInstantiate(&ge, g, 0);
+  for (int k = 0; k < steps && e == cudaSuccess; ++k) e = cudaGraphLaunch(ge, s);
+  std::vector<double> hs((size_t)B * (S + 1) * N), hc((size_t)B * S * M);
+  std::vector<int64_t> hj((size_t)B * S);
+  std::vector<uint64_t> ht((size_t)B * 2 * S);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(hl.data(), d_loop, sizeof(jm::LoopState) * B, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(hs.data(), d_hs, sizeof(double) * hs.size(), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(hc.data(), d_hc, sizeof(double) * hc.size(), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(hj.data(), d_hj, sizeof(int64_t) * hj.size(), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(ht.data(), d_ht, sizeof(uint64_t) * ht.size(), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (ge) cudaGraphExecDestroy(ge);
+  if (g) cudaGraphDestroy(g);
+  for (void* ptr : {(void*)d_loop, (void*)d_unom, (void*)d_unew, (void*)d_hs, (void*)d_hc, (void*)d_hj, (void*)d_ht,
+                    (void*)d_rec, (void*)d_cnt, (void*)d_scr})
+    dfree(ptr);
+  CK(e);
+  // per trial: the reference's post-divergence fill (harness.py:144-148), as jm_closed_loop_host
+  for (int b = 0; b < B; ++b) {
+    const jm::LoopState& h = hl[b];
+    const int done = h.step;
+    const int last = (h.diverged_at >= 0) ? h.diverged_at : done;
+    for (int k = 0; k <= steps; ++k) {
+      const int src = std::min(k, last);
+      if (states)
+        for (int i = 0; i < N; ++i)
+          states[((size_t)b * (S + 1) + k) * N + i] = hs[((size_t)b * (S + 1) + src) * N + i];
+    }
+    for (int k = 0; k < steps; ++k) {
+      const bool valid = (h.diverged_at >= 0) ? k <= h.diverged_at : k < done;
+      if (controls)
+        for (int j = 0; j < M; ++j)
+          controls[((size_t)b * S + k) * M + j] = valid ? hc[((size_t)b * S + k) * M + j] : 0.0;
+      if (jumps) jumps[(size_t)b * S + k] = valid ? hj[(size_t)b * S + k] : 0;
+      if (step_ns)
+        step_ns[(size_t)b * S + k] = valid ? double(ht[(size_t)b * 2 * S + S + k] - ht[(size_t)b * 2 * S + k]) : 0.0;
+    }
+    if (diverged_at) diverged_at[b] = h.diverged_at;
+    if (status) status[b] = h.status;
+  }
+  return JM_OK;
+}
+
 int jm_microbench(int device, double* fp32_tflops, double* mufu_tops, double* fp64_tflops) {
   jm_ctx* ctx = nullptr;
   CK(cudaSetDevice(device));

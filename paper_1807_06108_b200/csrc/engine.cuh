@@ -252,7 +252,7 @@ class Engine final : public EngineBase {
 
   template <int JM>
   cudaError_t launch(jm_ctx* c, const RolloutArgs<Real>& a, bool philox, bool trace) {
-    dim3 grid(c->grid), block(c->block);
+    dim3 grid(c->grid, c->launch_trials), block(c->block);
     if (philox && !trace && c->ws)
       return c->eps_smem ? launch_pdl(ws_kern<JM, true>(), grid, dim3(2 * c->block), c->main_smem, c->stream, a)
                          : launch_pdl(ws_kern<JM, false>(), grid, dim3(2 * c->block), c->main_smem, c->stream, a);
@@ -316,10 +316,10 @@ class Engine final : public EngineBase {
   cudaError_t finalize(jm_ctx* c, FinArgs f, LoopState* loop, double* u_nom_next) override {
     if (f.nrec > kMaxRecords) return cudaErrorInvalidValue;
     f.loop = loop;
-    f.counter = c->d_counter;
+    if (!f.counter) f.counter = c->d_counter;
     const PlantArgs p = plant_args(c, loop, f.u_new, u_nom_next);
     const int fgrid = (c->TM + kFinCols - 1) / kFinCols;
-    return launch_pdl(finalize_kernel<Dyn>, dim3(fgrid), dim3(kFinThreads), finalize_smem_bytes(f.nrec), c->stream,
+    return launch_pdl(finalize_kernel<Dyn>, dim3(fgrid, c->launch_trials), dim3(kFinThreads), finalize_smem_bytes(f.nrec), c->stream,
                       f, p);
   }
 

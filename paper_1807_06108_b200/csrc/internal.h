@@ -93,6 +93,7 @@ struct jm_ctx {
   int64_t* d_hist_jumps = nullptr;
   uint64_t* d_hist_t = nullptr;   // t_start | t_end
   int loop_cap = 0;
+  int launch_trials = 1;  // grid.y of the rollout / finalize launches (batched trials)
   unsigned int* d_counter = nullptr;  // finalize last-CTA counter
   std::vector<double*> stash;        // device weight buffers (K doubles)
   std::vector<int> stash_free;

@@ -389,8 +389,8 @@ __device__ __forceinline__ void jump_window(JumpClock& c, int w0, int wend, int 
 //   udt = u dt, a_t = 1/2 u'Ru dt, b_t = lambda u sqrt(dt)   (costs.py:98-111 times dt)),
 // accumulator reset and the gap table copy.
 template <int M, typename Real>
-__device__ __forceinline__ void rollout_prologue(const RolloutArgs<Real>& a, Real* tab, double* Nacc, double* s_acc,
-                                                 uint32_t* S) {
+__device__ __forceinline__ void rollout_prologue(const RolloutArgs<Real>& a, const double* u_nom, Real* tab,
+                                                 double* Nacc, double* s_acc, uint32_t* S) {
   constexpr int TS = 2 * M + 1;
   const int T = a.T;
   // read-only (.nc) loads, unrolled: the loop's global reads are issued
@@ -400,7 +400,7 @@ __device__ __forceinline__ void rollout_prologue(const RolloutArgs<Real>& a, Rea
     Real u[M];
 #pragma unroll
     for (int j = 0; j < M; ++j) {
-      Real v = Real(__ldg(a.u_nom + t * M + j));
+      Real v = Real(__ldg(u_nom + t * M + j));
       if (a.has_limits) v = fmin(fmax(v, a.u_lo[j]), a.u_hi[j]);
       u[j] = v;
     }
@@ -427,9 +427,11 @@ __device__ __forceinline__ void rollout_prologue(const RolloutArgs<Real>& a, Rea
   }
 }
 
+// Batched trials (jm_batch_loop_host): blockIdx.y is the trial; its loop
+// state, nominal controls, records and eps slabs are the trial-th slices.
 template <typename Real>
 __device__ __forceinline__ void write_record(const RolloutArgs<Real>& a, const double* s_acc, const double* Nacc) {
-  double* rec = a.records + (size_t)blockIdx.x * a.rec_stride;
+  double* rec = a.records + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * a.rec_stride;
   if (threadIdx.x == 0) {
     rec[0] = s_acc[0];
     rec[1] = s_acc[1];
@@ -481,18 +483,19 @@ __global__ void __launch_bounds__(kRolloutMaxThreads, (RolloutMinBlocks<Sys, Rea
   Real* sw = reinterpret_cast<Real*>(sb + sp_.sw);
   uint32_t* Sg = reinterpret_cast<uint32_t*>(sb + sp_.gap);
   Real* const wd = reinterpret_cast<Real*>(sb + sp_.marks) + (threadIdx.x >> 5) * 32 * a.jw_len * Q;
-  Real* const scr = in_smem ? reinterpret_cast<Real*>(sb + sp_.scr) : a.eps_out + (size_t)blockIdx.x * TM * tileK;
+  Real* const scr = in_smem ? reinterpret_cast<Real*>(sb + sp_.scr)
+                            : a.eps_out + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * TM * tileK;
 
   grid_dep_wait();    // u_nom / x / iteration come from the previous control step
   grid_dep_launch();  // (after the wait: the finalize's pre-wait prologue reads the
                       // plant state the previous finalize wrote) let the finalize
                       // grid get resident while the horizon runs
-  LoopState* L = a.loop;
+  LoopState* L = a.loop ? a.loop + blockIdx.y : nullptr;
   if (L != nullptr && L->halted) return;
   const uint64_t iter = L ? L->iteration : (a.iteration_dev ? *a.iteration_dev : a.iteration);
   const double* x0 = L ? L->x : a.x0;
   if (L != nullptr && blockIdx.x == 0 && threadIdx.x == 0) L->t_start[L->step] = globaltimer();
-  rollout_prologue<M, Real>(a, tab, Nacc, s_acc, Sg);
+  rollout_prologue<M, Real>(a, a.u_nom + (size_t)blockIdx.y * TM, tab, Nacc, s_acc, Sg);
   __syncthreads();
 
   // loop-invariant parameters, pinned in registers
@@ -523,7 +526,7 @@ __global__ void __launch_bounds__(kRolloutMaxThreads, (RolloutMinBlocks<Sys, Rea
   const bool jumps = PHILOX && a.jump_on;
 
   const StreamKey sk = make_stream_key(L ? L->seed : (a.seed_dev ? *a.seed_dev : a.seed), iter);
-  double* const costs_out = a.costs_dev ? *a.costs_dev : a.costs;
+  double* const costs_out = gridDim.y > 1 ? nullptr : (a.costs_dev ? *a.costs_dev : a.costs);
 
   for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
     const int base = tile * tileK;
@@ -766,23 +769,24 @@ __global__ void __launch_bounds__(MAXT) rollout_kernel_ws(const RolloutArgs<Real
   Real* sw = reinterpret_cast<Real*>(sb + sp_.sw);
   Real* ring = reinterpret_cast<Real*>(sb + sp_.ring);  // [slot][w][c]
   uint32_t* Sg = reinterpret_cast<uint32_t*>(sb + sp_.gap);
-  Real* const scr = SCR_SMEM ? reinterpret_cast<Real*>(sb + sp_.scr) : a.eps_out + (size_t)blockIdx.x * TM * C;
+  Real* const scr = SCR_SMEM ? reinterpret_cast<Real*>(sb + sp_.scr)
+                             : a.eps_out + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * TM * C;
 
   grid_dep_wait();
   grid_dep_launch();
-  LoopState* L = a.loop;
+  LoopState* L = a.loop ? a.loop + blockIdx.y : nullptr;
   if (L != nullptr && L->halted) return;
   const uint64_t iter = L ? L->iteration : (a.iteration_dev ? *a.iteration_dev : a.iteration);
   const double* x0 = L ? L->x : a.x0;
   if (L != nullptr && blockIdx.x == 0 && threadIdx.x == 0) L->t_start[L->step] = globaltimer();
-  rollout_prologue<M, Real>(a, tab, Nacc, s_acc, Sg);
+  rollout_prologue<M, Real>(a, a.u_nom + (size_t)blockIdx.y * TM, tab, Nacc, s_acc, Sg);
   __syncthreads();
 
   const bool producer = (int)threadIdx.x >= C;
   const int c = producer ? (int)threadIdx.x - C : (int)threadIdx.x;
   const int G = (T + 3) >> 2;
   const int nb = 2 * C;
-  double* const costs_out = a.costs_dev ? *a.costs_dev : a.costs;
+  double* const costs_out = gridDim.y > 1 ? nullptr : (a.costs_dev ? *a.costs_dev : a.costs);
 
   for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
     const int base = tile * C;
@@ -964,7 +968,7 @@ struct PlantPre {
 template <class Dyn>
 __device__ void plant_prepare(const PlantArgs& a, PlantPre& pre) {
   constexpr int N = Dyn::N, M = Dyn::M;
-  const LoopState* L = a.loop;
+  const LoopState* L = a.loop + blockIdx.y;
   const int k = L->step;
   pre.k = k;
   for (int i = 0; i < N; ++i) pre.x[i] = L->x[i];
@@ -995,7 +999,8 @@ __device__ void plant_prepare(const PlantArgs& a, PlantPre& pre) {
 template <class Dyn>
 __device__ void plant_finish(const PlantArgs& a, const PlantPre& pre, const double* u_src, bool u_src_global) {
   constexpr int N = Dyn::N, M = Dyn::M;
-  LoopState* L = a.loop;
+  LoopState* L = a.loop + blockIdx.y;
+  double* const u_nom = a.u_nom + (size_t)blockIdx.y * a.T * M;
   __shared__ int s_ok;
   if (threadIdx.x == 0) {
     const int k = pre.k;
@@ -1041,7 +1046,7 @@ __device__ void plant_finish(const PlantArgs& a, const PlantPre& pre, const doub
   if (!s_ok) return;
   const int TM = a.T * M;
   for (int i = threadIdx.x; i < TM; i += blockDim.x)
-    a.u_nom[i] = (i < TM - M) ? (u_src_global ? __ldcg(u_src + i + M) : u_src[i + M])
+    u_nom[i] = (i < TM - M) ? (u_src_global ? __ldcg(u_src + i + M) : u_src[i + M])
                               : L->u_init[i - (TM - M)];  // warm_start_shift
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -1087,7 +1092,13 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
   __shared__ double s_bc[4];
   __shared__ int s_last;
   __shared__ PlantPre s_pre;
-  LoopState* L = a.loop;
+  // batched trials: blockIdx.y selects the trial's records, controls, counter and loop state
+  const int trial = blockIdx.y;
+  const double* const recs = a.rec + (size_t)trial * a.nrec * a.rec_stride;
+  const double* const unom = a.u_nom ? a.u_nom + (size_t)trial * a.TM : nullptr;
+  double* const unew = a.u_new ? a.u_new + (size_t)trial * a.TM : nullptr;
+  unsigned int* const counter = a.counter ? a.counter + trial : nullptr;
+  LoopState* L = a.loop ? a.loop + trial : nullptr;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // closed loop: LoopState reads and the plant noise do not depend on the
   // rollout, so they run before the grid dependency resolves; so do the
@@ -1097,7 +1108,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
   const bool halted = L != nullptr && L->halted;
   const int c0 = blockIdx.x * kFinCols;
   const bool reduce_mode = a.rec_out != nullptr;
-  const double unom_c = (!reduce_mode && tid < kFinCols && c0 + tid < a.TM) ? a.u_nom[c0 + tid] : 0.0;
+  const double unom_c = (!reduce_mode && tid < kFinCols && c0 + tid < a.TM) ? unom[c0 + tid] : 0.0;
   grid_dep_wait();
   if (halted) return;
   const int rs = a.rec_stride;
@@ -1106,7 +1117,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
   {
     constexpr int CPL = kFinCols / 32;
     for (int b = warp; b < a.nrec; b += NW) {
-      const double* r = a.rec + (size_t)b * rs + 4;
+      const double* r = recs + (size_t)b * rs + 4;
 #pragma unroll
       for (int i = 0; i < CPL; ++i) {
         const int c = c0 + lane + 32 * i;
@@ -1123,7 +1134,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
   double m = CUDART_INF;
   if (one_pass) {
     if (tid < a.nrec) {
-      const double* r = a.rec + (size_t)tid * rs;
+      const double* r = recs + (size_t)tid * rs;
       h0 = r[0];
       h1 = r[1];
       h2 = r[2];
@@ -1131,7 +1142,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
     }
     m = h0;
   } else {
-    for (int b = tid; b < a.nrec; b += kFinThreads) m = fmin(m, a.rec[(size_t)b * rs]);
+    for (int b = tid; b < a.nrec; b += kFinThreads) m = fmin(m, recs[(size_t)b * rs]);
   }
   m = warp_min(m);
   if (lane == 0) s_red[0][warp] = m;
@@ -1153,7 +1164,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
     }
   } else {
     for (int b = tid; b < a.nrec; b += kFinThreads) {
-      const double* r = a.rec + (size_t)b * rs;
+      const double* r = recs + (size_t)b * rs;
       const double e = (r[0] == CUDART_INF || rho == CUDART_INF) ? 0.0 : exp(-(r[0] - rho) * a.inv_lam);
       se[b] = e;
       z += r[1] * e;
@@ -1203,7 +1214,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
       if (reduce_mode)
         a.rec_out[4 + c] = 0.0;
       else
-        a.u_new[c] = a.u_nom[c];
+        unew[c] = unom[c];
     }
     return;
   }
@@ -1214,7 +1225,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
   for (int i = 0; i < CPL; ++i) acc[i] = 0.0;
 #pragma unroll 4
   for (int b = warp; b < a.nrec; b += NW) {
-    const double* r = a.rec + (size_t)b * rs + 4;
+    const double* r = recs + (size_t)b * rs + 4;
     const double e = se[b];
 #pragma unroll
     for (int i = 0; i < CPL; ++i) {
@@ -1260,7 +1271,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
     s_delta[tid] = out;
     const double un = unom_c + out;  // u_nom + delta, unclamped (controller.py:161)
     s_unew[tid] = un;
-    a.u_new[c] = un;
+    unew[c] = un;
   }
   __syncthreads();
   if (a.norms) {  // per_step_update_norm (controller.py:168)
@@ -1289,14 +1300,14 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
   } else if (a.u_shift != nullptr) {
     __threadfence();
     __syncthreads();
-    if (tid == 0) s_last = (atomicAdd(a.counter, 1u) == gridDim.x - 1) ? 1 : 0;
+    if (tid == 0) s_last = (atomicAdd(counter, 1u) == gridDim.x - 1) ? 1 : 0;
     __syncthreads();
     if (s_last) {
       __threadfence();
       const int TM = a.TM, Mm = a.M;
       for (int i = tid; i < TM; i += kFinThreads)
-        a.u_shift[i] = (i < TM - Mm) ? __ldcg(a.u_new + i + Mm) : a.u_init[i - (TM - Mm)];
-      if (tid == 0) *a.counter = 0u;
+        a.u_shift[i] = (i < TM - Mm) ? __ldcg(unew + i + Mm) : a.u_init[i - (TM - Mm)];
+      if (tid == 0) *counter = 0u;
       if (a.done != nullptr) {
         __syncthreads();
         if (tid == 0) {
@@ -1315,12 +1326,12 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
     // several CTAs: the last one to finish runs the plant step + shift
     __threadfence();
     __syncthreads();
-    if (tid == 0) s_last = (atomicAdd(a.counter, 1u) == gridDim.x - 1) ? 1 : 0;
+    if (tid == 0) s_last = (atomicAdd(counter, 1u) == gridDim.x - 1) ? 1 : 0;
     __syncthreads();
     if (s_last) {
       __threadfence();
-      plant_finish<Dyn>(p, s_pre, a.u_new, true);
-      if (tid == 0) *a.counter = 0u;
+      plant_finish<Dyn>(p, s_pre, unew, true);
+      if (tid == 0) *counter = 0u;
     }
   }
 }

@@ -343,6 +343,26 @@ class Context:
             self.check(rc)
         return states, controls, jumps, step_ns, int(div.value), int(status.value)
 
+    def batch_loop(self, x0s, u_init, seeds, steps):
+        """`len(seeds)` independent closed loops advanced together (jm_batch_loop_host)."""
+        seeds = np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64).reshape(-1))
+        B = seeds.size
+        x0s = np.ascontiguousarray(np.broadcast_to(np.asarray(x0s, dtype=float), (B, self.N)))
+        u_init = np.ascontiguousarray(u_init, dtype=float).reshape(self.M)
+        states = np.empty((B, steps + 1, self.N))
+        controls = np.empty((B, steps, self.M))
+        jumps = np.empty((B, steps), dtype=np.int64)
+        step_ns = np.empty((B, steps))
+        div = np.empty(B, dtype=np.int32)
+        status = np.empty(B, dtype=np.int32)
+        rc = self.lib.jm_batch_loop_host(self.h, B, L.dptr(x0s), L.dptr(u_init),
+                                         seeds.ctypes.data_as(C.POINTER(C.c_uint64)), int(steps), L.dptr(states),
+                                         L.dptr(controls), L.i64ptr(jumps), L.dptr(step_ns),
+                                         div.ctypes.data_as(C.POINTER(C.c_int32)),
+                                         status.ctypes.data_as(C.POINTER(C.c_int32)))
+        self.check(rc)
+        return states, controls, jumps, step_ns, div, status
+
     def kernel_name(self) -> str:
         return self.lib.jm_kernel_name(self.h).decode()
 

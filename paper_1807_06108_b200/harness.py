@@ -3,16 +3,22 @@
 
 Each control step -- mppi_iteration, u0 = clamp(u[0]), plant noise (Sigma_D,
 jumps always on), Euler plant step with divergence check, warm_start_shift,
-iteration += 1 -- is one replay of a CUDA graph of three kernels (rollout,
-finalize, plant+shift); the loop never returns to the host until the trial
-ends.  Plant noise comes from the device Philox plant slot keyed on the trial
-seed (the reference's RngStream(seed, PLANT_STREAM_ID) role).
+iteration += 1 -- is one replay of a CUDA graph of two kernels (rollout;
+finalize, whose last CTA runs the plant step and the shift); the loop never
+returns to the host until the trial ends.  Plant noise comes from the device
+Philox plant slot keyed on the trial seed (the reference's
+RngStream(seed, PLANT_STREAM_ID) role).
+
+run_batch (harness.py:197-233) replaces the reference's process pool with a
+trial dimension on the GPU: every trial of a variant advances in the same two
+launches per control step (grid.y = trial), each trial bit-identical to its
+own run_trial.
 """
 
 from __future__ import annotations
 
-from dataclasses import dataclass
-from typing import Callable, Optional, Tuple
+from dataclasses import dataclass, replace
+from typing import Callable, Dict, List, Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -68,3 +74,75 @@ def run_trial(task: Task, cfg, seed: int, config_id: str = "", *, precision=None
     if not diverged and task.success is not None:
         ok = bool(task.success(np.asarray(states, dtype=float)))
     return TrialRecord(config_id, seed, states, controls, jumps, ok, step_ns * 1e-9, diverged)
+
+
+@dataclass(frozen=True)
+class BatchSummary:
+    """harness.py:95-100."""
+
+    success_rate: float
+    mean_states: np.ndarray     # (T+1, n)
+    ci_halfwidth: np.ndarray    # (T+1, n), 1.96 * sd / sqrt(trials)
+    total_variance: float
+
+
+def trial_seed(base_seed: int, trial_index: int) -> int:
+    """Per-trial master seed, identical across controller variants (harness.py:156-159)."""
+    ss = np.random.SeedSequence(base_seed, spawn_key=(trial_index,))
+    return int(ss.generate_state(1, np.uint64)[0])
+
+
+def total_variance(trials: Sequence[TrialRecord]) -> float:
+    """harness.py:162-167."""
+    if len(trials) < 2:
+        raise ValueError("variance undefined for fewer than 2 trials")
+    stacked = np.stack([t.states for t in trials])
+    return float(np.var(stacked, axis=0, ddof=1).sum())
+
+
+def summarize(trials: Sequence[TrialRecord]) -> BatchSummary:
+    """harness.py:170-182."""
+    stacked = np.stack([t.states for t in trials])
+    k = stacked.shape[0]
+    mean = stacked.mean(axis=0)
+    if k >= 2:
+        sd = stacked.std(axis=0, ddof=1)
+        ci = 1.96 * sd / np.sqrt(k)
+        tot_var = float(np.var(stacked, axis=0, ddof=1).sum())
+    else:
+        ci = np.zeros_like(mean)
+        tot_var = 0.0
+    rate = float(np.mean([t.success for t in trials]))
+    return BatchSummary(rate, mean, ci, tot_var)
+
+
+def run_batch(task: Task, cfg, n_trials: int, base_seed: int, variants: Sequence[str] = ("old", "new"),
+              n_workers: Optional[int] = None, config_id: str = "", *, precision=None,
+              device=None) -> Dict[str, Tuple[List[TrialRecord], BatchSummary]]:
+    """Paired trials per controller variant, summarised (harness.py:197-233).
+
+    Trial k uses the same master seed for every variant (paired plant noise).
+    All trials of a variant run together on the GPU (jm_batch_loop_host);
+    n_workers is accepted for signature compatibility and has no effect --
+    as in the reference, results do not depend on it."""
+    if n_trials < 1:
+        raise ValueError("trial count must be >= 1")
+    seeds = [trial_seed(base_seed, k) for k in range(n_trials)]
+    steps = int(task.duration_steps)
+    out: Dict[str, Tuple[List[TrialRecord], BatchSummary]] = {}
+    for variant in variants:
+        vcfg = replace(cfg, jump_sampling_enabled=(variant == "new"))
+        cid = f"{config_id}/{variant}" if config_id else variant
+        ctx = engine.get_context(task.model, task.cost_model, vcfg, precision=precision, device=device)
+        states, controls, jumps, step_ns, div, status = ctx.batch_loop(task.x0, vcfg.u_init, seeds, steps)
+        if np.any(status == L.JM_ERR_NO_VIABLE):
+            raise ControllerError("no viable rollout")  # run_trial would raise inside the pool
+        recs = []
+        for b, seed in enumerate(seeds):
+            diverged = bool(div[b] >= 0)
+            ok = False
+            if not diverged and task.success is not None:
+                ok = bool(task.success(np.asarray(states[b], dtype=float)))
+            recs.append(TrialRecord(cid, seed, states[b], controls[b], jumps[b], ok, step_ns[b] * 1e-9, diverged))
+        out[variant] = (recs, summarize(recs))
+    return out

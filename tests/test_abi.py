@@ -85,3 +85,30 @@ def test_no_cpu_fallback_without_library(tmp_path):
             _lib.load(tmp_path / "missing.so")
         finally:
             _lib._lib = saved
+
+
+def test_trial_seed_matches_reference_values():
+    """harness.py:156-159 (SeedSequence spawn); values produced by the reference's own trial_seed."""
+    from paper_1807_06108_b200.harness import trial_seed
+
+    assert [trial_seed(7, k) for k in range(3)] == [3386250816931739734, 4042502035264064771,
+                                                    17559002276220262541]
+    assert trial_seed(2024, 11) == 1093408664070836919
+    assert trial_seed(0, 0) == 8668861027912758289
+
+
+def test_summarize_matches_reference_formulas():
+    """harness.py:170-182 on synthetic trial records (host logic, no GPU)."""
+    import numpy as np
+
+    from paper_1807_06108_b200.harness import TrialRecord, summarize
+
+    rng = np.random.default_rng(3)
+    recs = [TrialRecord("x", k, rng.standard_normal((6, 4)), np.zeros((5, 1)), np.zeros(5, np.int64), k % 2 == 0,
+                        np.zeros(5)) for k in range(5)]
+    s = summarize(recs)
+    st = np.stack([r.states for r in recs])
+    assert s.success_rate == 0.6
+    assert np.allclose(s.mean_states, st.mean(0))
+    assert np.allclose(s.ci_halfwidth, 1.96 * st.std(0, ddof=1) / np.sqrt(5))
+    assert s.total_variance == np.var(st, axis=0, ddof=1).sum()

@@ -322,3 +322,27 @@ def test_lazy_weights_match_eager_and_survive_later_iterations(gpu_device):
     # the GPU-precomputed shift equals the device shift kernel
     assert np.array_equal(jb.warm_start_shift(s1, cfg.u_init).controls,
                           jb.warm_start_shift(jb.ControlSequence(s1.controls, cfg.dt), cfg.u_init).controls)
+
+
+def test_batched_trials_equal_single_trials(gpu_device):
+    """run_batch (trial dimension on the GPU) == run_trial per seed, bit for bit, both variants."""
+    import dataclasses
+
+    task, cfg = jb.baseline_config(0, K=640, T=30, steps=25)
+    out = jb.run_batch(task, cfg, n_trials=3, base_seed=7, config_id="b")
+    for variant, (recs, summ) in out.items():
+        vcfg = dataclasses.replace(cfg, jump_sampling_enabled=(variant == "new"))
+        assert [r.seed for r in recs] == [jb.trial_seed(7, k) for k in range(3)]
+        for r in recs:
+            one = jb.run_trial(task, vcfg, r.seed)
+            assert np.array_equal(r.states, one.states) and np.array_equal(r.controls, one.controls)
+            assert np.array_equal(r.jump_indicators, one.jump_indicators)
+            assert r.success == one.success and r.diverged == one.diverged
+            assert r.config_id == f"b/{variant}"
+        assert summ.mean_states.shape == recs[0].states.shape
+    # the quadrotor (12 states, 4 controls, 3-axis gusts) through the same path
+    qtask, qcfg = jb.baseline_config(2, K=512, T=20, steps=10)
+    q = jb.run_batch(qtask, qcfg, n_trials=2, base_seed=3, variants=("new",))["new"][0]
+    for r in q:
+        one = jb.run_trial(qtask, qcfg, r.seed)
+        assert np.array_equal(r.states, one.states) and np.array_equal(r.controls, one.controls)
