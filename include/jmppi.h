@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define JM_ABI_VERSION 1
+#define JM_ABI_VERSION 2
 #define JM_MAX_STATE 12
 #define JM_MAX_CONTROL 4
 #define JM_MAX_JUMP 4
@@ -90,6 +90,13 @@ typedef struct {
   double R[JM_MAX_CONTROL * JM_MAX_CONTROL]; /* control_cost_matrix, row-major m x m */
   double lambda_;             /* CostModel.lambda_ */
   double c;                   /* CostModel.c */
+  /* CostModel.control_channel == False (costs.py:50-54, :112-124): the
+   * correction matrices of the modified running cost.  The noise enters
+   * through B with as many components as controls (p = m). */
+  int32_t general_channel;    /* 0: control channel (cal_b = bb = I) */
+  int32_t pad2_;
+  double cal_b[JM_MAX_CONTROL * JM_MAX_CONTROL]; /* G' Sigma^-1 B, row-major m x p */
+  double bb[JM_MAX_CONTROL * JM_MAX_CONTROL];    /* B' Sigma^-1 B, row-major p x p */
 } jm_cost_desc;
 
 /* Replaces MppiConfig (types.py:57-87) plus the sampler extensions the

@@ -40,9 +40,13 @@ def _ref():
 
 def spec_json(model_kind, params, n, m, limits, jump_channel, jump_rows, jump_scale, cost, weights,
               target, terminal_scale, R, cost_lambda, cost_c, lam, c, sigma_d, sigma_j, nu, dt, T, K,
-              jump_enabled=True, mark_mean=None):
+              jump_enabled=True, mark_mean=None, cal_b=None, bb_term=None):
     q = m if jump_channel == "control" else len(jump_rows)
-    return dict(
+    extra = {}
+    if cal_b is not None or bb_term is not None:  # CostModel.control_channel == False (jm/costs.py:50-54)
+        extra = dict(cal_b=np.atleast_2d(cal_b).astype(float).tolist(),
+                     bb_term=np.atleast_2d(bb_term).astype(float).tolist())
+    return dict(**extra,
         model=model_kind, params=list(map(float, params)), n=n, m=m,
         limits=None if limits is None else [list(map(float, np.atleast_1d(limits[0]))),
                                             list(map(float, np.atleast_1d(limits[1])))],
@@ -233,6 +237,44 @@ def gen_control_channel(jm):
          keep_states=False)
 
 
+def gen_general_channel(jm):
+    """CostModel(control_channel=False, cal_b, bb_term): the general modified running cost
+    (jm/costs.py:112-124) through the reference's batched mppi_iteration."""
+    for task_name, K, T, seed, cal_b, bb in [
+        ("cartpole", 96, 40, 31, np.array([[0.7]]), np.array([[1.4]])),
+        ("quadrotor", 48, 30, 32,
+         np.array([[1.0, 0.2, 0.0, 0.0], [0.0, 0.8, 0.1, 0.0], [0.0, 0.0, 1.2, 0.3], [0.1, 0.0, 0.0, 0.9]]),
+         np.array([[2.0, 0.3, 0.0, 0.1], [0.3, 1.5, 0.2, 0.0], [0.0, 0.2, 1.0, 0.1], [0.1, 0.0, 0.1, 0.7]])),
+    ]:
+        ecfg = jm.config_from_dict({"task": task_name})
+        task = jm.build_task(ecfg)
+        cfg = jm.build_mppi_config(ecfg, samples_m=K)
+        cfg = jm.MppiConfig(cfg.lambda_, cfg.c, cfg.sigma_d, cfg.sigma_j, cfg.nu, cfg.dt, T, K, cfg.u_init,
+                            cfg.jump_sampling_enabled)
+        tcm = task.cost_model
+        cm = jm.CostModel(tcm.state_cost, tcm.terminal_cost, tcm.control_cost_matrix, tcm.lambda_, tcm.c,
+                          control_channel=False, cal_b=cal_b, bb_term=bb)
+        rng = np.random.default_rng(seed)
+        u_nom = np.tile(cfg.u_init, (T, 1)) + rng.normal(scale=0.5, size=(T, cfg.control_dim)) * (
+            np.array([5.0]) if task_name == "cartpole" else np.array([1.0, 0.02, 0.02, 0.02]))
+        x0 = np.zeros(task.model.state_dim)
+        ctrl = jm.ControllerState(jm.ControlSequence(u_nom, cfg.dt), 2, cfg)
+        noise, out = run_batched(jm, ctrl, task.model, cm, x0, seed)
+        fd = task.model.fused_drift_control.__self__
+        sc = tcm.state_cost
+        if task_name == "cartpole":
+            params = (fd.cart_mass, fd.pole_mass, fd.pole_half_length, fd.gravity)
+            cw, tgt, ck = (sc.w_pos, sc.w_vel, sc.w_angle, sc.w_avel), (), "cartpole_swingup"
+        else:
+            params = (fd.mass, fd.arm_length) + tuple(fd.inertia_diag) + (fd.gravity,)
+            cw, tgt, ck = (sc.w_pos, sc.w_vel, sc.w_att, sc.w_rate), tuple(sc.target), "quadrotor_hover"
+        spec = spec_json(task_name, params, task.model.state_dim, task.model.control_dim, task.model.control_limits,
+                         "control", (), "sqrt_dt", ck, cw, tgt, tcm.terminal_cost.scale, tcm.control_cost_matrix,
+                         tcm.lambda_, tcm.c, cfg.lambda_, cfg.c, cfg.sigma_d, cfg.sigma_j, cfg.nu, cfg.dt, T, K,
+                         cfg.jump_sampling_enabled, cal_b=cal_b, bb_term=bb)
+        save(f"r_{task_name}_general", spec, x0, u_nom, seed, 2, noise, out, keep_states=False)
+
+
 def gen_state_jumps(jm):
     """BASELINE configs 0 and 2 (state-space jumps) via the reference per-rollout path."""
     from oracle import mppi as om
@@ -309,6 +351,7 @@ def gen_state_jumps(jm):
 def main():
     jm = _ref()
     gen_control_channel(jm)
+    gen_general_channel(jm)
     gen_state_jumps(jm)
 
 

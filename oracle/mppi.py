@@ -58,6 +58,8 @@ class Spec:
     K: int
     jump_enabled: bool = True
     mark_mean: np.ndarray = field(default_factory=lambda: np.zeros(1))
+    cal_b: Optional[np.ndarray] = None   # CostModel.control_channel == False (jm/costs.py:50-54)
+    bb_term: Optional[np.ndarray] = None
 
     @property
     def q(self) -> int:
@@ -113,7 +115,16 @@ def spec_from_plugins(model, cost_model, cfg) -> Spec:
                 float(cost_model.lambda_), float(cost_model.c), float(cfg.lambda_), float(cfg.c),
                 np.asarray(cfg.sigma_d, float), np.asarray(cfg.sigma_j, float), float(cfg.nu),
                 float(cfg.dt), int(cfg.horizon_n), int(cfg.samples_m),
-                bool(getattr(cfg, "jump_sampling_enabled", True)), mm)
+                bool(getattr(cfg, "jump_sampling_enabled", True)), mm, *_general_channel(cost_model))
+
+
+def _general_channel(cost_model):
+    """(cal_b, bb_term) when the cost model is not control-channel (jm/costs.py:50-54), else (None, None)."""
+    if getattr(cost_model, "control_channel", True):
+        return None, None
+    cb, bb = getattr(cost_model, "cal_b", None), getattr(cost_model, "bb_term", None)
+    return (None if cb is None else np.atleast_2d(np.asarray(cb, float)),
+            None if bb is None else np.atleast_2d(np.asarray(bb, float)))
 
 
 # ---------------------------------------------------------------- noise (jm/noise.py:129-161)
@@ -285,9 +296,21 @@ def state_cost(spec: Spec, x, dt_type):
 
 
 def modified_cost(spec: Spec, q, u, eps, dt, dt_type):
-    """jm/costs.py:80-111, control-channel branch (u one shared row)."""
+    """jm/costs.py:80-124: control-channel branch (u one shared row, :95-111) or,
+    with cal_b / bb_term, the general branch (:112-124)."""
     lam, c = dt_type(spec.cost_lambda), dt_type(spec.cost_c)
     R = spec.R.astype(dt_type)
+    if spec.cal_b is not None or spec.bb_term is not None:
+        u_ru = np.einsum("...i,ij,...j->...", u, R, u)
+        mapped = eps if spec.cal_b is None else np.einsum("ij,...j->...i", spec.cal_b.astype(dt_type), eps)
+        cross = np.einsum("...i,...i->...", u, mapped)
+        if spec.bb_term is None:
+            quad = np.einsum("...i,...i->...", eps, eps)
+        else:
+            quad = np.einsum("...i,ij,...j->...", eps, spec.bb_term.astype(dt_type), eps)
+        dtt = dt_type(dt)
+        return (q + dt_type(0.5) * u_ru + lam * cross / np.sqrt(dtt)
+                + dt_type(0.5) * lam * (dt_type(1.0) - dt_type(1.0) / c) * quad / dtt)
     if u.shape[0] == 1:
         u_ru = u[0] * R[0, 0] * u[0]
         cross = u[0] * eps[..., 0]

@@ -54,6 +54,7 @@ class CostDesc(C.Structure):
         ("kind", _i32), ("pad_", _i32),
         ("weights", _d * 12), ("target", _d * 12), ("terminal_scale", _d),
         ("R", _d * 16), ("lambda_", _d), ("c", _d),
+        ("general_channel", _i32), ("pad2_", _i32), ("cal_b", _d * 16), ("bb", _d * 16),
     ]
 
 
@@ -138,7 +139,7 @@ def load(path: os.PathLike = LIB_PATH) -> C.CDLL:
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.jm_abi_version() != 1:
+        if lib.jm_abi_version() != 2:
             raise LibraryMissing("libjmppi.so ABI version mismatch")
         _lib = lib
         return lib

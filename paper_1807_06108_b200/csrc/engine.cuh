@@ -197,6 +197,8 @@ class Engine final : public EngineBase {
     a.lam_sdt = Real(lam * std::sqrt(dt));       // lambda u eps / sqrt(dt) * dt
     for (int i = 0; i < 16; ++i) {
       a.R[i] = Real(c->cost.R[i]);
+      a.calb[i] = Real(c->cost.cal_b[i]);
+      a.bb[i] = Real(c->cost.bb[i]);
       a.Ld[i] = Real(c->Ld[i]);
       a.Lj[i] = Real(c->Lj[i]);
     }
@@ -206,6 +208,7 @@ class Engine final : public EngineBase {
       a.mu_j[j] = Real(c->mppi.mark_mean[j]);
     }
     a.has_limits = c->model.has_limits;
+    a.general = c->cost.general_channel;
     a.jump_on = c->jthr != 0;
     a.gap_thr = c->d_gap;
     a.gap_n = c->gap_n;

@@ -104,6 +104,9 @@ struct RolloutArgs {
   long long sample_offset;
   Real dt, sdt, inv_lam, cq, lam_sdt;  // cq = 0.5*lam*(1-1/c); lam_sdt = lam*sqrt(dt)
   Real R[16];
+  int general;      // CostModel.control_channel == False: cal_b in the step table, eps' bb eps per step
+  Real calb[16];    // m x m row-major (costs.py:112-124)
+  Real bb[16];
   Real u_lo[4], u_hi[4];
   int has_limits;
   int jump_on;      // sampler draws jumps (jump_sampling_enabled && nu > 0)
@@ -412,7 +415,13 @@ __device__ __forceinline__ void rollout_prologue(const RolloutArgs<Real>& a, con
 #pragma unroll
     for (int j = 0; j < M; ++j) {
       tab[t * TS + j] = u[j] * a.dt;
-      tab[t * TS + M + 1 + j] = a.lam_sdt * u[j];
+      Real cu = u[j];
+      if (a.general) {  // lambda u' calB eps = lambda (calB' u) . eps (costs.py:116-117)
+        cu = Real(0);
+#pragma unroll
+        for (int i = 0; i < M; ++i) cu = fma(u[i], a.calb[i * M + j], cu);
+      }
+      tab[t * TS + M + 1 + j] = a.lam_sdt * cu;
     }
     tab[t * TS + M] = Real(0.5) * uru * a.dt;
   }
@@ -425,6 +434,26 @@ __device__ __forceinline__ void rollout_prologue(const RolloutArgs<Real>& a, con
     s_acc[2] = 0.0;
     s_acc[3] = 0.0;
   }
+}
+
+// eps' eps, or eps' bb eps for the general channel (costs.py:118-121); eps'eps
+// formed first (costs.py:101/:514), so an overflowing eps gives NaN even when c = 1
+template <int M, typename Real>
+__device__ __forceinline__ Real noise_quad(const RolloutArgs<Real>& a, const Real* eps) {
+  Real quad = eps[0] * eps[0];
+#pragma unroll
+  for (int j = 1; j < M; ++j) quad = fma(eps[j], eps[j], quad);
+  if (a.general) {
+    quad = Real(0);
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+      Real t = Real(0);
+#pragma unroll
+      for (int j = 0; j < M; ++j) t = fma(a.bb[i * M + j], eps[j], t);
+      quad = fma(eps[i], t, quad);
+    }
+  }
+  return quad;
 }
 
 // Batched trials (jm_batch_loop_host): blockIdx.y is the trial; its loop
@@ -558,9 +587,7 @@ __global__ void __launch_bounds__(kRolloutMaxThreads, (RolloutMinBlocks<Sys, Rea
       const Real qv = Cost::template q<Dyn, Real>(x, ax, sp);
       const Real* st = tab + t * TS;
       Real inc = fma(qv, dt, st[M]);
-      Real quad = eps[0] * eps[0];
-#pragma unroll
-      for (int j = 1; j < M; ++j) quad = fma(eps[j], eps[j], quad);
+      const Real quad = noise_quad<M, Real>(a, eps);
 #pragma unroll
       for (int j = 0; j < M; ++j) inc = fma(st[M + 1 + j], eps[j], inc);
       S += fma(cq, quad, inc);
@@ -882,9 +909,7 @@ __global__ void __launch_bounds__(MAXT) rollout_kernel_ws(const RolloutArgs<Real
         const Real qv = Cost::template q<Dyn, Real>(x, ax, sp);
         const Real* st = tab + t * TS;
         Real inc = fma(qv, dt, st[M]);
-        Real quad = eps[0] * eps[0];
-#pragma unroll
-        for (int j = 1; j < M; ++j) quad = fma(eps[j], eps[j], quad);
+        const Real quad = noise_quad<M, Real>(a, eps);
 #pragma unroll
         for (int j = 0; j < M; ++j) inc = fma(st[M + 1 + j], eps[j], inc);
         S += fma(cq, quad, inc);  // costs.py:98-111 times dt

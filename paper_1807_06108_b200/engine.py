@@ -141,9 +141,19 @@ def _cost_kind(cost, n):
 
 
 def describe_cost(cost_model, n: int, m: int) -> L.CostDesc:
-    if not getattr(cost_model, "control_channel", True):
-        raise NotImplementedError("only the control-channel modified cost (calB = bb = I) has a kernel")
     d = L.CostDesc()
+    if not getattr(cost_model, "control_channel", True):
+        # costs.py:50-54: the modified cost uses calB = G' Sigma^-1 B and bb = B' Sigma^-1 B
+        cb, bb = getattr(cost_model, "cal_b", None), getattr(cost_model, "bb_term", None)
+        cb = np.eye(m) if cb is None else np.atleast_2d(np.asarray(cb, float))
+        bb = np.eye(m) if bb is None else np.atleast_2d(np.asarray(bb, float))
+        if cb.shape != (m, m) or bb.shape != (m, m):
+            raise NotImplementedError(f"cal_b / bb_term must be {m}x{m} (noise with as many components as controls)")
+        d.general_channel = 1
+        for i in range(m):
+            for j in range(m):
+                d.cal_b[i * m + j] = float(cb[i, j])
+                d.bb[i * m + j] = float(bb[i, j])
     sc, tc = cost_model.state_cost, cost_model.terminal_cost
     kind, w, tgt = _cost_kind(sc, n)
     if type(tc).__name__ == "ScaledTerminalCost":

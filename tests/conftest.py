@@ -54,7 +54,14 @@ def oracle_spec(s):
                 s["jump_scale"], s["cost"], tuple(s["weights"]), tuple(s["target"]), s["terminal_scale"],
                 np.array(s["R"]), s["cost_lambda"], s["cost_c"], s["lam"], s["c"], np.array(s["sigma_d"]),
                 np.array(s["sigma_j"]), s["nu"], s["dt"], s["T"], s["K"], s["jump_enabled"],
-                np.array(s["mark_mean"]))
+                np.array(s["mark_mean"]), *_general(s))
+
+
+def _general(s):
+    """(cal_b, bb_term) of a CostModel(control_channel=False) fixture, else (None, None)."""
+    if "cal_b" not in s:
+        return None, None
+    return np.array(s["cal_b"]), np.array(s["bb_term"])
 
 
 def plugins(s, K=None, T=None):
@@ -78,7 +85,12 @@ def plugins(s, K=None, T=None):
     else:
         running = jb.DiagQuadraticCost(tuple(s["weights"]), tuple(s["target"]) if s["target"] else None)
     term = jb.ScaledTerminalCost(running, s["terminal_scale"]) if s["terminal_scale"] != 1.0 else running
-    cost = jb.CostModel(running, term, np.array(s["R"]), s["cost_lambda"], s["cost_c"])
+    cb, bb = _general(s)
+    if cb is None:
+        cost = jb.CostModel(running, term, np.array(s["R"]), s["cost_lambda"], s["cost_c"])
+    else:
+        cost = jb.CostModel(running, term, np.array(s["R"]), s["cost_lambda"], s["cost_c"], control_channel=False,
+                            cal_b=cb, bb_term=bb)
     q = s["m"] if s["jump_channel"] == "control" else len(s["jump_rows"])
     cfg = jb.MppiConfig(lambda_=s["lam"], c=s["c"], sigma_d=np.array(s["sigma_d"]), sigma_j=np.array(s["sigma_j"]),
                         nu=s["nu"], dt=s["dt"], horizon_n=s["T"] if T is None else T,
