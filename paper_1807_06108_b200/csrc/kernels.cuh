@@ -21,6 +21,7 @@
 #include <math_constants.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "philox.cuh"
 #include "systems.cuh"
@@ -438,12 +439,12 @@ __device__ __forceinline__ void rollout_prologue(const RolloutArgs<Real>& a, con
 
 // eps' eps, or eps' bb eps for the general channel (costs.py:118-121); eps'eps
 // formed first (costs.py:101/:514), so an overflowing eps gives NaN even when c = 1
-template <int M, typename Real>
+template <int M, typename Real, bool GEN>
 __device__ __forceinline__ Real noise_quad(const RolloutArgs<Real>& a, const Real* eps) {
   Real quad = eps[0] * eps[0];
 #pragma unroll
   for (int j = 1; j < M; ++j) quad = fma(eps[j], eps[j], quad);
-  if (a.general) {
+  if (GEN) {
     quad = Real(0);
 #pragma unroll
     for (int i = 0; i < M; ++i) {
@@ -557,6 +558,10 @@ __global__ void __launch_bounds__(kRolloutMaxThreads, (RolloutMinBlocks<Sys, Rea
   const StreamKey sk = make_stream_key(L ? L->seed : (a.seed_dev ? *a.seed_dev : a.seed), iter);
   double* const costs_out = gridDim.y > 1 ? nullptr : (a.costs_dev ? *a.costs_dev : a.costs);
 
+  // the general-channel cost (costs.py:112-124) as a compile-time variant of the tile loop:
+  // a runtime branch inside the step would be predicated and cost the control-channel path
+  auto tiles = [&](auto gen_tag) {
+  constexpr bool GEN = decltype(gen_tag)::value;
   for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
     const int base = tile * tileK;
     const int kl = base + threadIdx.x;
@@ -587,7 +592,7 @@ __global__ void __launch_bounds__(kRolloutMaxThreads, (RolloutMinBlocks<Sys, Rea
       const Real qv = Cost::template q<Dyn, Real>(x, ax, sp);
       const Real* st = tab + t * TS;
       Real inc = fma(qv, dt, st[M]);
-      const Real quad = noise_quad<M, Real>(a, eps);
+      const Real quad = noise_quad<M, Real, GEN>(a, eps);
 #pragma unroll
       for (int j = 0; j < M; ++j) inc = fma(st[M + 1 + j], eps[j], inc);
       S += fma(cq, quad, inc);
@@ -741,6 +746,11 @@ __global__ void __launch_bounds__(kRolloutMaxThreads, (RolloutMinBlocks<Sys, Rea
     tile_epilogue<Real, 1, (SCR_SMEM || N > 4) ? 8 : 16>(&Sf, &col, min(tileK, K - base), PHILOX ? scr : a.eps_in + base,
                            PHILOX ? (size_t)tileK : (size_t)K, TM, a.inv_lam, sw, Nacc, s_red, s_acc, s_bc);
   }
+  };
+  if (a.general)
+    tiles(std::true_type{});
+  else
+    tiles(std::false_type{});
   __syncthreads();
   write_record(a, s_acc, Nacc);
 }
@@ -909,7 +919,7 @@ __global__ void __launch_bounds__(MAXT) rollout_kernel_ws(const RolloutArgs<Real
         const Real qv = Cost::template q<Dyn, Real>(x, ax, sp);
         const Real* st = tab + t * TS;
         Real inc = fma(qv, dt, st[M]);
-        const Real quad = noise_quad<M, Real>(a, eps);
+        const Real quad = a.general ? noise_quad<M, Real, true>(a, eps) : noise_quad<M, Real, false>(a, eps);
 #pragma unroll
         for (int j = 0; j < M; ++j) inc = fma(st[M + 1 + j], eps[j], inc);
         S += fma(cq, quad, inc);  // costs.py:98-111 times dt
