@@ -87,3 +87,22 @@ def test_dropin_entry_equals_general_path(gpu_device):
     assert np.array_equal(u_new, ref.u_new) and np.array_equal(u_shift, ref.u_shift)
     assert np.array_equal(norms, ref.norms)
     assert (mc, ess, z, nf) == (ref.diag.min_cost, ref.diag.ess, ref.diag.normaliser, ref.diag.n_finite)
+
+
+def test_noise_wire_file_replays_the_device_stream(gpu_device, tmp_path):
+    """Device noise -> wire-format file -> fed (HBM-mode) iteration == the in-register Philox iteration."""
+    from paper_1807_06108_b200 import io as jio
+
+    g = load_golden("b_cartpole")
+    s = g["spec"]
+    model, cost, cfg = plugins(s, K=777, T=20)
+    u_nom = 0.3 * np.random.default_rng(4).standard_normal((20, 1))
+    ctrl = jb.ControllerState(jb.ControlSequence(u_nom, s["dt"]), 6, cfg)
+    a, _ = jb.mppi_iteration(ctrl, model, cost, g["x0"], 21, precision="f64")
+    noise = jb.sample_noise_batch(jb.RngStream(21, 6), cfg, 777, model=model, precision="f64")
+    p = tmp_path / "noise.bin"
+    jio.save_noise(str(p), noise, "state", seed=21, iteration=6)
+    _, ec, jw = jio.load_noise(str(p))
+    b, _ = jb.mppi_iteration(ctrl, model, cost, g["x0"], 21, noise=jio.from_wire(ec, jw), precision="f64")
+    # the file holds fp32 values: agreement to fp32 resolution of the noise
+    assert rel_err(b.controls, a.controls, floor=1e-3) <= 1e-5

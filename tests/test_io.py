@@ -1,0 +1,61 @@
+"""Result files and the noise wire format (reference jump_mppi/io.py)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from paper_1807_06108_b200 import io as jio
+from paper_1807_06108_b200.harness import TrialRecord
+
+
+def _records(n=3, steps=5, nx=4, m=1):
+    rng = np.random.default_rng(1)
+    return [TrialRecord("c", k, rng.standard_normal((steps + 1, nx)), rng.standard_normal((steps, m)),
+                        rng.integers(0, 2, steps), bool(k % 2), np.zeros(steps)) for k in range(n)]
+
+
+def test_trajectory_csv_round_trip_and_layout(tmp_path):
+    recs = _records()
+    p = tmp_path / "traj.csv"
+    jio.write_trajectory_csv(recs, str(p), ["x", "xd", "th", "thd"], ["F"], 0.02)
+    head = p.read_text().splitlines()[0]
+    assert head == "trial,step,t,x,xd,th,thd,F,jump_indicator"  # io.py:62-63 column order
+    cols = jio.read_trajectory_csv(str(p))
+    assert cols["trial"].size == 15
+    got = np.stack([cols[c] for c in ("x", "xd", "th", "thd")], 1).reshape(3, 5, 4)
+    assert np.array_equal(got, np.stack([r.states[:5] for r in recs]))  # 17 digits: exact
+    assert np.array_equal(cols["t"][:5], np.arange(5) * 0.02)
+    q = tmp_path / "traj2.csv"
+    jio.write_trajectory_csv(recs, str(q), ["x", "xd", "th", "thd"], ["F"], 0.02)
+    assert p.read_bytes() == q.read_bytes()  # deterministic bytes
+
+
+def test_summary_csv_round_trip(tmp_path):
+    rows = [jio.SummaryRow("cartpole", "new", 0.25, 2.0, 1000, 8, 0.875, 12.5, 3.25, 42),
+            jio.SummaryRow("cartpole", "old", 0.25, 2.0, 1000, 8, 0.5, 1.0 / 3.0, 3.5, 42)]
+    p = tmp_path / "s.csv"
+    jio.write_summary_csv(rows, str(p))
+    back = jio.read_summary_csv(str(p))
+    assert back[1]["total_variance"] == 1.0 / 3.0 and back[0]["trials"] == 8 and back[0]["variant"] == "new"
+
+
+@pytest.mark.parametrize("channel", ["control", "state"])
+def test_noise_wire_format_round_trip(tmp_path, channel):
+    rng = np.random.default_rng(2)
+    K, T, m, q = 7, 5, 2, 3 if channel == "state" else 2
+    eps_d = rng.standard_normal((K, T, m))
+    ind = (rng.random((K, T)) < 0.3).astype(np.int64)
+    eps_j = rng.standard_normal((K, T, q)) * ind[..., None]
+    eps_c = eps_d + eps_j if channel == "control" else eps_d
+    p = tmp_path / "noise.bin"
+    jio.save_noise(str(p), (eps_d, ind, eps_j, eps_c), channel, seed=3)
+    head, ec, jw = jio.load_noise(str(p))
+    assert head["seed"] == 3 and ec.shape == (T, m, K) and ec.dtype == np.float32
+    assert np.array_equal(ec, np.transpose(eps_c, (1, 2, 0)).astype(np.float32))
+    if channel == "state":
+        assert np.array_equal(jw, np.transpose(ind[..., None] * eps_j, (1, 2, 0)).astype(np.float32))
+        d, i2, j2, c2 = jio.from_wire(ec, jw)
+        assert np.array_equal(i2, ind) and np.allclose(j2, ind[..., None] * eps_j, atol=1e-6)
+    else:
+        assert jw is None
