@@ -84,6 +84,21 @@ class CostModel:
         object.__setattr__(self, "control_cost_matrix", r)
 
 
+def control_cost_matrix_from_dynamics(model, x, t: float, lambda_: float) -> np.ndarray:
+    """R = lambda G' (B B')^+ G at one state (costs.py:59-77); the pseudo-inverse
+    keeps a rank-deficient diffusion consistent.  Host-side utility."""
+    g = np.asarray(model.control_matrix(x, t), dtype=float)
+    b = np.asarray(model.diffusion_matrix(x, t), dtype=float)
+    try:
+        sig_pinv = np.linalg.pinv(b @ b.T, hermitian=True)
+    except np.linalg.LinAlgError as exc:
+        raise CostModelError("control cost undefined for this dynamics") from exc
+    r = lambda_ * (g.T @ sig_pinv @ g)
+    if not np.all(np.isfinite(r)):
+        raise CostModelError("control cost undefined for this dynamics")
+    return r
+
+
 def quadratic_cost_model(n: int, lambda_=1.0, c=1.0, m=1, r=1.0) -> CostModel:
     """tests/conftest.py:62-69: q = phi = x'x, R = r I."""
     q = DiagQuadraticCost(tuple([1.0] * n))

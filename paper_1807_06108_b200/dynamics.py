@@ -46,6 +46,15 @@ class CartpoleModel:
         if min(self.cart_mass, self.pole_mass, self.pole_half_length, self.gravity) <= 0:
             raise ValueError("cartpole parameters must be positive")
 
+    def control_matrix(self, x, t=0.0) -> np.ndarray:
+        """G(x) (4, 1) of dynamics.py:221-228, host-side (the kernels inline it)."""
+        th = float(np.asarray(x, float)[2])
+        den = self.cart_mass + self.pole_mass * np.sin(th) ** 2
+        g = np.zeros((4, 1))
+        g[1, 0] = 1.0 / den
+        g[3, 0] = -np.cos(th) / (self.pole_half_length * den)
+        return g
+
 
 @dataclass(frozen=True)
 class QuadrotorModel:
@@ -55,6 +64,16 @@ class QuadrotorModel:
     arm_length: float = 0.2
     inertia_diag: Tuple[float, float, float] = (0.01, 0.01, 0.02)
     gravity: float = 9.81
+
+    def control_matrix(self, x, t=0.0) -> np.ndarray:
+        """G(x) (12, 4) of dynamics.py:331-347, host-side: thrust along the body z axis
+        into the linear accelerations, torques through the inverse inertia."""
+        x = np.asarray(x, float)
+        (sr, cr), (sp, cp), (sy, cy) = ((np.sin(a), np.cos(a)) for a in x[6:9])
+        g = np.zeros((12, 4))
+        g[3:6, 0] = np.array([cr * sp * cy + sr * sy, cr * sp * sy - sr * cy, cr * cp]) / self.mass
+        g[9:12, 1:4] = np.diag(1.0 / np.asarray(self.inertia_diag, float))
+        return g
 
     def __post_init__(self):
         if self.mass <= 0 or self.arm_length <= 0 or min(self.inertia_diag) <= 0:
@@ -99,6 +118,15 @@ class DynamicsModel:
     @property
     def jump_dim(self) -> int:
         return self.control_dim if self.jump_channel == "control" else len(self.jump_rows)
+
+    def control_matrix(self, x, t=0.0) -> np.ndarray:
+        """G(x), host-side (utilities such as control_cost_matrix_from_dynamics)."""
+        cm = getattr(self.plant, "control_matrix", None)
+        return np.eye(self.state_dim, self.control_dim) if cm is None else cm(x, t)
+
+    def diffusion_matrix(self, x, t=0.0) -> np.ndarray:
+        """B(x): the diffusion enters through the control channel (B = G) in every model here."""
+        return self.control_matrix(x, t)
 
     def clamp(self, u: np.ndarray) -> np.ndarray:
         """np.clip to control_limits (dynamics.py:61-65); a host helper for callers."""

@@ -59,3 +59,21 @@ def test_noise_wire_format_round_trip(tmp_path, channel):
         assert np.array_equal(i2, ind) and np.allclose(j2, ind[..., None] * eps_j, atol=1e-6)
     else:
         assert jw is None
+
+
+def test_control_cost_matrix_from_dynamics_matches_reference_formula():
+    """costs.py:59-77 on this package's models: R = lambda G'(BB')^+ G with B = G."""
+    import paper_1807_06108_b200 as jb
+
+    cp = jb.cartpole_dynamics()
+    x = np.array([0.1, -0.2, 2.9, 0.4])
+    g = cp.control_matrix(x)
+    # reference expressions (dynamics.py:221-228)
+    den = 1.0 + 0.1 * np.sin(2.9) ** 2
+    assert np.allclose(g[:, 0], [0.0, 1.0 / den, 0.0, -np.cos(2.9) / (0.5 * den)])
+    r = jb.control_cost_matrix_from_dynamics(cp, x, 0.0, 2.5)
+    assert r.shape == (1, 1) and r[0, 0] == pytest.approx(2.5)  # full column rank G: G'(GG')^+G = I
+    q = jb.quadrotor_dynamics()
+    xq = np.array([0, 0, 0, 0, 0, 0, 0.1, -0.2, 0.3, 0, 0, 0.0])
+    rq = jb.control_cost_matrix_from_dynamics(q, xq, 0.0, 1.0)
+    assert np.allclose(rq, np.eye(4), atol=1e-9)
