@@ -665,18 +665,43 @@ __global__ void __launch_bounds__(kRolloutMaxThreads, (RolloutMinBlocks<Sys, Rea
     // mode reuses the group buffers as raw storage for the loaded noise.
     constexpr int ZW = PHILOX ? 4 * MP : (4 * M * (int)sizeof(Real) + 3) / 4;
     constexpr int ZMW = (4 * Q * (int)sizeof(Real) + 3) / 4;
+    // rows of this sample's column: one running pointer per tensor (advanced by
+    // a row per step) instead of a 64-bit index product per load; rows past the
+    // horizon are clamped to T-1 (only the last two groups can reach them)
+    const int kcol = act ? kl : 0;
+    const Real* pe = PHILOX ? nullptr : a.eps_in + kcol;
+    const Real* pj = (PHILOX || JM != 1 || a.jump_in == nullptr) ? nullptr : a.jump_in + kcol;
+    const size_t rowe = (size_t)M * K, rowj = (size_t)Q * K;
     auto load_group = [&](const int g0, float* zz, float* zzm) {
       Real* ze = reinterpret_cast<Real*>(zz);
       Real* zj = reinterpret_cast<Real*>(zzm);
-      const int k = act ? kl : 0;
+      if (g0 + 4 <= T) {
+        const Real* qe = pe + (size_t)g0 * rowe;
 #pragma unroll
-      for (int s2 = 0; s2 < 4; ++s2) {
-        const int t = min(g0 + s2, T - 1);
+        for (int s2 = 0; s2 < 4; ++s2) {
 #pragma unroll
-        for (int j = 0; j < M; ++j) ze[s2 * M + j] = __ldg(a.eps_in + (size_t)(t * M + j) * K + k);
-        if (JM == 1 && a.jump_in != nullptr) {
+          for (int j = 0; j < M; ++j) ze[s2 * M + j] = __ldg(qe + (size_t)j * K);
+          qe += rowe;
+        }
+        if (JM == 1 && pj != nullptr) {
+          const Real* qj = pj + (size_t)g0 * rowj;
 #pragma unroll
-          for (int i = 0; i < Q; ++i) zj[s2 * Q + i] = __ldg(a.jump_in + (size_t)(t * Q + i) * K + k);
+          for (int s2 = 0; s2 < 4; ++s2) {
+#pragma unroll
+            for (int i = 0; i < Q; ++i) zj[s2 * Q + i] = __ldg(qj + (size_t)i * K);
+            qj += rowj;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int s2 = 0; s2 < 4; ++s2) {
+          const int t = min(g0 + s2, T - 1);
+#pragma unroll
+          for (int j = 0; j < M; ++j) ze[s2 * M + j] = __ldg(pe + (size_t)t * rowe + (size_t)j * K);
+          if (JM == 1 && pj != nullptr) {
+#pragma unroll
+            for (int i = 0; i < Q; ++i) zj[s2 * Q + i] = __ldg(pj + (size_t)t * rowj + (size_t)i * K);
+          }
         }
       }
     };
