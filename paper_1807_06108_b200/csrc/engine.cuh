@@ -155,7 +155,8 @@ class Engine final : public EngineBase {
     // wave: also keep the eps scratch in shared memory if possible
     const size_t cap = (size_t)optin - 1024;
     const bool single = philox && !no_eps_smem && c->ntiles <= sms;
-    const size_t budget = single ? cap : std::min(cap, (size_t)64 * 1024);
+    // multi-wave: two CTAs per SM must still fit (the occupancy the 256-sample tiles need)
+    const size_t budget = single ? cap : std::min(cap, (size_t)optin / 2 - 2048);
     int W = 32;
     while (W > 8 && plan_bytes(c, block, mwarps, W, nring, single) > budget) W -= 4;
     c->jw_len = W;
