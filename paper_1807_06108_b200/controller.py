@@ -136,12 +136,12 @@ def warm_start_shift(controls: ControlSequence, u_init) -> ControlSequence:
     A sequence returned by mppi_iteration already carries its shift for the
     config's u_init, computed by the iteration's finalize kernel; any other
     sequence / u_init is shifted by a device kernel."""
+    pre = getattr(controls, "_shifted", None)
+    if pre is not None and (u_init is pre[0] or np.array_equal(np.atleast_1d(np.asarray(u_init, float)), pre[0])):
+        return ControlSequence._adopt(pre[1], controls.dt)
     u = np.ascontiguousarray(controls.controls, dtype=float)
     T, m = u.shape
     ui = np.ascontiguousarray(np.atleast_1d(np.asarray(u_init, dtype=float)).reshape(m))
-    pre = getattr(controls, "_shifted", None)
-    if pre is not None and np.array_equal(pre[0], ui):
-        return ControlSequence(pre[1], controls.dt)
     out = np.empty_like(u)
     rc = L.load().jm_shift_host(_device(), T, m, L.dptr(u), L.dptr(ui), L.dptr(out))
     engine.raise_status(rc)
@@ -195,7 +195,8 @@ def mppi_iteration(
         # the drop-in fast path: one compact C call (jm_iteration_dropin)
         u_new, norms, (mc, ess, z, _), u_shift, handle = ctx.iteration_dropin(
             x0, ctrl.nominal_controls.controls, master_seed, ctrl.iteration_index, u_init)
-        new_controls = ControlSequence(u_new, cfg.dt)
+        new_controls = ControlSequence._adopt(u_new, cfg.dt)  # views of a fresh output block
+        norms.setflags(write=False)
         object.__setattr__(new_controls, "_shifted", (u_init, u_shift))
         return new_controls, UpdateDiagnostics(weights=None, min_cost=mc, effective_sample_size=ess,
                                                per_step_update_norm=norms, _ctx=ctx, _handle=handle, _z=z)
