@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define JM_ABI_VERSION 2
+#define JM_ABI_VERSION 3
 #define JM_MAX_STATE 12
 #define JM_MAX_CONTROL 4
 #define JM_MAX_JUMP 4
@@ -50,7 +50,7 @@ typedef enum {
   JM_ERR_DIVERGED = 7      /* -> StateDivergedError  (dynamics.py:29-33), plant only    */
 } jm_status;
 
-typedef enum { JM_MODEL_INTEGRATOR = 0, JM_MODEL_CARTPOLE = 1, JM_MODEL_QUADROTOR = 2 } jm_model_kind;
+typedef enum { JM_MODEL_INTEGRATOR = 0, JM_MODEL_CARTPOLE = 1, JM_MODEL_QUADROTOR = 2, JM_MODEL_LINEAR = 3 } jm_model_kind;
 typedef enum {
   JM_COST_DIAG_QUADRATIC = 0,   /* q = sum_i w_i (x_i - x*_i)^2 (conftest quadratic_q, BASELINE cartpole) */
   JM_COST_CARTPOLE_SWINGUP = 1, /* CartpoleStateCost, costs.py:149-168                                  */
@@ -77,6 +77,12 @@ typedef struct {
   int32_t jump_dim;           /* q (== m for JM_JUMP_CONTROL) */
   int32_t jump_rows[JM_MAX_JUMP]; /* JM_JUMP_STATE: state rows hit by the jump (H selector) */
   int32_t jump_scale_unit;    /* 1: O(1) jump increment ("unit", dynamics.py:111); 0: sqrt(dt) */
+  /* JM_MODEL_LINEAR: a generic linear plugin f(x) = A x, G constant, B = H = G
+   * (a DynamicsModel with drift = A @ x and constant control/diffusion/jump
+   * matrices, noise_through_controls=True); (n, m) in {(2,1), (4,1), (4,2), (6,3)} */
+  int32_t pad_lin_;
+  double lin_A[JM_MAX_STATE * JM_MAX_STATE]; /* row-major n x n */
+  double lin_G[JM_MAX_STATE * JM_MAX_CONTROL]; /* row-major n x m */
 } jm_model_desc;
 
 /* Replaces the CostModel plugin (costs.py:28-56) with its state/terminal cost

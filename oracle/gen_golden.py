@@ -275,6 +275,52 @@ def gen_general_channel(jm):
         save(f"r_{task_name}_general", spec, x0, u_nom, seed, 2, noise, out, keep_states=False)
 
 
+def gen_linear(jm):
+    """A generic linear plugin (f = A x, constant G = B = H) through the reference's
+    batched mppi_iteration, with a diagonal quadratic cost."""
+    cases = [
+        ("r_linear_2x1", np.array([[0.0, 1.0], [-2.0, -0.3]]), np.array([[0.0], [1.0]]), 64, 30, 41),
+        ("r_linear_4x2", np.array([[0, 1, 0, 0], [-1.5, -0.2, 0.4, 0], [0, 0, 0, 1], [0.3, 0, -0.8, -0.1]], float),
+         np.array([[0, 0], [1.0, 0.2], [0, 0], [-0.1, 0.7]]), 48, 25, 42),
+        ("r_linear_6x3", np.kron(np.eye(3), np.array([[0.0, 1.0], [-1.0, -0.4]])) + 0.05 * np.ones((6, 6)),
+         np.kron(np.eye(3), np.array([[0.0], [1.0]])), 32, 20, 43),
+    ]
+    for name, A, G, K, T, seed in cases:
+        n, m = G.shape
+
+        def drift(x, t=0.0, A=A):
+            return np.asarray(x, dtype=float) @ A.T
+
+        def gmat(x, t=0.0, G=G):
+            x = np.asarray(x, dtype=float)
+            return np.broadcast_to(G, x.shape[:-1] + G.shape).copy()
+
+        model = jm.DynamicsModel(state_dim=n, control_dim=m, drift=drift, control_matrix=gmat,
+                                 diffusion_matrix=gmat, jump_matrix=gmat, noise_through_controls=True)
+        w = np.linspace(1.0, 2.0, n)
+
+        def q(x, t=0.0, w=w):
+            x = np.asarray(x, dtype=float)
+            return np.einsum("...i,i,...i->...", x, w, x)
+
+        def phi(x, w=w):
+            return 4.0 * q(x)
+
+        R = 0.1 * np.eye(m)
+        cm = jm.CostModel(state_cost=q, terminal_cost=phi, control_cost_matrix=R, lambda_=1.5, c=1.2)
+        sd = 0.5 * np.eye(m)
+        cfg = jm.MppiConfig(2.0, 1.2, sd, 2.0 * np.eye(m), 1.0, 0.05, T, K, np.zeros(m))
+        rng = np.random.default_rng(seed)
+        u_nom = 0.3 * rng.standard_normal((T, m))
+        x0 = rng.standard_normal(n)
+        ctrl = jm.ControllerState(jm.ControlSequence(u_nom, cfg.dt), 1, cfg)
+        noise, out = run_batched(jm, ctrl, model, cm, x0, seed)
+        spec = spec_json("linear", tuple(A.ravel()) + tuple(G.ravel()), n, m, None, "control", (), "sqrt_dt",
+                         "diag", tuple(w), (0.0,) * n, 4.0, R, 1.5, 1.2, cfg.lambda_, cfg.c, cfg.sigma_d,
+                         cfg.sigma_j, cfg.nu, cfg.dt, T, K, cfg.jump_sampling_enabled)
+        save(name, spec, x0, u_nom, seed, 1, noise, out, keep_states=False)
+
+
 def gen_state_jumps(jm):
     """BASELINE configs 0 and 2 (state-space jumps) via the reference per-rollout path."""
     from oracle import mppi as om
@@ -352,6 +398,7 @@ def main():
     jm = _ref()
     gen_control_channel(jm)
     gen_general_channel(jm)
+    gen_linear(jm)
     gen_state_jumps(jm)
 
 

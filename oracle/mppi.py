@@ -33,7 +33,7 @@ class OracleNoViable(RuntimeError):
 
 @dataclass
 class Spec:
-    model: str                 # "cartpole" | "quadrotor" | "integrator"
+    model: str                 # "cartpole" | "quadrotor" | "integrator" | "linear" (params = A, G flattened)
     n: int
     m: int
     params: Tuple[float, ...]  # cartpole: mc, mp, l, g; quadrotor: mass, arm, ixx, iyy, izz, g
@@ -84,6 +84,9 @@ def spec_from_plugins(model, cost_model, cfg) -> Spec:
         params = (plant.mass, plant.arm_length) + tuple(plant.inertia_diag) + (plant.gravity,)
     elif name == "IntegratorModel":
         kind, params = "integrator", ()
+    elif name == "LinearModel":
+        kind = "linear"
+        params = tuple(np.asarray(plant.A, float).ravel()) + tuple(np.asarray(plant.G, float).ravel())
     else:
         raise TypeError(f"oracle has no model {name}")
     sc = cost_model.state_cost
@@ -219,11 +222,21 @@ def integrator_fg(x, dt_type):
     return np.zeros_like(x), G
 
 
+def linear_fg(x, spec: Spec, dt_type):
+    """A generic linear DynamicsModel: drift A @ x, constant G (= B = H)."""
+    n, m = spec.n, spec.m
+    p = np.asarray(spec.params, dtype=dt_type)
+    A, G = p[: n * n].reshape(n, n), p[n * n: n * n + n * m].reshape(n, m)
+    return x @ A.T, np.broadcast_to(G, x.shape[:-1] + (n, m)).astype(x.dtype)
+
+
 def drift_control(spec: Spec, x, dt_type):
     if spec.model == "cartpole":
         return cartpole_fg(x, spec.params, dt_type)
     if spec.model == "quadrotor":
         return quadrotor_fg(x, spec.params, dt_type)
+    if spec.model == "linear":
+        return linear_fg(x, spec, dt_type)
     return integrator_fg(x, dt_type)
 
 

@@ -23,7 +23,7 @@ JM_ERR_CUDA = 5
 JM_ERR_UNSUPPORTED = 6
 JM_ERR_DIVERGED = 7
 
-JM_MODEL_INTEGRATOR, JM_MODEL_CARTPOLE, JM_MODEL_QUADROTOR = 0, 1, 2
+JM_MODEL_INTEGRATOR, JM_MODEL_CARTPOLE, JM_MODEL_QUADROTOR, JM_MODEL_LINEAR = 0, 1, 2, 3
 JM_COST_DIAG_QUADRATIC, JM_COST_CARTPOLE_SWINGUP, JM_COST_QUADROTOR_HOVER = 0, 1, 2
 JM_JUMP_CONTROL, JM_JUMP_STATE = 0, 1
 JM_NOISE_PHILOX, JM_NOISE_HBM = 0, 1
@@ -45,7 +45,7 @@ class ModelDesc(C.Structure):
         ("kind", _i32), ("state_dim", _i32), ("control_dim", _i32), ("has_limits", _i32),
         ("params", _d * 8), ("u_lo", _d * 4), ("u_hi", _d * 4),
         ("jump_channel", _i32), ("jump_dim", _i32), ("jump_rows", _i32 * 4),
-        ("jump_scale_unit", _i32),
+        ("jump_scale_unit", _i32), ("pad_lin_", _i32), ("lin_A", _d * 144), ("lin_G", _d * 48),
     ]
 
 
@@ -139,7 +139,7 @@ def load(path: os.PathLike = LIB_PATH) -> C.CDLL:
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.jm_abi_version() != 2:
+        if lib.jm_abi_version() != 3:
             raise LibraryMissing("libjmppi.so ABI version mismatch")
         _lib = lib
         return lib

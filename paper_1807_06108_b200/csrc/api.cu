@@ -429,6 +429,10 @@ int jm_create(const jm_model_desc* model, const jm_cost_desc* cost, const jm_mpp
       if (n != 12 || m != 4) break;
       ctx->eng = jm::make_engine_quadrotor(cost->kind, p.precision);
       break;
+    case JM_MODEL_LINEAR:
+      if (model->jump_channel != JM_JUMP_CONTROL) break;  // B = H = G
+      ctx->eng = jm::make_engine_linear(cost->kind, p.precision, n, m);
+      break;
     default:
       break;
   }
@@ -455,6 +459,16 @@ int jm_create(const jm_model_desc* model, const jm_cost_desc* cost, const jm_mpp
 
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (e == cudaSuccess && model->kind == JM_MODEL_LINEAR) {  // [A | G] for the Linear engine
+    std::vector<double> ag((size_t)n * n + (size_t)n * m);
+    for (int i = 0; i < n * n; ++i) ag[i] = model->lin_A[i];
+    for (int i = 0; i < n * m; ++i) ag[(size_t)n * n + i] = model->lin_G[i];
+    std::vector<float> agf(ag.begin(), ag.end());
+    e = cudaMalloc(&ctx->d_lin_d, sizeof(double) * ag.size());
+    if (e == cudaSuccess) e = cudaMalloc(&ctx->d_lin_f, sizeof(float) * agf.size());
+    if (e == cudaSuccess) e = cudaMemcpy(ctx->d_lin_d, ag.data(), sizeof(double) * ag.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(ctx->d_lin_f, agf.data(), sizeof(float) * agf.size(), cudaMemcpyHostToDevice);
+  }
   if (e == cudaSuccess && ctx->jthr) {
     const std::vector<uint32_t> S = gap_table(p.nu * p.dt, ctx->T, &ctx->gap_inv);
     ctx->gap_n = (int)S.size();
@@ -495,6 +509,8 @@ int jm_destroy(jm_ctx* ctx) {
   if (ctx->iter_exec) cudaGraphExecDestroy(ctx->iter_exec);
   dfree(ctx->d_scratch);
   dfree(ctx->d_gap);
+  dfree(ctx->d_lin_f);
+  dfree(ctx->d_lin_d);
   dfree(ctx->d_hbm_eps);
   dfree(ctx->d_hbm_jump);
   dfree(ctx->d_costs);

@@ -42,6 +42,7 @@ struct EngineBase {
 EngineBase* make_engine_integrator(int cost_kind, int precision, int n);
 EngineBase* make_engine_cartpole(int cost_kind, int precision);
 EngineBase* make_engine_quadrotor(int cost_kind, int precision);
+EngineBase* make_engine_linear(int cost_kind, int precision, int n, int m);
 
 }  // namespace jm
 
@@ -94,6 +95,8 @@ struct jm_ctx {
   uint64_t* d_hist_t = nullptr;   // t_start | t_end
   int loop_cap = 0;
   int launch_trials = 1;  // grid.y of the rollout / finalize launches (batched trials)
+  void* d_lin_f = nullptr;  // Linear model: [A | G] as float (rollout in fp32)
+  void* d_lin_d = nullptr;  //               and as double (fp64 rollout, the plant)
   unsigned int* d_counter = nullptr;  // finalize last-CTA counter
   std::vector<double*> stash;        // device weight buffers (K doubles)
   std::vector<int> stash_free;

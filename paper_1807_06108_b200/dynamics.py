@@ -94,6 +94,40 @@ class IntegratorModel:
             raise ValueError("the device integrator is compiled for dim 1 or 2")
 
 
+@dataclass(frozen=True, eq=False)
+class LinearModel:
+    """A generic linear plant dx = (A x + G u) dt + G (eps sqrt(dt) + jumps): the
+    reference's DynamicsModel with drift A @ x and constant G = B = H
+    (noise_through_controls=True).  Device kernels exist for (n, m) in
+    LINEAR_SHAPES."""
+
+    A: np.ndarray
+    G: np.ndarray
+
+    def __post_init__(self):
+        A = np.array(self.A, dtype=float, copy=True)
+        G = np.array(self.G, dtype=float, copy=True)
+        if G.ndim == 1:
+            G = G[:, None]
+        if A.ndim != 2 or A.shape[0] != A.shape[1] or G.shape[0] != A.shape[0]:
+            raise ValueError("A must be n x n and G n x m")
+        if (A.shape[0], G.shape[1]) not in LINEAR_SHAPES:
+            raise NotImplementedError(f"linear plugin kernels exist for (n, m) in {sorted(LINEAR_SHAPES)}")
+        A.setflags(write=False)
+        G.setflags(write=False)
+        object.__setattr__(self, "A", A)
+        object.__setattr__(self, "G", G)
+
+    def drift(self, x, t=0.0) -> np.ndarray:
+        return np.asarray(x, float) @ self.A.T
+
+    def control_matrix(self, x, t=0.0) -> np.ndarray:
+        return self.G.copy()
+
+
+LINEAR_SHAPES = frozenset({(2, 1), (4, 1), (4, 2), (6, 3)})
+
+
 @dataclass(frozen=True)
 class DynamicsModel:
     """Device-evaluable control-affine jump-diffusion model (dynamics.py:45-65)."""
@@ -193,3 +227,10 @@ def integrator_dynamics(dim: int = 1, control_limits=None) -> DynamicsModel:
         plant=IntegratorModel(dim),
         control_limits=_limits(control_limits, dim),
     )
+
+
+def linear_dynamics(A, G, control_limits=None) -> DynamicsModel:
+    """The generic linear plugin: f(x) = A x, constant G = B = H."""
+    plant = LinearModel(A, G)
+    n, m = plant.A.shape[0], plant.G.shape[1]
+    return DynamicsModel(state_dim=n, control_dim=m, plant=plant, control_limits=_limits(control_limits, m))

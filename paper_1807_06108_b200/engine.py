@@ -96,6 +96,14 @@ def describe_model(model) -> L.ModelDesc:
     elif name == "IntegratorModel":
         d.kind = L.JM_MODEL_INTEGRATOR
         vals = []
+    elif name == "LinearModel":
+        d.kind = L.JM_MODEL_LINEAR
+        vals = []
+        A, G = np.asarray(plant.A, float), np.asarray(plant.G, float)
+        for i, v in enumerate(A.ravel()):
+            d.lin_A[i] = float(v)
+        for i, v in enumerate(G.ravel()):
+            d.lin_G[i] = float(v)
     else:
         raise NotImplementedError(f"no device kernel for dynamics parameter object {name}")
     for i, v in enumerate(vals):

@@ -76,6 +76,10 @@ def plugins(s, K=None, T=None):
         p = s["params"]
         model = jb.quadrotor_dynamics(jb.QuadrotorModel(p[0], p[1], tuple(p[2:5]), p[5]), lim,
                                       jump_channel=s["jump_channel"], jump_scale_mode=s["jump_scale"])
+    elif s["model"] == "linear":
+        n, m = s["n"], s["m"]
+        p = np.array(s["params"])
+        model = jb.linear_dynamics(p[: n * n].reshape(n, n), p[n * n:].reshape(n, m), lim)
     else:
         model = jb.integrator_dynamics(s["n"], lim)
     if s["cost"] == "cartpole_swingup":

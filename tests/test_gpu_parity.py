@@ -109,7 +109,7 @@ def test_device_noise_matches_emulation(name, gpu_device):
 
 @pytest.mark.parametrize("name", ["r_integrator_big", "r_cartpole_task", "r_quadrotor_task", "r_quadrotor_map",
                                   "r_cartpole_twin_T25", "b_cartpole", "b_quadrotor", "r_cartpole_general",
-                                  "r_quadrotor_general"])
+                                  "r_quadrotor_general", "r_linear_2x1", "r_linear_4x2", "r_linear_6x3"])
 def test_f64_philox_iteration_matches_oracle(name, gpu_device):
     """The rollout kernel consumes exactly the noise sample_noise_batch exports."""
     g, s, model, cost, cfg = _philox_setup(name)
