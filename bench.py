@@ -272,7 +272,7 @@ def ours_arm(a):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world > 1 or os.environ.get("JM_SHARDED_BENCH"):  # (the env var: exercise the sharded path at N=1)
         from paper_1807_06108_b200 import distributed as jd
 
         return jd.bench_sharded(a, world, rank, local)

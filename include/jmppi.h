@@ -279,6 +279,22 @@ int jm_batch_loop_host(jm_ctx* ctx, int32_t trials, const double* x0, const doub
                        const uint64_t* seeds, int32_t steps, double* states, double* controls, int64_t* jumps,
                        double* step_ns, int32_t* diverged_at, int32_t* status);
 
+/* Peer-memory record exchange -- the multi-GPU step without a collective.
+ * Every rank owns a symmetric buffer (e.g. torch.distributed._symmetric_memory)
+ * of jm_peer_buffer_doubles(ctx, world) doubles, zeroed before the first step,
+ * whose base addresses on all ranks (device-addressable peer pointers over
+ * NVLink) are in peer_bases_dev (world entries, device memory).
+ * jm_loop_rollout_push: the rollout kernel's CTAs store their weighting
+ * records straight into every rank's buffer (slot rank x grid + cta) and raise
+ * their epoch flags there -- the exchange is fused into the compute kernel and
+ * overlaps its slower CTAs.  jm_loop_finish_peers: the finalize waits on its
+ * own buffer's flags on the device, merges the world x grid records in rank
+ * order, updates, steps the plant and shifts.  Stream-ordered, no host wait,
+ * graph-capturable; the epoch is the loop's step counter. */
+int64_t jm_peer_buffer_doubles(const jm_ctx* ctx, int32_t world);
+int jm_loop_rollout_push(jm_ctx* ctx, const unsigned long long* peer_bases_dev, int32_t rank, int32_t world);
+int jm_loop_finish_peers(jm_ctx* ctx, const double* my_buffer_dev, int32_t world);
+
 /* ---- measurement helpers ---- */
 /* Time `steps` closed-loop control steps (jm_loop_init first) with CUDA events
  * on the context's stream; before each step a cudaMemsetAsync of flush_bytes

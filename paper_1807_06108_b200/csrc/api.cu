@@ -981,6 +981,40 @@ int jm_loop_finish(jm_ctx* ctx, const double* records_dev, int32_t nrec) {
   return JM_OK;
 }
 
+int64_t jm_peer_buffer_doubles(const jm_ctx* ctx, int32_t world) {
+  if (!ctx || world < 1) return 0;
+  const int64_t n = (int64_t)world * ctx->grid;                      // one record per rank x CTA
+  return 2 * n * ctx->rec_stride + (n + 1) / 2;                      // 2 parities + uint32 flags
+}
+
+int jm_loop_rollout_push(jm_ctx* ctx, const unsigned long long* peer_bases_dev, int32_t rank, int32_t world) {
+  if (!ctx || !ctx->d_loop || !peer_bases_dev || world < 1 || rank < 0 || rank >= world ||
+      (int64_t)world * ctx->grid > jm::kMaxRecords)
+    return fail(ctx, JM_ERR_VALUE, "bad arguments (world x grid must be <= %d records)", jm::kMaxRecords);
+  CK(cudaSetDevice(ctx->device));
+  jm::RolloutCall rc;
+  rc.u_nom = ctx->d_loop_unom;
+  rc.loop = ctx->d_loop;
+  rc.push_peers = peer_bases_dev;
+  rc.push_rank = rank;
+  rc.push_world = world;
+  CK(ctx->eng->rollout(ctx, rc));
+  return JM_OK;
+}
+
+int jm_loop_finish_peers(jm_ctx* ctx, const double* my_buffer_dev, int32_t world) {
+  if (!ctx || !ctx->d_loop || !my_buffer_dev || world < 1 || (int64_t)world * ctx->grid > jm::kMaxRecords)
+    return fail(ctx, JM_ERR_VALUE, "bad arguments");
+  CK(cudaSetDevice(ctx->device));
+  const int nrec = world * ctx->grid;
+  jm::FinArgs f = fin_args(ctx, my_buffer_dev, nrec);
+  f.u_nom = ctx->d_loop_unom;
+  f.u_new = ctx->d_loop_unew;
+  f.wait_flags = reinterpret_cast<const unsigned int*>(my_buffer_dev + 2 * (size_t)nrec * ctx->rec_stride);
+  CK(ctx->eng->finalize(ctx, f, ctx->d_loop, ctx->d_loop_unom));
+  return JM_OK;
+}
+
 int jm_loop_step(jm_ctx* ctx) {
   if (!ctx || !ctx->graph_exec) return fail(ctx, JM_ERR_VALUE, "loop not initialised");
   CK(cudaGraphLaunch(ctx->graph_exec, ctx->own_stream));

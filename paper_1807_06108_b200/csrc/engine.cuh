@@ -235,6 +235,9 @@ class Engine final : public EngineBase {
     a.records = c->d_records;
     a.rec_stride = c->rec_stride;
     a.loop = rc.loop;
+    a.push_peers = rc.push_peers;
+    a.push_rank = rc.push_rank;
+    a.push_world = rc.push_world;
     return a;
   }
 

@@ -25,6 +25,8 @@ struct RolloutCall {
   double* states = nullptr;
   int64_t* diverged = nullptr;
   LoopState* loop = nullptr;
+  const unsigned long long* push_peers = nullptr;  // peer-memory exchange (write_record)
+  int push_rank = 0, push_world = 0;
 };
 
 struct EngineBase {

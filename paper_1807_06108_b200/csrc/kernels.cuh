@@ -72,6 +72,17 @@ __device__ __forceinline__ uint64_t globaltimer() {
 __device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 
+// System-scope acquire / release on the 32-bit epoch flags of the peer-memory
+// record exchange (peers write them over NVLink).
+__device__ __forceinline__ uint32_t ld_acquire_sys(const unsigned int* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned int* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll
@@ -136,6 +147,10 @@ struct RolloutArgs {
   double* records;       // gridDim.x * rec_stride
   int rec_stride;
   LoopState* loop;
+  // peer-memory exchange (jm_loop_rollout_push): the CTA's record goes straight
+  // into every rank's symmetric buffer instead of `records`
+  const unsigned long long* push_peers;
+  int push_rank, push_world;
 };
 
 // ---------------------------------------------------------------- noise
@@ -459,8 +474,42 @@ __device__ __forceinline__ Real noise_quad(const RolloutArgs<Real>& a, const Rea
 
 // Batched trials (jm_batch_loop_host): blockIdx.y is the trial; its loop
 // state, nominal controls, records and eps slabs are the trial-th slices.
+//
+// Peer-memory exchange: every rank's symmetric buffer (world W, grid G,
+// record stride rs) is [parity 0: W*G records][parity 1: W*G records][W*G
+// uint32 epoch flags].  A CTA stores its record into slot rank*G + cta of
+// parity (epoch & 1) of EVERY rank's buffer -- peer pointers, so the stores
+// travel over NVLink/NVSwitch as soon as the CTA's tile is done, overlapping
+// the slower CTAs -- then raises its flag there to the epoch (release after a
+// system-scope fence).  Double buffering by parity: a rank runs at most one
+// control step ahead of the slowest peer (its next push needs its own
+// finalize, which waited for every peer's records).
 template <typename Real>
 __device__ __forceinline__ void write_record(const RolloutArgs<Real>& a, const double* s_acc, const double* Nacc) {
+  if (a.push_peers != nullptr) {
+    const uint32_t epoch = (uint32_t)a.loop->step + 1u;
+    const int W = a.push_world, G = gridDim.x, slot = a.push_rank * G + blockIdx.x;
+    const size_t off = ((size_t)(epoch & 1u) * W * G + slot) * a.rec_stride;
+    for (int p = 0; p < W; ++p) {
+      double* dst = reinterpret_cast<double*>(a.push_peers[p]) + off;
+      if (threadIdx.x == 0) {
+        dst[0] = s_acc[0];
+        dst[1] = s_acc[1];
+        dst[2] = s_acc[2];
+        dst[3] = s_acc[3];
+      }
+      for (int r = threadIdx.x; r < a.TM; r += blockDim.x) dst[4 + r] = Nacc[r];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      for (int p = 0; p < W; ++p)
+        st_release_sys(reinterpret_cast<unsigned int*>(reinterpret_cast<double*>(a.push_peers[p]) +
+                                                       2 * (size_t)W * G * a.rec_stride) + slot,
+                       epoch);
+    }
+    return;
+  }
   double* rec = a.records + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * a.rec_stride;
   if (threadIdx.x == 0) {
     rec[0] = s_acc[0];
@@ -1133,6 +1182,10 @@ struct FinArgs {
   const double* u_init;   // optional: u_shift = warm_start_shift(u_new, u_init)
   double* u_shift;
   volatile int32_t* done; // optional: set to 1 (system-scope fence first) once every output is written
+  // peer-memory exchange (jm_loop_finish_peers): before merging, wait until the
+  // nrec (= world x grid) flags reach this step's epoch (L->step + 1); records
+  // of epoch parity e & 1 start at rec + (e & 1) * nrec * rec_stride
+  const unsigned int* wait_flags;
 };
 
 inline size_t finalize_smem_bytes(int nrec) {
@@ -1154,7 +1207,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
   __shared__ PlantPre s_pre;
   // batched trials: blockIdx.y selects the trial's records, controls, counter and loop state
   const int trial = blockIdx.y;
-  const double* const recs = a.rec + (size_t)trial * a.nrec * a.rec_stride;
+  const double* recs = a.rec + (size_t)trial * a.nrec * a.rec_stride;
   const double* const unom = a.u_nom ? a.u_nom + (size_t)trial * a.TM : nullptr;
   double* const unew = a.u_new ? a.u_new + (size_t)trial * a.TM : nullptr;
   unsigned int* const counter = a.counter ? a.counter + trial : nullptr;
@@ -1172,6 +1225,14 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
   grid_dep_wait();
   if (halted) return;
   const int rs = a.rec_stride;
+  if (a.wait_flags != nullptr) {  // every rank's CTA records arrive over NVLink (write_record)
+    const uint32_t epoch = (uint32_t)L->step + 1u;
+    for (int r = tid; r < a.nrec; r += kFinThreads)
+      while (ld_acquire_sys(a.wait_flags + r) < epoch) __nanosleep(32);
+    __syncthreads();
+    __threadfence();
+    recs += (size_t)(epoch & 1u) * a.nrec * rs;
+  }
   // the column pass below reads every record's N block: start those lines
   // towards L1 now, under the head reductions
   {

@@ -11,8 +11,18 @@ exp(-(rho_r - rho)/lambda) (the finalize kernel) and applies the identical
 update, plant step and shift -- one collective instead of a MIN all-reduce
 followed by a SUM all-reduce.
 
-torch.distributed is the plumbing (process group, NCCL over NVLink/NVSwitch,
-streams); all arithmetic is in libjmppi.so.  The host-side logic here
+Two transports for that exchange:
+  "p2p"  (default when available) -- no collective library on the data path:
+         each rank owns a symmetric buffer (torch.distributed._symmetric_memory,
+         peer pointers over NVLink/NVSwitch); a one-CTA kernel stores the
+         rank's record straight into slot `rank` of every peer's buffer and
+         raises an epoch flag there, and the finalize kernel waits on its own
+         flags on the device (jm_loop_rollout_push / jm_loop_finish_peers) --
+         the step never returns to the host or a collective launch;
+  "nccl" -- all_gather_into_tensor of the records (the fallback).
+
+torch.distributed is the plumbing (process group, rendezvous of the symmetric
+buffers, streams); all arithmetic is in libjmppi.so.  The host-side logic here
 (shard ranges, record exchange, rank-order merge) is covered on CPU by
 tests/test_distributed.py with world_size 2 over gloo.
 """
@@ -21,6 +31,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import sys
 from dataclasses import dataclass
 from typing import Tuple
 
@@ -74,13 +85,14 @@ class ShardedLoop:
     world: int
     rank: int
     group: object = None
+    transport: str = "nccl"
 
     @classmethod
-    def create(cls, task, cfg, rank: int, world: int, device: int, precision=None, group=None):
+    def create(cls, task, cfg, rank: int, world: int, device: int, precision=None, group=None, transport="nccl"):
         off, _ = shard(cfg.samples_m, rank)
         ctx = engine.get_context(task.model, task.cost_model, cfg, precision=precision, sample_offset=off,
                                  device=device)
-        return cls(ctx, world, rank, group)
+        return cls(ctx, world, rank, group, transport)
 
     def init(self, x0, u_init, seed: int, max_steps: int):
         import torch
@@ -100,13 +112,44 @@ class ShardedLoop:
             self.record = torch.zeros(rs.value, dtype=torch.float64, device=dev)
         self.ctx.check(lib.jm_set_stream(h, C.c_void_p(self.stream.cuda_stream)))
         torch.cuda.synchronize(dev)
+        if self.transport == "p2p":
+            self._init_peers(dev)
+
+    def _init_peers(self, dev):
+        """Symmetric exchange buffers + their peer addresses (jm_peer_buffer_doubles layout)."""
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+
+        lib, h = self.ctx.lib, self.ctx.h
+        n = int(lib.jm_peer_buffer_doubles(h, self.world))
+        buf = symm.empty(n, dtype=torch.float64, device=dev)
+        buf.zero_()  # epoch flags start at 0
+        torch.cuda.synchronize(dev)
+        hdl = symm.rendezvous(buf, self.group if self.group is not None else dist.group.WORLD)
+        ptrs = [int(p) for p in hdl.buffer_ptrs]
+        off = buf.data_ptr() - ptrs[self.rank]  # the same offset in every rank's symmetric allocation
+        self.peer_bases = torch.tensor([p + off for p in ptrs], dtype=torch.int64, device=dev)
+        self.peer_buf, self.symm_handle = buf, hdl
+        torch.cuda.synchronize(dev)
+        dist.barrier(group=self.group)  # every rank's flags are zero before anyone pushes
+        # the whole step is device-side (no collective, no host wait): one CUDA
+        # graph of its four kernels, replayed per control step
+        lib, h = self.ctx.lib, self.ctx.h
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=self.stream):
+            self.ctx.check(lib.jm_loop_rollout_push(h, C.c_void_p(self.peer_bases.data_ptr()), self.rank, self.world))
+            self.ctx.check(lib.jm_loop_finish_peers(h, C.c_void_p(self.peer_buf.data_ptr()), self.world))
 
     def step(self):
-        """One control step: local rollout + record, all_gather, merge/update/plant/shift."""
+        """One control step: local rollout + record, exchange, merge/update/plant/shift."""
         import torch
 
         lib, h = self.ctx.lib, self.ctx.h
         with torch.cuda.stream(self.stream):
+            if self.transport == "p2p":
+                self.graph.replay()
+                return
             self.ctx.check(lib.jm_loop_rollout(h, C.c_void_p(self.record.data_ptr())))
             gathered = exchange_records(self.record, self.group)
             self.ctx.check(lib.jm_loop_finish(h, C.c_void_p(gathered.data_ptr()), self.world))
@@ -149,25 +192,37 @@ def bench_sharded(a, world: int, rank: int, local: int):
     idx = {"cfg0": 0, "cfg1": 1, "cfg2": 2, "cfg3": 3}[a.workload]
     task, cfg = jb.baseline_config(idx, K=a.samples, T=a.horizon)
     K, T = cfg.samples_m, cfg.horizon_n
-    loop = ShardedLoop.create(task, cfg, rank, world, local, precision=a.precision)
     n_total = a.warmup + a.steps
-    loop.init(task.x0, cfg.u_init, 0, 2 * n_total + 64)
+    transport = os.environ.get("JM_EXCHANGE", "p2p")
+    try:
+        loop = ShardedLoop.create(task, cfg, rank, world, local, precision=a.precision, transport=transport)
+        loop.init(task.x0, cfg.u_init, 0, 2 * n_total + 64)
+    except Exception as exc:  # symmetric memory unavailable: the NCCL all_gather path
+        if transport != "p2p":
+            raise
+        print(f"[bench] peer-memory exchange unavailable ({exc}); using NCCL all_gather", file=sys.stderr)
+        transport = "nccl"
+        loop = ShardedLoop.create(task, cfg, rank, world, local, precision=a.precision, transport=transport)
+        loop.init(task.x0, cfg.u_init, 0, 2 * n_total + 64)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     for _ in range(a.warmup):
         loop.step()
     torch.cuda.synchronize()
-    times = []
+    # the timed steps are enqueued back to back (no host round trip between
+    # them, as the device-resident loop runs); per step an L2 flush outside the
+    # step's event pair; barrier + synchronize around the whole region
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    dist.barrier()
+    torch.cuda.synchronize()
     for i in range(a.steps):
         with torch.cuda.stream(loop.stream):
             flush.fill_(i & 0xFF)  # evict L2 between timed steps
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        dist.barrier()
-        torch.cuda.synchronize()
-        e0.record(loop.stream)  # events on the stream the kernels run on
+        evs[i][0].record(loop.stream)  # events on the stream the kernels run on
         loop.step()
-        e1.record(loop.stream)
-        torch.cuda.synchronize()
-        times.append(e0.elapsed_time(e1))
+        evs[i][1].record(loop.stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    times = [e0.elapsed_time(e1) for e0, e1 in evs]
     t = torch.tensor([float(np.mean(times))], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)  # max over ranks
     ms = float(t.item())
@@ -181,10 +236,13 @@ def bench_sharded(a, world: int, rank: int, local: int):
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": a.precision,
                 "data": "synthetic",
                 "config": {"workload": f"{a.workload}: BASELINE config {idx} closed-loop control step, "
-                                       f"K={K} per GPU (global {world * K}), T={T}, one NCCL all_gather "
-                                       "of the weighting records per step",
+                                       f"K={K} per GPU (global {world * K}), T={T}, one exchange of the "
+                                       "weighting records per step",
+                           "exchange": ("peer-memory records over NVLink (symmetric buffers, device-side epoch "
+                                        "flags, no collective launch)" if transport == "p2p"
+                                        else "NCCL all_gather_into_tensor"),
                            "K_per_gpu": K, "T": T, "parallelism": f"dp{world}",
                            "l2": "flushed (256 MiB fill) before each timed step"},
-                "mpc_iteration_latency_ms": ms, "gpu_launches": 3 * a.steps}
+                "mpc_iteration_latency_ms": ms, "gpu_launches": (4 if transport == "p2p" else 3) * a.steps}
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()

@@ -346,3 +346,36 @@ def test_batched_trials_equal_single_trials(gpu_device):
     for r in q:
         one = jb.run_trial(qtask, qcfg, r.seed)
         assert np.array_equal(r.states, one.states) and np.array_equal(r.controls, one.controls)
+
+
+def test_sharded_loop_world1_peer_memory_exchange(gpu_device):
+    """The NCCL-free exchange (symmetric buffer, push kernel, device-side epoch
+    wait) over a one-rank group reproduces the single-GPU graph loop."""
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1807_06108_b200 import distributed as jd
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        task, cfg = jb.baseline_config(0, K=2048, T=60, steps=12)
+        rec = jb.run_trial(task, cfg, seed=5, precision="f64")
+        loop = jd.ShardedLoop.create(task, cfg, 0, 1, 0, precision="f64", transport="p2p")
+        loop.init(task.x0, cfg.u_init, 5, 64)
+        for _ in range(12):
+            loop.step()
+        x, it, st, halted, status = loop.read()
+        assert st == 12 and it == 12 and not halted
+        assert np.allclose(x, rec.states[-1], rtol=1e-9, atol=1e-12)
+        sts, cos, jus = loop.history(12)
+        assert np.allclose(sts, rec.states, rtol=1e-9, atol=1e-12)
+    finally:
+        dist.destroy_process_group()
