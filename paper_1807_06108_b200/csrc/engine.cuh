@@ -143,7 +143,6 @@ class Engine final : public EngineBase {
     }
     const bool ws = philox && 2 * block <= kWsMaxThreads && (ws_env < 0 ? block <= kWsMaxTile : ws_env == 1);
     c->block = block;
-    c->spt = 1;
     c->ws = ws;
     const int threads = ws ? 2 * block : block;
     const int nring = ws ? ws_ring(c, block) : 0;

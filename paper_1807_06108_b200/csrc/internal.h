@@ -57,7 +57,7 @@ struct jm_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t own_stream = nullptr;
   int N = 0, M = 0, Q = 0, T = 0, K = 0, TM = 0, rec_stride = 0;
-  int block = 128, grid = 1, ntiles = 1, spt = 1;
+  int block = 128, grid = 1, ntiles = 1;
   int ws = 0;              // warp-specialised Philox rollout: block of 2*block threads
   int eps_smem = 0;        // Philox main kernel keeps the eps scratch in shared memory
   size_t main_smem = 0;    // dynamic smem of the Philox main kernel
