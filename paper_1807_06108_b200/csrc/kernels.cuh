@@ -259,7 +259,12 @@ __device__ __forceinline__ void tile_epilogue(const Real* Sf, const int* cols, i
   // quadrotor keeps 8, 16 spills its horizon loop), then one
   // transposing butterfly reduces the RPW row partials across the lanes
   // (9 shuffles for 8 rows instead of 40) -- fixed order, deterministic
-  for (int r0 = warp * RPW; r0 < TM; r0 += nwarps * RPW) {
+  // row blocks in reverse horizon order: a global slab's late rows were
+  // written last and are the ones still in L2 (the slabs of all resident
+  // tiles exceed it), so they are read before the other CTAs' writes evict them
+  const int nblk = (TM + RPW - 1) / RPW;
+  for (int bi = warp; bi < nblk; bi += nwarps) {
+    const int r0 = (nblk - 1 - bi) * RPW;
     Real acc[RPW];
 #pragma unroll
     for (int i = 0; i < RPW; ++i) acc[i] = Real(0);
