@@ -1232,9 +1232,28 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
   const int rs = a.rec_stride;
   if (a.wait_flags != nullptr) {  // every rank's CTA records arrive over NVLink (write_record)
     const uint32_t epoch = (uint32_t)L->step + 1u;
-    for (int r = tid; r < a.nrec; r += kFinThreads)
-      while (ld_acquire_sys(a.wait_flags + r) < epoch) __nanosleep(32);
+    // a peer that never pushes (a dead rank) must not hang the GPU: after 30 s
+    // the loop halts with JM_ERR_CUDA instead
+    __shared__ int s_timeout;
+    if (tid == 0) s_timeout = 0;
     __syncthreads();
+    const uint64_t t_begin = globaltimer();
+    for (int r = tid; r < a.nrec; r += kFinThreads)
+      while (ld_acquire_sys(a.wait_flags + r) < epoch) {
+        __nanosleep(32);
+        if (globaltimer() - t_begin > 30ull * 1000000000ull) {
+          s_timeout = 1;
+          break;
+        }
+      }
+    __syncthreads();
+    if (s_timeout) {
+      if (tid == 0) {
+        L->status = 5;  // JM_ERR_CUDA
+        L->halted = 1;
+      }
+      return;
+    }
     __threadfence();
     recs += (size_t)(epoch & 1u) * a.nrec * rs;
   }
