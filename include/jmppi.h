@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define JM_ABI_VERSION 3
+#define JM_ABI_VERSION 4
 #define JM_MAX_STATE 12
 #define JM_MAX_CONTROL 4
 #define JM_MAX_JUMP 4
@@ -62,6 +62,10 @@ typedef enum {
 } jm_jump_channel;
 typedef enum { JM_NOISE_PHILOX = 0, JM_NOISE_HBM = 1 } jm_noise_source;
 typedef enum { JM_F32 = 0, JM_F64 = 1 } jm_precision;
+/* Jump arrivals per (sample, step): the reference's zero-one law (an indicator
+ * U < nu dt, noise.py:151), or Poisson(nu dt) counts whose marks add up
+ * (compound Poisson; BASELINE north star "Poisson jump counts per step"). */
+typedef enum { JM_JUMPS_BERNOULLI = 0, JM_JUMPS_POISSON = 1 } jm_jump_process;
 
 /* Replaces the DynamicsModel plugin (dynamics.py:45-65) built by
  * cartpole_dynamics (:264-284) / quadrotor_dynamics (:389-409). */
@@ -106,7 +110,7 @@ typedef struct {
 } jm_cost_desc;
 
 /* Replaces MppiConfig (types.py:57-87) plus the sampler extensions the
- * BASELINE configs need (mark mean, Poisson-free zero-one law kept). */
+ * BASELINE configs need (mark mean, Poisson arrival counts). */
 typedef struct {
   double lambda_, c, dt, nu;
   int32_t horizon;            /* T = horizon_n */
@@ -120,7 +124,7 @@ typedef struct {
   int32_t noise_source;       /* jm_noise_source */
   int64_t sample_offset;      /* global index of local sample 0 (multi-GPU shards) */
   int32_t block_threads;      /* 0 = auto */
-  int32_t pad_;
+  int32_t jump_process;       /* jm_jump_process: arrivals per jump step */
 } jm_mppi_desc;
 
 /* UpdateDiagnostics scalars (controller.py:48-53). */

@@ -358,7 +358,9 @@ def mppi_iteration_oracle(spec: Spec, x0, u_nom, noise, dtype=np.float64, mappin
     eps_d_t = np.ascontiguousarray(np.swapaxes(eps_d, 0, 1), dtype=dtype)
     eps_j_t = np.ascontiguousarray(np.swapaxes(eps_j, 0, 1), dtype=dtype)
     eps_c_t = np.ascontiguousarray(np.swapaxes(eps_c, 0, 1), dtype=dtype)
-    ind_t = np.ascontiguousarray(np.swapaxes(ind, 0, 1))
+    # the reference's flag is the indicator; with Poisson counts (device sampler
+    # extension) eps_j already holds the sum of the step's marks, so n -> 1
+    ind_t = np.ascontiguousarray(np.swapaxes(np.minimum(ind, 1), 0, 1))
     u_nom = np.asarray(u_nom, dtype=dtype).reshape(T, m)
     u_eff = clamp(spec, u_nom)
     xs = np.repeat(np.asarray(x0, dtype=dtype)[None, :], K, axis=0)

@@ -11,13 +11,16 @@ lg2/sqrt/sin/cos approximations, this emulation float64 libm).
 
 from __future__ import annotations
 
+import math
+
 import numpy as np
 
 M0, M1 = np.uint64(0xD2511F53), np.uint64(0xCD9E8D57)
 W0, W1 = np.uint32(0x9E3779B9), np.uint32(0xBB67AE85)
 MASK = np.uint64(0xFFFFFFFF)
 
-SLOT_DIFFUSION, SLOT_JUMP_UNIFORM, SLOT_MARK, SLOT_PLANT = 0, 1, 2, 3
+SLOT_DIFFUSION, SLOT_JUMP_UNIFORM, SLOT_MARK, SLOT_PLANT, SLOT_COUNT = 0, 1, 2, 3, 4
+MAX_COUNT = 8
 
 
 def philox4x32_10(c0, c1, c2, c3, k0, k1):
@@ -99,6 +102,45 @@ def jump_events(key, k, T, p):
         e += 1
 
 
+def event_probability(nu_dt: float, poisson: bool = False) -> float:
+    """Per-step probability of a jump event: nu dt (zero-one law, noise.py:151) or
+    P(N >= 1) = 1 - exp(-nu dt) for Poisson(nu dt) arrivals (api.cu event_probability)."""
+    return -math.expm1(-nu_dt) if poisson else nu_dt
+
+
+def poisson_tail(lam: float, k: int) -> float:
+    """P(N > k), N ~ Poisson(lam): the forward sum of the next 40 pmf terms in the
+    device library's order (api.cu poisson_tail), so both round alike."""
+    term = math.exp(-lam)
+    for j in range(1, k + 1):
+        term *= lam / j
+    s = 0.0
+    for j in range(k + 1, k + 41):
+        term *= lam / j
+        s += term
+    return s
+
+
+def count_tables(lam: float):
+    """(event, plant) count thresholds of philox.cuh slot 4 / the plant draw:
+    event arrivals n = 1 + #{k : u24 < ev[k-1]}, ev[k-1] = floor(2^24 P(N > k) / P(N >= 1));
+    plant arrivals n = #{k : u24 < pl[k]}, pl[0] = ceil(P(N >= 1) 2^24), pl[k] = floor(2^24 P(N > k))."""
+    p1 = -math.expm1(-lam)
+    ev, pl = [], [jump_threshold(p1) >> 8]
+    for k in range(1, MAX_COUNT + 1):
+        t = poisson_tail(lam, k)
+        ev.append(int(math.floor(t / p1 * 16777216.0)) if p1 > 0 else 0)
+        pl.append(int(math.floor(t * 16777216.0)))
+    return np.array(ev, dtype=np.int64), np.array(pl, dtype=np.int64)
+
+
+def event_counts(key, k, e, ev):
+    """Arrival counts of event e for samples k (slot 4, word e&3 of block e>>2)."""
+    w = draw(key, SLOT_COUNT, np.uint32(e >> 2), k)
+    u = (w[e & 3] >> np.uint32(8)).astype(np.int64)
+    return 1 + np.sum(u[..., None] < np.asarray(ev, np.int64)[None, :], axis=-1)
+
+
 def jump_threshold(p: float) -> int:
     if not p > 0:
         return 0
@@ -107,12 +149,14 @@ def jump_threshold(p: float) -> int:
 
 
 def device_noise(seed, iteration, K, T, m, q, Ld, Lj, mark_mean, jthr, jump_channel="control",
-                 sample_offset=0):
+                 sample_offset=0, counts=None):
     """(eps_d, ind, eps_j, eps_c) as the device sampler draws them (float64).
 
     Ld (m x m) = chol(c Sigma_D), Lj (q x q) = chol(Sigma_J), jthr from
-    jump_threshold(nu dt) (0 = no jumps; the renewal clock's per-step
-    probability is its quantised ceil(nu dt 2^24) / 2^24)."""
+    jump_threshold(event_probability(nu dt)) (0 = no jumps; the renewal clock's
+    per-step probability is its quantised ceil(p 2^24) / 2^24).  counts: the
+    event table of count_tables(nu dt) for Poisson arrivals (ind = n, the mark
+    the sum of n marks, n mu + sqrt(n) Lj z); None = one arrival per event."""
     key = stream_key(seed, iteration)
     MP = 4 if m == 3 else m
     k = (np.arange(K, dtype=np.int64) + sample_offset).astype(np.uint32)[:, None]
@@ -134,7 +178,8 @@ def device_noise(seed, iteration, K, T, m, q, Ld, Lj, mark_mean, jthr, jump_chan
         for e, t, alive in jump_events(key, k, T, p):
             rows = np.nonzero(alive)[0]
             cols = t[rows]
-            ind[rows, cols] = 1
+            n = event_counts(key, k[rows, 0], e, counts) if counts is not None else np.ones(rows.size, np.int64)
+            ind[rows, cols] = n
             idx = np.int64(e * QP) + np.arange(q)[None, :]
             blk = np.broadcast_to((idx >> 2).astype(np.uint32), (rows.size, q))
             mw = draw(key, SLOT_MARK, blk, k[rows, 0][:, None])
@@ -142,6 +187,8 @@ def device_noise(seed, iteration, K, T, m, q, Ld, Lj, mark_mean, jthr, jump_chan
             a23 = box_muller(mw[2], mw[3])
             allz = np.stack([a01[0], a01[1], a23[0], a23[1]], axis=-1)  # (events, q, 4)
             zz = np.take_along_axis(allz, np.broadcast_to((idx & 3)[..., None], (rows.size, q, 1)), axis=-1)[..., 0]
-            eps_j[rows, cols] = np.asarray(mark_mean, float)[:q] + zz @ np.tril(Lj).T
+            nn = n.astype(float)[:, None]
+            eps_j[rows, cols] = np.where(nn > 1, nn * np.asarray(mark_mean, float)[:q] + np.sqrt(nn) * (zz @ np.tril(Lj).T),
+                                         np.asarray(mark_mean, float)[:q] + zz @ np.tril(Lj).T)
     eps_c = eps_d + eps_j if jump_channel == "control" else eps_d.copy()
     return eps_d, ind, eps_j, eps_c

@@ -28,6 +28,7 @@ JM_COST_DIAG_QUADRATIC, JM_COST_CARTPOLE_SWINGUP, JM_COST_QUADROTOR_HOVER = 0, 1
 JM_JUMP_CONTROL, JM_JUMP_STATE = 0, 1
 JM_NOISE_PHILOX, JM_NOISE_HBM = 0, 1
 JM_F32, JM_F64 = 0, 1
+JM_JUMPS_BERNOULLI, JM_JUMPS_POISSON = 0, 1
 
 _d = C.c_double
 _i32 = C.c_int32
@@ -64,7 +65,7 @@ class MppiDesc(C.Structure):
         ("horizon", _i32), ("samples", _i32), ("control_dim", _i32), ("jump_enabled", _i32),
         ("sigma_d", _d * 16), ("sigma_j", _d * 16), ("mark_mean", _d * 4),
         ("precision", _i32), ("noise_source", _i32), ("sample_offset", _i64),
-        ("block_threads", _i32), ("pad_", _i32),
+        ("block_threads", _i32), ("jump_process", _i32),
     ]
 
 
@@ -142,7 +143,7 @@ def load(path: os.PathLike = LIB_PATH) -> C.CDLL:
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.jm_abi_version() != 3:
+        if lib.jm_abi_version() != 4:
             raise LibraryMissing("libjmppi.so ABI version mismatch")
         _lib = lib
         return lib

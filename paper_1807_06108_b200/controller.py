@@ -188,7 +188,8 @@ def mppi_iteration(
         eps_arg = ctx.step_major(eps_c, m)
         if ctx.mdesc.jump_channel == L.JM_JUMP_STATE:
             q = ctx.Q
-            jump = np.asarray(ind, float).reshape(K, T, 1) * np.asarray(eps_j, float).reshape(K, T, q)
+            # indicator (or Poisson count: eps_j already sums the step's marks) * mark
+            jump = (np.asarray(ind) != 0).astype(float).reshape(K, T, 1) * np.asarray(eps_j, float).reshape(K, T, q)
             jump_arg = ctx.step_major(jump, q)
     u_init = np.atleast_1d(np.asarray(cfg.u_init, dtype=float))
     if noise is None and mapping is None and not return_rollouts:

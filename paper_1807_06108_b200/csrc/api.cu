@@ -67,6 +67,37 @@ uint32_t jump_threshold(double p) {
   return ((uint32_t)thr) << 8;
 }
 
+// Per-step probability of a jump event: the zero-one law's nu dt, or
+// P(N >= 1) = 1 - exp(-nu dt) for Poisson(nu dt) arrivals.
+double event_probability(double nu_dt, bool poisson) { return poisson ? -std::expm1(-nu_dt) : nu_dt; }
+
+// Poisson(lam) tail P(N > k) as the forward sum of the next 40 pmf terms
+// (the oracle restates this exact order, oracle/philox_stream.py).
+double poisson_tail(double lam, int k) {
+  double term = std::exp(-lam);
+  for (int j = 1; j <= k; ++j) term *= lam / j;
+  double s = 0.0;
+  for (int j = k + 1; j <= k + 40; ++j) {
+    term *= lam / j;
+    s += term;
+  }
+  return s;
+}
+
+// Count thresholds: event arrivals n = 1 + #{k : u24 < c[k-1]},
+// c[k-1] = floor(2^24 P(N > k) / P(N >= 1)); plant arrivals (no conditioning)
+// n = #{k : u24 < p[k]}, p[0] = ceil(P(N >= 1) 2^24) (the event threshold),
+// p[k] = floor(2^24 P(N > k)).
+void count_tables(double lam, jm::CountTable* ev, uint32_t* plant) {
+  const double p1 = -std::expm1(-lam);
+  for (int k = 1; k <= jm::kMaxCount; ++k) {
+    const double t = poisson_tail(lam, k);
+    ev->c[k - 1] = p1 > 0.0 ? (uint32_t)std::floor(t / p1 * 16777216.0) : 0u;
+    plant[k] = (uint32_t)std::floor(t * 16777216.0);
+  }
+  plant[0] = jump_threshold(p1) >> 8;
+}
+
 // Survival table of the geometric jump gaps (philox.cuh, slot 1):
 // S[0] = 2^24, S[g] = floor(S[g-1] (2^24 - q) / 2^24), q = ceil(p 2^24), g <= T;
 // *inv = 1 / log2((2^24 - q) / 2^24) for the sampler's first guess.
@@ -376,6 +407,8 @@ int jm_create(const jm_model_desc* model, const jm_cost_desc* cost, const jm_mpp
     if (!(cost->weights[i] >= 0.0))  // nonnegative state costs (costs.py:37)
       return fail(nullptr, JM_ERR_CONFIG, "invalid configuration: cost weights must be nonnegative");
   if (m != p.control_dim) return fail(nullptr, JM_ERR_CONFIG, "control_dim mismatch between model (%d) and config (%d)", m, p.control_dim);
+  if (p.jump_process != JM_JUMPS_BERNOULLI && p.jump_process != JM_JUMPS_POISSON)
+    return fail(nullptr, JM_ERR_CONFIG, "invalid configuration: jump_process must be bernoulli or poisson");
   if (p.jump_enabled && !(p.nu * p.dt < 0.1))  // noise.py:148-149
     return fail(nullptr, JM_ERR_VALUE, "zero-one jump law violated (nu*dt = %g)", p.nu * p.dt);
 
@@ -412,8 +445,11 @@ int jm_create(const jm_model_desc* model, const jm_cost_desc* cost, const jm_mpp
     delete ctx;
     return fail(nullptr, JM_ERR_NOISE, "covariance factorization failed for sigma_j");
   }
-  ctx->jthr = p.jump_enabled ? jump_threshold(p.nu * p.dt) : 0u;
-  ctx->jthr_plant = jump_threshold(p.nu * p.dt);
+  ctx->poisson = p.jump_process == JM_JUMPS_POISSON;
+  const double p_event = event_probability(p.nu * p.dt, ctx->poisson);
+  ctx->jthr = p.jump_enabled ? jump_threshold(p_event) : 0u;
+  ctx->jthr_plant = jump_threshold(p_event);
+  if (ctx->poisson) count_tables(p.nu * p.dt, &ctx->cnt, ctx->cnt_plant);
 
   // plugin -> kernel family
   switch (model->kind) {
@@ -470,7 +506,7 @@ int jm_create(const jm_model_desc* model, const jm_cost_desc* cost, const jm_mpp
     if (e == cudaSuccess) e = cudaMemcpy(ctx->d_lin_f, agf.data(), sizeof(float) * agf.size(), cudaMemcpyHostToDevice);
   }
   if (e == cudaSuccess && ctx->jthr) {
-    const std::vector<uint32_t> S = gap_table(p.nu * p.dt, ctx->T, &ctx->gap_inv);
+    const std::vector<uint32_t> S = gap_table(p_event, ctx->T, &ctx->gap_inv);
     ctx->gap_n = (int)S.size();
     e = cudaMalloc(&ctx->d_gap, S.size() * sizeof(uint32_t));
     if (e == cudaSuccess) e = cudaMemcpy(ctx->d_gap, S.data(), S.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
@@ -858,6 +894,8 @@ static jm::NoiseArgs noise_args(const jm_ctx* ctx, uint64_t seed, uint64_t itera
   na.jump_on = ctx->jthr != 0;
   na.gap_thr = ctx->d_gap;
   na.gap_inv = ctx->gap_inv;
+  na.poisson = ctx->poisson;
+  na.cnt = ctx->cnt;
   na.sample_offset = ctx->mppi.sample_offset;
   na.seed = seed;
   na.iteration = iteration;

@@ -214,6 +214,8 @@ class Engine final : public EngineBase {
     a.gap_thr = c->d_gap;
     a.gap_n = c->gap_n;
     a.gap_inv = c->gap_inv;
+    a.poisson = c->poisson;
+    a.cnt = c->cnt;
     a.jw_len = c->jw_len;
     a.jscale = Real(c->model.jump_scale_unit ? 1.0 : std::sqrt(dt));
     fill_sys<Real>(c, a.sp);
@@ -309,6 +311,8 @@ class Engine final : public EngineBase {
       p.u_hi[j] = c->model.u_hi[j];
     }
     p.jthr = c->jthr_plant;
+    p.poisson = c->poisson;
+    for (int i = 0; i <= kMaxCount; ++i) p.cnt0[i] = c->cnt_plant[i];
     p.q = c->Q;
     p.jmode = c->model.jump_channel;
     p.has_limits = c->model.has_limits;

@@ -66,6 +66,9 @@ struct jm_ctx {
   double Ld[16] = {0}, Lj[16] = {0}, Lp[16] = {0};  // chol(c Sigma_D), chol(Sigma_J), chol(Sigma_D)
   uint32_t jthr = 0;      // sampler jump threshold (0 = no jumps)
   uint32_t jthr_plant = 0;
+  int poisson = 0;            // jm_jump_process == JM_JUMPS_POISSON
+  jm::CountTable cnt{};         // zero-truncated count thresholds (philox.cuh slot 4)
+  uint32_t cnt_plant[jm::kMaxCount + 1] = {};  // plant: n = #{k : u24 < cnt_plant[k]}
   uint32_t* d_gap = nullptr;  // jump-gap survival table (philox.cuh), gap_n = T + 1 entries
   int gap_n = 0;
   float gap_inv = 0.f;        // 1 / log2(1 - p)

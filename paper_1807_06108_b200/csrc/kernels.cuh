@@ -125,6 +125,8 @@ struct RolloutArgs {
   const uint32_t* gap_thr;  // jump-gap survival table (philox.cuh), gap_n = T + 1 entries
   int gap_n;
   float gap_inv;    // 1 / log2(1 - p)
+  int poisson;      // jump_process = poisson: an event carries n >= 1 arrivals (philox.cuh slot 4)
+  CountTable cnt;
   int jw_len;       // jump window (steps, multiple of 4 in [8, 32])
   Real jscale;      // state-jump scale (1 or sqrt dt)
   Real Ld[16];      // chol(c * Sigma_D), m x m row-major
@@ -350,19 +352,32 @@ __device__ __forceinline__ float rmul<float>(float a, float b) { return __fmul_r
 template <>
 __device__ __forceinline__ double rmul<double>(double a, double b) { return __dmul_rn(a, b); }
 
+// Mark of jump event e: mu + Lj z, or -- Poisson counts -- the sum of the
+// event's n arrivals' iid N(mu, Sigma_J) marks, n mu + sqrt(n) Lj z (n = 1
+// leaves the single-mark value untouched).
 template <int Q, int QP, typename Real>
 __device__ __forceinline__ void mark_of(const StreamKey& sk, uint32_t kg, uint32_t e, const Real* Lj, const Real* mu,
-                                        Real* mk) {
+                                        Real* mk, bool poisson, const CountTable& ct) {
   float z[QP];
   event_mark_normals<QP>(sk, kg, e, z);
   apply_marks<Q, Real>(Lj, mu, z, mk);
+  if (poisson) {
+    const int n = event_count(sk, kg, e, ct);
+    if (n > 1) {
+      Real c[Q];
+      apply_chol<Q, Real>(Lj, z, c);
+      const Real rn = Real(n), sn = sqrt(rn);
+#pragma unroll
+      for (int i = 0; i < Q; ++i) mk[i] = fma(sn, c[i], rn * mu[i]);
+    }
+  }
 }
 
 // Called by all 32 lanes of a warp whose samples kg are consecutive by lane.
 template <int Q, int QP, int JM, typename Real>
 __device__ __forceinline__ void jump_window(JumpClock& c, int w0, int wend, int W, const StreamKey& sk, uint32_t kg,
                                             const GapSampler& gs, const Real* Lj, const Real* mu, Real jscale,
-                                            Real* wd) {
+                                            Real* wd, bool poisson, const CountTable& ct) {
   const int lane = threadIdx.x & 31;
   uint32_t mask = 0u;
   const uint32_t e0 = c.e;
@@ -400,7 +415,7 @@ __device__ __forceinline__ void jump_window(JumpClock& c, int w0, int wend, int 
       for (int r = 0; r < k; ++r) mL &= mL - 1u;  // the owner's k-th event step
       const int s = __ffs(mL) - 1;
       Real mk[Q];
-      mark_of<Q, QP, Real>(sk, kg - (uint32_t)lane + (uint32_t)L, eL, Lj, mu, mk);
+      mark_of<Q, QP, Real>(sk, kg - (uint32_t)lane + (uint32_t)L, eL, Lj, mu, mk, poisson, ct);
 #pragma unroll
       for (int i = 0; i < Q; ++i) wd[(s * Q + i) * 32 + L] = (JM == 1) ? rmul<Real>(jscale, mk[i]) : mk[i];
     }
@@ -771,7 +786,8 @@ __global__ void __launch_bounds__(kRolloutMaxThreads, (RolloutMinBlocks<Sys, Rea
     for (int t0 = 0; t0 < T; t0 += 4) {
       if (jumps && t0 == wnext) {
         wnext = t0 + JW;
-        jump_window<Q, QP, JM, Real>(clk, t0, min(wnext, T), JW, sk, kg, gs, Lj, mu, jscale, wd);
+        jump_window<Q, QP, JM, Real>(clk, t0, min(wnext, T), JW, sk, kg, gs, Lj, mu, jscale, wd, a.poisson != 0,
+                                       a.cnt);
         wl = wd + (threadIdx.x & 31);
       }
       if (t0 + 4 <= T) {
@@ -934,7 +950,8 @@ __global__ void __launch_bounds__(MAXT) rollout_kernel_ws(const RolloutArgs<Real
         const int t0 = 4 * g;
         if (jumps && t0 == wnext) {
           wnext = t0 + JW;
-          jump_window<Q, QP, JM, Real>(clk, t0, min(wnext, T), JW, sk, kg, gs, Lj, mu, jscale, wd);
+          jump_window<Q, QP, JM, Real>(clk, t0, min(wnext, T), JW, sk, kg, gs, Lj, mu, jscale, wd, a.poisson != 0,
+                                       a.cnt);
           wl = wd + (c & 31);
         }
         float z[4 * MP];
@@ -1061,6 +1078,8 @@ struct PlantArgs {
   double Lj[16];   // chol(Sigma_J)
   double mu_j[4];
   uint32_t jthr;   // plant always has jumps (harness.py:138)
+  int poisson;     // Poisson arrivals: n = #{k : u24 < cnt0[k]} (cnt0[0] = the event threshold)
+  uint32_t cnt0[kMaxCount + 1];
   int q, jmode, has_limits, T, M;
   double u_lo[4], u_hi[4];
   LoopState* loop;
@@ -1076,7 +1095,7 @@ struct PlantPre {
   double ed[4];   // L_D z  (Sigma_D, harness.py:137)
   double mk[4];   // mu + L_J z', drawn every step (harness.py:139)
   int k;
-  int jump;       // U < nu dt (harness.py:138)
+  int jump;       // U < nu dt (harness.py:138); Poisson: the arrival count
 };
 
 template <class Dyn>
@@ -1095,7 +1114,13 @@ __device__ void plant_prepare(const PlantArgs& a, PlantPre& pre) {
   apply_chol<M, double>(a.Lp, z, ed);
   for (int j = 0; j < M; ++j) pre.ed[j] = ed[j];
   const P4 ju = draw(sk, kSlotPlant, 3u * k + 1u, 0u);
-  pre.jump = ju.x < a.jthr ? 1 : 0;
+  if (a.poisson) {
+    int n = 0;
+    for (int i = 0; i <= kMaxCount; ++i) n += (ju.x >> 8) < a.cnt0[i] ? 1 : 0;
+    pre.jump = n;
+  } else {
+    pre.jump = ju.x < a.jthr ? 1 : 0;
+  }
   r = draw(sk, kSlotPlant, 3u * k + 2u, 0u);
   box_muller(r.x, r.y, z[0], z[1]);
   box_muller(r.z, r.w, z[2], z[3]);
@@ -1103,6 +1128,7 @@ __device__ void plant_prepare(const PlantArgs& a, PlantPre& pre) {
     double acc = 0.0;
     for (int l = 0; l <= i && i < a.q; ++l) acc = fma(a.Lj[i * a.q + l], double(z[l]), acc);
     pre.mk[i] = (i < a.q) ? a.mu_j[i] + acc : 0.0;
+    if (pre.jump > 1 && i < a.q) pre.mk[i] = fma(sqrt(double(pre.jump)), acc, double(pre.jump) * a.mu_j[i]);
   }
 }
 
@@ -1142,7 +1168,7 @@ __device__ void plant_finish(const PlantArgs& a, const PlantPre& pre, const doub
     bool fin = true;
     for (int i = 0; i < N; ++i) fin = fin && isfinite(x[i]);
     for (int j = 0; j < M; ++j) L->hist_controls[(size_t)k * M + j] = u0[j];
-    L->hist_jumps[k] = jump ? 1 : 0;
+    L->hist_jumps[k] = pre.jump;
     if (!fin) {  // StateDivergedError -> trial failure (harness.py:144-148)
       L->halted = 1;
       L->status = 7;
@@ -1486,6 +1512,8 @@ struct NoiseArgs {
   int K, T, q, jump_on;
   const uint32_t* gap_thr;  // jump-gap survival table (device), T + 1 entries
   float gap_inv;
+  int poisson;
+  CountTable cnt;
   long long sample_offset;
   uint64_t seed, iteration;
   double Ld[16], Lj[16], mu_j[4];
@@ -1532,10 +1560,12 @@ __global__ void __launch_bounds__(256) noise_kernel(const NoiseArgs a) {
       Real ed[M], ec[M], mk[Q];
       apply_chol<M, Real>(Ld, z + s * MP, ed);
       const bool jump = a.jump_on && t == clk.tj;
+      int count = 0;
 #pragma unroll
       for (int i = 0; i < Q; ++i) mk[i] = Real(0);
       if (jump) {
-        mark_of<Q, QP, Real>(sk, kg, clk.e, Lj, mu, mk);
+        mark_of<Q, QP, Real>(sk, kg, clk.e, Lj, mu, mk, a.poisson != 0, a.cnt);
+        count = a.poisson ? event_count(sk, kg, clk.e, a.cnt) : 1;
         clock_next(clk, sk, kg, gs);
       }
 #pragma unroll
@@ -1548,7 +1578,7 @@ __global__ void __launch_bounds__(256) noise_kernel(const NoiseArgs a) {
       if (a.eps_d)
 #pragma unroll
         for (int j = 0; j < M; ++j) a.eps_d[row * M + j] = double(ed[j]);
-      if (a.ind) a.ind[row] = jump ? 1 : 0;
+      if (a.ind) a.ind[row] = count;  // indicator, or the Poisson arrival count
       if (a.eps_j)
 #pragma unroll
         for (int i = 0; i < Q; ++i) a.eps_j[row * Q + i] = jump ? double(mk[i]) : 0.0;

@@ -28,6 +28,10 @@
 //   slot 2: marks of event e, normal index e*QP + i (QP = q, 3 padded to 4),
 //           block = index>>2, lane = index&3
 //   slot 3: closed-loop plant, block = 3*step + {0 diffusion, 1 uniform, 2 marks}
+//   slot 4: Poisson arrival counts (jump_process = poisson), event e: word e&3
+//           of block e>>2, u = word>>8; n = 1 + #{k in 1..8 : u < C[k]} with
+//           C[k] = floor(2^24 P(N > k | N >= 1)), N ~ Poisson(nu dt) (the
+//           event steps themselves come from slot 1 with p = 1 - exp(-nu dt))
 // Normals: Box-Muller on pairs of words with 23-bit mantissa uniforms.
 // The CPU emulation of this exact mapping is oracle/philox_stream.py.
 #pragma once
@@ -40,7 +44,7 @@ struct P4 {
   uint32_t x, y, z, w;
 };
 
-enum : uint32_t { kSlotDiffusion = 0, kSlotJumpUniform = 1, kSlotMark = 2, kSlotPlant = 3 };
+enum : uint32_t { kSlotDiffusion = 0, kSlotJumpUniform = 1, kSlotMark = 2, kSlotPlant = 3, kSlotCount = 4 };
 
 __host__ __device__ __forceinline__ P4 philox4x32_10(P4 c, uint32_t k0, uint32_t k1) {
 #pragma unroll
@@ -127,6 +131,23 @@ __host__ __device__ __forceinline__ void clock_next(JumpClock& c, const StreamKe
   c.e += 1;
   if ((c.e & 3u) == 0u) c.w = draw(sk, kSlotJumpUniform, c.e >> 2, kg);
   c.tj += 1 + jump_gap(gs, p4_word(c.w, c.e & 3u) >> 8);
+}
+
+// Compound-Poisson arrivals per jump step (BASELINE "Poisson jump counts per
+// step"): thresholds of the zero-truncated count distribution, zero-padded;
+// all zero = Bernoulli (one arrival per event, the reference's zero-one law).
+constexpr int kMaxCount = 8;
+struct CountTable {
+  uint32_t c[kMaxCount];  // c[k-1] = floor(2^24 P(N > k | N >= 1)), k = 1..8
+};
+
+__host__ __device__ __forceinline__ int event_count(const StreamKey& sk, uint32_t kg, uint32_t e,
+                                                    const CountTable& ct) {
+  const uint32_t u = p4_word(draw(sk, kSlotCount, e >> 2, kg), e & 3u) >> 8;
+  int n = 1;
+#pragma unroll
+  for (int k = 0; k < kMaxCount; ++k) n += u < ct.c[k] ? 1 : 0;
+  return n;
 }
 
 #ifdef __CUDACC__

@@ -217,6 +217,7 @@ def describe_mppi(cfg, m: int, q: int, *, samples=None, precision=None, hbm=Fals
     d.noise_source = L.JM_NOISE_HBM if hbm else L.JM_NOISE_PHILOX
     d.sample_offset = int(sample_offset)
     d.block_threads = int(block_threads)
+    d.jump_process = L.JM_JUMPS_POISSON if getattr(cfg, "jump_process", "bernoulli") == "poisson" else L.JM_JUMPS_BERNOULLI
     return d
 
 

@@ -9,6 +9,8 @@ distribution and draw-order contract are the reference's:
   eps_d ~ N(0, c Sigma_D); indicator = U < nu dt (zero-one law);
   marks ~ N(mark_mean, Sigma_J) only at jump events; eps_c = eps_d + eps_j
   for control-channel jumps (eps_d for state-space jumps).
+With MppiConfig.jump_process="poisson" the indicator becomes the Poisson(nu dt)
+arrival count n of the step and eps_j the sum of its n marks.
 """
 
 from __future__ import annotations
