@@ -127,6 +127,78 @@ QUADROTOR_DEFAULTS: Dict = {
 }
 
 
+# run-level keys of both tasks (experiment.py:43-46, :76, :81-84, :115)
+_RUN_DEFAULTS = {"cartpole": {"trials": 40}, "quadrotor": {"trials": 25}}
+_RUN_COMMON: Dict = {"base_seed": 2024, "out_dir": "results", "variants": "both",
+                     "sweep": {"nu": None, "sigma_j": None, "samples": None}}
+
+
+class ExperimentConfigError(ValueError):
+    """A config file that does not resolve (experiment.py:33)."""
+
+
+def _defaults(task) -> Dict:
+    base = {"cartpole": CARTPOLE_DEFAULTS, "quadrotor": QUADROTOR_DEFAULTS}.get(task)
+    if base is None:
+        raise ExperimentConfigError(f"unknown task {task!r}; expected one of ['cartpole', 'quadrotor']")
+    return _merge(_merge(base, _RUN_COMMON), _RUN_DEFAULTS[task])
+
+
+def _unknown_keys(given: Dict, allowed: Dict, path: str = ""):
+    for k, v in given.items():
+        where = f"{path}.{k}" if path else k
+        if k not in allowed:
+            raise ExperimentConfigError(f"unknown key '{where}'")
+        if isinstance(v, dict) and isinstance(allowed[k], dict):
+            _unknown_keys(v, allowed[k], where)
+
+
+def config_from_dict(raw: Dict) -> Dict:
+    """A raw mapping (a parsed pkg/configs/*.yaml) resolved against the task
+    defaults, unknown keys fatal (experiment.py:161-214).  Returns the resolved
+    mapping build_task / build_mppi_config / sweep_cells accept."""
+    if not isinstance(raw, dict):
+        raise ExperimentConfigError("config must be a mapping")
+    d = _defaults(raw.get("task"))
+    _unknown_keys(raw, d)
+    out = _merge(d, raw)
+    if out["variants"] not in ("old", "new", "both"):
+        raise ExperimentConfigError(f"variants must be old|new|both, got {out['variants']!r}")
+    return out
+
+
+def load_config(path: str) -> Dict:
+    """Parse a YAML experiment config (pkg/configs/*.yaml; experiment.py:217-226)."""
+    import yaml
+
+    with open(path) as fh:
+        try:
+            raw = yaml.safe_load(fh)
+        except yaml.YAMLError as exc:
+            raise ExperimentConfigError(f"config parse error: {exc}") from exc
+    return config_from_dict(raw or {})
+
+
+def sweep_cells(exp) -> list:
+    """(nu, sigma_j, samples_m) cells, one factor at a time around the base point
+    (experiment.py:229-243)."""
+    e = resolve(exp)
+    mp = e["mppi"]
+    sw = e.get("sweep") or {}
+    base_nu, base_sj = float(mp["nu"]), float(mp["sigma_j"])
+    if isinstance(exp, dict):
+        nus = [float(v) for v in (sw.get("nu") or [base_nu])]
+        sjs = [float(v) for v in (sw.get("sigma_j") or [base_sj])]
+        sams = [int(v) for v in (sw.get("samples") or [int(mp["samples"])])]
+    else:  # a reference ExperimentConfig
+        nus, sjs, sams = list(exp.sweep_nu), list(exp.sweep_sigma_j), list(exp.sweep_samples)
+    cells = []
+    for c in [(base_nu, s) for s in sjs] + [(v, base_sj) for v in nus if v != base_nu]:
+        if c not in cells:
+            cells.append(c)
+    return [(nu, s, m) for nu, s in cells for m in sams]
+
+
 def _merge(base: Dict, over: Dict) -> Dict:
     out = copy.deepcopy(base)
     for k, v in over.items():
@@ -142,11 +214,7 @@ def resolve(raw) -> Dict:
     """A reference ExperimentConfig (or a raw mapping with the same keys) ->
     plain dict with task defaults merged in."""
     if isinstance(raw, dict):
-        task = raw.get("task")
-        base = {"cartpole": CARTPOLE_DEFAULTS, "quadrotor": QUADROTOR_DEFAULTS}.get(task)
-        if base is None:
-            raise ValueError(f"unknown task {task!r}")
-        return _merge(base, raw)
+        return _merge(_defaults(raw.get("task")), raw)
     return {k: _field(raw, k) for k in ("task", "duration_seconds", "physical", "cost", "mppi",
                                          "control_limits", "diffusion_channel_scale",
                                          "jump_channel_scale")}
