@@ -71,6 +71,7 @@ class Engine final : public EngineBase {
     if constexpr (std::is_same<Dyn, Cartpole>::value) fill_cartpole<R>(c->model, sp);
     if constexpr (std::is_same<Dyn, Quadrotor>::value) fill_quadrotor<R>(c->model, sp);
     fill_cost<R>(c->cost, N, sp);
+    fill_trig(sp.tk);
     sp.ext = reinterpret_cast<const R*>(std::is_same<R, float>::value ? c->d_lin_f : c->d_lin_d);
   }
 

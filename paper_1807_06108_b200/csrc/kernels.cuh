@@ -606,6 +606,8 @@ __global__ void __launch_bounds__(kRolloutMaxThreads, (RolloutMinBlocks<Sys, Rea
     pin(sp.sw[i]);
     pin(sp.swt[i]);
   }
+#pragma unroll
+  for (int i = 0; i < 3; ++i) pin(sp.tk[i]);
   Real Ld[M * M], Lj[Q * Q], mu[Q];
 #pragma unroll
   for (int i = 0; i < M * M; ++i) {
@@ -1002,6 +1004,8 @@ __global__ void __launch_bounds__(MAXT) rollout_kernel_ws(const RolloutArgs<Real
         pin(sp.sw[i]);
         pin(sp.swt[i]);
       }
+#pragma unroll
+      for (int i = 0; i < 3; ++i) pin(sp.tk[i]);
       Real dt = a.dt, sdt = a.sdt, cq = a.cq;
       pin(dt);
       pin(sdt);
@@ -1220,7 +1224,7 @@ struct FinArgs {
 };
 
 inline size_t finalize_smem_bytes(int nrec) {
-  return sizeof(double) * ((size_t)nrec + (size_t)(kFinThreads / 32) * kFinCols);
+  return sizeof(double) * ((size_t)nrec + (size_t)(kFinThreads / 32) * (kFinCols + 1));
 }
 
 template <class Dyn>
@@ -1229,11 +1233,10 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
   constexpr int NW = kFinThreads / 32;
   static_assert(NW == 32, "warp-0 reductions assume 32 warps");
   double* se = fsm;                 // e_b = exp(-(rho_b - rho)/lambda), per record
-  double* part = fsm + a.nrec;      // [NW][kFinCols]
-  __shared__ double s_red[3][NW];
+  double* part = fsm + a.nrec;      // [NW][kFinCols + 1] (padded: conflict-free column reads)
+  __shared__ double s_red[4][NW];
   __shared__ double s_delta[kFinCols];
   __shared__ double s_unew[kFinCols];  // this CTA's u_new columns (single CTA: the whole sequence)
-  __shared__ double s_bc[4];
   __shared__ int s_last;
   __shared__ PlantPre s_pre;
   // batched trials: blockIdx.y selects the trial's records, controls, counter and loop state
@@ -1283,23 +1286,11 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
     __threadfence();
     recs += (size_t)(epoch & 1u) * a.nrec * rs;
   }
-  // the column pass below reads every record's N block: start those lines
-  // towards L1 now, under the head reductions
-  {
-    constexpr int CPL = kFinCols / 32;
-    for (int b = warp; b < a.nrec; b += NW) {
-      const double* r = recs + (size_t)b * rs + 4;
-#pragma unroll
-      for (int i = 0; i < CPL; ++i) {
-        const int c = c0 + lane + 32 * i;
-        if (c < a.TM && ((c & 15) == 0 || c == c0 + lane)) asm volatile("prefetch.global.L1 [%0];" ::"l"(r + c));
-      }
-    }
-  }
   // global rho (controller.py:69: min over finite costs) and the rescaled
   // sums in one pass over the record heads (<= 1024 records: one per thread,
-  // held in registers); block reductions finish in warp 0 with shuffles
-  // (fixed order), not serial thread-0 loops
+  // held in registers).  Block reductions: warp partials -> shared memory ->
+  // one barrier -> every warp reduces the 32 partials itself (fixed order, so
+  // all warps agree bit for bit), instead of warp 0 + a broadcast barrier.
   double h0 = CUDART_INF, h1 = 0.0, h2 = 0.0, h3 = 0.0;
   const bool one_pass = a.nrec <= kFinThreads;
   double m = CUDART_INF;
@@ -1315,15 +1306,23 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
   } else {
     for (int b = tid; b < a.nrec; b += kFinThreads) m = fmin(m, recs[(size_t)b * rs]);
   }
+  // the column pass below reads every record's N block: start those lines
+  // towards L1 now (after the head loads are issued), under the reductions
+  {
+    constexpr int CPL = kFinCols / 32;
+    for (int b = warp; b < a.nrec; b += NW) {
+      const double* r = recs + (size_t)b * rs + 4;
+#pragma unroll
+      for (int i = 0; i < CPL; ++i) {
+        const int c = c0 + lane + 32 * i;
+        if (c < a.TM && ((c & 15) == 0 || c == c0 + lane)) asm volatile("prefetch.global.L1 [%0];" ::"l"(r + c));
+      }
+    }
+  }
   m = warp_min(m);
   if (lane == 0) s_red[0][warp] = m;
   __syncthreads();
-  if (warp == 0) {
-    double mm = warp_min(s_red[0][lane]);
-    if (lane == 0) s_bc[0] = mm;
-  }
-  __syncthreads();
-  const double rho = s_bc[0];
+  const double rho = warp_min(s_red[0][lane]);
   double z = 0.0, w2 = 0.0, nf = 0.0;
   if (one_pass) {
     if (tid < a.nrec) {
@@ -1347,21 +1346,12 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
   w2 = warp_sum(w2);
   nf = warp_sum(nf);
   if (lane == 0) {
-    s_red[0][warp] = z;
-    s_red[1][warp] = w2;
-    s_red[2][warp] = nf;
+    s_red[1][warp] = z;
+    s_red[2][warp] = w2;
+    s_red[3][warp] = nf;
   }
   __syncthreads();
-  if (warp == 0) {
-    const double zz = warp_sum(s_red[0][lane]), ww = warp_sum(s_red[1][lane]), nn = warp_sum(s_red[2][lane]);
-    if (lane == 0) {
-      s_bc[1] = zz;
-      s_bc[2] = ww;
-      s_bc[3] = nn;
-    }
-  }
-  __syncthreads();
-  const double Z = s_bc[1], W2 = s_bc[2], NF = s_bc[3];
+  const double Z = warp_sum(s_red[1][lane]), W2 = warp_sum(s_red[2][lane]), NF = warp_sum(s_red[3][lane]);
   if (rho == CUDART_INF) {  // controller.py:66-67
     if (blockIdx.x == 0 && tid == 0) {
       if (a.status) *a.status = 3;  // JM_ERR_NO_VIABLE
@@ -1405,12 +1395,12 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
     }
   }
 #pragma unroll
-  for (int i = 0; i < CPL; ++i) part[warp * kFinCols + lane + 32 * i] = acc[i];
+  for (int i = 0; i < CPL; ++i) part[warp * (kFinCols + 1) + lane + 32 * i] = acc[i];
   __syncthreads();
   // cross-warp column sums: warp w reduces columns w, w+32, ... over the 32
   // warp partials with a shuffle tree (fixed order)
   for (int col = warp; col < kFinCols; col += NW) {
-    const double v = warp_sum(part[lane * kFinCols + col]);
+    const double v = warp_sum(part[lane * (kFinCols + 1) + col]);
     if (lane == 0) s_delta[col] = v;
   }
   __syncthreads();
