@@ -62,6 +62,8 @@ def parse():
     p.add_argument("--samples", type=int, default=None, help="override K per GPU")
     p.add_argument("--horizon", type=int, default=None, help="override T")
     p.add_argument("--block", type=int, default=0, help="override the rollout tile (block_threads, tuning)")
+    p.add_argument("--nu", type=float, default=None, help="override the jump rate (tuning; 0 = no jumps)")
+    p.add_argument("--jump-process", default=None, choices=["bernoulli", "poisson"], help="override the jump process")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--profile", action="store_true", help="ncu mode: no clock settle, e2e or CPU legs")
@@ -280,6 +282,11 @@ def ours_arm(a):
     w = WORKLOADS[a.workload]
     idx = w["index"]
     task, cfg = jb.baseline_config(idx, K=a.samples, T=a.horizon)
+    if a.nu is not None or a.jump_process is not None:
+        import dataclasses
+
+        cfg = dataclasses.replace(cfg, nu=cfg.nu if a.nu is None else a.nu,
+                                  jump_process=a.jump_process or cfg.jump_process)
     system = task.name
     K, T = cfg.samples_m, cfg.horizon_n
     hbm = a.noise == "hbm"
@@ -388,7 +395,8 @@ def ours_arm(a):
         "config": {"workload": f"{a.workload}: BASELINE config {idx} ({system}, K={K}, T={T}, "
                                f"{'closed-loop control step' if use_loop else 'single MPC iteration'}, "
                                f"state-space jumps, {a.noise} noise)",
-                   "K": K, "T": T, "system": system, "noise": a.noise, "l2": "flushed (256 MiB memset) before each timed step",
+                   "K": K, "T": T, "system": system, "noise": a.noise, "nu": cfg.nu, "jump_process": cfg.jump_process,
+                   "l2": "flushed (256 MiB memset) before each timed step",
                    "step": "rollout+weighting/update+plant+shift; the K timed steps are one CUDA graph (per step: L2 flush, event, 2 kernels, event)" if use_loop else "rollout+weighting/update"},
         "mpc_iteration_latency_ms": ms,
         "roofline": roof,

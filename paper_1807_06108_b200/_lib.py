@@ -12,7 +12,7 @@ import threading
 from pathlib import Path
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "libjmppi.so"
+LIB_PATH = Path(os.environ["JM_LIB"]) if os.environ.get("JM_LIB") else _HERE / "libjmppi.so"  # JM_LIB: tuning builds
 
 JM_OK = 0
 JM_ERR_CONFIG = 1

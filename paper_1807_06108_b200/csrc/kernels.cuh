@@ -29,7 +29,10 @@
 namespace jm {
 
 constexpr int kFinCols = 128;      // finalize: columns per CTA (multiple of m for m in {1,2,4})
-constexpr int kFinThreads = 1024;  // finalize: 32 warps split the records
+#ifndef JM_FIN_THREADS
+#define JM_FIN_THREADS 1024
+#endif
+constexpr int kFinThreads = JM_FIN_THREADS;  // finalize: its warps split the records
 constexpr int kMaxRecords = 4096;
 constexpr int kRolloutMaxThreads = 512;
 
@@ -94,6 +97,21 @@ __device__ __forceinline__ T warp_min(T v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
   return v;
+}
+
+// exact warp minimum of doubles (no NaNs) on the integer reduction unit: an
+// order-preserving 64-bit key, min of the high words, then of the low words
+// among the lanes holding that high word -- two REDUX instead of five rounds of
+// 64-bit shuffles
+__device__ __forceinline__ double warp_min_redux(double v) {
+  unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  b ^= (b >> 63) ? ~0ull : (1ull << 63);
+  const uint32_t hi = (uint32_t)(b >> 32), lo = (uint32_t)b;
+  const uint32_t mh = __reduce_min_sync(0xFFFFFFFFu, hi);
+  const uint32_t ml = __reduce_min_sync(0xFFFFFFFFu, hi == mh ? lo : 0xFFFFFFFFu);
+  unsigned long long k = ((unsigned long long)mh << 32) | ml;
+  k ^= (k >> 63) ? (1ull << 63) : ~0ull;
+  return __longlong_as_double((long long)k);
 }
 
 template <typename Real>
@@ -1201,6 +1219,14 @@ __device__ void plant_finish(const PlantArgs& a, const PlantPre& pre, const doub
 }
 
 // ---------------------------------------------------------------- finalize
+// -DJM_FIN_STAMPS (tuning builds only): thread 0 records clock64() at the phase
+// boundaries and writes the cycles since kernel entry into a.norms[0..] (the
+// drop-in call returns them as per_step_update_norm)
+#ifdef JM_FIN_STAMPS
+#define FIN_STAMP() (fin_ts[fin_nts++] = clock64())
+#else
+#define FIN_STAMP() ((void)0)
+#endif
 struct FinArgs {
   const double* rec;
   int nrec, rec_stride, TM, M;
@@ -1231,7 +1257,7 @@ template <class Dyn>
 __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, const PlantArgs p) {
   extern __shared__ double fsm[];
   constexpr int NW = kFinThreads / 32;
-  static_assert(NW == 32, "warp-0 reductions assume 32 warps");
+  static_assert(NW <= 32 && (NW & (NW - 1)) == 0, "block reductions: one partial per lane");
   double* se = fsm;                 // e_b = exp(-(rho_b - rho)/lambda), per record
   double* part = fsm + a.nrec;      // [NW][kFinCols + 1] (padded: conflict-free column reads)
   __shared__ double s_red[4][NW];
@@ -1247,6 +1273,11 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
   unsigned int* const counter = a.counter ? a.counter + trial : nullptr;
   LoopState* L = a.loop ? a.loop + trial : nullptr;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#ifdef JM_FIN_STAMPS
+  long long fin_ts[12];
+  int fin_nts = 0;
+  FIN_STAMP();
+#endif
   // closed loop: LoopState reads and the plant noise do not depend on the
   // rollout, so they run before the grid dependency resolves; so do the
   // nominal controls (written by the previous step's shift / the input copy,
@@ -1259,6 +1290,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
   grid_dep_wait();
   if (halted) return;
   const int rs = a.rec_stride;
+  FIN_STAMP();
   if (a.wait_flags != nullptr) {  // every rank's CTA records arrive over NVLink (write_record)
     const uint32_t epoch = (uint32_t)L->step + 1u;
     // a peer that never pushes (a dead rank) must not hang the GPU: after 30 s
@@ -1319,10 +1351,11 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
       }
     }
   }
-  m = warp_min(m);
+  m = warp_min_redux(m);
   if (lane == 0) s_red[0][warp] = m;
   __syncthreads();
-  const double rho = warp_min(s_red[0][lane]);
+  const double rho = warp_min_redux(lane < NW ? s_red[0][lane] : CUDART_INF);
+  FIN_STAMP();
   double z = 0.0, w2 = 0.0, nf = 0.0;
   if (one_pass) {
     if (tid < a.nrec) {
@@ -1351,7 +1384,9 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
     s_red[3][warp] = nf;
   }
   __syncthreads();
-  const double Z = warp_sum(s_red[1][lane]), W2 = warp_sum(s_red[2][lane]), NF = warp_sum(s_red[3][lane]);
+  const double Z = warp_sum(lane < NW ? s_red[1][lane] : 0.0), W2 = warp_sum(lane < NW ? s_red[2][lane] : 0.0),
+               NF = warp_sum(lane < NW ? s_red[3][lane] : 0.0);
+  FIN_STAMP();
   if (rho == CUDART_INF) {  // controller.py:66-67
     if (blockIdx.x == 0 && tid == 0) {
       if (a.status) *a.status = 3;  // JM_ERR_NO_VIABLE
@@ -1397,13 +1432,23 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
 #pragma unroll
   for (int i = 0; i < CPL; ++i) part[warp * (kFinCols + 1) + lane + 32 * i] = acc[i];
   __syncthreads();
-  // cross-warp column sums: warp w reduces columns w, w+32, ... over the 32
-  // warp partials with a shuffle tree (fixed order)
-  for (int col = warp; col < kFinCols; col += NW) {
-    const double v = warp_sum(part[lane * (kFinCols + 1) + col]);
-    if (lane == 0) s_delta[col] = v;
+  FIN_STAMP();
+  // cross-warp column sums: thread c adds the NW warp partials of column c
+  // (consecutive columns: conflict-free) in four interleaved chains, then
+  // combines them -- fixed order, no 64-bit shuffle rounds
+  if (tid < kFinCols) {
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; w += 4) {
+      v0 += part[(w + 0) * (kFinCols + 1) + tid];
+      if (w + 1 < NW) v1 += part[(w + 1) * (kFinCols + 1) + tid];
+      if (w + 2 < NW) v2 += part[(w + 2) * (kFinCols + 1) + tid];
+      if (w + 3 < NW) v3 += part[(w + 3) * (kFinCols + 1) + tid];
+    }
+    s_delta[tid] = (v0 + v1) + (v2 + v3);
   }
   __syncthreads();
+  FIN_STAMP();
   if (reduce_mode) {
     if (blockIdx.x == 0 && tid == 0) {
       a.rec_out[0] = rho;
@@ -1435,6 +1480,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
     unew[c] = un;
   }
   __syncthreads();
+  FIN_STAMP();
   if (a.norms) {  // per_step_update_norm (controller.py:168)
     const int tl = tid, t = c0 / M + tl;
     if (tl < kFinCols / M && t * M < a.TM) {
@@ -1451,6 +1497,12 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
     const int TM = a.TM, Mm = a.M;
     for (int i = tid; i < TM; i += kFinThreads)
       a.u_shift[i] = (i < TM - Mm) ? s_unew[i + Mm] : a.u_init[i - (TM - Mm)];
+#ifdef JM_FIN_STAMPS
+    FIN_STAMP();
+    __syncthreads();
+    if (tid == 0 && a.norms)
+      for (int i = 1; i < fin_nts; ++i) a.norms[i - 1] = double(fin_ts[i] - fin_ts[0]);
+#endif
     if (a.done != nullptr) {
       __syncthreads();
       if (tid == 0) {
