@@ -161,8 +161,15 @@ class Engine final : public EngineBase {
     int W = 32;
     while (W > 8 && plan_bytes(c, block, mwarps, W, nring, single) > budget) W -= 4;
     c->jw_len = W;
-    c->eps_smem = single && plan_bytes(c, block, mwarps, W, nring, true) <= cap;
-    const size_t msmem = plan_bytes(c, block, mwarps, W, nring, c->eps_smem);
+    // the non-WS single-wave kernel stages its jump marks in the eps slab rows
+    // (kernels.cuh jump_window): no mark buffer, windows of up to 64 steps,
+    // balanced over the horizon (T = 100: two windows of 52 and 48)
+    const int nwin = (c->T + 63) / 64;
+    c->jw_slab = std::min(64, ((c->T + nwin - 1) / nwin + 3) / 4 * 4);
+    c->eps_smem = single && (ws ? plan_bytes(c, block, mwarps, W, nring, true)
+                                : plan_bytes(c, block, 0, 0, nring, true)) <= cap;
+    const size_t msmem = (c->eps_smem && !ws) ? plan_bytes(c, block, 0, 0, nring, true)
+                                              : plan_bytes(c, block, mwarps, W, nring, c->eps_smem);
     const size_t smem = plan_bytes(c, block, mwarps, W, 0, false);  // trace / HBM kernels
     const void* fn = nullptr;
     const bool sj = c->model.jump_channel == JM_JUMP_STATE;
@@ -266,8 +273,11 @@ class Engine final : public EngineBase {
     if (philox && !trace && c->ws)
       return c->eps_smem ? launch_pdl(ws_kern<JM, true>(), grid, dim3(2 * c->block), c->main_smem, c->stream, a)
                          : launch_pdl(ws_kern<JM, false>(), grid, dim3(2 * c->block), c->main_smem, c->stream, a);
-    if (philox && !trace && c->eps_smem)
-      return launch_pdl(rollout_kernel<Sys, Real, true, false, JM, true>, grid, block, c->main_smem, c->stream, a);
+    if (philox && !trace && c->eps_smem) {
+      RolloutArgs<Real> b = a;
+      b.jw_len = c->jw_slab;  // marks staged in the eps slab (jump_window, 64-bit masks)
+      return launch_pdl(rollout_kernel<Sys, Real, true, false, JM, true>, grid, block, c->main_smem, c->stream, b);
+    }
     if (philox && !trace)
       return launch_pdl(rollout_kernel<Sys, Real, true, false, JM>, grid, block, c->main_smem, c->stream, a);
     RolloutArgs<Real> b = a;

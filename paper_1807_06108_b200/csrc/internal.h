@@ -71,6 +71,7 @@ struct jm_ctx {
   uint32_t cnt_plant[jm::kMaxCount + 1] = {};  // plant: n = #{k : u24 < cnt_plant[k]}
   uint32_t* d_gap = nullptr;  // jump-gap survival table (philox.cuh), gap_n = T + 1 entries
   int gap_n = 0;
+  int jw_slab = 0;             // jump window of the slab-staged (single-wave, non-WS) rollout
   float gap_inv = 0.f;        // 1 / log2(1 - p)
   int jw_len = 32;            // jump window of the rollout kernels (steps)
   jm::EngineBase* eng = nullptr;

@@ -392,17 +392,22 @@ __device__ __forceinline__ void mark_of(const StreamKey& sk, uint32_t kg, uint32
 }
 
 // Called by all 32 lanes of a warp whose samples kg are consecutive by lane.
-template <int Q, int QP, int JM, typename Real>
+// Staging layout: entry (step s of the window, component i, lane L) at
+// wd[(s * RQ + i) * CS + L] -- a per-warp buffer (RQ = Q, CS = 32), or the
+// rows of the CTA's shared-memory eps slab that steps w0.. have not written
+// yet (RQ = m, CS = tile; the step reads its mark there just before storing
+// its eps_combined over it).  MaskT: 32- or 64-bit event masks (W <= 64).
+template <int Q, int QP, int JM, typename Real, typename MaskT = uint32_t, int RQ = Q>
 __device__ __forceinline__ void jump_window(JumpClock& c, int w0, int wend, int W, const StreamKey& sk, uint32_t kg,
                                             const GapSampler& gs, const Real* Lj, const Real* mu, Real jscale,
-                                            Real* wd, bool poisson, const CountTable& ct) {
+                                            Real* wd, bool poisson, const CountTable& ct, int CS = 32) {
   const int lane = threadIdx.x & 31;
-  uint32_t mask = 0u;
+  MaskT mask = 0u;
   const uint32_t e0 = c.e;
   int n = 0;
   while (__any_sync(0xFFFFFFFFu, c.tj < wend)) {
     if (c.tj < wend) {
-      mask |= 1u << (c.tj - w0);
+      mask |= MaskT(1) << (c.tj - w0);
       ++n;
       clock_next(c, sk, kg, gs);
     }
@@ -416,7 +421,10 @@ __device__ __forceinline__ void jump_window(JumpClock& c, int w0, int wend, int 
   const int off = inc - n;
   const int tot = __shfl_sync(0xFFFFFFFFu, inc, 31);
   __syncwarp();  // the previous window's marks have been read
-  for (int i = 0; i < W * Q; ++i) wd[i * 32 + lane] = Real(0);
+  // (only the window's steps: the slab has no rows past the horizon)
+  for (int t = 0; t < wend - w0; ++t)
+#pragma unroll
+    for (int i = 0; i < Q; ++i) wd[(t * RQ + i) * CS + lane] = Real(0);
   __syncwarp();
   for (int j0 = 0; j0 < tot; j0 += 32) {
     const int j = j0 + lane;
@@ -428,14 +436,14 @@ __device__ __forceinline__ void jump_window(JumpClock& c, int w0, int wend, int 
     }
     const int k = j - __shfl_sync(0xFFFFFFFFu, off, L);
     const uint32_t eL = __shfl_sync(0xFFFFFFFFu, e0, L) + (uint32_t)k;
-    uint32_t mL = __shfl_sync(0xFFFFFFFFu, mask, L);
+    MaskT mL = __shfl_sync(0xFFFFFFFFu, mask, L);
     if (j < tot) {
       for (int r = 0; r < k; ++r) mL &= mL - 1u;  // the owner's k-th event step
-      const int s = __ffs(mL) - 1;
+      const int s = (sizeof(MaskT) == 8 ? __ffsll((long long)mL) : __ffs((int)mL)) - 1;
       Real mk[Q];
       mark_of<Q, QP, Real>(sk, kg - (uint32_t)lane + (uint32_t)L, eL, Lj, mu, mk, poisson, ct);
 #pragma unroll
-      for (int i = 0; i < Q; ++i) wd[(s * Q + i) * 32 + L] = (JM == 1) ? rmul<Real>(jscale, mk[i]) : mk[i];
+      for (int i = 0; i < Q; ++i) wd[(s * RQ + i) * CS + L] = (JM == 1) ? rmul<Real>(jscale, mk[i]) : mk[i];
     }
   }
   __syncwarp();
@@ -591,7 +599,8 @@ __global__ void __launch_bounds__(kRolloutMaxThreads, (RolloutMinBlocks<Sys, Rea
   const int tileK = blockDim.x, nwarps = blockDim.x >> 5;
   static_assert(!SCR_SMEM || (PHILOX && !TRACE), "shared-memory scratch: Philox main kernel only");
   constexpr bool in_smem = SCR_SMEM;
-  const SmemPlan sp_ = smem_plan(TM, T * TS, tileK, a.jump_on ? nwarps * 32 * a.jw_len * Q : 0, 0,
+  // SCR_SMEM: jump marks are staged in the eps slab itself (no separate buffer)
+  const SmemPlan sp_ = smem_plan(TM, T * TS, tileK, (a.jump_on && !SCR_SMEM) ? nwarps * 32 * a.jw_len * Q : 0, 0,
                                  in_smem ? TM * tileK : 0, a.gap_n, (int)sizeof(Real));
   (void)nwarps;
   char* const sb = reinterpret_cast<char*>(smem_d);
@@ -723,15 +732,18 @@ __global__ void __launch_bounds__(kRolloutMaxThreads, (RolloutMinBlocks<Sys, Rea
       if (PHILOX) {
         apply_chol<M, Real>(Ld, zz + s2 * MP, eps);
         if (jumps) {
+          // staged marks: the separate buffer, or this step's own slab rows (SCR_SMEM)
+          const Real* mrow = SCR_SMEM ? ep : wl;
+          const int mcs = SCR_SMEM ? tileK : 32;
           if (JM == 0) {
 #pragma unroll
-            for (int j = 0; j < M; ++j) eps[j] = radd<Real>(eps[j], wl[j * 32]);  // eps_c = eps_d + eps_j (noise.py:156-157)
+            for (int j = 0; j < M; ++j) eps[j] = radd<Real>(eps[j], mrow[j * mcs]);  // eps_c = eps_d + eps_j (noise.py:156-157)
           } else {
 #pragma unroll
-            for (int i = 0; i < Q; ++i) sj[i] = wl[i * 32];  // jscale * ind * mark
+            for (int i = 0; i < Q; ++i) sj[i] = mrow[i * mcs];  // jscale * ind * mark
             has_sj = true;
           }
-          wl += Q * 32;
+          if (!SCR_SMEM) wl += Q * 32;
         }
 #pragma unroll
         for (int j = 0; j < M; ++j) ep[(size_t)j * tileK] = eps[j];
@@ -806,9 +818,15 @@ __global__ void __launch_bounds__(kRolloutMaxThreads, (RolloutMinBlocks<Sys, Rea
     for (int t0 = 0; t0 < T; t0 += 4) {
       if (jumps && t0 == wnext) {
         wnext = t0 + JW;
-        jump_window<Q, QP, JM, Real>(clk, t0, min(wnext, T), JW, sk, kg, gs, Lj, mu, jscale, wd, a.poisson != 0,
+        if (SCR_SMEM) {
+          jump_window<Q, QP, JM, Real, uint64_t, M>(clk, t0, min(wnext, T), JW, sk, kg, gs, Lj, mu, jscale,
+                                                    scr + (size_t)t0 * M * tileK + (threadIdx.x & ~31), a.poisson != 0,
+                                                    a.cnt, tileK);
+        } else {
+          jump_window<Q, QP, JM, Real>(clk, t0, min(wnext, T), JW, sk, kg, gs, Lj, mu, jscale, wd, a.poisson != 0,
                                        a.cnt);
-        wl = wd + (threadIdx.x & 31);
+          wl = wd + (threadIdx.x & 31);
+        }
       }
       if (t0 + 4 <= T) {
         float zn[ZW], zmn[ZMW];
