@@ -223,25 +223,24 @@ template <typename Real, int SPT, int RPW>
 __device__ __forceinline__ void tile_epilogue(const Real* Sf, const int* cols, int nk, const Real* src,
                                               size_t rstride, int TM, Real inv_lam, Real* sw, double* Nacc,
                                               double (*s_red)[32], double* s_acc, double* s_bc) {
+  (void)s_bc;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  Real mloc = Sf[0];
+  // tile minimum: warp minimum on the REDUX unit (NaN costs count as +inf,
+  // they get weight 0 either way), partials in shared memory, one barrier,
+  // then every warp reduces the partials itself -- no serial thread-0 pass
+  Real mloc = r_inf<Real>();
 #pragma unroll
-  for (int u = 1; u < SPT; ++u) mloc = fmin(mloc, Sf[u]);
-  const Real m = warp_min(mloc);
-  if (lane == 0) s_red[0][warp] = double(m);
+  for (int u = 0; u < SPT; ++u) mloc = fmin(mloc, Sf[u]);
+  const double m = warp_min_redux(double(mloc));
+  if (lane == 0) s_red[0][warp] = m;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    double mm = CUDART_INF;
-    for (int w = 0; w < nwarps; ++w) mm = fmin(mm, s_red[0][w]);
-    const double rho_prev = s_acc[0];
-    const double rho_new = fmin(rho_prev, mm);
-    s_bc[0] = rho_new;
-    s_bc[1] = (rho_prev == CUDART_INF) ? 0.0 : exp((rho_new - rho_prev) * double(inv_lam));
-  }
-  __syncthreads();
-  const double rho_new = s_bc[0], scale_old = s_bc[1];
+  const double mm = warp_min_redux(lane < nwarps ? s_red[0][lane] : CUDART_INF);
+  const double rho_prev = s_acc[0];
+  const double rho_new = fmin(rho_prev, mm);
   if (rho_new == CUDART_INF) return;  // no finite cost yet in this CTA (uniform)
-  double z1 = 0.0, z2 = 0.0, nf = 0.0;
+  const double scale_old = (rho_prev == CUDART_INF) ? 0.0 : exp((rho_new - rho_prev) * double(inv_lam));
+  double z1 = 0.0, z2 = 0.0;
+  int nf = 0;
 #pragma unroll
   for (int u = 0; u < SPT; ++u) {
     const bool fin = Sf[u] < r_inf<Real>();
@@ -249,24 +248,23 @@ __device__ __forceinline__ void tile_epilogue(const Real* Sf, const int* cols, i
     if (cols[u] >= 0) sw[cols[u]] = w;
     z1 += double(w);
     z2 += double(w) * double(w);
-    nf += fin ? 1.0 : 0.0;
+    nf += fin ? 1 : 0;
   }
   z1 = warp_sum(z1);
   z2 = warp_sum(z2);
-  nf = warp_sum(nf);
-  __syncwarp();
+  nf = __reduce_add_sync(0xFFFFFFFFu, nf);
   if (lane == 0) {
-    s_red[0][warp] = z1;
-    s_red[1][warp] = z2;
-    s_red[2][warp] = nf;
+    s_red[1][warp] = z1;
+    s_red[2][warp] = z2;
+    s_red[3][warp] = double(nf);
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  __syncthreads();  // sw[] and the partials are complete; s_acc[0] has been read by every thread
+  if (warp == nwarps - 1 && lane == 0) {  // the last warp has the fewest row blocks below
     double a1 = 0.0, a2 = 0.0, a3 = 0.0;
     for (int w2 = 0; w2 < nwarps; ++w2) {
-      a1 += s_red[0][w2];
-      a2 += s_red[1][w2];
-      a3 += s_red[2][w2];
+      a1 += s_red[1][w2];
+      a2 += s_red[2][w2];
+      a3 += s_red[3][w2];
     }
     s_acc[0] = rho_new;
     s_acc[1] = s_acc[1] * scale_old + a1;
@@ -591,7 +589,7 @@ __global__ void __launch_bounds__(kRolloutMaxThreads, (RolloutMinBlocks<Sys, Rea
   constexpr int TS = 2 * M + 1;
 
   extern __shared__ double smem_d[];
-  __shared__ double s_red[3][32];
+  __shared__ double s_red[4][32];
   __shared__ double s_acc[4];  // rho, Z, W2, nfinite of this CTA
   __shared__ double s_bc[2];
 
@@ -611,6 +609,14 @@ __global__ void __launch_bounds__(kRolloutMaxThreads, (RolloutMinBlocks<Sys, Rea
   Real* const wd = reinterpret_cast<Real*>(sb + sp_.marks) + (threadIdx.x >> 5) * 32 * a.jw_len * Q;
   Real* const scr = in_smem ? reinterpret_cast<Real*>(sb + sp_.scr)
                             : a.eps_out + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * TM * tileK;
+#ifdef JM_ROLL_STAMPS  // tuning builds: CTA 0's phase clocks land in costs[0..6] (costs requested)
+  long long rts[8];
+  int rn = 0;
+  rts[rn++] = clock64();
+#define ROLL_STAMP() (rts[rn++] = clock64())
+#else
+#define ROLL_STAMP() ((void)0)
+#endif
 
   grid_dep_wait();    // u_nom / x / iteration come from the previous control step
   grid_dep_launch();  // (after the wait: the finalize's pre-wait prologue reads the
@@ -621,8 +627,10 @@ __global__ void __launch_bounds__(kRolloutMaxThreads, (RolloutMinBlocks<Sys, Rea
   const uint64_t iter = L ? L->iteration : (a.iteration_dev ? *a.iteration_dev : a.iteration);
   const double* x0 = L ? L->x : a.x0;
   if (L != nullptr && blockIdx.x == 0 && threadIdx.x == 0) L->t_start[L->step] = globaltimer();
+  ROLL_STAMP();
   rollout_prologue<M, Real>(a, a.u_nom + (size_t)blockIdx.y * TM, tab, Nacc, s_acc, Sg);
   __syncthreads();
+  ROLL_STAMP();
 
   // loop-invariant parameters, pinned in registers
   SysParams<Real> sp = a.sp;
@@ -875,9 +883,15 @@ __global__ void __launch_bounds__(kRolloutMaxThreads, (RolloutMinBlocks<Sys, Rea
     if (act && costs_out) costs_out[kl] = double(S);
     const Real Sf = act ? S : r_inf<Real>();
     const int col = threadIdx.x;
+    ROLL_STAMP();
+#ifdef JM_ROLL_STAMPS
+    __syncthreads();
+    ROLL_STAMP();
+#endif
     // ---- per-CTA online softmax over this tile (K3/K4 partials) ----
     tile_epilogue<Real, 1, (SCR_SMEM || N > 4) ? 8 : 16>(&Sf, &col, min(tileK, K - base), PHILOX ? scr : a.eps_in + base,
                            PHILOX ? (size_t)tileK : (size_t)K, TM, a.inv_lam, sw, Nacc, s_red, s_acc, s_bc);
+    ROLL_STAMP();
   }
   };
   if (a.general)
@@ -886,6 +900,12 @@ __global__ void __launch_bounds__(kRolloutMaxThreads, (RolloutMinBlocks<Sys, Rea
     tiles(std::false_type{});
   __syncthreads();
   write_record(a, s_acc, Nacc);
+#ifdef JM_ROLL_STAMPS
+  ROLL_STAMP();
+  double* const co = a.costs_dev ? *a.costs_dev : a.costs;
+  if (co && blockIdx.x == 0 && threadIdx.x == 0)
+    for (int i = 1; i < rn; ++i) co[i - 1] = double(rts[i] - rts[0]);
+#endif
 }
 
 // ---------------------------------------------------------------- rollout, warp-specialised
@@ -925,7 +945,7 @@ __global__ void __launch_bounds__(MAXT) rollout_kernel_ws(const RolloutArgs<Real
   constexpr int GW = WsShape<Sys, JM>::GW;
 
   extern __shared__ double smem_d[];
-  __shared__ double s_red[3][32];
+  __shared__ double s_red[4][32];
   __shared__ double s_acc[4];
   __shared__ double s_bc[2];
 
