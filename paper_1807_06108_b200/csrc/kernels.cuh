@@ -238,7 +238,12 @@ __device__ __forceinline__ void tile_epilogue(const Real* Sf, const int* cols, i
   const double rho_prev = s_acc[0];
   const double rho_new = fmin(rho_prev, mm);
   if (rho_new == CUDART_INF) return;  // no finite cost yet in this CTA (uniform)
-  const double scale_old = (rho_prev == CUDART_INF) ? 0.0 : exp((rho_new - rho_prev) * double(inv_lam));
+  // rescale of the CTA's earlier tiles (multi-tile CTAs): one exp per warp
+  double scale_old = 0.0;
+  if (rho_prev != CUDART_INF) {
+    const double e = lane == 0 ? exp((rho_new - rho_prev) * double(inv_lam)) : 0.0;
+    scale_old = __shfl_sync(0xFFFFFFFFu, e, 0);
+  }
   double z1 = 0.0, z2 = 0.0;
   int nf = 0;
 #pragma unroll
@@ -641,8 +646,10 @@ __global__ void __launch_bounds__(kRolloutMaxThreads, (RolloutMinBlocks<Sys, Rea
     pin(sp.sw[i]);
     pin(sp.swt[i]);
   }
+  if (SCR_SMEM) {  // (the multi-wave kernels run at the 128-register cap: no room to pin them)
 #pragma unroll
-  for (int i = 0; i < 3; ++i) pin(sp.tk[i]);
+    for (int i = 0; i < 3; ++i) pin(sp.tk[i]);
+  }
   Real Ld[M * M], Lj[Q * Q], mu[Q];
 #pragma unroll
   for (int i = 0; i < M * M; ++i) {
@@ -694,7 +701,7 @@ __global__ void __launch_bounds__(kRolloutMaxThreads, (RolloutMinBlocks<Sys, Rea
       // q dt + 1/2 u'Ru dt + lambda sqrt(dt) u'eps + 1/2 lambda (1-1/c) eps'eps
       // (eps'eps formed first, as costs.py:101/:514, so an overflowing eps
       // gives NaN even when c = 1)
-      const auto ax = Dyn::template aux<Real>(x, sp);
+      const auto ax = Dyn::template aux<Real, SCR_SMEM || !PHILOX>(x, sp);
       const Real qv = Cost::template q<Dyn, Real>(x, ax, sp);
       const Real* st = tab + t * TS;
       Real inc = fma(qv, dt, st[M]);
@@ -875,7 +882,7 @@ __global__ void __launch_bounds__(kRolloutMaxThreads, (RolloutMinBlocks<Sys, Rea
       if (act) a.diverged[kl] = dstep;
     }
     if (fin) {
-      const auto ax = Dyn::template aux<Real>(x, sp);
+      const auto ax = Dyn::template aux<Real, SCR_SMEM || !PHILOX>(x, sp);
       S += sp.term_scale * Cost::template q<Dyn, Real>(x, ax, sp);  // controller.py:155
     } else {
       S = r_inf<Real>();
@@ -1071,7 +1078,7 @@ __global__ void __launch_bounds__(MAXT) rollout_kernel_ws(const RolloutArgs<Real
       for (int i = 0; i < N; ++i) x[i] = Real(x0[i]);
       Real S = Real(0);
       auto step = [&](const int t, const Real* eps, const Real* sj) {
-        const auto ax = Dyn::template aux<Real>(x, sp);
+        const auto ax = Dyn::template aux<Real, true>(x, sp);
         const Real qv = Cost::template q<Dyn, Real>(x, ax, sp);
         const Real* st = tab + t * TS;
         Real inc = fma(qv, dt, st[M]);
@@ -1114,7 +1121,7 @@ __global__ void __launch_bounds__(MAXT) rollout_kernel_ws(const RolloutArgs<Real
 #pragma unroll
       for (int i = 0; i < N; ++i) fin = fin && isfinite(x[i]);
       if (fin) {
-        const auto ax = Dyn::template aux<Real>(x, sp);
+        const auto ax = Dyn::template aux<Real, true>(x, sp);
         S += sp.term_scale * Cost::template q<Dyn, Real>(x, ax, sp);  // controller.py:155
       } else {
         S = r_inf<Real>();
