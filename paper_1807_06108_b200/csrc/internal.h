@@ -96,6 +96,11 @@ struct jm_ctx {
   jm::LoopState* d_loop = nullptr;
   double* d_loop_unom = nullptr;
   double* d_loop_unew = nullptr;
+  // single-GPU closed loop: the CTA records travel through the same epoch-flag
+  // buffer as the multi-GPU exchange (world 1), so the finalize merges them as
+  // the rollout's CTAs finish instead of after the whole grid
+  double* d_self_push = nullptr;                 // jm_peer_buffer_doubles(ctx, 1)
+  unsigned long long* d_self_base = nullptr;     // {d_self_push}
   double* d_hist = nullptr;       // states | controls
   int64_t* d_hist_jumps = nullptr;
   uint64_t* d_hist_t = nullptr;   // t_start | t_end
