@@ -168,3 +168,23 @@ def test_closed_loop_plant_poisson_counts(gpu_device):
     n = np.sum(u24[:, None] < pl[None, :], axis=1)
     assert np.array_equal(rec.jump_indicators, n)
     assert n.max() >= 2
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["b_cartpole", "b_quadrotor", "r_cartpole_task"])
+def test_fed_poisson_noise_matches_oracle(name, gpu_device):
+    """HBM (fed-noise) mode with a Poisson noise table: counts > 1 carry the
+    summed marks in eps_j, the kernels apply them once (flag = count != 0)."""
+    import paper_1807_06108_b200 as jb
+
+    g, s, model, cost, cfg = _poisson_cfg(name, 512, None)
+    noise = jb.sample_noise_batch(jb.RngStream(5, 3), cfg, 512, model=model, precision="f64")
+    assert noise[1].max() >= 2
+    ctrl = jb.ControllerState(jb.ControlSequence(g["u_nom"], s["dt"]), 3, cfg)
+    seq, diag = jb.mppi_iteration(ctrl, model, cost, g["x0"], 5, noise=noise, precision="f64")
+    spec = dataclasses.replace(oracle_spec(s), K=512, nu=cfg.nu)
+    out = om.mppi_iteration_oracle(spec, g["x0"], g["u_nom"], noise, np.float64)
+    assert rel_err(seq.controls, out["u_new"], floor=1e-9) <= G_DOUBLE
+    # and the fed table reproduces the in-kernel Philox iteration of the same stream
+    seq_p, _ = jb.mppi_iteration(ctrl, model, cost, g["x0"], 5, precision="f64")
+    assert rel_err(seq_p.controls, seq.controls, floor=1e-9) <= G_DOUBLE
