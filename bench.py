@@ -38,6 +38,7 @@ sys.path.insert(0, str(ROOT))
 
 # algorithmic work per state-step (frozen as the roofline numerator)
 FLOPS_PER_STATE_STEP = {"cartpole": 53, "quadrotor": 126}
+SFU_OPS_PER_STATE_STEP = {"cartpole": 3, "quadrotor": 7}
 # HBM bytes per state-step in noise-from-memory mode (fp32 eps_d + jump tensor, BASELINE noise model)
 HBM_BYTES_PER_STATE_STEP = {"cartpole": 8, "quadrotor": 28}
 FLUSH_BYTES = 256 << 20
@@ -367,6 +368,12 @@ def ours_arm(a):
             "flops_per_state_step": FLOPS_PER_STATE_STEP[system],
             "peak_source": "live FFMA microbenchmark (jm_microbench), no FP32 entry in MEASURED_PEAKS.json",
             "mufu_peak_tops": peaks["mufu_tops"], "fp64_peak_tflops": peaks["fp64_tflops"]}
+    # SFU view: the algorithmic MUFU-class ops per state-step (SURVEY Appendix C:
+    # sin, cos, rcp for the cartpole; 6 trig + rcp for the quadrotor) against the
+    # live MUFU microbenchmark peak
+    sfu_ops = SFU_OPS_PER_STATE_STEP[system] * K * T / (rms * 1e-3) / 1e12
+    roof["sfu"] = {"ops_per_state_step": SFU_OPS_PER_STATE_STEP[system], "achieved_tops": sfu_ops,
+                   "peak_tops": peaks["mufu_tops"], "frac": sfu_ops / peaks["mufu_tops"]}
     # issue-slot view of the same kernel: warp-instructions per state-step from the
     # committed ncu capture, and the rate at which 4 schedulers/SM issuing every
     # cycle would retire them -- what bounds this FP32-light, latency-bound loop
