@@ -162,6 +162,19 @@ def run_cpu(system, K, T, iters, procs, seed=0):
     return per_step, res[0]["kind"], kp * procs, wall
 
 
+def _host_cpu():
+    """CPU model and logical core count of the box (state the host)."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"model": model, "logical_cores": os.cpu_count()}
+
+
 def reference_arm(a):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -188,7 +201,8 @@ def reference_arm(a):
         "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{a.workload} (control-channel twin)", "system": system, "K": Kdone, "T": T},
-        "cpu_baseline": {"value": val, "unit": "state-steps/s", "cores": procs, "kind": kind, "sample": sample},
+        "cpu_baseline": {"value": val, "unit": "state-steps/s", "cores": procs, "kind": kind, "sample": sample,
+                         "host": _host_cpu()},
         "e2e": {"value": val, "unit": "state-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -441,7 +455,7 @@ def ours_arm(a):
             per_step, kind, Kdone, _ = run_cpu(system, min(K, 65536 if system == "cartpole" else 8192), T, 3, 1)
             cs = statistics.mean(per_step)
             line["cpu_baseline"] = {
-                "value": Kdone * T / cs, "unit": "state-steps/s", "cores": 1, "kind": kind,
+                "value": Kdone * T / cs, "unit": "state-steps/s", "cores": 1, "kind": kind, "host": _host_cpu(),
                 "sample": f"3 x jump_mppi.mppi_iteration+warm_start_shift at K={Kdone}, T={T}, control-channel twin "
                           f"of {a.workload}, 1 thread ({cs:.3f} s/iteration)"}
         except Exception as exc:  # noqa: BLE001
