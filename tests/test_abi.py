@@ -112,3 +112,35 @@ def test_summarize_matches_reference_formulas():
     assert np.allclose(s.mean_states, st.mean(0))
     assert np.allclose(s.ci_halfwidth, 1.96 * st.std(0, ddof=1) / np.sqrt(5))
     assert s.total_variance == np.var(st, axis=0, ddof=1).sum()
+
+
+def test_ctypes_structs_match_the_header(tmp_path):
+    """The ctypes mirrors of the descriptor structs have the C layout of
+    include/jmppi.h (sizes and field offsets, compiled with the host C compiler)."""
+    import ctypes as C
+    import shutil
+    import subprocess
+
+    from paper_1807_06108_b200 import _lib as L
+
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    structs = {"jm_model_desc": L.ModelDesc, "jm_cost_desc": L.CostDesc, "jm_mppi_desc": L.MppiDesc,
+               "jm_diag": L.Diag}
+    lines = ["#include <stdio.h>", "#include <stddef.h>", '#include "jmppi.h"', "int main(void) {"]
+    for cname, py in structs.items():
+        lines.append(f'  printf("{cname} size %zu\\n", sizeof({cname}));')
+        for f, _ in py._fields_:
+            lines.append(f'  printf("{cname} {f} %zu\\n", offsetof({cname}, {f}));')
+    lines += ["  return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run([cc, "-I", str(ROOT / "include"), str(src), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split("\n")
+    for line in filter(None, out):
+        cname, field, val = line.split()
+        py = structs[cname]
+        got = C.sizeof(py) if field == "size" else getattr(py, field).offset
+        assert got == int(val), (cname, field, got, val)
