@@ -162,10 +162,10 @@ class Engine final : public EngineBase {
     while (W > 8 && plan_bytes(c, block, mwarps, W, nring, single) > budget) W -= 4;
     c->jw_len = W;
     // the non-WS single-wave kernel stages its jump marks in the eps slab rows
-    // (kernels.cuh jump_window): no mark buffer, windows of up to 64 steps,
-    // balanced over the horizon (T = 100: two windows of 52 and 48)
-    const int nwin = (c->T + 63) / 64;
-    c->jw_slab = std::min(64, ((c->T + nwin - 1) / nwin + 3) / 4 * 4);
+    // (kernels.cuh jump_window): no mark buffer, windows of up to 128 steps
+    // (128-bit event masks), balanced over the horizon (T = 100: one window)
+    const int nwin = (c->T + 127) / 128;
+    c->jw_slab = std::min(128, ((c->T + nwin - 1) / nwin + 3) / 4 * 4);
     c->eps_smem = single && (ws ? plan_bytes(c, block, mwarps, W, nring, true)
                                 : plan_bytes(c, block, 0, 0, nring, true)) <= cap;
     const size_t msmem = (c->eps_smem && !ws) ? plan_bytes(c, block, 0, 0, nring, true)

@@ -404,23 +404,51 @@ __device__ __forceinline__ void mark_of(const StreamKey& sk, uint32_t kg, uint32
   }
 }
 
+// Event masks of a window: 32-bit (W <= 32) or 128-bit (W <= 128) words.
+struct Mask128 {
+  uint64_t lo, hi;
+};
+__device__ __forceinline__ void mask_set(uint32_t& m, int b) { m |= 1u << b; }
+__device__ __forceinline__ void mask_set(Mask128& m, int b) {
+  const uint64_t bit = 1ull << (b & 63);
+  if (b < 64)
+    m.lo |= bit;
+  else
+    m.hi |= bit;
+}
+__device__ __forceinline__ void mask_pop(uint32_t& m) { m &= m - 1u; }
+__device__ __forceinline__ void mask_pop(Mask128& m) {
+  if (m.lo)
+    m.lo &= m.lo - 1ull;
+  else
+    m.hi &= m.hi - 1ull;
+}
+__device__ __forceinline__ int mask_low(uint32_t m) { return __ffs((int)m) - 1; }
+__device__ __forceinline__ int mask_low(const Mask128& m) {
+  return m.lo ? __ffsll((long long)m.lo) - 1 : 64 + __ffsll((long long)m.hi) - 1;
+}
+__device__ __forceinline__ uint32_t mask_shfl(uint32_t m, int L) { return __shfl_sync(0xFFFFFFFFu, m, L); }
+__device__ __forceinline__ Mask128 mask_shfl(const Mask128& m, int L) {
+  return Mask128{__shfl_sync(0xFFFFFFFFu, m.lo, L), __shfl_sync(0xFFFFFFFFu, m.hi, L)};
+}
+
 // Called by all 32 lanes of a warp whose samples kg are consecutive by lane.
 // Staging layout: entry (step s of the window, component i, lane L) at
 // wd[(s * RQ + i) * CS + L] -- a per-warp buffer (RQ = Q, CS = 32), or the
 // rows of the CTA's shared-memory eps slab that steps w0.. have not written
 // yet (RQ = m, CS = tile; the step reads its mark there just before storing
-// its eps_combined over it).  MaskT: 32- or 64-bit event masks (W <= 64).
+// its eps_combined over it).  MaskT: 32- or 128-bit event masks (W <= 32 / 128).
 template <int Q, int QP, int JM, typename Real, typename MaskT = uint32_t, int RQ = Q>
 __device__ __forceinline__ void jump_window(JumpClock& c, int w0, int wend, int W, const StreamKey& sk, uint32_t kg,
                                             const GapSampler& gs, const Real* Lj, const Real* mu, Real jscale,
                                             Real* wd, bool poisson, const CountTable& ct, int CS = 32) {
   const int lane = threadIdx.x & 31;
-  MaskT mask = 0u;
+  MaskT mask{};
   const uint32_t e0 = c.e;
   int n = 0;
   while (__any_sync(0xFFFFFFFFu, c.tj < wend)) {
     if (c.tj < wend) {
-      mask |= MaskT(1) << (c.tj - w0);
+      mask_set(mask, c.tj - w0);
       ++n;
       clock_next(c, sk, kg, gs);
     }
@@ -449,10 +477,10 @@ __device__ __forceinline__ void jump_window(JumpClock& c, int w0, int wend, int 
     }
     const int k = j - __shfl_sync(0xFFFFFFFFu, off, L);
     const uint32_t eL = __shfl_sync(0xFFFFFFFFu, e0, L) + (uint32_t)k;
-    MaskT mL = __shfl_sync(0xFFFFFFFFu, mask, L);
+    MaskT mL = mask_shfl(mask, L);
     if (j < tot) {
-      for (int r = 0; r < k; ++r) mL &= mL - 1u;  // the owner's k-th event step
-      const int s = (sizeof(MaskT) == 8 ? __ffsll((long long)mL) : __ffs((int)mL)) - 1;
+      for (int r = 0; r < k; ++r) mask_pop(mL);  // the owner's k-th event step
+      const int s = mask_low(mL);
       Real mk[Q];
       mark_of<Q, QP, Real>(sk, kg - (uint32_t)lane + (uint32_t)L, eL, Lj, mu, mk, poisson, ct);
 #pragma unroll
@@ -853,7 +881,7 @@ __global__ void __launch_bounds__(kRolloutMaxThreads, (RolloutMinBlocks<Sys, Rea
       if (jumps && t0 == wnext) {
         wnext = t0 + JW;
         if (SCR_SMEM) {
-          jump_window<Q, QP, JM, Real, uint64_t, M>(clk, t0, min(wnext, T), JW, sk, kg, gs, Lj, mu, jscale,
+          jump_window<Q, QP, JM, Real, Mask128, M>(clk, t0, min(wnext, T), JW, sk, kg, gs, Lj, mu, jscale,
                                                     scr + (size_t)t0 * M * tileK + (threadIdx.x & ~31), a.poisson != 0,
                                                     a.cnt, tileK);
         } else {
