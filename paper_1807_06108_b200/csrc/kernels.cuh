@@ -438,7 +438,7 @@ __device__ __forceinline__ Mask128 mask_shfl(const Mask128& m, int L) {
 // rows of the CTA's shared-memory eps slab that steps w0.. have not written
 // yet (RQ = m, CS = tile; the step reads its mark there just before storing
 // its eps_combined over it).  MaskT: 32- or 128-bit event masks (W <= 32 / 128).
-template <int Q, int QP, int JM, typename Real, typename MaskT = uint32_t, int RQ = Q>
+template <int Q, int QP, int JM, typename Real, typename MaskT = uint32_t, int RQ = Q, bool ZERO = true>
 __device__ __forceinline__ void jump_window(JumpClock& c, int w0, int wend, int W, const StreamKey& sk, uint32_t kg,
                                             const GapSampler& gs, const Real* Lj, const Real* mu, Real jscale,
                                             Real* wd, bool poisson, const CountTable& ct, int CS = 32) {
@@ -462,10 +462,12 @@ __device__ __forceinline__ void jump_window(JumpClock& c, int w0, int wend, int 
   const int off = inc - n;
   const int tot = __shfl_sync(0xFFFFFFFFu, inc, 31);
   __syncwarp();  // the previous window's marks have been read
-  // (only the window's steps: the slab has no rows past the horizon)
-  for (int t = 0; t < wend - w0; ++t)
+  // (only the window's steps: the slab has no rows past the horizon; a slab
+  // zeroed in the prologue needs none)
+  if (ZERO)
+    for (int t = 0; t < wend - w0; ++t)
 #pragma unroll
-    for (int i = 0; i < Q; ++i) wd[(t * RQ + i) * CS + lane] = Real(0);
+      for (int i = 0; i < Q; ++i) wd[(t * RQ + i) * CS + lane] = Real(0);
   __syncwarp();
   for (int j0 = 0; j0 < tot; j0 += 32) {
     const int j = j0 + lane;
@@ -681,6 +683,11 @@ __global__ void __launch_bounds__(kRolloutMaxThreads, (RolloutMinBlocks<Sys, Rea
   if (L != nullptr && blockIdx.x == 0 && threadIdx.x == 0) L->t_start[L->step] = globaltimer();
   ROLL_STAMP();
   rollout_prologue<M, Real>(a, a.u_nom + (size_t)blockIdx.y * TM, tab, Nacc, s_acc, Sg);
+  if (SCR_SMEM && a.jump_on) {  // the slab rows double as the jump-mark staging: zero them once, 16 B a store
+    float4* z4 = reinterpret_cast<float4*>(scr);
+    const int n4 = (int)((size_t)TM * tileK * sizeof(Real) / 16);
+    for (int i = threadIdx.x; i < n4; i += blockDim.x) z4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   __syncthreads();
   ROLL_STAMP();
 
@@ -881,7 +888,7 @@ __global__ void __launch_bounds__(kRolloutMaxThreads, (RolloutMinBlocks<Sys, Rea
       if (jumps && t0 == wnext) {
         wnext = t0 + JW;
         if (SCR_SMEM) {
-          jump_window<Q, QP, JM, Real, Mask128, M>(clk, t0, min(wnext, T), JW, sk, kg, gs, Lj, mu, jscale,
+          jump_window<Q, QP, JM, Real, Mask128, M, false>(clk, t0, min(wnext, T), JW, sk, kg, gs, Lj, mu, jscale,
                                                     scr + (size_t)t0 * M * tileK + (threadIdx.x & ~31), a.poisson != 0,
                                                     a.cnt, tileK);
         } else {
