@@ -127,7 +127,9 @@ class Engine final : public EngineBase {
   // eps scratch the epilogue reads is kept in shared memory when it fits, and
   // tiles of <= kWsMaxTile samples run the warp-specialised kernel (measured:
   // it wins only where a few warps per SM leave the issue slots idle).
-  static constexpr int kWsMaxTile = 128;
+  // (measured: cartpole tiles of 128 run 20.9 us without WS vs 26.3 with it, 64 tie;
+  // the quadrotor's longer chain still wins with WS at 128: 79.6 vs 83.8 us)
+  static constexpr int kWsMaxTile = (N <= 4) ? 64 : 128;
   cudaError_t configure(jm_ctx* c) override {
     const bool philox = c->mppi.noise_source == JM_NOISE_PHILOX;
     static const int ws_env = std::getenv("JM_WS") ? std::atoi(std::getenv("JM_WS")) : -1;  // A/B: 0 off, 1 on
