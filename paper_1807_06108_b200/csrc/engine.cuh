@@ -160,7 +160,8 @@ class Engine final : public EngineBase {
     const bool single = philox && !no_eps_smem && c->ntiles <= sms;
     // multi-wave: two CTAs per SM must still fit (the occupancy the 256-sample tiles need)
     const size_t budget = single ? cap : std::min(cap, (size_t)optin / 2 - 2048);
-    int W = 32;
+    // (128-bit event masks: windows up to 128 steps, as long as the mark staging fits)
+    int W = std::min(128, (c->T + 3) / 4 * 4);
     while (W > 8 && plan_bytes(c, block, mwarps, W, nring, single) > budget) W -= 4;
     c->jw_len = W;
     // the non-WS single-wave kernel stages its jump marks in the eps slab rows
@@ -277,7 +278,7 @@ class Engine final : public EngineBase {
                          : launch_pdl(ws_kern<JM, false>(), grid, dim3(2 * c->block), c->main_smem, c->stream, a);
     if (philox && !trace && c->eps_smem) {
       RolloutArgs<Real> b = a;
-      b.jw_len = c->jw_slab;  // marks staged in the eps slab (jump_window, 64-bit masks)
+      b.jw_len = c->jw_slab;  // marks staged in the eps slab (jump_window, 128-bit masks)
       return launch_pdl(rollout_kernel<Sys, Real, true, false, JM, true>, grid, block, c->main_smem, c->stream, b);
     }
     if (philox && !trace)

@@ -438,7 +438,7 @@ __device__ __forceinline__ Mask128 mask_shfl(const Mask128& m, int L) {
 // rows of the CTA's shared-memory eps slab that steps w0.. have not written
 // yet (RQ = m, CS = tile; the step reads its mark there just before storing
 // its eps_combined over it).  MaskT: 32- or 128-bit event masks (W <= 32 / 128).
-template <int Q, int QP, int JM, typename Real, typename MaskT = uint32_t, int RQ = Q, bool ZERO = true>
+template <int Q, int QP, int JM, typename Real, typename MaskT = Mask128, int RQ = Q, bool ZERO = true>
 __device__ __forceinline__ void jump_window(JumpClock& c, int w0, int wend, int W, const StreamKey& sk, uint32_t kg,
                                             const GapSampler& gs, const Real* Lj, const Real* mu, Real jscale,
                                             Real* wd, bool poisson, const CountTable& ct, int CS = 32) {
