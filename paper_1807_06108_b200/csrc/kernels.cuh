@@ -1358,7 +1358,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
   extern __shared__ double fsm[];
   constexpr int NW = kFinThreads / 32;
   static_assert(NW <= 32 && (NW & (NW - 1)) == 0, "block reductions: one partial per lane");
-  __shared__ double se[NW];         // e_w = exp(-(rho_w - rho)/lambda), per warp's merged records
+  double* se = fsm;                 // e_b = exp(-(rho_b - rho)/lambda), per record
   double* part = fsm + a.nrec;      // [NW][kFinCols + 1] (padded: conflict-free column reads)
   __shared__ double s_red[4][NW];
   __shared__ double s_delta[kFinCols];
@@ -1387,71 +1387,26 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
   const int c0 = blockIdx.x * kFinCols;
   const bool reduce_mode = a.rec_out != nullptr;
   const double unom_c = (!reduce_mode && tid < kFinCols && c0 + tid < a.TM) ? unom[c0 + tid] : 0.0;
-  // records arriving behind epoch flags (the rollout's CTAs release them as
-  // their tiles finish) are merged as they come, overlapping the rollout's
-  // tail; otherwise the whole rollout grid is waited for first
-  const bool flags = a.wait_flags != nullptr;
-  if (!flags) grid_dep_wait();
+  grid_dep_wait();
   if (halted) return;
   const int rs = a.rec_stride;
   FIN_STAMP();
-  uint32_t epoch = 0u;
-  if (flags) {
-    epoch = (uint32_t)L->step + 1u;
-    recs += (size_t)(epoch & 1u) * a.nrec * rs;
-  }
-  // Per-warp online-softmax merge in fixed order: warp w folds records w,
-  // w + NW, ... into a running (rho_w, Z_w, W2_w, nf_w, N_w[its columns]);
-  // each fold needs one exp (the side with the larger minimum is rescaled).
-  // A flag wait gives up after 30 s (a peer that never pushes must not hang
-  // the GPU: the loop halts with JM_ERR_CUDA instead).
-  constexpr int CPL = kFinCols / 32;
-  double wr = CUDART_INF, wz = 0.0, ww = 0.0, wn = 0.0;
-  double acc[CPL];
-#pragma unroll
-  for (int i = 0; i < CPL; ++i) acc[i] = 0.0;
-  int timed_out = 0;
-  const uint64_t t_begin = flags ? globaltimer() : 0ull;
-  for (int b = warp; b < a.nrec; b += NW) {
-    if (flags) {
-      if (lane == 0) {
-        while ((a.wait_gpu ? ld_acquire_gpu(a.wait_flags + b) : ld_acquire_sys(a.wait_flags + b)) < epoch) {
-          if (!a.wait_gpu) __nanosleep(32);  // (local records: spin, a sleep would outlast the hand-off)
-          if (globaltimer() - t_begin > 30ull * 1000000000ull) {
-            timed_out = 1;
-            break;
-          }
-        }
-      }
-      timed_out = __shfl_sync(0xFFFFFFFFu, timed_out, 0);
-      if (timed_out) break;
-      __syncwarp();
-    }
-    const double* r = recs + (size_t)b * rs;
-    const double h0 = __ldcg(r), h1 = __ldcg(r + 1), h2 = __ldcg(r + 2), h3 = __ldcg(r + 3);
-    double nb[CPL];
-#pragma unroll
-    for (int i = 0; i < CPL; ++i) {
-      const int c = c0 + lane + 32 * i;
-      nb[i] = c < a.TM ? __ldcg(r + 4 + c) : 0.0;
-    }
-    if (h0 != CUDART_INF) {  // (a record without finite costs carries N = 0 and no weight)
-      const bool new_min = h0 < wr;
-      const double e = (wr == CUDART_INF) ? 0.0 : exp(-fabs(wr - h0) * a.inv_lam);
-      const double so = new_min ? e : 1.0, sn = new_min ? 1.0 : e;
-      wz = fma(h1, sn, wz * so);
-      ww = fma(h2, sn * sn, ww * (so * so));
-#pragma unroll
-      for (int i = 0; i < CPL; ++i) acc[i] = fma(nb[i], sn, acc[i] * so);
-      wr = fmin(wr, h0);
-    }
-    wn += h3;
-  }
-  if (flags) {
+  if (a.wait_flags != nullptr) {  // every rank's CTA records arrive over NVLink (write_record)
+    const uint32_t epoch = (uint32_t)L->step + 1u;
+    // a peer that never pushes (a dead rank) must not hang the GPU: after 30 s
+    // the loop halts with JM_ERR_CUDA instead
     __shared__ int s_timeout;
     if (tid == 0) s_timeout = 0;
     __syncthreads();
-    if (lane == 0 && timed_out) s_timeout = 1;
+    const uint64_t t_begin = globaltimer();
+    for (int r = tid; r < a.nrec; r += kFinThreads)
+      while ((a.wait_gpu ? ld_acquire_gpu(a.wait_flags + r) : ld_acquire_sys(a.wait_flags + r)) < epoch) {
+        if (!a.wait_gpu) __nanosleep(32);
+        if (globaltimer() - t_begin > 30ull * 1000000000ull) {
+          s_timeout = 1;
+          break;
+        }
+      }
     __syncthreads();
     if (s_timeout) {
       if (tid == 0) {
@@ -1460,25 +1415,76 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
       }
       return;
     }
+    __threadfence();
+    recs += (size_t)(epoch & 1u) * a.nrec * rs;
   }
-  if (lane == 0) {
-    s_red[0][warp] = wr;
-    s_red[1][warp] = wz;
-    s_red[2][warp] = ww;
-    s_red[3][warp] = wn;
+  // global rho (controller.py:69: min over finite costs) and the rescaled
+  // sums in one pass over the record heads (<= 1024 records: one per thread,
+  // held in registers).  Block reductions: warp partials -> shared memory ->
+  // one barrier -> every warp reduces the 32 partials itself (fixed order, so
+  // all warps agree bit for bit), instead of warp 0 + a broadcast barrier.
+  double h0 = CUDART_INF, h1 = 0.0, h2 = 0.0, h3 = 0.0;
+  const bool one_pass = a.nrec <= kFinThreads;
+  double m = CUDART_INF;
+  if (one_pass) {
+    if (tid < a.nrec) {
+      const double* r = recs + (size_t)tid * rs;
+      h0 = r[0];
+      h1 = r[1];
+      h2 = r[2];
+      h3 = r[3];
+    }
+    m = h0;
+  } else {
+    for (int b = tid; b < a.nrec; b += kFinThreads) m = fmin(m, recs[(size_t)b * rs]);
   }
+  // the column pass below reads every record's N block: start those lines
+  // towards L1 now (after the head loads are issued), under the reductions
+  {
+    constexpr int CPL = kFinCols / 32;
+    for (int b = warp; b < a.nrec; b += NW) {
+      const double* r = recs + (size_t)b * rs + 4;
 #pragma unroll
-  for (int i = 0; i < CPL; ++i) part[warp * (kFinCols + 1) + lane + 32 * i] = acc[i];
+      for (int i = 0; i < CPL; ++i) {
+        const int c = c0 + lane + 32 * i;
+        if (c < a.TM && ((c & 15) == 0 || c == c0 + lane)) asm volatile("prefetch.global.L1 [%0];" ::"l"(r + c));
+      }
+    }
+  }
+  m = warp_min_redux(m);
+  if (lane == 0) s_red[0][warp] = m;
   __syncthreads();
+  const double rho = warp_min_redux(lane < NW ? s_red[0][lane] : CUDART_INF);
   FIN_STAMP();
-  // cross-warp merge: global rho (controller.py:69), each warp's rescale e_w
-  // (every warp computes the same values in the same order)
-  const double wr_l = lane < NW ? s_red[0][lane] : CUDART_INF;
-  const double rho = warp_min_redux(wr_l);
-  const double ew = (wr_l == CUDART_INF || rho == CUDART_INF) ? 0.0 : exp((rho - wr_l) * a.inv_lam);
-  if (warp == 0 && lane < NW) se[lane] = ew;
-  const double Z = warp_sum(lane < NW ? s_red[1][lane] * ew : 0.0),
-               W2 = warp_sum(lane < NW ? s_red[2][lane] * (ew * ew) : 0.0),
+  double z = 0.0, w2 = 0.0, nf = 0.0;
+  if (one_pass) {
+    if (tid < a.nrec) {
+      const double e = (h0 == CUDART_INF || rho == CUDART_INF) ? 0.0 : exp(-(h0 - rho) * a.inv_lam);
+      se[tid] = e;
+      z = h1 * e;
+      w2 = h2 * e * e;
+      nf = h3;
+    }
+  } else {
+    for (int b = tid; b < a.nrec; b += kFinThreads) {
+      const double* r = recs + (size_t)b * rs;
+      const double e = (r[0] == CUDART_INF || rho == CUDART_INF) ? 0.0 : exp(-(r[0] - rho) * a.inv_lam);
+      se[b] = e;
+      z += r[1] * e;
+      w2 += r[2] * e * e;
+      nf += r[3];
+    }
+  }
+  z = warp_sum(z);
+  w2 = warp_sum(w2);
+  nf = warp_sum(nf);
+  if (lane == 0) {
+    s_red[1][warp] = z;
+    s_red[2][warp] = w2;
+    s_red[3][warp] = nf;
+  }
+  __syncthreads();
+  const double Z = warp_sum(lane < NW ? s_red[1][lane] : 0.0), W2 = warp_sum(lane < NW ? s_red[2][lane] : 0.0),
                NF = warp_sum(lane < NW ? s_red[3][lane] : 0.0);
   FIN_STAMP();
   if (rho == CUDART_INF) {  // controller.py:66-67
@@ -1508,7 +1514,25 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
     }
     return;
   }
-  __syncthreads();  // se[] (the warp rescales) complete
+  // columns: warps split records (several in flight), lanes split columns
+  constexpr int CPL = kFinCols / 32;
+  double acc[CPL];
+#pragma unroll
+  for (int i = 0; i < CPL; ++i) acc[i] = 0.0;
+#pragma unroll 4
+  for (int b = warp; b < a.nrec; b += NW) {
+    const double* r = recs + (size_t)b * rs + 4;
+    const double e = se[b];
+#pragma unroll
+    for (int i = 0; i < CPL; ++i) {
+      const int c = c0 + lane + 32 * i;
+      if (c < a.TM) acc[i] = fma(r[c], e, acc[i]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < CPL; ++i) part[warp * (kFinCols + 1) + lane + 32 * i] = acc[i];
+  __syncthreads();
+  FIN_STAMP();
   // cross-warp column sums: thread c adds the NW warp partials of column c
   // (consecutive columns: conflict-free) in four interleaved chains, then
   // combines them -- fixed order, no 64-bit shuffle rounds
@@ -1516,10 +1540,10 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
     double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
 #pragma unroll
     for (int w = 0; w < NW; w += 4) {
-      v0 = fma(part[(w + 0) * (kFinCols + 1) + tid], se[w + 0], v0);
-      if (w + 1 < NW) v1 = fma(part[(w + 1) * (kFinCols + 1) + tid], se[w + 1], v1);
-      if (w + 2 < NW) v2 = fma(part[(w + 2) * (kFinCols + 1) + tid], se[w + 2], v2);
-      if (w + 3 < NW) v3 = fma(part[(w + 3) * (kFinCols + 1) + tid], se[w + 3], v3);
+      v0 += part[(w + 0) * (kFinCols + 1) + tid];
+      if (w + 1 < NW) v1 += part[(w + 1) * (kFinCols + 1) + tid];
+      if (w + 2 < NW) v2 += part[(w + 2) * (kFinCols + 1) + tid];
+      if (w + 3 < NW) v3 += part[(w + 3) * (kFinCols + 1) + tid];
     }
     s_delta[tid] = (v0 + v1) + (v2 + v3);
   }
