@@ -35,3 +35,34 @@ for world in (1, 2, 4, 8):
                             C.c_void_p(unew.data_ptr()), None, None, None)
     e1.record(); torch.cuda.synchronize()
     print(f"world {world}: nrec {n}: finalize {e0.elapsed_time(e1) / 50 * 1e3:.1f} us")
+
+# Two-level alternative (DESIGN 7b item 3): each rank first reduces its own 147 CTA
+# records into one (jm_reduce_dev, the NCCL transport's reduce step), then merges
+# `world` records.  Critical path per step = reduce(147) + finalize(world).
+ctx.iteration(np.zeros(ctx.N), np.zeros(TM), 1, 0)  # populate this context's CTA records
+rec1 = torch.zeros(rs, dtype=torch.float64, device=dev)
+
+
+def timed(fn, reps=50):
+    for _ in range(5):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record(); torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps * 1e3
+
+
+lib.jm_set_stream(ctx.h, C.c_void_p(torch.cuda.current_stream().cuda_stream))
+t_red = timed(lambda: lib.jm_reduce_dev(ctx.h, C.c_void_p(rec1.data_ptr())))
+for world in (1, 2, 4, 8):
+    recw = rec1.repeat(world, 1).contiguous()
+    t_fin = timed(lambda: lib.jm_finalize_dev(ctx.h, C.c_void_p(recw.data_ptr()), world, C.c_void_p(unom.data_ptr()),
+                                              None, C.c_void_p(unew.data_ptr()), None, None, None))
+    t_both = timed(lambda: (lib.jm_reduce_dev(ctx.h, C.c_void_p(rec1.data_ptr())),
+                            lib.jm_finalize_dev(ctx.h, C.c_void_p(recw.data_ptr()), world, C.c_void_p(unom.data_ptr()),
+                                                None, C.c_void_p(unew.data_ptr()), None, None, None)))
+    print(f"world {world}: two-level: reduce(147) {t_red:.1f} us + finalize({world}) {t_fin:.1f} us; "
+          f"back to back {t_both:.1f} us")
