@@ -104,6 +104,8 @@ SIGNATURES = {
     "jm_peer_buffer_doubles": (C.c_int64, [_vp, _i32]),
     "jm_loop_rollout_push": (C.c_int, [_vp, _vp, _i32, _i32]),
     "jm_loop_finish_peers": (C.c_int, [_vp, _vp, _i32]),
+    "jm_loop_rollout_reduce_push": (C.c_int, [_vp, _vp, _i32, _i32]),
+    "jm_loop_finish_reduced_peers": (C.c_int, [_vp, _vp, _i32]),
     "jm_batch_loop_host": (C.c_int, [_vp, _i32, _pd, _pd, _pu64, _i32, _pd, _pd, _pi64, _pd, _pi32, _pi32]),
     "jm_loop_init": (C.c_int, [_vp, _pd, _pd, _u64, _u64, _i32]),
     "jm_loop_step": (C.c_int, [_vp]),

@@ -1076,6 +1076,39 @@ int jm_loop_finish_peers(jm_ctx* ctx, const double* my_buffer_dev, int32_t world
   return JM_OK;
 }
 
+int jm_loop_rollout_reduce_push(jm_ctx* ctx, const unsigned long long* peer_bases_dev, int32_t rank, int32_t world) {
+  const int ncb = ctx ? (ctx->TM + jm::kFinCols - 1) / jm::kFinCols : 0;
+  if (!ctx || !ctx->d_loop || !peer_bases_dev || world < 1 || rank < 0 || rank >= world || ncb > ctx->grid)
+    return fail(ctx, JM_ERR_VALUE, "bad arguments");
+  CK(cudaSetDevice(ctx->device));
+  jm::RolloutCall rc;
+  rc.u_nom = ctx->d_loop_unom;
+  rc.costs = ctx->d_costs;
+  rc.loop = ctx->d_loop;
+  CK(ctx->eng->rollout(ctx, rc));
+  jm::FinArgs f = fin_args(ctx, nullptr, 0);  // reduce this rank's CTA records ...
+  f.push_peers = peer_bases_dev;              // ... into slot `rank` of every peer buffer
+  f.push_rank = rank;
+  f.push_world = world;
+  f.push_loop = ctx->d_loop;
+  CK(ctx->eng->finalize(ctx, f, nullptr, nullptr));
+  return JM_OK;
+}
+
+int jm_loop_finish_reduced_peers(jm_ctx* ctx, const double* my_buffer_dev, int32_t world) {
+  if (!ctx || !ctx->d_loop || !my_buffer_dev || world < 1 || world > jm::kMaxRecords)
+    return fail(ctx, JM_ERR_VALUE, "bad arguments");
+  CK(cudaSetDevice(ctx->device));
+  const int ncb = (ctx->TM + jm::kFinCols - 1) / jm::kFinCols;
+  jm::FinArgs f = fin_args(ctx, my_buffer_dev, world);
+  f.u_nom = ctx->d_loop_unom;
+  f.u_new = ctx->d_loop_unew;
+  f.wait_flags = reinterpret_cast<const unsigned int*>(my_buffer_dev + 2 * (size_t)world * ctx->rec_stride);
+  f.wait_nflags = world * ncb;
+  CK(ctx->eng->finalize(ctx, f, ctx->d_loop, ctx->d_loop_unom));
+  return JM_OK;
+}
+
 int jm_loop_step(jm_ctx* ctx) {
   if (!ctx || !ctx->graph_exec) return fail(ctx, JM_ERR_VALUE, "loop not initialised");
   CK(cudaGraphLaunch(ctx->graph_exec, ctx->own_stream));

@@ -1346,8 +1346,66 @@ struct FinArgs {
   // nrec (= world x grid) flags reach this step's epoch (L->step + 1); records
   // of epoch parity e & 1 start at rec + (e & 1) * nrec * rec_stride
   const unsigned int* wait_flags;
-  int wait_gpu;  // the flags are released at GPU scope (single-GPU use of the exchange)
+  int wait_gpu;     // the flags are released at GPU scope (single-GPU use of the exchange)
+  int wait_nflags;  // flags to wait on (0: nrec)
+  // two-level exchange (jm_loop_reduce_push): reduce mode stores the merged
+  // record into slot push_rank of parity (epoch & 1) of every peer buffer
+  // ([2 parities x push_world records][flags]) and raises flag
+  // push_rank * gridDim.x + blockIdx.x there (one per column block);
+  // epoch = push_loop->step + 1
+  const unsigned long long* push_peers;
+  int push_rank, push_world;
+  const LoopState* push_loop;
 };
+
+// reduce mode: write this CTA's part of the merged record (the head from
+// CTA 0, columns [c0, c0 + kFinCols)) into rec_out, or into every peer's
+// buffer followed by this CTA's flag release
+__device__ __forceinline__ void fin_emit_record(const FinArgs& a, int c0, double rho, double Z, double W2, double NF,
+                                                const double* cols) {
+  const int tid = threadIdx.x;
+  const int ncol = min(kFinCols, a.TM - c0);
+  if (a.push_peers == nullptr) {
+    if (blockIdx.x == 0 && tid == 0) {
+      a.rec_out[0] = rho;
+      a.rec_out[1] = Z;
+      a.rec_out[2] = W2;
+      a.rec_out[3] = NF;
+    }
+    if (tid < ncol) a.rec_out[4 + c0 + tid] = cols ? cols[tid] : 0.0;
+    return;
+  }
+  const uint32_t epoch = (uint32_t)a.push_loop->step + 1u;
+  const int W = a.push_world;
+  const size_t off = ((size_t)(epoch & 1u) * W + a.push_rank) * a.rec_stride;
+  for (int p = 0; p < W; ++p) {
+    double* dst = reinterpret_cast<double*>(a.push_peers[p]) + off;
+    if (blockIdx.x == 0 && tid == 0) {
+      dst[0] = rho;
+      dst[1] = Z;
+      dst[2] = W2;
+      dst[3] = NF;
+    }
+    if (tid < ncol) dst[4 + c0 + tid] = cols ? cols[tid] : 0.0;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const int slot = a.push_rank * gridDim.x + blockIdx.x;
+    if (W == 1) {
+      __threadfence();
+    } else {
+      __threadfence_system();
+    }
+    for (int p = 0; p < W; ++p) {
+      unsigned int* flags =
+          reinterpret_cast<unsigned int*>(reinterpret_cast<double*>(a.push_peers[p]) + 2 * (size_t)W * a.rec_stride);
+      if (W == 1)
+        st_release_gpu(flags + slot, epoch);
+      else
+        st_release_sys(flags + slot, epoch);
+    }
+  }
+}
 
 inline size_t finalize_smem_bytes(int nrec) {
   return sizeof(double) * ((size_t)nrec + (size_t)(kFinThreads / 32) * (kFinCols + 1));
@@ -1385,7 +1443,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
   if (L != nullptr && tid == kFinThreads - 1) plant_prepare<Dyn>(p, s_pre);
   const bool halted = L != nullptr && L->halted;
   const int c0 = blockIdx.x * kFinCols;
-  const bool reduce_mode = a.rec_out != nullptr;
+  const bool reduce_mode = a.rec_out != nullptr || a.push_peers != nullptr;
   const double unom_c = (!reduce_mode && tid < kFinCols && c0 + tid < a.TM) ? unom[c0 + tid] : 0.0;
   grid_dep_wait();
   if (halted) return;
@@ -1399,7 +1457,8 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
     if (tid == 0) s_timeout = 0;
     __syncthreads();
     const uint64_t t_begin = globaltimer();
-    for (int r = tid; r < a.nrec; r += kFinThreads)
+    const int nflags = a.wait_nflags > 0 ? a.wait_nflags : a.nrec;
+    for (int r = tid; r < nflags; r += kFinThreads)
       while ((a.wait_gpu ? ld_acquire_gpu(a.wait_flags + r) : ld_acquire_sys(a.wait_flags + r)) < epoch) {
         if (!a.wait_gpu) __nanosleep(32);
         if (globaltimer() - t_begin > 30ull * 1000000000ull) {
@@ -1495,23 +1554,16 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
         L->status = 3;
         L->halted = 1;
       }
-      if (reduce_mode) {
-        a.rec_out[0] = CUDART_INF;
-        a.rec_out[1] = 0.0;
-        a.rec_out[2] = 0.0;
-        a.rec_out[3] = 0.0;
-      }
       if (a.done != nullptr) {  // the caller only reads the status in this case
         __threadfence_system();
         *a.done = 1;
       }
     }
-    for (int c = c0 + tid; c < min(c0 + kFinCols, a.TM); c += kFinThreads) {
-      if (reduce_mode)
-        a.rec_out[4 + c] = 0.0;
-      else
-        unew[c] = unom[c];
+    if (reduce_mode) {
+      fin_emit_record(a, c0, CUDART_INF, 0.0, 0.0, 0.0, nullptr);
+      return;
     }
+    for (int c = c0 + tid; c < min(c0 + kFinCols, a.TM); c += kFinThreads) unew[c] = unom[c];
     return;
   }
   // columns: warps split records (several in flight), lanes split columns
@@ -1550,13 +1602,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
   __syncthreads();
   FIN_STAMP();
   if (reduce_mode) {
-    if (blockIdx.x == 0 && tid == 0) {
-      a.rec_out[0] = rho;
-      a.rec_out[1] = Z;
-      a.rec_out[2] = W2;
-      a.rec_out[3] = NF;
-    }
-    if (tid < kFinCols && c0 + tid < a.TM) a.rec_out[4 + c0 + tid] = s_delta[tid];
+    fin_emit_record(a, c0, rho, Z, W2, NF, s_delta);
     return;
   }
   // delta = N / (Z sqrt(dt))  (controller.py:158), then mapping (:159-160)

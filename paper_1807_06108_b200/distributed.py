@@ -21,6 +21,13 @@ Two transports for that exchange:
          the step never returns to the host or a collective launch;
   "nccl" -- all_gather_into_tensor of the records (the fallback).
 
+The p2p exchange has two forms.  Flat (world < 4): the rollout kernel's CTAs
+push their own records, every rank merges world x grid of them.  Two-level
+(world >= 4, `two_level`; env JM_P2P_TWO_LEVEL=0/1 overrides): a reduce
+kernel merges the rank's CTA records into one and pushes that, every rank
+merges `world` records -- the NCCL transport's merge tree, bit for bit
+(measured: 11.2 vs 19.6 us of merge at world 8; DESIGN 7b).
+
 torch.distributed is the plumbing (process group, rendezvous of the symmetric
 buffers, streams); all arithmetic is in libjmppi.so.  The host-side logic here
 (shard ranges, record exchange, rank-order merge) is covered on CPU by
@@ -86,6 +93,9 @@ class ShardedLoop:
     rank: int
     group: object = None
     transport: str = "nccl"
+    two_level: bool = None  # p2p only; None: world >= TWO_LEVEL_MIN_WORLD (or JM_P2P_TWO_LEVEL)
+
+    TWO_LEVEL_MIN_WORLD = 4
 
     @classmethod
     def create(cls, task, cfg, rank: int, world: int, device: int, precision=None, group=None, transport="nccl"):
@@ -113,6 +123,9 @@ class ShardedLoop:
         self.ctx.check(lib.jm_set_stream(h, C.c_void_p(self.stream.cuda_stream)))
         torch.cuda.synchronize(dev)
         if self.transport == "p2p":
+            if self.two_level is None:
+                env = os.environ.get("JM_P2P_TWO_LEVEL")
+                self.two_level = bool(int(env)) if env else self.world >= self.TWO_LEVEL_MIN_WORLD
             self._init_peers(dev)
 
     def _init_peers(self, dev):
@@ -137,9 +150,13 @@ class ShardedLoop:
         # graph of its four kernels, replayed per control step
         lib, h = self.ctx.lib, self.ctx.h
         self.graph = torch.cuda.CUDAGraph()
+        if self.two_level:
+            push, finish = lib.jm_loop_rollout_reduce_push, lib.jm_loop_finish_reduced_peers
+        else:
+            push, finish = lib.jm_loop_rollout_push, lib.jm_loop_finish_peers
         with torch.cuda.graph(self.graph, stream=self.stream):
-            self.ctx.check(lib.jm_loop_rollout_push(h, C.c_void_p(self.peer_bases.data_ptr()), self.rank, self.world))
-            self.ctx.check(lib.jm_loop_finish_peers(h, C.c_void_p(self.peer_buf.data_ptr()), self.world))
+            self.ctx.check(push(h, C.c_void_p(self.peer_bases.data_ptr()), self.rank, self.world))
+            self.ctx.check(finish(h, C.c_void_p(self.peer_buf.data_ptr()), self.world))
 
     def step(self):
         """One control step: local rollout + record, exchange, merge/update/plant/shift."""
@@ -238,11 +255,13 @@ def bench_sharded(a, world: int, rank: int, local: int):
                 "config": {"workload": f"{a.workload}: BASELINE config {idx} closed-loop control step, "
                                        f"K={K} per GPU (global {world * K}), T={T}, one exchange of the "
                                        "weighting records per step",
-                           "exchange": ("peer-memory records over NVLink (symmetric buffers, device-side epoch "
-                                        "flags, no collective launch)" if transport == "p2p"
+                           "exchange": ((("two-level: one reduced record per rank" if loop.two_level
+                                          else "flat: per-CTA records") +
+                                         " over peer memory (symmetric buffers, device-side epoch flags, "
+                                         "no collective launch)") if transport == "p2p"
                                         else "NCCL all_gather_into_tensor"),
                            "K_per_gpu": K, "T": T, "parallelism": f"dp{world}",
                            "l2": "flushed (256 MiB fill) before each timed step"},
-                "mpc_iteration_latency_ms": ms, "gpu_launches": (4 if transport == "p2p" else 3) * a.steps}
+                "mpc_iteration_latency_ms": ms, "gpu_launches": ((5 if loop.two_level else 4) if transport == "p2p" else 3) * a.steps}
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()

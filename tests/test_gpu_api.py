@@ -379,3 +379,41 @@ def test_sharded_loop_world1_peer_memory_exchange(gpu_device):
         assert np.allclose(sts, rec.states, rtol=1e-9, atol=1e-12)
     finally:
         dist.destroy_process_group()
+
+
+def test_sharded_loop_world1_two_level_exchange_matches_nccl(gpu_device):
+    """The two-level peer-memory exchange (rank-local reduce kernel pushes one
+    record per rank, the finalize waits on world x column-block flags) runs the
+    NCCL transport's merge tree: bit-identical trajectories, cartpole (one
+    column block) and quadrotor (T*m = 240: two column blocks, two flags)."""
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1807_06108_b200 import distributed as jd
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        for idx, K, T in ((0, 2048, 60), (2, 512, 60)):
+            task, cfg = jb.baseline_config(idx, K=K, T=T, steps=10)
+            hist = {}
+            for transport, two in (("nccl", None), ("p2p", True)):
+                loop = jd.ShardedLoop.create(task, cfg, 0, 1, 0, precision="f64", transport=transport)
+                loop.two_level = two
+                loop.init(task.x0, cfg.u_init, 7, 64)
+                for _ in range(10):
+                    loop.step()
+                x, it, st, halted, status = loop.read()
+                assert st == 10 and not halted, (transport, status)
+                hist[transport] = [np.array(h) for h in loop.history(10)]
+            for a, b in zip(hist["nccl"], hist["p2p"]):
+                assert np.array_equal(a, b)
+    finally:
+        dist.destroy_process_group()
