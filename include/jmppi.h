@@ -298,7 +298,7 @@ int jm_batch_loop_host(jm_ctx* ctx, int32_t trials, const double* x0, const doub
 int64_t jm_peer_buffer_doubles(const jm_ctx* ctx, int32_t world);
 int jm_loop_rollout_push(jm_ctx* ctx, const unsigned long long* peer_bases_dev, int32_t rank, int32_t world);
 int jm_loop_finish_peers(jm_ctx* ctx, const double* my_buffer_dev, int32_t world);
-/* Two-level form of the same exchange (world >= 4, where merging world x grid
+/* Two-level form of the same exchange (large worlds, where merging world x grid
  * CTA records outgrows the finalize): the rollout, then a reduce of this rank's
  * CTA records into ONE record (the NCCL transport's jm_loop_rollout reduce,
  * bit for bit) stored into slot `rank` of every peer buffer with its epoch

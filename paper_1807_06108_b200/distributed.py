@@ -21,12 +21,14 @@ Two transports for that exchange:
          the step never returns to the host or a collective launch;
   "nccl" -- all_gather_into_tensor of the records (the fallback).
 
-The p2p exchange has two forms.  Flat (world < 4): the rollout kernel's CTAs
+The p2p exchange has two forms.  Flat (world < 6): the rollout kernel's CTAs
 push their own records, every rank merges world x grid of them.  Two-level
-(world >= 4, `two_level`; env JM_P2P_TWO_LEVEL=0/1 overrides): a reduce
+(world >= 6, `two_level`; env JM_P2P_TWO_LEVEL=0/1 overrides): a reduce
 kernel merges the rank's CTA records into one and pushes that, every rank
-merges `world` records -- the NCCL transport's merge tree, bit for bit
-(measured: 11.2 vs 19.6 us of merge at world 8; DESIGN 7b).
+merges `world` records -- the NCCL transport's merge tree, bit for bit.
+Measured on one B200 (DESIGN 7b): the reduce kernel adds 5.8 us to a cfg1
+step (43.7 -> 49.5 us at world 1) while the flat merge grows by 1.6 / 5.2 /
+13.1 us at world 2 / 4 / 8 -- the crossover lies between 4 and 8.
 
 torch.distributed is the plumbing (process group, rendezvous of the symmetric
 buffers, streams); all arithmetic is in libjmppi.so.  The host-side logic here
@@ -95,7 +97,7 @@ class ShardedLoop:
     transport: str = "nccl"
     two_level: bool = None  # p2p only; None: world >= TWO_LEVEL_MIN_WORLD (or JM_P2P_TWO_LEVEL)
 
-    TWO_LEVEL_MIN_WORLD = 4
+    TWO_LEVEL_MIN_WORLD = 6
 
     @classmethod
     def create(cls, task, cfg, rank: int, world: int, device: int, precision=None, group=None, transport="nccl"):
