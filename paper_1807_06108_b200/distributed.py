@@ -82,6 +82,19 @@ def exchange_records(local, group=None):
     return out
 
 
+TWO_LEVEL_MIN_WORLD = 6
+
+
+def use_two_level(world: int, env=None) -> bool:
+    """Whether the p2p exchange reduces each rank's CTA records to one before
+    the push: from TWO_LEVEL_MIN_WORLD ranks, unless JM_P2P_TWO_LEVEL=0/1 says."""
+    env = os.environ if env is None else env
+    v = env.get("JM_P2P_TWO_LEVEL", "")
+    if v not in ("", "0", "1"):
+        raise ValueError(f"JM_P2P_TWO_LEVEL must be 0 or 1, got {v!r}")
+    return bool(int(v)) if v else world >= TWO_LEVEL_MIN_WORLD
+
+
 @dataclass
 class ShardedLoop:
     """Closed-loop MPC with the sample set sharded over the ranks of a process group.
@@ -95,9 +108,7 @@ class ShardedLoop:
     rank: int
     group: object = None
     transport: str = "nccl"
-    two_level: bool = None  # p2p only; None: world >= TWO_LEVEL_MIN_WORLD (or JM_P2P_TWO_LEVEL)
-
-    TWO_LEVEL_MIN_WORLD = 6
+    two_level: bool = None  # p2p only; None: use_two_level(world)
 
     @classmethod
     def create(cls, task, cfg, rank: int, world: int, device: int, precision=None, group=None, transport="nccl"):
@@ -126,8 +137,7 @@ class ShardedLoop:
         torch.cuda.synchronize(dev)
         if self.transport == "p2p":
             if self.two_level is None:
-                env = os.environ.get("JM_P2P_TWO_LEVEL")
-                self.two_level = bool(int(env)) if env else self.world >= self.TWO_LEVEL_MIN_WORLD
+                self.two_level = use_two_level(self.world)
             self._init_peers(dev)
 
     def _init_peers(self, dev):

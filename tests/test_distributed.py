@@ -84,3 +84,15 @@ def test_gloo_world2_exchange(case):
     ref = om.mppi_iteration_oracle(spec, g["x0"], g["u_nom"], full)
     assert np.allclose(np.array(outs[0]["u_new"]), ref["u_new"], rtol=1e-11, atol=1e-11)
     assert outs[0]["rho"] == pytest.approx(ref["min_cost"], rel=1e-13)
+
+
+def test_two_level_exchange_policy():
+    """p2p exchange form: flat below 6 ranks, rank-local reduce from 6 (DESIGN 7b
+    measurements), JM_P2P_TWO_LEVEL forcing either, anything else rejected."""
+    from paper_1807_06108_b200 import distributed as jd
+
+    assert [jd.use_two_level(w, {}) for w in (1, 2, 4, 5, 6, 8)] == [False] * 4 + [True] * 2
+    assert jd.use_two_level(8, {"JM_P2P_TWO_LEVEL": "0"}) is False
+    assert jd.use_two_level(1, {"JM_P2P_TWO_LEVEL": "1"}) is True
+    with pytest.raises(ValueError):
+        jd.use_two_level(2, {"JM_P2P_TWO_LEVEL": "yes"})
