@@ -327,7 +327,9 @@ int jm_bench_iteration(jm_ctx* ctx, int32_t reps, int64_t flush_bytes, double* i
 /* FP32 FFMA and MUFU throughput microbenchmarks (the roofline denominators
  * SURVEY 8(d) asks to measure): returns TFLOP/s and Tops/s. */
 int jm_microbench(int device, double* fp32_tflops, double* mufu_tops, double* fp64_tflops);
-/* Name of the rollout kernel selected for this context (for ncu -k). */
+/* The non-trace rollout kernel variant this context launches (the one the bench
+ * times): "<kernel>/<noise>/<shape>/<precision>", e.g.
+ * "rollout_kernel/philox/single_wave_smem/f32" (ncu -k regex:<kernel>). */
 const char* jm_kernel_name(const jm_ctx* ctx);
 /* Number of kernel launches one jm_iteration_host / loop step enqueues. */
 int jm_launches_per_iteration(const jm_ctx* ctx, int32_t* iteration, int32_t* loop_step);

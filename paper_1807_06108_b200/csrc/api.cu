@@ -193,6 +193,7 @@ jm::FinArgs fin_args(const jm_ctx* ctx, const double* records, int nrec) {
   f.rec_stride = ctx->rec_stride;
   f.TM = ctx->TM;
   f.M = ctx->M;
+  f.cols = jm::fin_cols(ctx->M);
   f.inv_lam = 1.0 / ctx->mppi.lambda_;
   f.inv_sdt = 1.0 / std::sqrt(ctx->mppi.dt);
   return f;
@@ -1008,6 +1009,9 @@ int jm_loop_init(jm_ctx* ctx, const double* x0, const double* u_init, uint64_t s
   for (int t = 0; t < ctx->T; ++t)
     for (int j = 0; j < M; ++j) unom[(size_t)t * M + j] = u_init[j];  // initial_controller_state (controller.py:56-59)
   cudaStream_t s = ctx->own_stream;
+  // the last-CTA ticket of a previous run may have been left mid-count (a finalize CTA
+  // that timed out on a dead peer returns without taking its ticket)
+  CK(cudaMemsetAsync(ctx->d_counter, 0, sizeof(unsigned int), s));
   if (ctx->d_self_push)  // epochs restart at 1: clear the flags of the previous run
     CK(cudaMemsetAsync(ctx->d_self_push, 0, sizeof(double) * (size_t)jm_peer_buffer_doubles(ctx, 1), s));
   CK(cudaMemcpyAsync(ctx->d_loop, &h, sizeof(h), cudaMemcpyHostToDevice, s));
@@ -1077,7 +1081,7 @@ int jm_loop_finish_peers(jm_ctx* ctx, const double* my_buffer_dev, int32_t world
 }
 
 int jm_loop_rollout_reduce_push(jm_ctx* ctx, const unsigned long long* peer_bases_dev, int32_t rank, int32_t world) {
-  const int ncb = ctx ? (ctx->TM + jm::kFinCols - 1) / jm::kFinCols : 0;
+  const int ncb = ctx ? (ctx->TM + jm::fin_cols(ctx->M) - 1) / jm::fin_cols(ctx->M) : 0;
   if (!ctx || !ctx->d_loop || !peer_bases_dev || world < 1 || rank < 0 || rank >= world || ncb > ctx->grid)
     return fail(ctx, JM_ERR_VALUE, "bad arguments");
   CK(cudaSetDevice(ctx->device));
@@ -1099,7 +1103,7 @@ int jm_loop_finish_reduced_peers(jm_ctx* ctx, const double* my_buffer_dev, int32
   if (!ctx || !ctx->d_loop || !my_buffer_dev || world < 1 || world > jm::kMaxRecords)
     return fail(ctx, JM_ERR_VALUE, "bad arguments");
   CK(cudaSetDevice(ctx->device));
-  const int ncb = (ctx->TM + jm::kFinCols - 1) / jm::kFinCols;
+  const int ncb = (ctx->TM + jm::fin_cols(ctx->M) - 1) / jm::fin_cols(ctx->M);
   jm::FinArgs f = fin_args(ctx, my_buffer_dev, world);
   f.u_nom = ctx->d_loop_unom;
   f.u_new = ctx->d_loop_unew;
@@ -1496,7 +1500,7 @@ int jm_bench_iteration(jm_ctx* ctx, int32_t reps, int64_t flush_bytes, double* i
   return JM_OK;
 }
 
-const char* jm_kernel_name(const jm_ctx* ctx) { return ctx && ctx->eng ? ctx->eng->kernel_name(false) : ""; }
+const char* jm_kernel_name(const jm_ctx* ctx) { return ctx ? ctx->variant.c_str() : ""; }
 
 int jm_launches_per_iteration(const jm_ctx* ctx, int32_t* iteration, int32_t* loop_step) {
   if (!ctx) return fail(nullptr, JM_ERR_VALUE, "null context");

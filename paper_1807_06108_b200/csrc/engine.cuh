@@ -90,12 +90,21 @@ class Engine final : public EngineBase {
     return reinterpret_cast<const void*>(&rollout_kernel<Sys, Real, PH, TR, JM>);
   }
 
+  // (the dynamic-smem attribute is per FUNCTION, shared by every context of this
+  // engine type: it is raised to the device's opt-in maximum -- a bound, not a
+  // reservation -- so one context's configure never shrinks another's launch)
+  static cudaError_t raise_smem(const void* f, int optin) {
+    cudaFuncAttributes fa{};
+    cudaError_t e = cudaFuncGetAttributes(&fa, f);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
+  }
   template <int JM>
-  cudaError_t set_attrs(size_t smem, const void** main_fn, bool philox, bool scr_smem) {
+  cudaError_t set_attrs(int optin, const void** main_fn, bool philox, bool scr_smem) {
     const void* fns[4] = {kfn<true, false, JM>(), kfn<true, true, JM>(), kfn<false, false, JM>(),
                           kfn<false, true, JM>()};
     for (const void* f : fns) {
-      cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaError_t e = raise_smem(f, optin);
       if (e != cudaSuccess) return e;
     }
     *main_fn = philox ? (scr_smem ? reinterpret_cast<const void*>(&rollout_kernel<Sys, Real, true, false, JM, true>)
@@ -156,7 +165,7 @@ class Engine final : public EngineBase {
     c->ntiles = (K + block - 1) / block;
     // jump window: the longest (fewer window passes) whose staging fits; single
     // wave: also keep the eps scratch in shared memory if possible
-    const size_t cap = (size_t)optin - 1024;
+    const size_t cap = (size_t)optin - 2048;  // (static shared memory of the rollout kernels: ~1.1 KB)
     const bool single = philox && !no_eps_smem && c->ntiles <= sms;
     // multi-wave: two CTAs per SM must still fit (the occupancy the 256-sample tiles need)
     const size_t budget = single ? cap : std::min(cap, (size_t)optin / 2 - 2048);
@@ -176,10 +185,10 @@ class Engine final : public EngineBase {
     const size_t smem = plan_bytes(c, block, mwarps, W, 0, false);  // trace / HBM kernels
     const void* fn = nullptr;
     const bool sj = c->model.jump_channel == JM_JUMP_STATE;
-    e = sj ? set_attrs<1>(smem, &fn, philox, c->eps_smem) : set_attrs<0>(smem, &fn, philox, c->eps_smem);
+    e = sj ? set_attrs<1>(optin, &fn, philox, c->eps_smem) : set_attrs<0>(optin, &fn, philox, c->eps_smem);
     if (e != cudaSuccess) return e;
     if (ws) fn = sj ? ws_fn<1>(c->eps_smem) : ws_fn<0>(c->eps_smem);
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem);
+    e = raise_smem(fn, optin);
     if (e != cudaSuccess) return e;
     int occ = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, msmem);
@@ -188,6 +197,10 @@ class Engine final : public EngineBase {
     c->smem = smem;
     c->main_smem = msmem;
     c->grid = std::min(c->ntiles, occ * sms);
+    // the non-trace kernel this context launches (jm_kernel_name; ncu -k regex:rollout_kernel)
+    c->variant = std::string(ws ? "rollout_kernel_ws" : "rollout_kernel") + "/" + (philox ? "philox" : "hbm") + "/" +
+                 (ws ? "ws" : (!philox ? "hbm" : (c->eps_smem ? "single_wave_smem" : "multi_wave"))) + "/" +
+                 (sizeof(Real) == 4 ? "f32" : "f64");
     if (c->grid > kMaxRecords) c->grid = kMaxRecords;
     const size_t fsm = finalize_smem_bytes(kMaxRecords);
     return cudaFuncSetAttribute(reinterpret_cast<const void*>(&finalize_kernel<Dyn>),
@@ -343,15 +356,12 @@ class Engine final : public EngineBase {
     f.loop = loop;
     if (!f.counter) f.counter = c->d_counter;
     const PlantArgs p = plant_args(c, loop, f.u_new, u_nom_next);
-    const int fgrid = (c->TM + kFinCols - 1) / kFinCols;
+    f.cols = fin_cols(M);
+    const int fgrid = (c->TM + f.cols - 1) / f.cols;
     return launch_pdl(finalize_kernel<Dyn>, dim3(fgrid, c->launch_trials), dim3(kFinThreads), finalize_smem_bytes(f.nrec), c->stream,
                       f, p);
   }
 
-  const char* kernel_name(bool trace) const override {
-    (void)trace;
-    return "rollout_kernel";  // ncu -k regex:rollout_kernel
-  }
 };
 
 }  // namespace jm

@@ -38,7 +38,6 @@ struct EngineBase {
   // combine records -> u_new (+ diagnostics); loop != null: the last CTA also
   // runs the plant step and writes the shifted sequence to u_nom_next
   virtual cudaError_t finalize(jm_ctx* c, FinArgs f, LoopState* loop, double* u_nom_next) = 0;
-  virtual const char* kernel_name(bool trace) const = 0;
 };
 
 EngineBase* make_engine_integrator(int cost_kind, int precision, int n);
@@ -117,6 +116,7 @@ struct jm_ctx {
   cudaGraphExec_t iter_exec = nullptr;  // graph of one drop-in iteration (H2D..D2H)
   cudaGraphExec_t graph_exec = nullptr;
   std::string err;
+  std::string variant;  // rollout kernel variant the launcher picked (jm_kernel_name)
 
   // d_small / h_small layout (doubles):
   //   inputs  [x0:16][u_nom:TM][mapping:16][u_init:16]   (x0 slots 13..15 of

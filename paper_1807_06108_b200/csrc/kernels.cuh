@@ -28,7 +28,9 @@
 
 namespace jm {
 
-constexpr int kFinCols = 128;      // finalize: columns per CTA (multiple of m for m in {1,2,4})
+constexpr int kFinCols = 128;      // finalize: column capacity of a CTA; it owns fin_cols(m) <= 128 of them
+// columns per finalize CTA: a multiple of m, so a CTA holds whole steps (mapping rows, per-step norms)
+__host__ __device__ __forceinline__ int fin_cols(int m) { return (kFinCols / m) * m; }
 #ifndef JM_FIN_THREADS
 #define JM_FIN_THREADS 1024
 #endif
@@ -1329,6 +1331,7 @@ __device__ void plant_finish(const PlantArgs& a, const PlantPre& pre, const doub
 struct FinArgs {
   const double* rec;
   int nrec, rec_stride, TM, M;
+  int cols;  // columns per CTA, fin_cols(M)
   double inv_lam, inv_sdt;
   const double* u_nom;
   const double* mapping;  // m x m or null
@@ -1364,7 +1367,7 @@ struct FinArgs {
 __device__ __forceinline__ void fin_emit_record(const FinArgs& a, int c0, double rho, double Z, double W2, double NF,
                                                 const double* cols) {
   const int tid = threadIdx.x;
-  const int ncol = min(kFinCols, a.TM - c0);
+  const int ncol = min(a.cols, a.TM - c0);
   if (a.push_peers == nullptr) {
     if (blockIdx.x == 0 && tid == 0) {
       a.rec_out[0] = rho;
@@ -1441,10 +1444,12 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
   // nominal controls (written by the previous step's shift / the input copy,
   // both complete before this step's rollout released us) and `halted`
   if (L != nullptr && tid == kFinThreads - 1) plant_prepare<Dyn>(p, s_pre);
-  const bool halted = L != nullptr && L->halted;
-  const int c0 = blockIdx.x * kFinCols;
+  // (the two-level reduce runs without a loop of its own: it stops with the loop it pushes for,
+  // so a halted rank no longer re-pushes stale records and raises peers' flags)
+  const bool halted = (L != nullptr && L->halted) || (a.push_loop != nullptr && a.push_loop->halted);
+  const int c0 = blockIdx.x * a.cols;
   const bool reduce_mode = a.rec_out != nullptr || a.push_peers != nullptr;
-  const double unom_c = (!reduce_mode && tid < kFinCols && c0 + tid < a.TM) ? unom[c0 + tid] : 0.0;
+  const double unom_c = (!reduce_mode && tid < a.cols && c0 + tid < a.TM) ? unom[c0 + tid] : 0.0;
   grid_dep_wait();
   if (halted) return;
   const int rs = a.rec_stride;
@@ -1506,7 +1511,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
 #pragma unroll
       for (int i = 0; i < CPL; ++i) {
         const int c = c0 + lane + 32 * i;
-        if (c < a.TM && ((c & 15) == 0 || c == c0 + lane)) asm volatile("prefetch.global.L1 [%0];" ::"l"(r + c));
+        if (c < a.TM && lane + 32 * i < a.cols && ((c & 15) == 0 || c == c0 + lane)) asm volatile("prefetch.global.L1 [%0];" ::"l"(r + c));
       }
     }
   }
@@ -1563,7 +1568,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
       fin_emit_record(a, c0, CUDART_INF, 0.0, 0.0, 0.0, nullptr);
       return;
     }
-    for (int c = c0 + tid; c < min(c0 + kFinCols, a.TM); c += kFinThreads) unew[c] = unom[c];
+    for (int c = c0 + tid; c < min(c0 + a.cols, a.TM); c += kFinThreads) unew[c] = unom[c];
     return;
   }
   // columns: warps split records (several in flight), lanes split columns
@@ -1578,7 +1583,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
 #pragma unroll
     for (int i = 0; i < CPL; ++i) {
       const int c = c0 + lane + 32 * i;
-      if (c < a.TM) acc[i] = fma(r[c], e, acc[i]);
+      if (c < a.TM && lane + 32 * i < a.cols) acc[i] = fma(r[c], e, acc[i]);
     }
   }
 #pragma unroll
@@ -1610,7 +1615,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
   double out = 0.0;
   const int c = c0 + tid;
   const int M = a.M;
-  if (tid < kFinCols && c < a.TM) {
+  if (tid < a.cols && c < a.TM) {
     const int j = c % M, cb = tid - j;
     if (a.mapping) {
       for (int l = 0; l < M; ++l) out = fma(a.mapping[j * M + l], s_delta[cb + l] * scale, out);
@@ -1619,7 +1624,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
     }
   }
   __syncthreads();
-  if (tid < kFinCols && c < a.TM) {
+  if (tid < a.cols && c < a.TM) {
     s_delta[tid] = out;
     const double un = unom_c + out;  // u_nom + delta, unclamped (controller.py:161)
     s_unew[tid] = un;
@@ -1629,7 +1634,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
   FIN_STAMP();
   if (a.norms) {  // per_step_update_norm (controller.py:168)
     const int tl = tid, t = c0 / M + tl;
-    if (tl < kFinCols / M && t * M < a.TM) {
+    if (tl < a.cols / M && t * M < a.TM) {
       double s2 = 0.0;
       for (int j = 0; j < M; ++j) s2 += s_delta[tl * M + j] * s_delta[tl * M + j];
       a.norms[t] = sqrt(s2);

@@ -175,3 +175,21 @@ def test_shards_reproduce_the_unsharded_noise(gpu_device):
     hi = engine.get_context(model, cost, half, precision="f64", sample_offset=256).sample_noise(3, 4)
     for f, a, b in zip(full, lo, hi):
         assert np.array_equal(f, np.concatenate([a, b]))
+
+
+def test_linear_6x3_long_horizon_with_mapping(gpu_device):
+    """m = 3 with T*m > 128: each finalize CTA owns whole steps (fin_cols = 126),
+    so the mapping rows and per-step norms of later steps stay aligned."""
+    g, s, model, cost, cfg = _philox_setup("r_linear_6x3", K=300, T=60)
+    mapping = np.array([[1.0, 0.2, 0.0], [0.1, 0.9, 0.3], [0.0, -0.2, 1.1]])
+    u_nom = 0.1 * np.sin(np.arange(60 * 3, dtype=float)).reshape(60, 3)
+    spec = oracle_spec(s)
+    spec.T, spec.K = 60, 300
+    for prec in ("f64", "f32"):
+        ctrl = jb.ControllerState(jb.ControlSequence(u_nom, s["dt"]), 5, cfg)
+        seq, diag = jb.mppi_iteration(ctrl, model, cost, g["x0"], 77, mapping=mapping, precision=prec)
+        noise = jb.sample_noise_batch(jb.RngStream(77, 5), cfg, 300, model=model, precision=prec)
+        out = om.mppi_iteration_oracle(spec, g["x0"], u_nom, noise, np.float64, mapping=mapping)
+        tol = G_DOUBLE if prec == "f64" else 1e-4
+        assert normwise(seq.controls - u_nom, out["u_new"] - u_nom) <= tol, prec
+        assert np.allclose(diag.per_step_update_norm, out["norms"], rtol=10 * tol, atol=1e-12), prec
