@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define JM_ABI_VERSION 4
+#define JM_ABI_VERSION 5
 #define JM_MAX_STATE 12
 #define JM_MAX_CONTROL 4
 #define JM_MAX_JUMP 4
@@ -270,18 +270,21 @@ int jm_loop_rollout(jm_ctx* ctx, double* record_dev);
 int jm_loop_finish(jm_ctx* ctx, const double* records_dev, int32_t nrec);
 
 /* Batched closed-loop trials (run_batch, harness.py:197-233, with the process
- * pool replaced by a trial dimension on the GPU): `trials` independent
+ * pool replaced by a trial dimension on the GPU): `trials` (<= 128) independent
  * run_trial loops of `steps` control steps, trial b from x0[b*n..] with
  * master seed seeds[b], all advanced by the same two launches per control
- * step (grid.y = trial).  Each trial's outputs equal a jm_closed_loop_host
+ * step (grid.y = trial).  sampler_jumps[b] = 0 makes trial b's sampler draw
+ * no jumps -- the "old" controller variant (jump_sampling_enabled = False,
+ * harness.py:218-221) -- so both variants of a paired batch run as ONE batch
+ * (NULL: every trial as the context's config says).  Each trial's outputs equal a jm_closed_loop_host
  * run with its seed, bit for bit.  Outputs are trial-major:
  * states (trials, steps+1, n), controls (trials, steps, m), jumps (trials,
  * steps), step_ns (trials, steps), diverged_at / status (trials); any may be
  * NULL.  A trial halts on its own (divergence, no viable rollout) without
  * stopping the others. */
 int jm_batch_loop_host(jm_ctx* ctx, int32_t trials, const double* x0, const double* u_init,
-                       const uint64_t* seeds, int32_t steps, double* states, double* controls, int64_t* jumps,
-                       double* step_ns, int32_t* diverged_at, int32_t* status);
+                       const uint64_t* seeds, const int32_t* sampler_jumps, int32_t steps, double* states,
+                       double* controls, int64_t* jumps, double* step_ns, int32_t* diverged_at, int32_t* status);
 
 /* Peer-memory record exchange -- the multi-GPU step without a collective.
  * Every rank owns a symmetric buffer (e.g. torch.distributed._symmetric_memory)

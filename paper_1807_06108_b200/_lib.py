@@ -106,7 +106,7 @@ SIGNATURES = {
     "jm_loop_finish_peers": (C.c_int, [_vp, _vp, _i32]),
     "jm_loop_rollout_reduce_push": (C.c_int, [_vp, _vp, _i32, _i32]),
     "jm_loop_finish_reduced_peers": (C.c_int, [_vp, _vp, _i32]),
-    "jm_batch_loop_host": (C.c_int, [_vp, _i32, _pd, _pd, _pu64, _i32, _pd, _pd, _pi64, _pd, _pi32, _pi32]),
+    "jm_batch_loop_host": (C.c_int, [_vp, _i32, _pd, _pd, _pu64, _pi32, _i32, _pd, _pd, _pi64, _pd, _pi32, _pi32]),
     "jm_loop_init": (C.c_int, [_vp, _pd, _pd, _u64, _u64, _i32]),
     "jm_loop_step": (C.c_int, [_vp]),
     "jm_loop_history": (C.c_int, [_vp, _i32, _pd, _pd, _pi64]),
@@ -145,7 +145,7 @@ def load(path: os.PathLike = LIB_PATH) -> C.CDLL:
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.jm_abi_version() != 4:
+        if lib.jm_abi_version() != 5:
             raise LibraryMissing("libjmppi.so ABI version mismatch")
         _lib = lib
         return lib

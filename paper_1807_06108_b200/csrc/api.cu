@@ -246,9 +246,22 @@ int stash_acquire(jm_ctx* ctx, uint64_t* handle) {
 // raises a done word there last -- the host spins on that word instead of a
 // stream synchronisation.  Weights are formed from the stashed costs when
 // first read (jm_stash_fetch).  seed / iteration / stash pointer travel in the
-// staged block (x0 slots 13..15), so replays need no parameter updates.
-int capture_iteration_graph(jm_ctx* ctx) {
-  if (ctx->iter_exec) return JM_OK;
+// staged block (x0 slots 13 and 15), so replays need no parameter updates; the master
+// seed is a kernel parameter (uniform-register Philox keys): one graph per seed, a few
+// kept (a controller keeps its seed: run_trial, the CLI bench loop).
+constexpr size_t kIterGraphs = 8;
+int capture_iteration_graph(jm_ctx* ctx, uint64_t seed, cudaGraphExec_t* out) {
+  auto& v = ctx->iter_execs;
+  for (size_t i = 0; i < v.size(); ++i)
+    if (v[i].first == seed) {
+      *out = v[i].second;
+      if (i + 1 != v.size()) std::rotate(v.begin() + i, v.begin() + i + 1, v.end());  // most recent last
+      return JM_OK;
+    }
+  if (v.size() >= kIterGraphs) {
+    cudaGraphExecDestroy(v.front().second);
+    v.erase(v.begin());
+  }
   cudaStream_t saved = ctx->stream;
   ctx->stream = ctx->own_stream;
   double* ds = ctx->d_small;
@@ -260,7 +273,7 @@ int capture_iteration_graph(jm_ctx* ctx) {
   jm::RolloutCall rc;
   rc.x0 = ds + ctx->off_x0();
   rc.u_nom = ds + ctx->off_unom();
-  rc.seed_dev = words + 14;
+  rc.seed = seed;
   rc.iteration_dev = words + 15;
   rc.costs_dev = reinterpret_cast<double* const*>(words + 13);  // costs straight into the stash buffer
   if (e == cudaSuccess) e = ctx->eng->rollout(ctx, rc);
@@ -281,9 +294,12 @@ int capture_iteration_graph(jm_ctx* ctx) {
   ctx->stream = saved;
   CK(e);
   CK(e2);
-  cudaError_t e3 = cudaGraphInstantiate(&ctx->iter_exec, g, 0);
+  cudaGraphExec_t ge = nullptr;
+  cudaError_t e3 = cudaGraphInstantiate(&ge, g, 0);
   cudaGraphDestroy(g);
   CK(e3);
+  v.emplace_back(seed, ge);
+  *out = ge;
   return JM_OK;
 }
 
@@ -292,7 +308,8 @@ int capture_iteration_graph(jm_ctx* ctx) {
 // (h_small from off_unew on).
 int dropin_launch(jm_ctx* ctx, const double* x0, const double* u_nom, const double* u_init, uint64_t seed,
                   uint64_t iteration, uint64_t* weights_stash) {
-  int r = capture_iteration_graph(ctx);
+  cudaGraphExec_t ge = nullptr;
+  int r = capture_iteration_graph(ctx, seed, &ge);
   if (r != JM_OK) return r;
   uint64_t handle = 0;
   r = stash_acquire(ctx, &handle);
@@ -303,12 +320,11 @@ int dropin_launch(jm_ctx* ctx, const double* x0, const double* u_nom, const doub
   std::memcpy(hs + ctx->off_uinit(), u_init, sizeof(double) * ctx->M);
   uint64_t* words = reinterpret_cast<uint64_t*>(hs + ctx->off_x0());
   words[13] = reinterpret_cast<uint64_t>(ctx->stash[handle - 1]);
-  words[14] = seed;
   words[15] = iteration;
   volatile int32_t* st = reinterpret_cast<volatile int32_t*>(hs + ctx->off_status());
   st[0] = 0;
   st[1] = 0;  // done word, raised by the finalize after its last output
-  CK(cudaGraphLaunch(ctx->iter_exec, ctx->stream));
+  CK(cudaGraphLaunch(ge, ctx->stream));
   // spin on the done word (a stream synchronisation wakes the host several
   // microseconds later); fall back to the synchronisation after 2 s so a
   // faulting launch still reports its error
@@ -349,6 +365,7 @@ cudaError_t loop_step_launches(jm_ctx* ctx, cudaEvent_t mid) {
   rc.u_nom = ctx->d_loop_unom;
   rc.costs = ctx->d_costs;
   rc.loop = ctx->d_loop;
+  rc.seed = ctx->loop_seed;  // the loop's master seed (a kernel parameter)
   // opt-in (JM_SELF_PUSH=1): measured 46.2 vs 43.4 us per cfg1 step -- the 147
   // CTAs finish within ~1 us of each other, so merging behind the flags
   // overlaps little and the per-record flag polls lengthen each warp's chain
@@ -556,7 +573,7 @@ int jm_destroy(jm_ctx* ctx) {
   if (ctx->own_stream) cudaStreamSynchronize(ctx->own_stream);
   if (ctx->graph_exec) cudaGraphExecDestroy(ctx->graph_exec);
   if (ctx->graph) cudaGraphDestroy(ctx->graph);
-  if (ctx->iter_exec) cudaGraphExecDestroy(ctx->iter_exec);
+  for (auto& pe : ctx->iter_execs) cudaGraphExecDestroy(pe.second);
   dfree(ctx->d_scratch);
   dfree(ctx->d_gap);
   dfree(ctx->d_lin_f);
@@ -966,11 +983,14 @@ int jm_loop_init(jm_ctx* ctx, const double* x0, const double* u_init, uint64_t s
     return fail(ctx, JM_ERR_UNSUPPORTED, "the device closed loop samples its own (Philox) noise");
   CK(cudaSetDevice(ctx->device));
   const int N = ctx->N, M = ctx->M, TM = ctx->TM;
-  if (max_steps > ctx->loop_cap) {
+  if (max_steps > ctx->loop_cap || (ctx->graph_exec && seed != ctx->loop_seed)) {  // (re)capture
     if (ctx->graph_exec) cudaGraphExecDestroy(ctx->graph_exec);
     if (ctx->graph) cudaGraphDestroy(ctx->graph);
     ctx->graph_exec = nullptr;
     ctx->graph = nullptr;
+  }
+  ctx->loop_seed = seed;
+  if (max_steps > ctx->loop_cap) {
     dfree(ctx->d_hist);
     dfree(ctx->d_hist_jumps);
     dfree(ctx->d_hist_t);
@@ -1000,6 +1020,7 @@ int jm_loop_init(jm_ctx* ctx, const double* x0, const double* u_init, uint64_t s
   h.halted = 0;
   h.status = 0;
   h.diverged_at = -1;
+  h.sampler_jumps = 1;
   h.hist_states = ctx->d_hist;
   h.hist_controls = ctx->d_hist + (size_t)(ctx->loop_cap + 1) * N;
   h.hist_jumps = ctx->d_hist_jumps;
@@ -1028,6 +1049,7 @@ int jm_loop_rollout(jm_ctx* ctx, double* record_dev) {
   rc.u_nom = ctx->d_loop_unom;
   rc.costs = ctx->d_costs;
   rc.loop = ctx->d_loop;
+  rc.seed = ctx->loop_seed;  // the loop's master seed (a kernel parameter)
   CK(ctx->eng->rollout(ctx, rc));
   jm::FinArgs f = fin_args(ctx, nullptr, 0);
   f.rec_out = record_dev;
@@ -1060,6 +1082,7 @@ int jm_loop_rollout_push(jm_ctx* ctx, const unsigned long long* peer_bases_dev, 
   jm::RolloutCall rc;
   rc.u_nom = ctx->d_loop_unom;
   rc.loop = ctx->d_loop;
+  rc.seed = ctx->loop_seed;  // the loop's master seed (a kernel parameter)
   rc.push_peers = peer_bases_dev;
   rc.push_rank = rank;
   rc.push_world = world;
@@ -1089,6 +1112,7 @@ int jm_loop_rollout_reduce_push(jm_ctx* ctx, const unsigned long long* peer_base
   rc.u_nom = ctx->d_loop_unom;
   rc.costs = ctx->d_costs;
   rc.loop = ctx->d_loop;
+  rc.seed = ctx->loop_seed;  // the loop's master seed (a kernel parameter)
   CK(ctx->eng->rollout(ctx, rc));
   jm::FinArgs f = fin_args(ctx, nullptr, 0);  // reduce this rank's CTA records ...
   f.push_peers = peer_bases_dev;              // ... into slot `rank` of every peer buffer
@@ -1192,12 +1216,13 @@ int jm_closed_loop_host(jm_ctx* ctx, const double* x0, const double* u_init, uin
 }
 
 int jm_batch_loop_host(jm_ctx* ctx, int32_t trials, const double* x0, const double* u_init,
-                       const uint64_t* seeds, int32_t steps, double* states, double* controls, int64_t* jumps,
-                       double* step_ns, int32_t* diverged_at, int32_t* status) {
+                       const uint64_t* seeds, const int32_t* sampler_jumps, int32_t steps, double* states,
+                       double* controls, int64_t* jumps, double* step_ns, int32_t* diverged_at, int32_t* status) {
   if (!ctx || !x0 || !u_init || !seeds || trials < 1 || steps < 1) return fail(ctx, JM_ERR_VALUE, "bad arguments");
   if (ctx->mppi.noise_source != JM_NOISE_PHILOX)
     return fail(ctx, JM_ERR_UNSUPPORTED, "the device closed loop samples its own (Philox) noise");
-  if (trials > 65535) return fail(ctx, JM_ERR_VALUE, "at most 65535 trials per batch");
+  if (trials > jm::kMaxSeeds)
+    return fail(ctx, JM_ERR_VALUE, "at most %d trials per batch (the master seeds are kernel parameters)", jm::kMaxSeeds);
   CK(cudaSetDevice(ctx->device));
   const int N = ctx->N, M = ctx->M, TM = ctx->TM, B = trials;
   const size_t S = (size_t)steps;
@@ -1228,6 +1253,7 @@ int jm_batch_loop_host(jm_ctx* ctx, int32_t trials, const double* x0, const doub
     for (int i = 0; i < N; ++i) h.x[i] = x0[(size_t)b * N + i];
     for (int j = 0; j < M; ++j) h.u_init[j] = u_init[j];
     h.seed = seeds[b];
+    h.sampler_jumps = sampler_jumps ? (sampler_jumps[b] != 0) : 1;
     h.iteration = 0;
     h.max_steps = steps;
     h.diverged_at = -1;
@@ -1260,6 +1286,8 @@ int jm_batch_loop_host(jm_ctx* ctx, int32_t trials, const double* x0, const doub
       jm::RolloutCall rc;
       rc.u_nom = d_unom;
       rc.loop = d_loop;
+      rc.seeds = seeds;  // trial b's master seed is the kernels' seeds[b] (blockIdx.y = b)
+      rc.nseeds = B;
       cudaError_t e1 = ctx->eng->rollout(ctx, rc);
       if (e1 == cudaSuccess) {
         jm::FinArgs f = fin_args(ctx, nullptr, 0);

@@ -9,6 +9,7 @@
 #include <utility>
 
 #include "internal.h"
+#include "rollout_fast.cuh"
 
 namespace jm {
 
@@ -113,6 +114,33 @@ class Engine final : public EngineBase {
     return cudaSuccess;
   }
 
+  // the product (non-trace) kernel, rollout_fast: SPT samples per thread
+  // (2: packed f32x2, for the BASELINE systems in fp32)
+  static constexpr bool kPackable = std::is_same<Real, float>::value &&
+                                    (std::is_same<Dyn, Cartpole>::value || std::is_same<Dyn, Quadrotor>::value);
+  template <bool PH, int JM, int SPT>
+  static const void* fast_fn() {
+    if constexpr (SPT == 2 && kPackable)
+      return reinterpret_cast<const void*>(&rollout_fast<Sys, Real, PH, JM, 2, 256>);
+    else
+      return reinterpret_cast<const void*>(&rollout_fast<Sys, Real, PH, JM, 1, 512>);
+  }
+  static const void* fast_fn_rt(bool ph, int jm, int spt) {
+    if (ph) {
+      if (jm) return spt == 2 ? fast_fn<true, 1, 2>() : fast_fn<true, 1, 1>();
+      return spt == 2 ? fast_fn<true, 0, 2>() : fast_fn<true, 0, 1>();
+    }
+    if (jm) return spt == 2 ? fast_fn<false, 1, 2>() : fast_fn<false, 1, 1>();
+    return spt == 2 ? fast_fn<false, 0, 2>() : fast_fn<false, 0, 1>();
+  }
+  // steps per regeneration item (kernel GS) and the fast kernel's shared memory
+  int fast_gs(bool philox) const { return philox ? 4 / Pad<M>::value : (M >= 3 ? 1 : 4); }
+  size_t fast_bytes(const jm_ctx* c, int tile, int spt, int W, bool philox) const {
+    const int nb = regen_items(c->T, fast_gs(philox));
+    const int nmarks = (philox && c->jthr) ? tile * W * q_of(c) : 0;
+    return fast_plan(c->TM, c->T * (2 * M + 1), tile, tile / spt, nb, nmarks, c->gap_n, (int)sizeof(Real)).total;
+  }
+
   // warp-specialised kernel (Philox, non-trace): block = 2 x tile
   static constexpr int kWsMaxThreads = (N <= 4) ? 1024 : 512;
   static constexpr int kWsBufs = 6;  // ring depth: slack for the producers' jump-window bursts
@@ -143,14 +171,21 @@ class Engine final : public EngineBase {
     const bool philox = c->mppi.noise_source == JM_NOISE_PHILOX;
     static const int ws_env = std::getenv("JM_WS") ? std::atoi(std::getenv("JM_WS")) : -1;  // A/B: 0 off, 1 on
     static const bool no_eps_smem = std::getenv("JM_NO_EPS_SMEM") != nullptr;
+    static const int spt_env = std::getenv("JM_SPT") ? std::atoi(std::getenv("JM_SPT")) : 0;  // A/B: 1 or 2
     int block = c->mppi.block_threads;
     const int K = c->K, sms = c->num_sms;
+    // samples per thread of the product kernel: packed pairs need an even K
+    // (adjacent HBM columns) and tiles of whole 64-sample warp pairs
+    // default (measured, DESIGN 6): pairs where the kernel is issue-bound (multi-wave, HBM
+    // mode); one sample per thread in the latency-bound single wave (more warps in flight)
+    const bool want2 = spt_env ? spt_env == 2 : (!philox || K > sms * kRolloutMaxThreads);
+    int spt = (kPackable && want2 && K % 2 == 0 && (block <= 0 || block % 64 == 0)) ? 2 : 1;
     if (block <= 0) {
       if (K <= sms * kRolloutMaxThreads) {
         const int per = (K + sms - 1) / sms;
-        block = std::max(32, ((per + 31) / 32) * 32);
+        block = std::max(32 * spt, ((per + 32 * spt - 1) / (32 * spt)) * (32 * spt));
       } else {
-        block = 256;
+        block = 256 * spt;
       }
     }
     const bool ws = philox && 2 * block <= kWsMaxThreads && (ws_env < 0 ? block <= kWsMaxTile : ws_env == 1);
@@ -182,25 +217,41 @@ class Engine final : public EngineBase {
                                 : plan_bytes(c, block, 0, 0, nring, true)) <= cap;
     const size_t msmem = (c->eps_smem && !ws) ? plan_bytes(c, block, 0, 0, nring, true)
                                               : plan_bytes(c, block, mwarps, W, nring, c->eps_smem);
-    const size_t smem = plan_bytes(c, block, mwarps, W, 0, false);  // trace / HBM kernels
+    const size_t smem = plan_bytes(c, block, mwarps, W, 0, false);  // trace kernels
+    const bool fast = !ws;  // the product kernel (Philox without warp specialisation, and HBM)
+    c->fast = fast;
+    c->spt = spt;
+    size_t fsmem = 0;
+    int WF = 0;
+    if (fast) {
+      // multi-wave: two CTAs per SM must fit; single wave: the whole SM
+      const size_t fbudget = (c->ntiles <= sms) ? cap : std::min(cap, (size_t)optin / 2 - 2048);
+      WF = std::min(128, (c->T + 3) / 4 * 4);
+      while (WF > 8 && fast_bytes(c, block, spt, WF, philox) > fbudget) WF -= 4;
+      fsmem = fast_bytes(c, block, spt, WF, philox);
+      if (fsmem > cap) return cudaErrorInvalidConfiguration;
+    }
+    c->jw_fast = WF;
+    c->fast_smem = fsmem;
     const void* fn = nullptr;
     const bool sj = c->model.jump_channel == JM_JUMP_STATE;
     e = sj ? set_attrs<1>(optin, &fn, philox, c->eps_smem) : set_attrs<0>(optin, &fn, philox, c->eps_smem);
     if (e != cudaSuccess) return e;
     if (ws) fn = sj ? ws_fn<1>(c->eps_smem) : ws_fn<0>(c->eps_smem);
+    if (fast) fn = fast_fn_rt(philox, sj ? 1 : 0, spt);
     e = raise_smem(fn, optin);
     if (e != cudaSuccess) return e;
     int occ = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, msmem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, fast ? block / spt : threads, fast ? fsmem : msmem);
     if (e != cudaSuccess) return e;
     if (occ < 1) return cudaErrorInvalidConfiguration;
     c->smem = smem;
     c->main_smem = msmem;
     c->grid = std::min(c->ntiles, occ * sms);
     // the non-trace kernel this context launches (jm_kernel_name; ncu -k regex:rollout_kernel)
-    c->variant = std::string(ws ? "rollout_kernel_ws" : "rollout_kernel") + "/" + (philox ? "philox" : "hbm") + "/" +
-                 (ws ? "ws" : (!philox ? "hbm" : (c->eps_smem ? "single_wave_smem" : "multi_wave"))) + "/" +
-                 (sizeof(Real) == 4 ? "f32" : "f64");
+    c->variant = std::string(ws ? "rollout_kernel_ws" : "rollout_fast") + "/" + (philox ? "philox" : "hbm") + "/" +
+                 (ws ? "ws" : (c->ntiles <= sms ? "single_wave" : "multi_wave")) + "/" +
+                 (sizeof(Real) == 4 ? "f32" : "f64") + (fast ? "/spt" + std::to_string(spt) : "");
     if (c->grid > kMaxRecords) c->grid = kMaxRecords;
     const size_t fsm = finalize_smem_bytes(kMaxRecords);
     return cudaFuncSetAttribute(reinterpret_cast<const void*>(&finalize_kernel<Dyn>),
@@ -243,10 +294,9 @@ class Engine final : public EngineBase {
     a.jw_len = c->jw_len;
     a.jscale = Real(c->model.jump_scale_unit ? 1.0 : std::sqrt(dt));
     fill_sys<Real>(c, a.sp);
-    a.seed = rc.seed;
+    for (int i = 0; i < kMaxSeeds; ++i) a.seeds[i] = (rc.seeds && i < rc.nseeds) ? rc.seeds[i] : rc.seed;
     a.iteration = rc.iteration;
     a.iteration_dev = rc.iteration_dev;
-    a.seed_dev = rc.seed_dev;
     a.x0 = rc.x0;
     a.u_nom = rc.u_nom;
     a.eps_in = reinterpret_cast<const Real*>(rc.eps_in);
@@ -283,9 +333,24 @@ class Engine final : public EngineBase {
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
   }
 
+  template <bool PH, int JM, int SPT>
+  cudaError_t launch_fast(jm_ctx* c, const RolloutArgs<Real>& a) {
+    RolloutArgs<Real> b = a;
+    b.jw_len = c->jw_fast;
+    dim3 grid(c->grid, c->launch_trials), block(c->block / SPT);
+    if constexpr (SPT == 2 && kPackable)
+      return launch_pdl(rollout_fast<Sys, Real, PH, JM, 2, 256>, grid, block, c->fast_smem, c->stream, b);
+    else
+      return launch_pdl(rollout_fast<Sys, Real, PH, JM, 1, 512>, grid, block, c->fast_smem, c->stream, b);
+  }
+
   template <int JM>
   cudaError_t launch(jm_ctx* c, const RolloutArgs<Real>& a, bool philox, bool trace) {
     dim3 grid(c->grid, c->launch_trials), block(c->block);
+    if (!trace && c->fast) {
+      if (philox) return c->spt == 2 ? launch_fast<true, JM, 2>(c, a) : launch_fast<true, JM, 1>(c, a);
+      return c->spt == 2 ? launch_fast<false, JM, 2>(c, a) : launch_fast<false, JM, 1>(c, a);
+    }
     if (philox && !trace && c->ws)
       return c->eps_smem ? launch_pdl(ws_kern<JM, true>(), grid, dim3(2 * c->block), c->main_smem, c->stream, a)
                          : launch_pdl(ws_kern<JM, false>(), grid, dim3(2 * c->block), c->main_smem, c->stream, a);

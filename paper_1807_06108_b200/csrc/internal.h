@@ -16,8 +16,9 @@ struct RolloutCall {
   const double* x0 = nullptr;
   const double* u_nom = nullptr;
   uint64_t seed = 0, iteration = 0;
+  const uint64_t* seeds = nullptr;  // batched trials: one master seed per grid.y slice (nseeds <= kMaxSeeds)
+  int nseeds = 0;
   const uint64_t* iteration_dev = nullptr;
-  const uint64_t* seed_dev = nullptr;
   double* const* costs_dev = nullptr;
   const void* eps_in = nullptr;
   const void* jump_in = nullptr;
@@ -59,6 +60,10 @@ struct jm_ctx {
   int block = 128, grid = 1, ntiles = 1;
   int ws = 0;              // warp-specialised Philox rollout: block of 2*block threads
   int eps_smem = 0;        // Philox main kernel keeps the eps scratch in shared memory
+  int fast = 0;            // non-trace launches use rollout_fast (rollout_fast.cuh)
+  int spt = 1;             // rollout_fast: samples per thread (2 = packed f32x2)
+  int jw_fast = 0;         // rollout_fast: jump window (steps)
+  size_t fast_smem = 0;    // rollout_fast: dynamic shared memory
   size_t main_smem = 0;    // dynamic smem of the Philox main kernel
   size_t smem = 0;
   size_t real_size = 4;
@@ -113,7 +118,10 @@ struct jm_ctx {
   void* d_flush = nullptr;         // L2 flush buffer (bench)
   size_t flush_cap = 0;
   cudaGraph_t graph = nullptr;
-  cudaGraphExec_t iter_exec = nullptr;  // graph of one drop-in iteration (H2D..D2H)
+  // graphs of one drop-in iteration (H2D..D2H), one per master seed (the seed is a
+  // kernel parameter), most recent last
+  std::vector<std::pair<uint64_t, cudaGraphExec_t>> iter_execs;
+  uint64_t loop_seed = 0;  // master seed the loop graph was captured with
   cudaGraphExec_t graph_exec = nullptr;
   std::string err;
   std::string variant;  // rollout kernel variant the launcher picked (jm_kernel_name)

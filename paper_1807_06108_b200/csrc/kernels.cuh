@@ -37,6 +37,12 @@ __host__ __device__ __forceinline__ int fin_cols(int m) { return (kFinCols / m) 
 constexpr int kFinThreads = JM_FIN_THREADS;  // finalize: its warps split the records
 constexpr int kMaxRecords = 4096;
 constexpr int kRolloutMaxThreads = 512;
+// Master seeds travel in the kernel parameters, one per grid.y slice (batched
+// trials), indexed by the CTA-uniform blockIdx.y: the Philox round keys
+// (seed + r * golden-ratio constants) then live in uniform registers, computed
+// once per kernel, and the rounds' key XORs read them as uniform operands --
+// no per-thread key schedule in the hot loop.
+constexpr int kMaxSeeds = 128;
 
 // Device-resident closed-loop controller state (ControllerState +
 // the plant state of run_trial).
@@ -50,7 +56,7 @@ struct LoopState {
   int32_t halted;          // 1 after divergence / no viable rollout / max_steps
   int32_t status;          // jm_status
   int32_t diverged_at;     // step index or -1
-  int32_t pad_;
+  int32_t sampler_jumps;   // the controller's sampler draws jumps ("new" variant; "old": 0, harness.py:218-221)
   // history buffers (device)
   double* hist_states;     // (max_steps+1) * n
   double* hist_controls;   // max_steps * m
@@ -163,9 +169,9 @@ struct RolloutArgs {
   Real Lj[16];      // chol(Sigma_J), q x q row-major
   Real mu_j[4];     // mark mean
   SysParams<Real> sp;
-  uint64_t seed, iteration;
-  const uint64_t* iteration_dev;
-  const uint64_t* seed_dev;  // graph-replayed drop-in call: seed staged in device memory
+  uint64_t iteration;
+  const uint64_t* iteration_dev;  // graph-replayed drop-in call: iteration staged in device memory
+  uint64_t seeds[kMaxSeeds];      // master seed of grid.y slice b (batched trials; [0] otherwise)
   const double* x0;
   const double* u_nom;
   const Real* eps_in;    // HBM mode: step-major eps_combined
@@ -722,9 +728,9 @@ __global__ void __launch_bounds__(kRolloutMaxThreads, (RolloutMinBlocks<Sys, Rea
   pin(cq);
   const GapSampler gs{Sg, T, a.gap_inv};
   const int JW = a.jw_len;
-  const bool jumps = PHILOX && a.jump_on;
+  const bool jumps = PHILOX && a.jump_on && (L == nullptr || L->sampler_jumps);
 
-  const StreamKey sk = make_stream_key(L ? L->seed : (a.seed_dev ? *a.seed_dev : a.seed), iter);
+  const StreamKey sk = make_stream_key(a.seeds[blockIdx.y], iter);
   double* const costs_out = gridDim.y > 1 ? nullptr : (a.costs_dev ? *a.costs_dev : a.costs);
 
   // the general-channel cost (costs.py:112-124) as a compile-time variant of the tile loop:
@@ -1047,7 +1053,7 @@ __global__ void __launch_bounds__(MAXT) rollout_kernel_ws(const RolloutArgs<Real
     const bool act = kl < K;
     Real Sf = r_inf<Real>();
     if (producer) {
-      const StreamKey sk = make_stream_key(L ? L->seed : (a.seed_dev ? *a.seed_dev : a.seed), iter);
+      const StreamKey sk = make_stream_key(a.seeds[blockIdx.y], iter);
       const uint32_t kg = (uint32_t)(a.sample_offset + kl);
       Real Ld[M * M], Lj[Q * Q], mu[Q];
 #pragma unroll
@@ -1059,7 +1065,7 @@ __global__ void __launch_bounds__(MAXT) rollout_kernel_ws(const RolloutArgs<Real
       const Real jscale = a.jscale;
       const GapSampler gs{Sg, T, a.gap_inv};
       const int JW = a.jw_len;
-      const bool jumps = a.jump_on;
+      const bool jumps = a.jump_on && (L == nullptr || L->sampler_jumps);
       Real* const wd = reinterpret_cast<Real*>(sb + sp_.marks) + (c >> 5) * 32 * JW * Q;
       Real* ep = scr + c;
       JumpClock clk;

@@ -1,0 +1,681 @@
+// rollout_fast.cuh -- the product rollout kernel (non-trace: Philox or HBM noise).
+//
+// Replaces controller.py:118-158 (sample_noise_batch, the T-step loop of
+// modified cost + step_unchecked, the per-CTA half of compute_weights and the
+// weighted noise sum) for every launch that does not return trajectories.
+// Differences from rollout_kernel (kernels.cuh, kept for the TRACE path):
+//
+//  * No eps slab.  The weighted sum N[t,j] = sum_k w_k eps[k,t,j] needs eps
+//    again once the weights are known; instead of storing every sample's
+//    T*m noise values (a 179 KB shared slab at cfg1, 240 MB of L2/HBM slabs at
+//    cfg3) the epilogue REGENERATES the noise of the samples that carry
+//    weight.  With lambda = 1 and costs spread over 1e2..1e4 a tile has
+//    1-3 samples within (S - rho)/lambda <= 55 of its minimum
+//    (tools/weight_sparsity.py, B200: 0.4-1% of a tile at cfg1/cfg2/cfg3);
+//    the others' weights, < e^-55 = 1.3e-24 of the tile's best, are dropped
+//    from N (their sum over K <= 2^24 samples changes N by < 1e-16
+//    relative) but not from Z, sum w^2 or the finite count.  Regeneration is
+//    exact: the same Philox blocks, Box-Muller, Cholesky product and jump
+//    marks (jump clock walked from t = 0) as the rollout, so N is the dense
+//    sum minus the negligible terms.  HBM mode re-reads the fed columns of
+//    those samples instead, and also revisits non-finite-cost samples with
+//    weight 0 so a non-finite fed eps still turns N into NaN as the
+//    reference's einsum does (controller.py:78).
+//  * SPT = 2 samples per thread in packed f32x2 registers (vec2.cuh): one
+//    FFMA2/FMUL2/FADD2 issue slot for both samples' dynamics, cost and
+//    sincos.  Noise: per sample, per Philox block (4 normals: 4 cartpole
+//    steps, 1 quadrotor step), one block pipelined ahead.
+//  * Jump-mark staging buffer cleared per event (each lane zeroes the entries
+//    of its previous window's events) instead of per window row.
+//  * c = 1 (cq = 0) with Philox noise: the eps'eps term is fma(0, quad, inc) =
+//    inc exactly (finite noise), so it is not formed (QUAD = false).
+#pragma once
+#include "kernels.cuh"
+
+namespace jm {
+
+constexpr float kSparseCut = 55.0f;  // (S - rho) / lambda above which N drops the sample (w < e^-55)
+
+template <int SPT, typename Real>
+struct VecOf {
+  using type = Real;
+};
+template <>
+struct VecOf<2, float> {
+  using type = F2;
+};
+
+// build V from SPT per-sample scalars / read half u of V
+__device__ __forceinline__ float vpack(const float* s, std::integral_constant<int, 1>) { return s[0]; }
+__device__ __forceinline__ double vpack(const double* s, std::integral_constant<int, 1>) { return s[0]; }
+__device__ __forceinline__ F2 vpack(const float* s, std::integral_constant<int, 2>) { return F2(s[0], s[1]); }
+template <typename V, typename R>
+__device__ __forceinline__ V vcast(R s) {
+  return V(scalar_t<V>(s));
+}
+
+// uncontracted add / mul on every arithmetic type (marks, jump increments:
+// the rollout and the regeneration round them alike)
+__device__ __forceinline__ float vadd(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double vadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ F2 vadd(F2 a, F2 b) { return a + b; }
+
+// eps = L z with z given per sample (float normals), fixed fma order
+// (apply_chol in kernels.cuh: the same operations per sample)
+template <int M, int SPT, typename V, typename S>
+__device__ __forceinline__ void chol_v(const S* L, const float (*z)[4], int o, V* eps) {
+#pragma unroll
+  for (int j = 0; j < M; ++j) {
+    V zz[M];
+#pragma unroll
+    for (int l = 0; l <= j; ++l) {
+      if constexpr (SPT == 2) {
+        zz[l] = F2(z[0][o + l], z[1][o + l]);
+      } else {
+        zz[l] = V(z[0][o + l]);
+      }
+    }
+    V acc = L[j * M] * zz[0];
+#pragma unroll
+    for (int l = 1; l <= j; ++l) acc = fma(L[j * M + l], zz[l], acc);
+    eps[j] = acc;
+  }
+}
+
+// one Philox block of diffusion normals (4 words -> 4 normals)
+__device__ __forceinline__ void block_normals(const StreamKey& sk, uint32_t b, uint32_t kg, float* z) {
+  const P4 r = draw(sk, kSlotDiffusion, b, kg);
+  box_muller(r.x, r.y, z[0], z[1]);
+  box_muller(r.z, r.w, z[2], z[3]);
+}
+
+// ---------------------------------------------------------------- jump windows (clearing form)
+// jump_window (kernels.cuh) with (a) the owner lane's sample at kg + (L - lane)
+// * kstride (two samples per thread: the even / odd samples of a warp form one
+// 32-lane window each), (b) a buffer that stays zero outside event entries:
+// each lane first clears the entries of its previous window's events (prev),
+// instead of the warp zeroing every row of the window.
+template <int Q, int QP, int JM, typename Real>
+__device__ __forceinline__ void jump_window_c(JumpClock& c, Mask128& prev, int w0, int wend, const StreamKey& sk,
+                                              uint32_t kg, int kstride, const GapSampler& gs, const Real* Lj,
+                                              const Real* mu, Real jscale, Real* wd, bool poisson,
+                                              const CountTable& ct) {
+  const int lane = threadIdx.x & 31;
+  Mask128 mask{};
+  const uint32_t e0 = c.e;
+  int n = 0;
+  while (__any_sync(0xFFFFFFFFu, c.tj < wend)) {
+    if (c.tj < wend) {
+      mask_set(mask, c.tj - w0);
+      ++n;
+      clock_next(c, sk, kg, gs);
+    }
+  }
+  int inc = n;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+    if (lane >= o) inc += v;
+  }
+  const int off = inc - n;
+  const int tot = __shfl_sync(0xFFFFFFFFu, inc, 31);
+  __syncwarp();  // the previous window's marks have been read
+  for (Mask128 m = prev; m.lo | m.hi; mask_pop(m)) {
+    const int s = mask_low(m);
+#pragma unroll
+    for (int i = 0; i < Q; ++i) wd[(s * Q + i) * 32 + lane] = Real(0);
+  }
+  prev = mask;
+  __syncwarp();
+  for (int j0 = 0; j0 < tot; j0 += 32) {
+    const int j = j0 + lane;
+    int L = 0;  // owner lane of entry j: the last lane with off <= j
+#pragma unroll
+    for (int bb = 16; bb > 0; bb >>= 1) {
+      const int oc = __shfl_sync(0xFFFFFFFFu, off, L + bb);
+      if (oc <= j) L += bb;
+    }
+    const int k = j - __shfl_sync(0xFFFFFFFFu, off, L);
+    const uint32_t eL = __shfl_sync(0xFFFFFFFFu, e0, L) + (uint32_t)k;
+    Mask128 mL = mask_shfl(mask, L);
+    if (j < tot) {
+      for (int r = 0; r < k; ++r) mask_pop(mL);
+      const int s = mask_low(mL);
+      Real mk[Q];
+      mark_of<Q, QP, Real>(sk, kg + (uint32_t)((L - lane) * kstride), eL, Lj, mu, mk, poisson, ct);
+#pragma unroll
+      for (int i = 0; i < Q; ++i) wd[(s * Q + i) * 32 + L] = (JM == 1) ? rmul<Real>(jscale, mk[i]) : mk[i];
+    }
+  }
+  __syncwarp();
+}
+
+// ---------------------------------------------------------------- regeneration
+// eps_combined of sample kg over the steps of Philox block b (4 / MP steps) into
+// out[t * M + j] -- the rollout's own draws: block_normals, the same Cholesky
+// fma order, control-channel marks added with an uncontracted add.
+template <int M, int MP, int Q, int QP, int JM, typename Real>
+__device__ __forceinline__ void regen_philox(const RolloutArgs<Real>& a, const StreamKey& sk, const GapSampler& gs,
+                                             uint32_t kg, int b, const Real* Ld, const Real* Lj, const Real* mu,
+                                             bool jumps, Real* out) {
+  constexpr int SB = 4 / MP;
+  const int t0 = b * SB;
+  float z[4];
+  block_normals(sk, (uint32_t)b, kg, z);
+  JumpClock clk;
+  const bool marks = JM == 0 && jumps;
+  if (marks) {
+    clock_start(clk, sk, kg, gs);
+    while (clk.tj < t0) clock_next(clk, sk, kg, gs);
+  }
+#pragma unroll
+  for (int s2 = 0; s2 < SB; ++s2) {
+    const int t = t0 + s2;
+    if (t >= a.T) break;
+    Real eps[M];
+    apply_chol<M, Real>(Ld, z + s2 * MP, eps);
+    if (marks && clk.tj == t) {
+      Real mk[Q];
+      mark_of<Q, QP, Real>(sk, kg, clk.e, Lj, mu, mk, a.poisson != 0, a.cnt);
+#pragma unroll
+      for (int j = 0; j < M; ++j) eps[j] = radd<Real>(eps[j], mk[(j < Q) ? j : 0]);
+      clock_next(clk, sk, kg, gs);
+    }
+#pragma unroll
+    for (int j = 0; j < M; ++j) out[t * M + j] = eps[j];
+  }
+}
+
+// ---------------------------------------------------------------- sparse tile epilogue
+// Online softmax of one tile into the CTA accumulator (the per-CTA half of
+// compute_weights + _weighted_noise_average, controller.py:62-78):
+// rho_new = min(rho_acc, min_tile S); w_k = exp(-(S_k - rho_new)/lambda);
+// Z, sum w^2 and n_finite over every sample; N[r] += w_k eps[r, k] over the
+// samples with (S_k - rho_new)/lambda <= kSparseCut, whose eps rows
+// regen(col, item, row_out) rewrites (nb items of ipt steps per sample) into a
+// chunk scratch, summed in list order (fixed: deterministic).  Every thread
+// calls it; Sf/cols hold its SPT samples (+inf / -1 for none).
+struct SparseSmem {
+  double (*s_red)[32];
+  double* s_acc;
+  int* s_cnt;
+  int* sig_col;
+  float* sig_w;  // weights as float (the fp32 kernels' w; fp64 kernels round the weight of a
+  double* sig_wd;  // ... or as double)
+  void* scratch;
+  int chunk;     // samples per regeneration chunk
+};
+
+template <int SPT, typename Real, class Regen>
+__device__ __forceinline__ void sparse_epilogue(const Real* Sf, const int* cols, int TM, Real inv_lam, double* Nacc,
+                                                const SparseSmem& sm, int nb, bool keep_nonfinite, Regen regen) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int nthreads = blockDim.x;
+  Real mloc = r_inf<Real>();
+#pragma unroll
+  for (int u = 0; u < SPT; ++u) mloc = fmin(mloc, Sf[u]);
+  const double m = warp_min_redux(double(mloc));
+  if (lane == 0) sm.s_red[0][warp] = m;
+  __syncthreads();
+  const double mm = warp_min_redux(lane < nwarps ? sm.s_red[0][lane] : CUDART_INF);
+  const double rho_prev = sm.s_acc[0];
+  const double rho_new = fmin(rho_prev, mm);
+  if (rho_new == CUDART_INF) return;  // no finite cost yet in this CTA (uniform)
+  double scale_old = 0.0;
+  if (rho_prev != CUDART_INF) {
+    const double e = lane == 0 ? exp((rho_new - rho_prev) * double(inv_lam)) : 0.0;
+    scale_old = __shfl_sync(0xFFFFFFFFu, e, 0);
+  }
+  double z1 = 0.0, z2 = 0.0;
+  int nf = 0, cnt = 0;
+  Real w[SPT];
+  bool sig[SPT];
+  uint32_t bal[SPT];
+#pragma unroll
+  for (int u = 0; u < SPT; ++u) {
+    const bool fin = Sf[u] < r_inf<Real>();
+    const Real d = (Sf[u] - Real(rho_new)) * inv_lam;
+    w[u] = fin ? r_exp<Real>(-d) : Real(0);
+    z1 += double(w[u]);
+    z2 += double(w[u]) * double(w[u]);
+    nf += fin ? 1 : 0;
+    sig[u] = cols[u] >= 0 && (fin ? d <= Real(kSparseCut) : keep_nonfinite);
+    bal[u] = __ballot_sync(0xFFFFFFFFu, sig[u]);
+    cnt += __popc(bal[u]);
+  }
+  z1 = warp_sum(z1);
+  z2 = warp_sum(z2);
+  nf = __reduce_add_sync(0xFFFFFFFFu, nf);
+  if (lane == 0) {
+    sm.s_red[1][warp] = z1;
+    sm.s_red[2][warp] = z2;
+    sm.s_red[3][warp] = double(nf);
+    sm.s_cnt[warp] = cnt;
+  }
+  __syncthreads();  // partials and counts complete; s_acc[0] has been read by every thread
+  if (warp == nwarps - 1 && lane == 0) {
+    double a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    for (int w2 = 0; w2 < nwarps; ++w2) {
+      a1 += sm.s_red[1][w2];
+      a2 += sm.s_red[2][w2];
+      a3 += sm.s_red[3][w2];
+    }
+    sm.s_acc[0] = rho_new;
+    sm.s_acc[1] = sm.s_acc[1] * scale_old + a1;
+    sm.s_acc[2] = sm.s_acc[2] * scale_old * scale_old + a2;
+    sm.s_acc[3] += a3;
+  }
+  // the list of weighted samples: warp order, then sample slot u, then lane
+  int off = 0, nsig = 0;
+  for (int w2 = 0; w2 < nwarps; ++w2) {
+    const int c = sm.s_cnt[w2];
+    off += (w2 < warp) ? c : 0;
+    nsig += c;
+  }
+  const uint32_t below = (1u << lane) - 1u;
+#pragma unroll
+  for (int u = 0; u < SPT; ++u) {
+    if (sig[u]) {
+      const int p = off + __popc(bal[u] & below);
+      sm.sig_col[p] = cols[u];
+      if constexpr (sizeof(Real) == 4)
+        sm.sig_w[p] = float(w[u]);
+      else
+        sm.sig_wd[p] = double(w[u]);
+    }
+    off += __popc(bal[u]);
+  }
+  // the earlier tiles' N relative to the new minimum (multi-tile CTAs)
+  if (scale_old != 1.0)
+    for (int r = threadIdx.x; r < TM; r += nthreads) Nacc[r] = (rho_prev == CUDART_INF) ? 0.0 : Nacc[r] * scale_old;
+  __syncthreads();  // the list is complete
+  Real* scr = reinterpret_cast<Real*>(sm.scratch);
+  for (int c0 = 0; c0 < nsig; c0 += sm.chunk) {
+    const int nc = min(sm.chunk, nsig - c0);
+    for (int it = threadIdx.x; it < nc * nb; it += nthreads) {
+      const int si = it / nb;
+      regen(sm.sig_col[c0 + si], it - si * nb, scr + (size_t)si * TM);
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < TM; r += nthreads) {
+      double acc = 0.0;
+      for (int si = 0; si < nc; ++si) {
+        const double wk = (sizeof(Real) == 4) ? double(sm.sig_w[c0 + si]) : sm.sig_wd[c0 + si];
+        acc = fma(wk, double(scr[(size_t)si * TM + r]), acc);  // 0 * inf = NaN like controller.py:78
+      }
+      Nacc[r] += acc;
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- shared memory plan (fast kernel)
+//   Nacc (TM doubles) | marks (SPT x nwarps x 32 x W x q Real) | step table (T x (2m+1) Real) |
+//   sig_col (tile int) | sig_w (tile double) | scratch (chunk x TM Real) | gap table (uint32)
+struct FastPlan {
+  size_t nacc, marks, tab, sigc, sigw, scr, gap, total;
+  int chunk;
+};
+__host__ __device__ __forceinline__ FastPlan fast_plan(int TM, int tabn, int tile, int nthreads, int nb, int nmarks,
+                                                       int ngap, int rs) {
+  FastPlan p;
+  p.chunk = nthreads / nb > 1 ? nthreads / nb : 1;
+  if (p.chunk > tile) p.chunk = tile;
+  size_t o = 0;
+  p.nacc = o;
+  o = al16(o + sizeof(double) * (size_t)TM);
+  p.marks = o;
+  o = al16(o + (size_t)rs * nmarks);
+  p.tab = o;
+  o = al16(o + (size_t)rs * tabn);
+  p.sigc = o;
+  o = al16(o + sizeof(int) * (size_t)tile);
+  p.sigw = o;
+  o = al16(o + sizeof(double) * (size_t)tile);
+  p.scr = o;
+  o = al16(o + (size_t)rs * p.chunk * TM);
+  p.gap = o;
+  o = al16(o + sizeof(uint32_t) * (size_t)ngap);
+  p.total = o;
+  return p;
+}
+
+// regeneration items per sample: Philox blocks (4 / MP steps each), or HBM groups of GS steps
+template <int MP>
+__host__ __device__ constexpr int philox_steps_per_block() {
+  return 4 / MP;
+}
+__host__ __device__ __forceinline__ int regen_items(int T, int steps_per_item) {
+  return (T + steps_per_item - 1) / steps_per_item;
+}
+
+// ---------------------------------------------------------------- the kernel
+// MODE: 0 = control-channel cost with the eps'eps term dropped (c = 1, Philox),
+//       1 = control-channel cost with it, 2 = general channel (cal_b, bb).
+template <class Sys, typename Real, bool PHILOX, int JM, int SPT, int MAXT>
+__global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const RolloutArgs<Real> a) {
+  using Dyn = typename Sys::Dyn;
+  using Cost = typename Sys::Cost;
+  using V = typename VecOf<SPT, Real>::type;
+  static_assert(SPT == 1 || std::is_same<Real, float>::value, "two samples per thread: fp32 only");
+  constexpr int N = Sys::N, M = Sys::M;
+  constexpr int MP = Pad<M>::value;
+  constexpr int Q = (JM == 0) ? M : Dyn::QJ;
+  constexpr int QP = Pad<Q>::value;
+  constexpr int TS = 2 * M + 1;
+  // steps per noise group: one Philox block (4 normals); HBM mode: 4 steps of
+  // the small systems, one quadrotor step (its loads are 7 words a step)
+  constexpr int GS = PHILOX ? 4 / MP : (M >= 3 ? 1 : 4);
+
+  extern __shared__ double smem_d[];
+  __shared__ double s_red[4][32];
+  __shared__ double s_acc[4];
+  __shared__ int s_cnt[32];
+
+  const int TM = a.TM, T = a.T, K = a.K;
+  const int nthreads = blockDim.x, nwarps = nthreads >> 5;
+  const int tileK = SPT * nthreads;
+  const int nb = regen_items(T, GS);
+  // (batched old/new variants: the "old" trials' sampler draws no jumps)
+  const bool jumps = PHILOX && a.jump_on && (a.loop == nullptr || a.loop[blockIdx.y].sampler_jumps);
+  const FastPlan pl = fast_plan(TM, T * TS, tileK, nthreads, nb, jumps ? SPT * nwarps * 32 * a.jw_len * Q : 0,
+                                a.gap_n, (int)sizeof(Real));
+  char* const sb = reinterpret_cast<char*>(smem_d);
+  double* Nacc = reinterpret_cast<double*>(sb + pl.nacc);
+  Real* tab = reinterpret_cast<Real*>(sb + pl.tab);
+  uint32_t* Sg = reinterpret_cast<uint32_t*>(sb + pl.gap);
+  Real* const marks = reinterpret_cast<Real*>(sb + pl.marks);
+  SparseSmem sm{s_red, s_acc, s_cnt, reinterpret_cast<int*>(sb + pl.sigc), reinterpret_cast<float*>(sb + pl.sigw),
+                reinterpret_cast<double*>(sb + pl.sigw), sb + pl.scr, pl.chunk};
+
+  grid_dep_wait();    // u_nom / x / iteration come from the previous control step
+  grid_dep_launch();  // let the finalize grid get resident while the horizon runs
+  LoopState* L = a.loop ? a.loop + blockIdx.y : nullptr;
+  if (L != nullptr && L->halted) return;
+  const uint64_t iter = L ? L->iteration : (a.iteration_dev ? *a.iteration_dev : a.iteration);
+  const double* x0 = L ? L->x : a.x0;
+  if (L != nullptr && blockIdx.x == 0 && threadIdx.x == 0) L->t_start[L->step] = globaltimer();
+  rollout_prologue<M, Real>(a, a.u_nom + (size_t)blockIdx.y * TM, tab, Nacc, s_acc, Sg);
+  if (jumps) {  // the mark staging is zero outside event entries (jump_window_c)
+    const int n4 = (int)((size_t)SPT * nwarps * 32 * a.jw_len * Q * sizeof(Real) / 16);
+    float4* z4 = reinterpret_cast<float4*>(marks);
+    for (int i = threadIdx.x; i < n4; i += nthreads) z4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  __syncthreads();
+
+  using S = Real;  // parameter type (scalar_t<V>)
+  SysParams<S> sp = a.sp;
+#pragma unroll
+  for (int i = 0; i < 10; ++i) pin(sp.mp[i]);
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    pin(sp.sw[i]);
+    pin(sp.swt[i]);
+  }
+  S Ld[M * M], Lj[Q * Q], mu[Q];
+#pragma unroll
+  for (int i = 0; i < M * M; ++i) {
+    Ld[i] = a.Ld[i];
+    pin(Ld[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < Q * Q; ++i) Lj[i] = a.Lj[i];
+#pragma unroll
+  for (int i = 0; i < Q; ++i) mu[i] = a.mu_j[i];
+  S dt = a.dt, sdt = a.sdt, cq = a.cq;
+  const S jscale = a.jscale;
+  pin(dt);
+  pin(sdt);
+  pin(cq);
+  const GapSampler gs{Sg, T, a.gap_inv};
+  const int JW = a.jw_len;
+  const StreamKey sk = make_stream_key(a.seeds[blockIdx.y], iter);
+  double* const costs_out = gridDim.y > 1 ? nullptr : (a.costs_dev ? *a.costs_dev : a.costs);
+  const int lane = threadIdx.x & 31;
+  Real* wdu[SPT];
+#pragma unroll
+  for (int u = 0; u < SPT; ++u) wdu[u] = marks + ((size_t)(threadIdx.x >> 5) * SPT + u) * 32 * JW * Q;
+  Mask128 prev[SPT];
+#pragma unroll
+  for (int u = 0; u < SPT; ++u) prev[u] = Mask128{0ull, 0ull};
+
+  auto tiles = [&](auto mode_tag) {
+    constexpr int MODE = decltype(mode_tag)::value;
+    for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+      const int base = tile * tileK;
+      int col[SPT], kl[SPT];
+      bool act[SPT];
+      uint32_t kg[SPT];
+#pragma unroll
+      for (int u = 0; u < SPT; ++u) {
+        col[u] = SPT * (int)threadIdx.x + u;
+        kl[u] = base + col[u];
+        act[u] = kl[u] < K;
+        kg[u] = (uint32_t)(a.sample_offset + kl[u]);
+      }
+      V x[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) x[i] = vcast<V>(x0[i]);
+      V Sacc = vcast<V>(0.0);
+      JumpClock clk[SPT];
+      const Real* wl[SPT];
+      int wnext = 0;
+#pragma unroll
+      for (int u = 0; u < SPT; ++u) {
+        wl[u] = wdu[u] + lane;
+        if (jumps) clock_start(clk[u], sk, kg[u], gs);
+      }
+
+      // one horizon step t with its eps_combined and state-jump increment
+      auto step = [&](const int t, const V* eps, const V* sj, const bool has_sj) {
+        const auto ax = Dyn::template aux<V, true>(x, sp);
+        const V qv = Cost::template q<Dyn, V>(x, ax, sp);
+        const Real* st = tab + t * TS;
+        V inc = fma(qv, dt, st[M]);
+#pragma unroll
+        for (int j = 0; j < M; ++j) inc = fma(st[M + 1 + j], eps[j], inc);
+        if constexpr (MODE == 0) {
+          Sacc += inc;
+        } else {
+          V quad = eps[0] * eps[0];
+#pragma unroll
+          for (int j = 1; j < M; ++j) quad = fma(eps[j], eps[j], quad);
+          if constexpr (MODE == 2) {  // eps' bb eps (costs.py:118-121)
+            quad = vcast<V>(0.0);
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+              V tq = vcast<V>(0.0);
+#pragma unroll
+              for (int j = 0; j < M; ++j) tq = fma(a.bb[i * M + j], eps[j], tq);
+              quad = fma(eps[i], tq, quad);
+            }
+          }
+          Sacc += fma(cq, quad, inc);
+        }
+        V v[M];
+#pragma unroll
+        for (int j = 0; j < M; ++j) v[j] = fma(eps[j], sdt, st[j]);
+        Dyn::template advance<V>(x, ax, v, dt, sp);
+        if (JM == 1 && has_sj) {
+#pragma unroll
+          for (int i = 0; i < Q; ++i) x[Dyn::jump_row(i)] = vadd(x[Dyn::jump_row(i)], sj[i]);
+        }
+      };
+
+      if constexpr (PHILOX) {
+        float z[SPT][4], zn[SPT][4];
+#pragma unroll
+        for (int u = 0; u < SPT; ++u) block_normals(sk, 0u, kg[u], z[u]);
+        auto noisy = [&](const int t, const int s2) {
+          V eps[M], sj[Q];
+          bool has_sj = false;
+          chol_v<M, SPT>(Ld, z, s2 * MP, eps);
+          if (jumps) {
+            Real mv[SPT][Q];
+#pragma unroll
+            for (int u = 0; u < SPT; ++u) {
+#pragma unroll
+              for (int i = 0; i < Q; ++i) mv[u][i] = wl[u][i * 32];
+              wl[u] += Q * 32;
+            }
+            if (JM == 0) {
+#pragma unroll
+              for (int j = 0; j < M; ++j) {
+                Real mj[SPT];
+#pragma unroll
+                for (int u = 0; u < SPT; ++u) mj[u] = mv[u][j];
+                eps[j] = vadd(eps[j], vpack(mj, std::integral_constant<int, SPT>{}));  // noise.py:156-157
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < Q; ++i) {
+                Real mi[SPT];
+#pragma unroll
+                for (int u = 0; u < SPT; ++u) mi[u] = mv[u][i];
+                sj[i] = vpack(mi, std::integral_constant<int, SPT>{});
+              }
+              has_sj = true;
+            }
+          }
+          step(t, eps, sj, has_sj);
+        };
+        for (int t0 = 0; t0 < T; t0 += GS) {
+          if (jumps && t0 == wnext) {
+            wnext = t0 + JW;
+#pragma unroll
+            for (int u = 0; u < SPT; ++u) {
+              jump_window_c<Q, QP, JM, Real>(clk[u], prev[u], t0, min(wnext, T), sk, kg[u], SPT, gs, Lj, mu, jscale,
+                                             wdu[u], a.poisson != 0, a.cnt);
+              wl[u] = wdu[u] + lane;
+            }
+          }
+          if (t0 + GS <= T) {
+            if (t0 + GS < T) {
+#pragma unroll
+              for (int u = 0; u < SPT; ++u) block_normals(sk, (uint32_t)((t0 + GS) / GS), kg[u], zn[u]);
+            }
+#pragma unroll
+            for (int s2 = 0; s2 < GS; ++s2) noisy(t0 + s2, s2);
+#pragma unroll
+            for (int u = 0; u < SPT; ++u)
+#pragma unroll
+              for (int i = 0; i < 4; ++i) z[u][i] = zn[u][i];
+          } else {
+#pragma unroll
+            for (int s2 = 0; s2 < GS; ++s2)
+              if (t0 + s2 < T) noisy(t0 + s2, s2);
+          }
+        }
+      } else {
+        // HBM wire format eps[(t*M + j)*K + k], jump[(t*Q + i)*K + k]: a thread's
+        // SPT samples are adjacent columns (one 8-byte load for both), groups
+        // of GS steps loaded two groups ahead
+        constexpr int EW = GS * M * SPT, JWD = (JM == 1) ? GS * Q * SPT : 1;
+        const bool hj = JM == 1 && a.jump_in != nullptr;
+        const int kc = act[0] ? kl[0] : 0;
+        const Real* pe = a.eps_in + kc;
+        const Real* pj = hj ? a.jump_in + kc : nullptr;
+        const size_t rowe = (size_t)M * K, rowj = (size_t)Q * K;
+        auto load = [&](const Real* p) -> V {
+          if constexpr (SPT == 2) {
+            const float2 v2 = __ldg(reinterpret_cast<const float2*>(p));
+            return F2(v2);
+          } else {
+            return V(__ldg(p));
+          }
+        };
+        auto load_group = [&](int g0, V* ze, V* zj) {
+#pragma unroll
+          for (int s2 = 0; s2 < GS; ++s2) {
+            const int t = min(g0 + s2, T - 1);
+#pragma unroll
+            for (int j = 0; j < M; ++j) ze[s2 * M + j] = load(pe + (size_t)t * rowe + (size_t)j * K);
+            if (JM == 1) {
+#pragma unroll
+              for (int i = 0; i < Q; ++i) zj[s2 * Q + i] = hj ? load(pj + (size_t)t * rowj + (size_t)i * K) : vcast<V>(0.0);
+            }
+          }
+        };
+        constexpr int GE = GS * M, GJ = (JM == 1) ? GS * Q : 1;
+        (void)EW;
+        (void)JWD;
+        V e0[GE], e1[GE], j0[GJ], j1[GJ];
+        load_group(0, e0, j0);
+        load_group(GS, e1, j1);
+        for (int t0 = 0; t0 < T; t0 += GS) {
+          V en[GE], jn[GJ];
+          load_group(t0 + 2 * GS, en, jn);  // (clamped inside the horizon)
+#pragma unroll
+          for (int s2 = 0; s2 < GS; ++s2) {
+            if (GS == 1 || t0 + s2 < T) {
+              V sj[Q];
+              if (JM == 1) {
+#pragma unroll
+                for (int i = 0; i < Q; ++i) sj[i] = jscale * j0[s2 * Q + i];
+              }
+              step(t0 + s2, e0 + s2 * M, sj, JM == 1 && hj);
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < GE; ++i) {
+            e0[i] = e1[i];
+            e1[i] = en[i];
+          }
+#pragma unroll
+          for (int i = 0; i < GJ; ++i) {
+            j0[i] = j1[i];
+            j1[i] = jn[i];
+          }
+        }
+      }
+      // Once non-finite, an Euler state x += dx stays non-finite, so the final
+      // state decides divergence (the reference checks every step).
+      Real Sf[SPT];
+      int cols[SPT];
+      {
+        const auto ax = Dyn::template aux<V, true>(x, sp);
+        const V term = Cost::template q<Dyn, V>(x, ax, sp);
+#pragma unroll
+        for (int u = 0; u < SPT; ++u) {
+          bool fin = true;
+#pragma unroll
+          for (int i = 0; i < N; ++i) fin = fin && isfinite(half_of(x[i], u));
+          const Real Su = fin ? fma(sp.term_scale, Real(half_of(term, u)), Real(half_of(Sacc, u)))  // controller.py:155
+                              : r_inf<Real>();
+          if (act[u] && costs_out) costs_out[kl[u]] = double(Su);
+          Sf[u] = act[u] ? Su : r_inf<Real>();
+          cols[u] = act[u] ? col[u] : -1;
+        }
+      }
+      // ---- per-CTA online softmax over this tile (K3/K4 partials), sparse N
+      if constexpr (PHILOX) {
+        sparse_epilogue<SPT, Real>(Sf, cols, TM, a.inv_lam, Nacc, sm, nb, false, [&](int c, int b, Real* out) {
+          regen_philox<M, MP, Q, QP, JM, Real>(a, sk, gs, (uint32_t)(a.sample_offset + base + c), b, Ld, Lj, mu, jumps,
+                                               out);
+        });
+      } else {
+        sparse_epilogue<SPT, Real>(Sf, cols, TM, a.inv_lam, Nacc, sm, nb, true, [&](int c, int b, Real* out) {
+          const int k = base + c;
+#pragma unroll
+          for (int s2 = 0; s2 < GS; ++s2) {
+            const int t = b * GS + s2;
+            if (t < T) {
+#pragma unroll
+              for (int j = 0; j < M; ++j) out[t * M + j] = a.eps_in[(size_t)(t * M + j) * K + k];
+            }
+          }
+        });
+      }
+    }
+  };
+  if (a.general)
+    tiles(std::integral_constant<int, 2>{});
+  else if (PHILOX && a.cq == Real(0))
+    tiles(std::integral_constant<int, 0>{});
+  else
+    tiles(std::integral_constant<int, 1>{});
+  __syncthreads();
+  write_record(a, s_acc, Nacc);
+}
+
+}  // namespace jm

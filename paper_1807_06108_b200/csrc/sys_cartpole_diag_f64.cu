@@ -1,0 +1,7 @@
+// Engine instantiation: Cartpole (dynamics.py:194-284) x CostDiagQuadratic, double (one unit per
+// (model, cost, precision): the units compile in parallel).
+#include "engine.cuh"
+
+namespace jm {
+EngineBase* make_cartpole_diag_f64() { return new Engine<Cartpole, CostDiagQuadratic, double>(); }
+}  // namespace jm

@@ -1,0 +1,7 @@
+// Engine instantiation: the generic linear plugin f(x) = A x, G constant, B = H = G
+// (systems.cuh Linear) with the diagonal quadratic cost, n=4, m=2, double.
+#include "engine.cuh"
+
+namespace jm {
+EngineBase* make_linear_4x2_f64() { return new Engine<Linear<4, 2>, CostDiagQuadratic, double>(); }
+}  // namespace jm

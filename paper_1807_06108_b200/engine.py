@@ -362,24 +362,38 @@ class Context:
             self.check(rc)
         return states, controls, jumps, step_ns, int(div.value), int(status.value)
 
-    def batch_loop(self, x0s, u_init, seeds, steps):
-        """`len(seeds)` independent closed loops advanced together (jm_batch_loop_host)."""
+    BATCH_MAX = 128  # trials per jm_batch_loop_host launch (kMaxSeeds: the seeds are kernel parameters)
+
+    def batch_loop(self, x0s, u_init, seeds, steps, sampler_jumps=None):
+        """`len(seeds)` independent closed loops advanced together (jm_batch_loop_host),
+        in launches of up to BATCH_MAX trials.  sampler_jumps[b] = 0 runs trial b as the
+        "old" variant (its sampler draws no jumps)."""
         seeds = np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64).reshape(-1))
         B = seeds.size
         x0s = np.ascontiguousarray(np.broadcast_to(np.asarray(x0s, dtype=float), (B, self.N)))
         u_init = np.ascontiguousarray(u_init, dtype=float).reshape(self.M)
+        sj = None if sampler_jumps is None else np.ascontiguousarray(np.asarray(sampler_jumps, dtype=np.int32)
+                                                                     .reshape(B))
         states = np.empty((B, steps + 1, self.N))
         controls = np.empty((B, steps, self.M))
         jumps = np.empty((B, steps), dtype=np.int64)
         step_ns = np.empty((B, steps))
         div = np.empty(B, dtype=np.int32)
         status = np.empty(B, dtype=np.int32)
-        rc = self.lib.jm_batch_loop_host(self.h, B, L.dptr(x0s), L.dptr(u_init),
-                                         seeds.ctypes.data_as(C.POINTER(C.c_uint64)), int(steps), L.dptr(states),
-                                         L.dptr(controls), L.i64ptr(jumps), L.dptr(step_ns),
-                                         div.ctypes.data_as(C.POINTER(C.c_int32)),
-                                         status.ctypes.data_as(C.POINTER(C.c_int32)))
-        self.check(rc)
+        i32p = C.POINTER(C.c_int32)
+        for b0 in range(0, B, self.BATCH_MAX):
+            sl = slice(b0, min(B, b0 + self.BATCH_MAX))
+            n = sl.stop - sl.start
+            part = [np.ascontiguousarray(a[sl]) for a in (x0s, seeds, states, controls, jumps, step_ns, div, status)]
+            sjp = None if sj is None else np.ascontiguousarray(sj[sl])
+            rc = self.lib.jm_batch_loop_host(self.h, n, L.dptr(part[0]), L.dptr(u_init),
+                                             part[1].ctypes.data_as(C.POINTER(C.c_uint64)),
+                                             None if sjp is None else sjp.ctypes.data_as(i32p), int(steps),
+                                             L.dptr(part[2]), L.dptr(part[3]), L.i64ptr(part[4]), L.dptr(part[5]),
+                                             part[6].ctypes.data_as(i32p), part[7].ctypes.data_as(i32p))
+            self.check(rc)
+            for dst, src in zip((states, controls, jumps, step_ns, div, status), part[2:]):
+                dst[sl] = src
         return states, controls, jumps, step_ns, div, status
 
     def kernel_name(self) -> str:

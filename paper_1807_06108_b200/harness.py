@@ -10,8 +10,9 @@ Philox plant slot keyed on the trial seed (the reference's
 RngStream(seed, PLANT_STREAM_ID) role).
 
 run_batch (harness.py:197-233) replaces the reference's process pool with a
-trial dimension on the GPU: every trial of a variant advances in the same two
-launches per control step (grid.y = trial), each trial bit-identical to its
+trial dimension on the GPU: every trial of every controller variant advances
+in the same two launches per control step (grid.y = variant x trial, the
+"old" variant's sampler drawing no jumps), each trial bit-identical to its
 own run_trial.
 """
 
@@ -122,23 +123,34 @@ def run_batch(task: Task, cfg, n_trials: int, base_seed: int, variants: Sequence
     """Paired trials per controller variant, summarised (harness.py:197-233).
 
     Trial k uses the same master seed for every variant (paired plant noise).
-    All trials of a variant run together on the GPU (jm_batch_loop_host);
-    n_workers is accepted for signature compatibility and has no effect --
-    as in the reference, results do not depend on it."""
+    The jobs the reference fans out over its pool -- variants x trials
+    (harness.py:215-221) -- run as ONE batch on the GPU (jm_batch_loop_host,
+    grid.y = variant x trial; an "old" trial's sampler draws no jumps, exactly
+    what jump_sampling_enabled=False does); n_workers is accepted for
+    signature compatibility and has no effect -- as in the reference,
+    results do not depend on it."""
     if n_trials < 1:
         raise ValueError("trial count must be >= 1")
+    for v in variants:
+        if v not in ("old", "new"):
+            raise ValueError(f"unknown variant {v!r}")
     seeds = [trial_seed(base_seed, k) for k in range(n_trials)]
     steps = int(task.duration_steps)
+    # one context whose sampler can draw jumps ("new"), unless only "old" runs
+    bcfg = replace(cfg, jump_sampling_enabled=("new" in variants))
+    ctx = engine.get_context(task.model, task.cost_model, bcfg, precision=precision, device=device)
+    job_seeds = [s for _ in variants for s in seeds]
+    flags = [1 if v == "new" else 0 for v in variants for _ in seeds]
+    states, controls, jumps, step_ns, div, status = ctx.batch_loop(task.x0, bcfg.u_init, job_seeds, steps,
+                                                                    sampler_jumps=flags)
+    if np.any(status == L.JM_ERR_NO_VIABLE):
+        raise ControllerError("no viable rollout")  # run_trial would raise inside the pool
     out: Dict[str, Tuple[List[TrialRecord], BatchSummary]] = {}
-    for variant in variants:
-        vcfg = replace(cfg, jump_sampling_enabled=(variant == "new"))
+    for vi, variant in enumerate(variants):
         cid = f"{config_id}/{variant}" if config_id else variant
-        ctx = engine.get_context(task.model, task.cost_model, vcfg, precision=precision, device=device)
-        states, controls, jumps, step_ns, div, status = ctx.batch_loop(task.x0, vcfg.u_init, seeds, steps)
-        if np.any(status == L.JM_ERR_NO_VIABLE):
-            raise ControllerError("no viable rollout")  # run_trial would raise inside the pool
         recs = []
-        for b, seed in enumerate(seeds):
+        for k, seed in enumerate(seeds):
+            b = vi * n_trials + k
             diverged = bool(div[b] >= 0)
             ok = False
             if not diverged and task.success is not None:

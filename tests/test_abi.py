@@ -36,7 +36,7 @@ def test_library_exports_every_declared_symbol():
     for name in declared_functions():
         assert hasattr(lib, name), name
         assert name in _lib.SIGNATURES, f"{name} has no ctypes signature"
-    assert lib.jm_abi_version() == 4
+    assert lib.jm_abi_version() == 5
 
 
 def test_library_is_sm100a():
