@@ -1243,8 +1243,7 @@ int jm_batch_loop_host(jm_ctx* ctx, int32_t trials, const double* x0, const doub
   if (e == cudaSuccess) e = dalloc(&d_rec, (size_t)B * ctx->grid * ctx->rec_stride);
   if (e == cudaSuccess) e = dalloc(&d_cnt, (size_t)B);
   if (e == cudaSuccess) e = cudaMemset(d_cnt, 0, sizeof(unsigned int) * B);
-  if (e == cudaSuccess && !ctx->eps_smem)  // global eps slabs: one set per trial
-    e = cudaMalloc(&d_scr, (size_t)B * ctx->grid * TM * ctx->block * ctx->real_size);
+  // (the batch runs the product kernels only: no eps slabs -- their sparse epilogue regenerates noise)
   std::vector<jm::LoopState> hl((size_t)B);
   std::vector<double> unom((size_t)B * TM), hs0((size_t)B * (S + 1) * N, 0.0);
   for (int b = 0; b < B && e == cudaSuccess; ++b) {

@@ -90,6 +90,14 @@ class Engine final : public EngineBase {
   static const void* kfn() {
     return reinterpret_cast<const void*>(&rollout_kernel<Sys, Real, PH, TR, JM>);
   }
+  // the warp-specialised kernel's shared memory (its sparse epilogue's chunk scratch included)
+  size_t ws_bytes(const jm_ctx* c, int tile, int W) const {
+    const int nmarks = c->jthr ? tile * W * q_of(c) : 0;
+    const int chunk = ws_chunk(tile, regen_items(c->T, 4 / Pad<M>::value));
+    return smem_plan(c->TM, c->T * (2 * M + 1), tile, nmarks, ws_ring(c, tile), chunk * c->TM, c->gap_n,
+                     (int)sizeof(Real))
+        .total;
+  }
 
   // (the dynamic-smem attribute is per FUNCTION, shared by every context of this
   // engine type: it is raised to the device's opt-in maximum -- a bound, not a
@@ -100,17 +108,14 @@ class Engine final : public EngineBase {
     if (e != cudaSuccess) return e;
     return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
   }
+  // the TRACE kernels (rollout_kernel: per-step states for return_rollouts)
   template <int JM>
-  cudaError_t set_attrs(int optin, const void** main_fn, bool philox, bool scr_smem) {
-    const void* fns[4] = {kfn<true, false, JM>(), kfn<true, true, JM>(), kfn<false, false, JM>(),
-                          kfn<false, true, JM>()};
+  cudaError_t set_attrs(int optin) {
+    const void* fns[2] = {kfn<true, true, JM>(), kfn<false, true, JM>()};
     for (const void* f : fns) {
       cudaError_t e = raise_smem(f, optin);
       if (e != cudaSuccess) return e;
     }
-    *main_fn = philox ? (scr_smem ? reinterpret_cast<const void*>(&rollout_kernel<Sys, Real, true, false, JM, true>)
-                                  : fns[0])
-                      : fns[2];
     return cudaSuccess;
   }
 
@@ -118,20 +123,30 @@ class Engine final : public EngineBase {
   // (2: packed f32x2, for the BASELINE systems in fp32)
   static constexpr bool kPackable = std::is_same<Real, float>::value &&
                                     (std::is_same<Dyn, Cartpole>::value || std::is_same<Dyn, Quadrotor>::value);
-  template <bool PH, int JM, int SPT>
-  static const void* fast_fn() {
+  // (QUAD: the eps'eps term of the modified cost is formed -- c != 1, the general
+  // channel, or fed noise, whose non-finite values must still poison the cost)
+  template <bool PH, int JM, int SPT, bool QUAD>
+  static auto fast_kern() {
     if constexpr (SPT == 2 && kPackable)
-      return reinterpret_cast<const void*>(&rollout_fast<Sys, Real, PH, JM, 2, 256>);
+      return &rollout_fast<Sys, Real, PH, JM, 2, 256, QUAD>;
     else
-      return reinterpret_cast<const void*>(&rollout_fast<Sys, Real, PH, JM, 1, 512>);
+      return &rollout_fast<Sys, Real, PH, JM, 1, 512, QUAD>;
   }
-  static const void* fast_fn_rt(bool ph, int jm, int spt) {
+  template <bool PH, int JM, int SPT>
+  static const void* fast_fn_q(bool quad) {
+    return quad ? reinterpret_cast<const void*>(fast_kern<PH, JM, SPT, true>())
+                : reinterpret_cast<const void*>(fast_kern<PH, JM, SPT, false>());
+  }
+  static const void* fast_fn_rt(bool ph, int jm, int spt, bool quad) {
     if (ph) {
-      if (jm) return spt == 2 ? fast_fn<true, 1, 2>() : fast_fn<true, 1, 1>();
-      return spt == 2 ? fast_fn<true, 0, 2>() : fast_fn<true, 0, 1>();
+      if (jm) return spt == 2 ? fast_fn_q<true, 1, 2>(quad) : fast_fn_q<true, 1, 1>(quad);
+      return spt == 2 ? fast_fn_q<true, 0, 2>(quad) : fast_fn_q<true, 0, 1>(quad);
     }
-    if (jm) return spt == 2 ? fast_fn<false, 1, 2>() : fast_fn<false, 1, 1>();
-    return spt == 2 ? fast_fn<false, 0, 2>() : fast_fn<false, 0, 1>();
+    if (jm) return spt == 2 ? fast_fn_q<false, 1, 2>(true) : fast_fn_q<false, 1, 1>(true);
+    return spt == 2 ? fast_fn_q<false, 0, 2>(true) : fast_fn_q<false, 0, 1>(true);
+  }
+  static bool fast_quad(const jm_ctx* c) {
+    return c->mppi.noise_source != JM_NOISE_PHILOX || c->cost.general_channel || c->cost.c != 1.0;
   }
   // steps per regeneration item (kernel GS) and the fast kernel's shared memory
   int fast_gs(bool philox) const { return philox ? 4 / Pad<M>::value : (M >= 3 ? 1 : 4); }
@@ -144,13 +159,9 @@ class Engine final : public EngineBase {
   // warp-specialised kernel (Philox, non-trace): block = 2 x tile
   static constexpr int kWsMaxThreads = (N <= 4) ? 1024 : 512;
   static constexpr int kWsBufs = 6;  // ring depth: slack for the producers' jump-window bursts
-  template <int JM, bool SS>
-  static auto ws_kern() {
-    return &rollout_kernel_ws<Sys, Real, JM, kWsMaxThreads, kWsBufs, SS>;
-  }
   template <int JM>
-  static const void* ws_fn(bool ss) {
-    return ss ? reinterpret_cast<const void*>(ws_kern<JM, true>()) : reinterpret_cast<const void*>(ws_kern<JM, false>());
+  static auto ws_kern() {
+    return &rollout_kernel_ws<Sys, Real, JM, kWsMaxThreads, kWsBufs>;
   }
   int ws_ring(const jm_ctx* c, int tile) const {
     const int gw = (c->model.jump_channel == JM_JUMP_STATE) ? WsShape<Sys, 1>::GW : WsShape<Sys, 0>::GW;
@@ -170,7 +181,6 @@ class Engine final : public EngineBase {
   cudaError_t configure(jm_ctx* c) override {
     const bool philox = c->mppi.noise_source == JM_NOISE_PHILOX;
     static const int ws_env = std::getenv("JM_WS") ? std::atoi(std::getenv("JM_WS")) : -1;  // A/B: 0 off, 1 on
-    static const bool no_eps_smem = std::getenv("JM_NO_EPS_SMEM") != nullptr;
     static const int spt_env = std::getenv("JM_SPT") ? std::atoi(std::getenv("JM_SPT")) : 0;  // A/B: 1 or 2
     int block = c->mppi.block_threads;
     const int K = c->K, sms = c->num_sms;
@@ -198,25 +208,17 @@ class Engine final : public EngineBase {
     cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device);
     if (e != cudaSuccess) return e;
     c->ntiles = (K + block - 1) / block;
-    // jump window: the longest (fewer window passes) whose staging fits; single
-    // wave: also keep the eps scratch in shared memory if possible
-    const size_t cap = (size_t)optin - 2048;  // (static shared memory of the rollout kernels: ~1.1 KB)
-    const bool single = philox && !no_eps_smem && c->ntiles <= sms;
-    // multi-wave: two CTAs per SM must still fit (the occupancy the 256-sample tiles need)
-    const size_t budget = single ? cap : std::min(cap, (size_t)optin / 2 - 2048);
-    // (128-bit event masks: windows up to 128 steps, as long as the mark staging fits)
+    // jump window: the longest (fewer window passes) whose staging fits
+    // (128-bit event masks: windows up to 128 steps); single wave: the whole SM,
+    // multi-wave: two CTAs per SM must still fit (the occupancy 256-thread tiles need)
+    const size_t cap = (size_t)optin - 2048;  // (static shared memory of the rollout kernels: < 2 KB)
+    const size_t cap_ws = (size_t)optin - 8192;  // (the WS kernel's static regeneration list: up to 6 KB)
+    const size_t budget = ws ? cap_ws : (c->ntiles <= sms ? cap : std::min(cap, (size_t)optin / 2 - 2048));
     int W = std::min(128, (c->T + 3) / 4 * 4);
-    while (W > 8 && plan_bytes(c, block, mwarps, W, nring, single) > budget) W -= 4;
+    while (W > 8 && (ws ? ws_bytes(c, block, W) : plan_bytes(c, block, mwarps, W, 0, false)) > budget) W -= 4;
     c->jw_len = W;
-    // the non-WS single-wave kernel stages its jump marks in the eps slab rows
-    // (kernels.cuh jump_window): no mark buffer, windows of up to 128 steps
-    // (128-bit event masks), balanced over the horizon (T = 100: one window)
-    const int nwin = (c->T + 127) / 128;
-    c->jw_slab = std::min(128, ((c->T + nwin - 1) / nwin + 3) / 4 * 4);
-    c->eps_smem = single && (ws ? plan_bytes(c, block, mwarps, W, nring, true)
-                                : plan_bytes(c, block, 0, 0, nring, true)) <= cap;
-    const size_t msmem = (c->eps_smem && !ws) ? plan_bytes(c, block, 0, 0, nring, true)
-                                              : plan_bytes(c, block, mwarps, W, nring, c->eps_smem);
+    c->eps_smem = 0;
+    const size_t msmem = ws ? ws_bytes(c, block, W) : 0;              // the warp-specialised kernel
     const size_t smem = plan_bytes(c, block, mwarps, W, 0, false);  // trace kernels
     const bool fast = !ws;  // the product kernel (Philox without warp specialisation, and HBM)
     c->fast = fast;
@@ -228,6 +230,7 @@ class Engine final : public EngineBase {
       const size_t fbudget = (c->ntiles <= sms) ? cap : std::min(cap, (size_t)optin / 2 - 2048);
       WF = std::min(128, (c->T + 3) / 4 * 4);
       while (WF > 8 && fast_bytes(c, block, spt, WF, philox) > fbudget) WF -= 4;
+      (void)budget;
       fsmem = fast_bytes(c, block, spt, WF, philox);
       if (fsmem > cap) return cudaErrorInvalidConfiguration;
     }
@@ -235,10 +238,10 @@ class Engine final : public EngineBase {
     c->fast_smem = fsmem;
     const void* fn = nullptr;
     const bool sj = c->model.jump_channel == JM_JUMP_STATE;
-    e = sj ? set_attrs<1>(optin, &fn, philox, c->eps_smem) : set_attrs<0>(optin, &fn, philox, c->eps_smem);
+    e = sj ? set_attrs<1>(optin) : set_attrs<0>(optin);
     if (e != cudaSuccess) return e;
-    if (ws) fn = sj ? ws_fn<1>(c->eps_smem) : ws_fn<0>(c->eps_smem);
-    if (fast) fn = fast_fn_rt(philox, sj ? 1 : 0, spt);
+    if (ws) fn = sj ? reinterpret_cast<const void*>(ws_kern<1>()) : reinterpret_cast<const void*>(ws_kern<0>());
+    if (fast) fn = fast_fn_rt(philox, sj ? 1 : 0, spt, fast_quad(c));
     e = raise_smem(fn, optin);
     if (e != cudaSuccess) return e;
     int occ = 0;
@@ -338,10 +341,9 @@ class Engine final : public EngineBase {
     RolloutArgs<Real> b = a;
     b.jw_len = c->jw_fast;
     dim3 grid(c->grid, c->launch_trials), block(c->block / SPT);
-    if constexpr (SPT == 2 && kPackable)
-      return launch_pdl(rollout_fast<Sys, Real, PH, JM, 2, 256>, grid, block, c->fast_smem, c->stream, b);
-    else
-      return launch_pdl(rollout_fast<Sys, Real, PH, JM, 1, 512>, grid, block, c->fast_smem, c->stream, b);
+    if (fast_quad(c)) return launch_pdl(fast_kern<PH, JM, SPT, true>(), grid, block, c->fast_smem, c->stream, b);
+    if constexpr (PH) return launch_pdl(fast_kern<PH, JM, SPT, false>(), grid, block, c->fast_smem, c->stream, b);
+    return cudaErrorInvalidValue;
   }
 
   template <int JM>
@@ -352,19 +354,11 @@ class Engine final : public EngineBase {
       return c->spt == 2 ? launch_fast<false, JM, 2>(c, a) : launch_fast<false, JM, 1>(c, a);
     }
     if (philox && !trace && c->ws)
-      return c->eps_smem ? launch_pdl(ws_kern<JM, true>(), grid, dim3(2 * c->block), c->main_smem, c->stream, a)
-                         : launch_pdl(ws_kern<JM, false>(), grid, dim3(2 * c->block), c->main_smem, c->stream, a);
-    if (philox && !trace && c->eps_smem) {
-      RolloutArgs<Real> b = a;
-      b.jw_len = c->jw_slab;  // marks staged in the eps slab (jump_window, 128-bit masks)
-      return launch_pdl(rollout_kernel<Sys, Real, true, false, JM, true>, grid, block, c->main_smem, c->stream, b);
-    }
-    if (philox && !trace)
-      return launch_pdl(rollout_kernel<Sys, Real, true, false, JM>, grid, block, c->main_smem, c->stream, a);
+      return launch_pdl(ws_kern<JM>(), grid, dim3(2 * c->block), c->main_smem, c->stream, a);
+    if (!trace) return cudaErrorInvalidValue;  // (every non-trace launch is fast or WS)
     RolloutArgs<Real> b = a;
     b.eps_smem = 0;
     if (philox) return launch_pdl(rollout_kernel<Sys, Real, true, true, JM>, grid, block, c->smem, c->stream, b);
-    if (!trace) return launch_pdl(rollout_kernel<Sys, Real, false, false, JM>, grid, block, c->smem, c->stream, b);
     return launch_pdl(rollout_kernel<Sys, Real, false, true, JM>, grid, block, c->smem, c->stream, b);
   }
 

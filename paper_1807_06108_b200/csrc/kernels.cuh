@@ -977,228 +977,6 @@ __global__ void __launch_bounds__(kRolloutMaxThreads, (RolloutMinBlocks<Sys, Rea
 #endif
 }
 
-// ---------------------------------------------------------------- rollout, warp-specialised
-// Philox, non-trace.  The block is 2C threads: warps [0, C/32) are consumers
-// (one sample each: dynamics + modified cost), warps [C/32, 2C/32) producers
-// (thread C+c draws the noise of consumer c's sample).  Per 4-step group a
-// producer writes eps_combined (and the state-jump increments, JM = 1) into
-// a shared-memory ring of NBUF slots and the eps rows into the per-CTA
-// scratch the epilogue reads; full/empty handshakes are named barriers
-// (bar.arrive / bar.sync over all 2C threads).  Used for small tiles, where
-// a few warps per SM cannot hide the dynamics chain's latency: moving the
-// noise to other warps roughly doubles the warps in flight (measured: a win
-// up to ~128 samples per SM, a loss above, where the +30% instructions of
-// the hand-off dominate).  Same noise bits, same tiles and records
-// as rollout_kernel<..., PHILOX, !TRACE, ..>.
-__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-__device__ __forceinline__ void named_arrive(int id, int n) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
-template <class Sys, int JM>
-struct WsShape {
-  static constexpr int M = Sys::M;
-  static constexpr int Q = (JM == 0) ? M : Sys::Dyn::QJ;
-  static constexpr int GW = 4 * M + (JM == 1 ? 4 * Q : 0);  // Reals per sample per group
-};
-
-template <class Sys, typename Real, int JM, int MAXT, int kWsBuf, bool SCR_SMEM>
-__global__ void __launch_bounds__(MAXT) rollout_kernel_ws(const RolloutArgs<Real> a) {
-  using Dyn = typename Sys::Dyn;
-  using Cost = typename Sys::Cost;
-  constexpr int N = Sys::N, M = Sys::M;
-  constexpr int MP = Pad<M>::value;
-  constexpr int Q = (JM == 0) ? M : Dyn::QJ;
-  constexpr int QP = Pad<Q>::value;
-  constexpr int TS = 2 * M + 1;
-  constexpr int GW = WsShape<Sys, JM>::GW;
-
-  extern __shared__ double smem_d[];
-  __shared__ double s_red[4][32];
-  __shared__ double s_acc[4];
-  __shared__ double s_bc[2];
-
-  const int TM = a.TM, T = a.T, K = a.K;
-  const int C = blockDim.x >> 1;  // samples per tile
-  const SmemPlan sp_ = smem_plan(TM, T * TS, C, a.jump_on ? (C >> 5) * 32 * a.jw_len * Q : 0, kWsBuf * GW * C,
-                                 SCR_SMEM ? TM * C : 0, a.gap_n, (int)sizeof(Real));
-  char* const sb = reinterpret_cast<char*>(smem_d);
-  double* Nacc = reinterpret_cast<double*>(sb + sp_.nacc);
-  Real* tab = reinterpret_cast<Real*>(sb + sp_.tab);
-  Real* sw = reinterpret_cast<Real*>(sb + sp_.sw);
-  Real* ring = reinterpret_cast<Real*>(sb + sp_.ring);  // [slot][w][c]
-  uint32_t* Sg = reinterpret_cast<uint32_t*>(sb + sp_.gap);
-  Real* const scr = SCR_SMEM ? reinterpret_cast<Real*>(sb + sp_.scr)
-                             : a.eps_out + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * TM * C;
-
-  grid_dep_wait();
-  grid_dep_launch();
-  LoopState* L = a.loop ? a.loop + blockIdx.y : nullptr;
-  if (L != nullptr && L->halted) return;
-  const uint64_t iter = L ? L->iteration : (a.iteration_dev ? *a.iteration_dev : a.iteration);
-  const double* x0 = L ? L->x : a.x0;
-  if (L != nullptr && blockIdx.x == 0 && threadIdx.x == 0) L->t_start[L->step] = globaltimer();
-  rollout_prologue<M, Real>(a, a.u_nom + (size_t)blockIdx.y * TM, tab, Nacc, s_acc, Sg);
-  __syncthreads();
-
-  const bool producer = (int)threadIdx.x >= C;
-  const int c = producer ? (int)threadIdx.x - C : (int)threadIdx.x;
-  const int G = (T + 3) >> 2;
-  const int nb = 2 * C;
-  double* const costs_out = gridDim.y > 1 ? nullptr : (a.costs_dev ? *a.costs_dev : a.costs);
-
-  for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
-    const int base = tile * C;
-    const int kl = base + c;
-    const bool act = kl < K;
-    Real Sf = r_inf<Real>();
-    if (producer) {
-      const StreamKey sk = make_stream_key(a.seeds[blockIdx.y], iter);
-      const uint32_t kg = (uint32_t)(a.sample_offset + kl);
-      Real Ld[M * M], Lj[Q * Q], mu[Q];
-#pragma unroll
-      for (int i = 0; i < M * M; ++i) Ld[i] = a.Ld[i];
-#pragma unroll
-      for (int i = 0; i < Q * Q; ++i) Lj[i] = a.Lj[i];
-#pragma unroll
-      for (int i = 0; i < Q; ++i) mu[i] = a.mu_j[i];
-      const Real jscale = a.jscale;
-      const GapSampler gs{Sg, T, a.gap_inv};
-      const int JW = a.jw_len;
-      const bool jumps = a.jump_on && (L == nullptr || L->sampler_jumps);
-      Real* const wd = reinterpret_cast<Real*>(sb + sp_.marks) + (c >> 5) * 32 * JW * Q;
-      Real* ep = scr + c;
-      JumpClock clk;
-      const Real* wl = wd + (c & 31);
-      int wnext = 0;
-      if (jumps) clock_start(clk, sk, kg, gs);
-      for (int g = 0; g < G; ++g) {
-        const int slot = g % kWsBuf;
-        const int t0 = 4 * g;
-        if (jumps && t0 == wnext) {
-          wnext = t0 + JW;
-          jump_window<Q, QP, JM, Real>(clk, t0, min(wnext, T), JW, sk, kg, gs, Lj, mu, jscale, wd, a.poisson != 0,
-                                       a.cnt);
-          wl = wd + (c & 31);
-        }
-        float z[4 * MP];
-        group_normals<MP>(sk, (uint32_t)t0, kg, z);
-        Real eps[4][M], sj[4][Q];
-#pragma unroll
-        for (int s = 0; s < 4; ++s) {
-          apply_chol<M, Real>(Ld, z + s * MP, eps[s]);
-#pragma unroll
-          for (int i = 0; i < Q; ++i) sj[s][i] = Real(0);
-          if (jumps) {  // staged marks (zero where no event, and past T)
-            if (JM == 0) {
-#pragma unroll
-              for (int j = 0; j < M; ++j) eps[s][j] = radd<Real>(eps[s][j], wl[j * 32]);  // noise.py:156-157
-            } else {
-#pragma unroll
-              for (int i = 0; i < Q; ++i) sj[s][i] = wl[i * 32];
-            }
-            wl += Q * 32;
-          }
-        }
-        if (g >= kWsBuf) named_sync(1 + kWsBuf + slot, nb);  // slot drained by the consumers
-        Real* rs = ring + (size_t)slot * GW * C + c;
-#pragma unroll
-        for (int s = 0; s < 4; ++s) {
-#pragma unroll
-          for (int j = 0; j < M; ++j) rs[(s * M + j) * C] = eps[s][j];
-          if (JM == 1) {
-#pragma unroll
-            for (int i = 0; i < Q; ++i) rs[(4 * M + s * Q + i) * C] = sj[s][i];
-          }
-        }
-        named_arrive(1 + slot, nb);  // slot full
-#pragma unroll
-        for (int s = 0; s < 4; ++s)
-          if (t0 + s < T) {
-#pragma unroll
-            for (int j = 0; j < M; ++j) ep[(size_t)j * C] = eps[s][j];
-            ep += (size_t)M * C;
-          }
-      }
-    } else {
-      SysParams<Real> sp = a.sp;
-#pragma unroll
-      for (int i = 0; i < 10; ++i) pin(sp.mp[i]);
-#pragma unroll
-      for (int i = 0; i < N; ++i) {
-        pin(sp.sw[i]);
-        pin(sp.swt[i]);
-      }
-#pragma unroll
-      for (int i = 0; i < 3; ++i) pin(sp.tk[i]);
-      Real dt = a.dt, sdt = a.sdt, cq = a.cq;
-      pin(dt);
-      pin(sdt);
-      pin(cq);
-      Real x[N];
-#pragma unroll
-      for (int i = 0; i < N; ++i) x[i] = Real(x0[i]);
-      Real S = Real(0);
-      auto step = [&](const int t, const Real* eps, const Real* sj) {
-        const auto ax = Dyn::template aux<Real, true>(x, sp);
-        const Real qv = Cost::template q<Dyn, Real>(x, ax, sp);
-        const Real* st = tab + t * TS;
-        Real inc = fma(qv, dt, st[M]);
-        const Real quad = a.general ? noise_quad<M, Real, true>(a, eps) : noise_quad<M, Real, false>(a, eps);
-#pragma unroll
-        for (int j = 0; j < M; ++j) inc = fma(st[M + 1 + j], eps[j], inc);
-        S += fma(cq, quad, inc);  // costs.py:98-111 times dt
-        Real v[M];
-#pragma unroll
-        for (int j = 0; j < M; ++j) v[j] = fma(eps[j], sdt, st[j]);
-        Dyn::template advance<Real>(x, ax, v, dt, sp);  // dynamics.py:130-135
-        if (JM == 1) {
-#pragma unroll
-          for (int i = 0; i < Q; ++i) x[Dyn::jump_row(i)] = radd<Real>(x[Dyn::jump_row(i)], sj[i]);  // x + H (ind * mark)
-        }
-      };
-      for (int g = 0; g < G; ++g) {
-        const int slot = g % kWsBuf;
-        named_sync(1 + slot, nb);
-        const Real* rs = ring + (size_t)slot * GW * C + c;
-        Real e[4 * M], jv[(JM == 1) ? 4 * Q : 1];
-#pragma unroll
-        for (int i = 0; i < 4 * M; ++i) e[i] = rs[i * C];
-        if (JM == 1) {
-#pragma unroll
-          for (int i = 0; i < 4 * Q; ++i) jv[i] = rs[(4 * M + i) * C];
-        }
-        if (g < G - kWsBuf) named_arrive(1 + kWsBuf + slot, nb);
-        const int t0 = 4 * g;
-        if (t0 + 4 <= T) {
-#pragma unroll
-          for (int s = 0; s < 4; ++s) step(t0 + s, e + s * M, jv + (JM == 1 ? s * Q : 0));
-        } else {
-#pragma unroll
-          for (int s = 0; s < 4; ++s)
-            if (t0 + s < T) step(t0 + s, e + s * M, jv + (JM == 1 ? s * Q : 0));
-        }
-      }
-      bool fin = true;
-#pragma unroll
-      for (int i = 0; i < N; ++i) fin = fin && isfinite(x[i]);
-      if (fin) {
-        const auto ax = Dyn::template aux<Real, true>(x, sp);
-        S += sp.term_scale * Cost::template q<Dyn, Real>(x, ax, sp);  // controller.py:155
-      } else {
-        S = r_inf<Real>();
-      }
-      if (act && costs_out) costs_out[kl] = double(S);
-      Sf = act ? S : r_inf<Real>();
-    }
-    const int col = producer ? -1 : c;
-    tile_epilogue<Real, 1, (SCR_SMEM || N > 4) ? 8 : 16>(&Sf, &col, min(C, K - base), scr, (size_t)C, TM, a.inv_lam, sw, Nacc,
-                                              s_red, s_acc, s_bc);
-  }
-  __syncthreads();
-  write_record(a, s_acc, Nacc);
-}
-
 // ---------------------------------------------------------------- plant + shift (closed loop)
 struct PlantArgs {
   SysParams<double> sp;

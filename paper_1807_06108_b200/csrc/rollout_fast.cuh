@@ -60,24 +60,14 @@ __device__ __forceinline__ float vadd(float a, float b) { return __fadd_rn(a, b)
 __device__ __forceinline__ double vadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ F2 vadd(F2 a, F2 b) { return a + b; }
 
-// eps = L z with z given per sample (float normals), fixed fma order
-// (apply_chol in kernels.cuh: the same operations per sample)
-template <int M, int SPT, typename V, typename S>
-__device__ __forceinline__ void chol_v(const S* L, const float (*z)[4], int o, V* eps) {
+// eps = L z, fixed fma order (apply_chol in kernels.cuh: the same operations per sample)
+template <int M, typename V, typename S>
+__device__ __forceinline__ void chol_v(const S* L, const V* z, V* eps) {
 #pragma unroll
   for (int j = 0; j < M; ++j) {
-    V zz[M];
+    V acc = L[j * M] * z[0];
 #pragma unroll
-    for (int l = 0; l <= j; ++l) {
-      if constexpr (SPT == 2) {
-        zz[l] = F2(z[0][o + l], z[1][o + l]);
-      } else {
-        zz[l] = V(z[0][o + l]);
-      }
-    }
-    V acc = L[j * M] * zz[0];
-#pragma unroll
-    for (int l = 1; l <= j; ++l) acc = fma(L[j * M + l], zz[l], acc);
+    for (int l = 1; l <= j; ++l) acc = fma(L[j * M + l], z[l], acc);
     eps[j] = acc;
   }
 }
@@ -89,13 +79,53 @@ __device__ __forceinline__ void block_normals(const StreamKey& sk, uint32_t b, u
   box_muller(r.z, r.w, z[2], z[3]);
 }
 
+// box_muller (philox.cuh) of two samples at once: its FADD / FFMA / FMULs packed,
+// the MUFU steps per half -- every operation per half as the scalar form, so the
+// normals are bit-identical (the regeneration draws them with the scalar form)
+__device__ __forceinline__ void box_muller2(uint32_t a0, uint32_t a1, uint32_t b0, uint32_t b1, F2& z0, F2& z1) {
+  const F2 u1 = 2.0f - F2(__uint_as_float(0x3F800000u | (a0 >> 9)), __uint_as_float(0x3F800000u | (a1 >> 9)));
+  const F2 ang = fma(F2(__uint_as_float(0x3F800000u | (b0 >> 9)), __uint_as_float(0x3F800000u | (b1 >> 9))),
+                     6.2831853071795865f, -9.4247779607693797f);
+  float l0, l1, r0, r1;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l0) : "f"(u1.v.x));
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l1) : "f"(u1.v.y));
+  const F2 rr = -1.3862943611198906f * F2(l0, l1);
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r0) : "f"(rr.v.x));
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r1) : "f"(rr.v.y));
+  float s0, c0, s1, c1;
+  __sincosf(ang.v.x, &s0, &c0);
+  __sincosf(ang.v.y, &s1, &c1);
+  const F2 r(r0, r1);
+  z0 = r * F2(c0, c1);
+  z1 = r * F2(s0, s1);
+}
+
+// the block's normals of this thread's SPT samples, as V
+__device__ __forceinline__ void block_normals_v(const StreamKey& sk, uint32_t b, const uint32_t* kg, float* z) {
+  block_normals(sk, b, kg[0], z);
+}
+__device__ __forceinline__ void block_normals_v(const StreamKey& sk, uint32_t b, const uint32_t* kg, double* z) {
+  float f[4];
+  block_normals(sk, b, kg[0], f);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) z[i] = double(f[i]);
+}
+__device__ __forceinline__ void block_normals_v(const StreamKey& sk, uint32_t b, const uint32_t* kg, F2* z) {
+  const P4 r0 = draw(sk, kSlotDiffusion, b, kg[0]);
+  const P4 r1 = draw(sk, kSlotDiffusion, b, kg[1]);
+  box_muller2(r0.x, r1.x, r0.y, r1.y, z[0], z[1]);
+  box_muller2(r0.z, r1.z, r0.w, r1.w, z[2], z[3]);
+}
+
 // ---------------------------------------------------------------- jump windows (clearing form)
 // jump_window (kernels.cuh) with (a) the owner lane's sample at kg + (L - lane)
 // * kstride (two samples per thread: the even / odd samples of a warp form one
 // 32-lane window each), (b) a buffer that stays zero outside event entries:
 // each lane first clears the entries of its previous window's events (prev),
 // instead of the warp zeroing every row of the window.
-template <int Q, int QP, int JM, typename Real>
+// Entry (s, i, L) at wd[((s * Q + i) * 32 + L) * ES]: ES = SPT interleaves the
+// two halves of a thread (one 8-byte load reads both samples' marks).
+template <int Q, int QP, int JM, int ES, typename Real>
 __device__ __forceinline__ void jump_window_c(JumpClock& c, Mask128& prev, int w0, int wend, const StreamKey& sk,
                                               uint32_t kg, int kstride, const GapSampler& gs, const Real* Lj,
                                               const Real* mu, Real jscale, Real* wd, bool poisson,
@@ -123,7 +153,7 @@ __device__ __forceinline__ void jump_window_c(JumpClock& c, Mask128& prev, int w
   for (Mask128 m = prev; m.lo | m.hi; mask_pop(m)) {
     const int s = mask_low(m);
 #pragma unroll
-    for (int i = 0; i < Q; ++i) wd[(s * Q + i) * 32 + lane] = Real(0);
+    for (int i = 0; i < Q; ++i) wd[((s * Q + i) * 32 + lane) * ES] = Real(0);
   }
   prev = mask;
   __syncwarp();
@@ -144,7 +174,7 @@ __device__ __forceinline__ void jump_window_c(JumpClock& c, Mask128& prev, int w
       Real mk[Q];
       mark_of<Q, QP, Real>(sk, kg + (uint32_t)((L - lane) * kstride), eL, Lj, mu, mk, poisson, ct);
 #pragma unroll
-      for (int i = 0; i < Q; ++i) wd[(s * Q + i) * 32 + L] = (JM == 1) ? rmul<Real>(jscale, mk[i]) : mk[i];
+      for (int i = 0; i < Q; ++i) wd[((s * Q + i) * 32 + L) * ES] = (JM == 1) ? rmul<Real>(jscale, mk[i]) : mk[i];
     }
   }
   __syncwarp();
@@ -309,6 +339,248 @@ __device__ __forceinline__ void sparse_epilogue(const Real* Sf, const int* cols,
   }
 }
 
+// regeneration items per sample: Philox blocks (4 / MP steps each), or HBM groups of GS steps
+__host__ __device__ __forceinline__ int regen_items(int T, int steps_per_item) {
+  return (T + steps_per_item - 1) / steps_per_item;
+}
+
+// ---------------------------------------------------------------- rollout, warp-specialised
+// Philox, non-trace.  The block is 2C threads: warps [0, C/32) are consumers
+// (one sample each: dynamics + modified cost), warps [C/32, 2C/32) producers
+// (thread C+c draws the noise of consumer c's sample).  Per 4-step group a
+// producer writes eps_combined (and the state-jump increments, JM = 1) into
+// a shared-memory ring of NBUF slots; full/empty handshakes are named barriers
+// (bar.arrive / bar.sync over all 2C threads).  Used for small tiles, where
+// a few warps per SM cannot hide the dynamics chain's latency: moving the
+// noise to other warps roughly doubles the warps in flight (measured: a win
+// up to ~128 samples per SM, a loss above, where the +30% instructions of
+// the hand-off dominate).  Same noise bits as rollout_fast; the
+// same sparse epilogue (the weighted samples' noise regenerated by all 2C
+// threads, no eps slab).
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void named_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+template <class Sys, int JM>
+struct WsShape {
+  static constexpr int M = Sys::M;
+  static constexpr int Q = (JM == 0) ? M : Sys::Dyn::QJ;
+  static constexpr int GW = 4 * M + (JM == 1 ? 4 * Q : 0);  // Reals per sample per group
+};
+
+// regeneration chunk of the WS kernel: samples per pass of its 2C threads over nb items each
+__host__ __device__ __forceinline__ int ws_chunk(int C, int nb) {
+  const int c = (2 * C) / nb;
+  return c < 1 ? 1 : (c > C ? C : c);
+}
+
+template <class Sys, typename Real, int JM, int MAXT, int kWsBuf>
+__global__ void __launch_bounds__(MAXT) rollout_kernel_ws(const RolloutArgs<Real> a) {
+  using Dyn = typename Sys::Dyn;
+  using Cost = typename Sys::Cost;
+  constexpr int N = Sys::N, M = Sys::M;
+  constexpr int MP = Pad<M>::value;
+  constexpr int Q = (JM == 0) ? M : Dyn::QJ;
+  constexpr int QP = Pad<Q>::value;
+  constexpr int TS = 2 * M + 1;
+  constexpr int GW = WsShape<Sys, JM>::GW;
+
+  extern __shared__ double smem_d[];
+  __shared__ double s_red[4][32];
+  __shared__ double s_acc[4];
+  __shared__ int s_cnt[32];
+  __shared__ int s_sigc[MAXT / 2];
+  __shared__ double s_sigw[MAXT / 2];
+
+  const int TM = a.TM, T = a.T, K = a.K;
+  const int C = blockDim.x >> 1;  // samples per tile
+  const int nitems = regen_items(T, 4 / MP);  // regeneration items (Philox blocks) per sample
+  const int chunk = ws_chunk(C, nitems);
+  const SmemPlan sp_ = smem_plan(TM, T * TS, C, a.jump_on ? (C >> 5) * 32 * a.jw_len * Q : 0, kWsBuf * GW * C,
+                                 chunk * TM, a.gap_n, (int)sizeof(Real));
+  char* const sb = reinterpret_cast<char*>(smem_d);
+  double* Nacc = reinterpret_cast<double*>(sb + sp_.nacc);
+  Real* tab = reinterpret_cast<Real*>(sb + sp_.tab);
+  Real* ring = reinterpret_cast<Real*>(sb + sp_.ring);  // [slot][w][c]
+  uint32_t* Sg = reinterpret_cast<uint32_t*>(sb + sp_.gap);
+  const SparseSmem sm{s_red, s_acc, s_cnt, s_sigc, reinterpret_cast<float*>(s_sigw), s_sigw, sb + sp_.scr, chunk};
+
+  grid_dep_wait();
+  grid_dep_launch();
+  LoopState* L = a.loop ? a.loop + blockIdx.y : nullptr;
+  if (L != nullptr && L->halted) return;
+  const uint64_t iter = L ? L->iteration : (a.iteration_dev ? *a.iteration_dev : a.iteration);
+  const double* x0 = L ? L->x : a.x0;
+  if (L != nullptr && blockIdx.x == 0 && threadIdx.x == 0) L->t_start[L->step] = globaltimer();
+  rollout_prologue<M, Real>(a, a.u_nom + (size_t)blockIdx.y * TM, tab, Nacc, s_acc, Sg);
+  __syncthreads();
+
+  const bool producer = (int)threadIdx.x >= C;
+  const int c = producer ? (int)threadIdx.x - C : (int)threadIdx.x;
+  const int G = (T + 3) >> 2;
+  const int nb = 2 * C;
+  double* const costs_out = gridDim.y > 1 ? nullptr : (a.costs_dev ? *a.costs_dev : a.costs);
+
+  for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+    const int base = tile * C;
+    const int kl = base + c;
+    const bool act = kl < K;
+    Real Sf = r_inf<Real>();
+    if (producer) {
+      const StreamKey sk = make_stream_key(a.seeds[blockIdx.y], iter);
+      const uint32_t kg = (uint32_t)(a.sample_offset + kl);
+      Real Ld[M * M], Lj[Q * Q], mu[Q];
+#pragma unroll
+      for (int i = 0; i < M * M; ++i) Ld[i] = a.Ld[i];
+#pragma unroll
+      for (int i = 0; i < Q * Q; ++i) Lj[i] = a.Lj[i];
+#pragma unroll
+      for (int i = 0; i < Q; ++i) mu[i] = a.mu_j[i];
+      const Real jscale = a.jscale;
+      const GapSampler gs{Sg, T, a.gap_inv};
+      const int JW = a.jw_len;
+      const bool jumps = a.jump_on && (L == nullptr || L->sampler_jumps);
+      Real* const wd = reinterpret_cast<Real*>(sb + sp_.marks) + (c >> 5) * 32 * JW * Q;
+      JumpClock clk;
+      const Real* wl = wd + (c & 31);
+      int wnext = 0;
+      if (jumps) clock_start(clk, sk, kg, gs);
+      for (int g = 0; g < G; ++g) {
+        const int slot = g % kWsBuf;
+        const int t0 = 4 * g;
+        if (jumps && t0 == wnext) {
+          wnext = t0 + JW;
+          jump_window<Q, QP, JM, Real>(clk, t0, min(wnext, T), JW, sk, kg, gs, Lj, mu, jscale, wd, a.poisson != 0,
+                                       a.cnt);
+          wl = wd + (c & 31);
+        }
+        float z[4 * MP];
+        group_normals<MP>(sk, (uint32_t)t0, kg, z);
+        Real eps[4][M], sj[4][Q];
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+          apply_chol<M, Real>(Ld, z + s * MP, eps[s]);
+#pragma unroll
+          for (int i = 0; i < Q; ++i) sj[s][i] = Real(0);
+          if (jumps) {  // staged marks (zero where no event, and past T)
+            if (JM == 0) {
+#pragma unroll
+              for (int j = 0; j < M; ++j) eps[s][j] = radd<Real>(eps[s][j], wl[j * 32]);  // noise.py:156-157
+            } else {
+#pragma unroll
+              for (int i = 0; i < Q; ++i) sj[s][i] = wl[i * 32];
+            }
+            wl += Q * 32;
+          }
+        }
+        if (g >= kWsBuf) named_sync(1 + kWsBuf + slot, nb);  // slot drained by the consumers
+        Real* rs = ring + (size_t)slot * GW * C + c;
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+#pragma unroll
+          for (int j = 0; j < M; ++j) rs[(s * M + j) * C] = eps[s][j];
+          if (JM == 1) {
+#pragma unroll
+            for (int i = 0; i < Q; ++i) rs[(4 * M + s * Q + i) * C] = sj[s][i];
+          }
+        }
+        named_arrive(1 + slot, nb);  // slot full
+      }
+    } else {
+      SysParams<Real> sp = a.sp;
+#pragma unroll
+      for (int i = 0; i < 10; ++i) pin(sp.mp[i]);
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        pin(sp.sw[i]);
+        pin(sp.swt[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < 3; ++i) pin(sp.tk[i]);
+      Real dt = a.dt, sdt = a.sdt, cq = a.cq;
+      pin(dt);
+      pin(sdt);
+      pin(cq);
+      Real x[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) x[i] = Real(x0[i]);
+      Real S = Real(0);
+      auto step = [&](const int t, const Real* eps, const Real* sj) {
+        const auto ax = Dyn::template aux<Real, true>(x, sp);
+        const Real qv = Cost::template q<Dyn, Real>(x, ax, sp);
+        const Real* st = tab + t * TS;
+        Real inc = fma(qv, dt, st[M]);
+        const Real quad = a.general ? noise_quad<M, Real, true>(a, eps) : noise_quad<M, Real, false>(a, eps);
+#pragma unroll
+        for (int j = 0; j < M; ++j) inc = fma(st[M + 1 + j], eps[j], inc);
+        S += fma(cq, quad, inc);  // costs.py:98-111 times dt
+        Real v[M];
+#pragma unroll
+        for (int j = 0; j < M; ++j) v[j] = fma(eps[j], sdt, st[j]);
+        Dyn::template advance<Real>(x, ax, v, dt, sp);  // dynamics.py:130-135
+        if (JM == 1) {
+#pragma unroll
+          for (int i = 0; i < Q; ++i) x[Dyn::jump_row(i)] = radd<Real>(x[Dyn::jump_row(i)], sj[i]);  // x + H (ind * mark)
+        }
+      };
+      for (int g = 0; g < G; ++g) {
+        const int slot = g % kWsBuf;
+        named_sync(1 + slot, nb);
+        const Real* rs = ring + (size_t)slot * GW * C + c;
+        Real e[4 * M], jv[(JM == 1) ? 4 * Q : 1];
+#pragma unroll
+        for (int i = 0; i < 4 * M; ++i) e[i] = rs[i * C];
+        if (JM == 1) {
+#pragma unroll
+          for (int i = 0; i < 4 * Q; ++i) jv[i] = rs[(4 * M + i) * C];
+        }
+        if (g < G - kWsBuf) named_arrive(1 + kWsBuf + slot, nb);
+        const int t0 = 4 * g;
+        if (t0 + 4 <= T) {
+#pragma unroll
+          for (int s = 0; s < 4; ++s) step(t0 + s, e + s * M, jv + (JM == 1 ? s * Q : 0));
+        } else {
+#pragma unroll
+          for (int s = 0; s < 4; ++s)
+            if (t0 + s < T) step(t0 + s, e + s * M, jv + (JM == 1 ? s * Q : 0));
+        }
+      }
+      bool fin = true;
+#pragma unroll
+      for (int i = 0; i < N; ++i) fin = fin && isfinite(x[i]);
+      if (fin) {
+        const auto ax = Dyn::template aux<Real, true>(x, sp);
+        S += sp.term_scale * Cost::template q<Dyn, Real>(x, ax, sp);  // controller.py:155
+      } else {
+        S = r_inf<Real>();
+      }
+      if (act && costs_out) costs_out[kl] = double(S);
+      Sf = act ? S : r_inf<Real>();
+    }
+    const int col = (producer || !act) ? -1 : c;
+    {
+      const StreamKey sk = make_stream_key(a.seeds[blockIdx.y], iter);
+      const GapSampler gs{Sg, T, a.gap_inv};
+      const bool jumps = a.jump_on && (L == nullptr || L->sampler_jumps);
+      Real Ld[M * M], Lj[Q * Q], mu[Q];
+#pragma unroll
+      for (int i = 0; i < M * M; ++i) Ld[i] = a.Ld[i];
+#pragma unroll
+      for (int i = 0; i < Q * Q; ++i) Lj[i] = a.Lj[i];
+#pragma unroll
+      for (int i = 0; i < Q; ++i) mu[i] = a.mu_j[i];
+      sparse_epilogue<1, Real>(&Sf, &col, TM, a.inv_lam, Nacc, sm, nitems, false, [&](int cc, int b, Real* out) {
+        regen_philox<M, MP, Q, QP, JM, Real>(a, sk, gs, (uint32_t)(a.sample_offset + base + cc), b, Ld, Lj, mu, jumps,
+                                             out);
+      });
+    }
+  }
+  __syncthreads();
+  write_record(a, s_acc, Nacc);
+}
+
+
 // ---------------------------------------------------------------- shared memory plan (fast kernel)
 //   Nacc (TM doubles) | marks (SPT x nwarps x 32 x W x q Real) | step table (T x (2m+1) Real) |
 //   sig_col (tile int) | sig_w (tile double) | scratch (chunk x TM Real) | gap table (uint32)
@@ -340,19 +612,13 @@ __host__ __device__ __forceinline__ FastPlan fast_plan(int TM, int tabn, int til
   return p;
 }
 
-// regeneration items per sample: Philox blocks (4 / MP steps each), or HBM groups of GS steps
-template <int MP>
-__host__ __device__ constexpr int philox_steps_per_block() {
-  return 4 / MP;
-}
-__host__ __device__ __forceinline__ int regen_items(int T, int steps_per_item) {
-  return (T + steps_per_item - 1) / steps_per_item;
-}
 
 // ---------------------------------------------------------------- the kernel
-// MODE: 0 = control-channel cost with the eps'eps term dropped (c = 1, Philox),
-//       1 = control-channel cost with it, 2 = general channel (cal_b, bb).
-template <class Sys, typename Real, bool PHILOX, int JM, int SPT, int MAXT>
+// QUAD = false: the c = 1 Philox case, the eps'eps term dropped (fma(0, quad,
+// inc) = inc exactly for finite noise); true: the term formed, eps' eps or, for
+// the general channel (costs.py:118-121, a rare plugin: a uniform branch),
+// eps' bb eps.  Separate kernels, so each carries one copy of the tile loop.
+template <class Sys, typename Real, bool PHILOX, int JM, int SPT, int MAXT, bool QUAD>
 __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const RolloutArgs<Real> a) {
   using Dyn = typename Sys::Dyn;
   using Cost = typename Sys::Cost;
@@ -434,13 +700,12 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
   const int lane = threadIdx.x & 31;
   Real* wdu[SPT];
 #pragma unroll
-  for (int u = 0; u < SPT; ++u) wdu[u] = marks + ((size_t)(threadIdx.x >> 5) * SPT + u) * 32 * JW * Q;
+  for (int u = 0; u < SPT; ++u) wdu[u] = marks + (size_t)(threadIdx.x >> 5) * SPT * 32 * JW * Q + u;
   Mask128 prev[SPT];
 #pragma unroll
   for (int u = 0; u < SPT; ++u) prev[u] = Mask128{0ull, 0ull};
 
-  auto tiles = [&](auto mode_tag) {
-    constexpr int MODE = decltype(mode_tag)::value;
+  {
     for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
       const int base = tile * tileK;
       int col[SPT], kl[SPT];
@@ -462,7 +727,7 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
       int wnext = 0;
 #pragma unroll
       for (int u = 0; u < SPT; ++u) {
-        wl[u] = wdu[u] + lane;
+        wl[u] = wdu[u] + lane * SPT;
         if (jumps) clock_start(clk[u], sk, kg[u], gs);
       }
 
@@ -474,13 +739,13 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
         V inc = fma(qv, dt, st[M]);
 #pragma unroll
         for (int j = 0; j < M; ++j) inc = fma(st[M + 1 + j], eps[j], inc);
-        if constexpr (MODE == 0) {
+        if constexpr (!QUAD) {
           Sacc += inc;
         } else {
           V quad = eps[0] * eps[0];
 #pragma unroll
           for (int j = 1; j < M; ++j) quad = fma(eps[j], eps[j], quad);
-          if constexpr (MODE == 2) {  // eps' bb eps (costs.py:118-121)
+          if (a.general) {  // eps' bb eps (costs.py:118-121)
             quad = vcast<V>(0.0);
 #pragma unroll
             for (int i = 0; i < M; ++i) {
@@ -503,37 +768,28 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
       };
 
       if constexpr (PHILOX) {
-        float z[SPT][4], zn[SPT][4];
-#pragma unroll
-        for (int u = 0; u < SPT; ++u) block_normals(sk, 0u, kg[u], z[u]);
+        V z[4], zn[4];
+        block_normals_v(sk, 0u, kg, z);
         auto noisy = [&](const int t, const int s2) {
           V eps[M], sj[Q];
           bool has_sj = false;
-          chol_v<M, SPT>(Ld, z, s2 * MP, eps);
+          chol_v<M>(Ld, z + s2 * MP, eps);
           if (jumps) {
-            Real mv[SPT][Q];
+            V mv[Q];  // the staged marks of both halves: one load (interleaved pairs)
 #pragma unroll
-            for (int u = 0; u < SPT; ++u) {
-#pragma unroll
-              for (int i = 0; i < Q; ++i) mv[u][i] = wl[u][i * 32];
-              wl[u] += Q * 32;
+            for (int i = 0; i < Q; ++i) {
+              if constexpr (SPT == 2)
+                mv[i] = F2(*reinterpret_cast<const float2*>(wl[0] + i * 32 * SPT));
+              else
+                mv[i] = wl[0][i * 32];
             }
+            wl[0] += Q * 32 * SPT;
             if (JM == 0) {
 #pragma unroll
-              for (int j = 0; j < M; ++j) {
-                Real mj[SPT];
-#pragma unroll
-                for (int u = 0; u < SPT; ++u) mj[u] = mv[u][j];
-                eps[j] = vadd(eps[j], vpack(mj, std::integral_constant<int, SPT>{}));  // noise.py:156-157
-              }
+              for (int j = 0; j < M; ++j) eps[j] = vadd(eps[j], mv[j]);  // noise.py:156-157
             } else {
 #pragma unroll
-              for (int i = 0; i < Q; ++i) {
-                Real mi[SPT];
-#pragma unroll
-                for (int u = 0; u < SPT; ++u) mi[u] = mv[u][i];
-                sj[i] = vpack(mi, std::integral_constant<int, SPT>{});
-              }
+              for (int i = 0; i < Q; ++i) sj[i] = mv[i];
               has_sj = true;
             }
           }
@@ -544,22 +800,17 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
             wnext = t0 + JW;
 #pragma unroll
             for (int u = 0; u < SPT; ++u) {
-              jump_window_c<Q, QP, JM, Real>(clk[u], prev[u], t0, min(wnext, T), sk, kg[u], SPT, gs, Lj, mu, jscale,
-                                             wdu[u], a.poisson != 0, a.cnt);
-              wl[u] = wdu[u] + lane;
+              jump_window_c<Q, QP, JM, SPT, Real>(clk[u], prev[u], t0, min(wnext, T), sk, kg[u], SPT, gs, Lj, mu,
+                                                  jscale, wdu[u], a.poisson != 0, a.cnt);
+              wl[u] = wdu[u] + lane * SPT;
             }
           }
           if (t0 + GS <= T) {
-            if (t0 + GS < T) {
-#pragma unroll
-              for (int u = 0; u < SPT; ++u) block_normals(sk, (uint32_t)((t0 + GS) / GS), kg[u], zn[u]);
-            }
+            if (t0 + GS < T) block_normals_v(sk, (uint32_t)((t0 + GS) / GS), kg, zn);
 #pragma unroll
             for (int s2 = 0; s2 < GS; ++s2) noisy(t0 + s2, s2);
 #pragma unroll
-            for (int u = 0; u < SPT; ++u)
-#pragma unroll
-              for (int i = 0; i < 4; ++i) z[u][i] = zn[u][i];
+            for (int i = 0; i < 4; ++i) z[i] = zn[i];
           } else {
 #pragma unroll
             for (int s2 = 0; s2 < GS; ++s2)
@@ -667,13 +918,7 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
         });
       }
     }
-  };
-  if (a.general)
-    tiles(std::integral_constant<int, 2>{});
-  else if (PHILOX && a.cq == Real(0))
-    tiles(std::integral_constant<int, 0>{});
-  else
-    tiles(std::integral_constant<int, 1>{});
+  }
   __syncthreads();
   write_record(a, s_acc, Nacc);
 }

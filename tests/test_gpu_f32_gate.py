@@ -135,9 +135,16 @@ def test_benchmarked_hbm_kernel_f32_gate(case, idx, K, T, variant, gpu_device):
                         want_costs=True, want_weights=False)
     spec = om.spec_from_plugins(task.model, task.cost_model, cfg)
     g_float(case, out.costs, out.u_new, spec, x0, u_nom, noise)
-    # fed the same draws, the HBM kernel and the Philox kernel compute the same costs
+    # fed the same draws, the HBM kernel computes the Philox kernel's costs bit for bit:
+    # the in-register normals (packed Box-Muller for sample pairs) equal the sampler's
+    # scalar ones, and the sparse epilogue's regenerated eps equal the fed columns
     po = philox.iteration(x0, u_nom, 5, 1, want_costs=True, want_weights=False)
-    assert np.allclose(out.costs, po.costs, rtol=1e-5, atol=1e-4)
+    if ctx.kernel_name().split("/")[-1] == philox.kernel_name().split("/")[-1]:  # same samples per thread
+        assert np.array_equal(out.costs, po.costs)
+        if philox.kernel_name().split("/")[2] == "single_wave" == ctx.kernel_name().split("/")[2]:
+            assert np.array_equal(out.u_new, po.u_new)  # same tiles: the same records, merged alike
+    else:  # one sample per thread vs packed pairs: the compiler contracts the scalar code its own way
+        assert np.allclose(out.costs, po.costs, rtol=1e-5, atol=1e-4)
 
 
 @pytest.mark.parametrize("case,idx,K,T", [("cfg0", 0, 1024, 100), ("cfg2", 2, 8192, 150)])

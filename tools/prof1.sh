@@ -7,4 +7,4 @@ env $envs ncu --set full --clock-control none --import-source on -k regex:rollou
 python tools/ncu_summary.py /tmp/prof_$name.ncu-rep > gpurun_out/prof_$name.summary.txt 2>&1
 python tools/ncu_stalls.py /tmp/prof_$name.ncu-rep 60 > gpurun_out/prof_$name.stalls.txt 2>&1
 ncu -i /tmp/prof_$name.ncu-rep --page raw --csv > gpurun_out/prof_$name.raw.csv 2>&1
-ncu -i /tmp/prof_$name.ncu-rep --page source --csv --print-source sass > gpurun_out/prof_$name.sass.csv 2>&1 || true
+python tools/ncu_lines.py /tmp/prof_$name.ncu-rep 70 > gpurun_out/prof_$name.lines.txt 2>&1 || true
