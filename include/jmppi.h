@@ -260,6 +260,11 @@ int jm_loop_read(jm_ctx* ctx, double* x_out, uint64_t* iteration_out, int32_t* s
 /* Raw loop histories of the first `steps` control steps: states ((steps+1)*n),
  * controls (steps*m), jumps (steps); synchronises the context's stream. */
 int jm_loop_history(jm_ctx* ctx, int32_t steps, double* states, double* controls, int64_t* jumps);
+/* Tuning instrumentation: %globaltimer stamps (ns) of the first `steps` loop steps,
+ * 12 per step (kernel entries / grid-dependency waits / horizon ends of the rollout
+ * and finalize kernels, kernels.cuh kTl*); JM_ERR_UNSUPPORTED unless the
+ * environment had JM_TIMELINE set when jm_loop_init ran. */
+int jm_loop_timeline(jm_ctx* ctx, int32_t steps, uint64_t* out);
 
 /* Closed-loop control step split around a cross-GPU exchange (one process per
  * GPU, samples sharded by mppi.sample_offset): stage 1 = rollout of the local

@@ -110,6 +110,7 @@ SIGNATURES = {
     "jm_loop_init": (C.c_int, [_vp, _pd, _pd, _u64, _u64, _i32]),
     "jm_loop_step": (C.c_int, [_vp]),
     "jm_loop_history": (C.c_int, [_vp, _i32, _pd, _pd, _pi64]),
+    "jm_loop_timeline": (C.c_int, [_vp, _i32, _pu64]),
     "jm_loop_rollout": (C.c_int, [_vp, _vp]),
     "jm_loop_finish": (C.c_int, [_vp, _vp, _i32]),
     "jm_loop_read": (C.c_int, [_vp, _pd, _pu64, _pi32, _pi32, _pi32]),

@@ -597,6 +597,7 @@ int jm_destroy(jm_ctx* ctx) {
   dfree(ctx->d_hist);
   dfree(ctx->d_hist_jumps);
   dfree(ctx->d_hist_t);
+  dfree(ctx->d_tl);
   dfree(ctx->d_flush);
   if (ctx->h_small) cudaFreeHost(ctx->h_small);
   if (ctx->h_big) cudaFreeHost(ctx->h_big);
@@ -994,9 +995,11 @@ int jm_loop_init(jm_ctx* ctx, const double* x0, const double* u_init, uint64_t s
     dfree(ctx->d_hist);
     dfree(ctx->d_hist_jumps);
     dfree(ctx->d_hist_t);
+    dfree(ctx->d_tl);
+    ctx->d_tl = nullptr;
     if (!ctx->d_loop) {
       CK(dalloc(reinterpret_cast<char**>(&ctx->d_loop), sizeof(LoopState)));
-      CK(dalloc(&ctx->d_loop_unom, (size_t)TM));
+      CK(dalloc(&ctx->d_loop_unom, 2 * (size_t)TM));  // two parities (LoopState::unom)
       CK(dalloc(&ctx->d_loop_unew, (size_t)TM));
       if (ctx->grid <= jm::kMaxRecords) {
         CK(dalloc(&ctx->d_self_push, (size_t)jm_peer_buffer_doubles(ctx, 1)));
@@ -1026,6 +1029,11 @@ int jm_loop_init(jm_ctx* ctx, const double* x0, const double* u_init, uint64_t s
   h.hist_jumps = ctx->d_hist_jumps;
   h.t_start = ctx->d_hist_t;
   h.t_end = ctx->d_hist_t + ctx->loop_cap;
+  static const bool timeline = std::getenv("JM_TIMELINE") != nullptr;
+  if (timeline && !ctx->d_tl) CK(dalloc(&ctx->d_tl, (size_t)ctx->loop_cap * jm::kTlSlots));
+  if (ctx->d_tl) CK(cudaMemsetAsync(ctx->d_tl, 0, sizeof(uint64_t) * (size_t)ctx->loop_cap * jm::kTlSlots, ctx->own_stream));
+  h.tl = ctx->d_tl;
+  h.unom = ctx->d_loop_unom;
   std::vector<double> unom((size_t)TM);
   for (int t = 0; t < ctx->T; ++t)
     for (int j = 0; j < M; ++j) unom[(size_t)t * M + j] = u_init[j];  // initial_controller_state (controller.py:56-59)
@@ -1158,6 +1166,14 @@ int jm_loop_read(jm_ctx* ctx, double* x_out, uint64_t* iteration_out, int32_t* s
   return JM_OK;
 }
 
+int jm_loop_timeline(jm_ctx* ctx, int32_t steps, uint64_t* out) {
+  if (!ctx || !out || steps < 1 || steps > ctx->loop_cap) return fail(ctx, JM_ERR_VALUE, "bad arguments");
+  if (!ctx->d_tl) return fail(ctx, JM_ERR_UNSUPPORTED, "loop timeline off (set JM_TIMELINE=1 before jm_loop_init)");
+  CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaMemcpy(out, ctx->d_tl, sizeof(uint64_t) * (size_t)steps * jm::kTlSlots, cudaMemcpyDeviceToHost));
+  return JM_OK;
+}
+
 int jm_loop_history(jm_ctx* ctx, int32_t steps, double* states, double* controls, int64_t* jumps) {
   if (!ctx || !ctx->d_loop || steps < 0 || steps > ctx->loop_cap) return fail(ctx, JM_ERR_VALUE, "bad arguments");
   CK(cudaSetDevice(ctx->device));
@@ -1234,7 +1250,7 @@ int jm_batch_loop_host(jm_ctx* ctx, int32_t trials, const double* x0, const doub
   uint64_t* d_ht = nullptr;
   unsigned int* d_cnt = nullptr;
   cudaError_t e = dalloc(reinterpret_cast<char**>(&d_loop), sizeof(jm::LoopState) * (size_t)B);
-  if (e == cudaSuccess) e = dalloc(&d_unom, (size_t)B * TM);
+  if (e == cudaSuccess) e = dalloc(&d_unom, 2 * (size_t)B * TM);  // per trial: two parities
   if (e == cudaSuccess) e = dalloc(&d_unew, (size_t)B * TM);
   if (e == cudaSuccess) e = dalloc(&d_hs, (size_t)B * (S + 1) * N);
   if (e == cudaSuccess) e = dalloc(&d_hc, (size_t)B * S * M);
@@ -1245,7 +1261,7 @@ int jm_batch_loop_host(jm_ctx* ctx, int32_t trials, const double* x0, const doub
   if (e == cudaSuccess) e = cudaMemset(d_cnt, 0, sizeof(unsigned int) * B);
   // (the batch runs the product kernels only: no eps slabs -- their sparse epilogue regenerates noise)
   std::vector<jm::LoopState> hl((size_t)B);
-  std::vector<double> unom((size_t)B * TM), hs0((size_t)B * (S + 1) * N, 0.0);
+  std::vector<double> unom((size_t)B * 2 * TM, 0.0), hs0((size_t)B * (S + 1) * N, 0.0);
   for (int b = 0; b < B && e == cudaSuccess; ++b) {
     jm::LoopState& h = hl[b];
     h = jm::LoopState{};
@@ -1261,8 +1277,9 @@ int jm_batch_loop_host(jm_ctx* ctx, int32_t trials, const double* x0, const doub
     h.hist_jumps = d_hj + (size_t)b * S;
     h.t_start = d_ht + (size_t)b * 2 * S;
     h.t_end = h.t_start + S;
+    h.unom = d_unom + (size_t)b * 2 * TM;
     for (int t = 0; t < ctx->T; ++t)
-      for (int j = 0; j < M; ++j) unom[(size_t)b * TM + (size_t)t * M + j] = u_init[j];  // controller.py:56-59
+      for (int j = 0; j < M; ++j) unom[(size_t)b * 2 * TM + (size_t)t * M + j] = u_init[j];  // controller.py:56-59
     for (int i = 0; i < N; ++i) hs0[(size_t)b * (S + 1) * N + i] = x0[(size_t)b * N + i];
   }
   cudaStream_t s = ctx->own_stream;

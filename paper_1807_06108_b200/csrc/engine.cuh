@@ -9,6 +9,7 @@
 #include <utility>
 
 #include "internal.h"
+#include "finalize.cuh"
 #include "rollout_fast.cuh"
 
 namespace jm {
@@ -415,6 +416,14 @@ class Engine final : public EngineBase {
     f.loop = loop;
     if (!f.counter) f.counter = c->d_counter;
     const PlantArgs p = plant_args(c, loop, f.u_new, u_nom_next);
+    // the column-parallel finalize wherever no cross-GPU exchange is involved
+    static const bool no_cols = std::getenv("JM_FIN_ONE_CTA") != nullptr;  // A/B: the one-CTA merge
+    if (!no_cols && f.rec_out == nullptr && f.push_peers == nullptr && f.wait_flags == nullptr) {
+      f.cols = fincol_width(M);
+      const int g = (c->TM + f.cols - 1) / f.cols;
+      return launch_pdl(finalize_cols<Dyn>, dim3(g, c->launch_trials), dim3(fincol_threads(f.nrec)), 0, c->stream,
+                        f, p);
+    }
     f.cols = fin_cols(M);
     const int fgrid = (c->TM + f.cols - 1) / f.cols;
     return launch_pdl(finalize_kernel<Dyn>, dim3(fgrid, c->launch_trials), dim3(kFinThreads), finalize_smem_bytes(f.nrec), c->stream,

@@ -108,6 +108,7 @@ struct jm_ctx {
   double* d_hist = nullptr;       // states | controls
   int64_t* d_hist_jumps = nullptr;
   uint64_t* d_hist_t = nullptr;   // t_start | t_end
+  uint64_t* d_tl = nullptr;       // tuning timeline (JM_TIMELINE=1): loop_cap x kTlSlots stamps
   int loop_cap = 0;
   int launch_trials = 1;  // grid.y of the rollout / finalize launches (batched trials)
   void* d_lin_f = nullptr;  // Linear model: [A | G] as float (rollout in fp32)

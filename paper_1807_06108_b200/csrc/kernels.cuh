@@ -63,8 +63,32 @@ struct LoopState {
   int64_t* hist_jumps;     // max_steps
   uint64_t* t_start;       // max_steps, %globaltimer ns
   uint64_t* t_end;         // max_steps
+  uint64_t* tl;            // tuning timeline (JM_TIMELINE=1): kTlSlots %globaltimer stamps per step, or null
+  double* unom;            // nominal sequences, 2 x T*m: step k reads parity k & 1 and the finalize writes
+                           // the warm-started (shifted) sequence for step k + 1 into the other parity, so
+                           // no finalize CTA overwrites columns another CTA has yet to read
 };
 
+// the nominal sequence a closed-loop step reads (parity = step & 1) / writes for the next step
+__device__ __forceinline__ double* loop_unom(const LoopState* L, int step, int TM) {
+  return L->unom + (size_t)(step & 1) * TM;
+}
+
+// Timeline slots of one control step (jm_loop_timeline; tuning only, off unless
+// JM_TIMELINE is set when the loop is initialised)
+enum : int {
+  kTlRollEntry = 0,    // rollout CTA 0 entry (before the grid dependency wait)
+  kTlRollWait = 1,     // rollout CTA 0 past the wait
+  kTlRollHorizon = 2,  // rollout CTA 0 after the prologue (first step about to run)
+  kTlRollHorizonEndMin = 3,  // first CTA to finish its horizon
+  kTlRollHorizonEndMax = 4,  // last CTA to finish its horizon
+  kTlRollEndMax = 5,   // last CTA to write its record
+  kTlFinEntry = 6,     // finalize CTA 0 entry
+  kTlFinWait = 7,      // finalize CTA 0 past the wait
+  kTlFinMerged = 8,    // finalize CTA 0: update computed (before the plant)
+  kTlFinEnd = 9,       // finalize: plant + shift done
+  kTlSlots = 12
+};
 struct DiagOut {
   double min_cost, ess, normaliser;
   int64_t n_finite;
@@ -74,6 +98,16 @@ __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
+}
+
+__device__ __forceinline__ void tl_stamp(LoopState* L, int slot) {
+  if (L != nullptr && L->tl != nullptr) L->tl[(size_t)L->step * kTlSlots + slot] = globaltimer();
+}
+__device__ __forceinline__ void tl_max(LoopState* L, int slot) {
+  if (L != nullptr && L->tl != nullptr) atomicMax(reinterpret_cast<unsigned long long*>(L->tl) + (size_t)L->step * kTlSlots + slot, (unsigned long long)globaltimer());
+}
+__device__ __forceinline__ void tl_min(LoopState* L, int slot) {
+  if (L != nullptr && L->tl != nullptr) atomicMin(reinterpret_cast<unsigned long long*>(L->tl) + (size_t)L->step * kTlSlots + slot, (unsigned long long)globaltimer());
 }
 
 // Programmatic dependent launch (sm_90+): a kernel launched with
@@ -516,7 +550,7 @@ __device__ __forceinline__ void rollout_prologue(const RolloutArgs<Real>& a, con
     Real u[M];
 #pragma unroll
     for (int j = 0; j < M; ++j) {
-      Real v = Real(__ldg(u_nom + t * M + j));
+      Real v = Real(u_nom[t * M + j]);  // (plain load: written by the previous step's finalize)
       if (a.has_limits) v = fmin(fmax(v, a.u_lo[j]), a.u_hi[j]);
       u[j] = v;
     }
@@ -690,7 +724,7 @@ __global__ void __launch_bounds__(kRolloutMaxThreads, (RolloutMinBlocks<Sys, Rea
   const double* x0 = L ? L->x : a.x0;
   if (L != nullptr && blockIdx.x == 0 && threadIdx.x == 0) L->t_start[L->step] = globaltimer();
   ROLL_STAMP();
-  rollout_prologue<M, Real>(a, a.u_nom + (size_t)blockIdx.y * TM, tab, Nacc, s_acc, Sg);
+  rollout_prologue<M, Real>(a, L ? loop_unom(L, L->step, TM) : a.u_nom + (size_t)blockIdx.y * TM, tab, Nacc, s_acc, Sg);
   if (SCR_SMEM && a.jump_on) {  // the slab rows double as the jump-mark staging: zero them once, 16 B a store
     float4* z4 = reinterpret_cast<float4*>(scr);
     const int n4 = (int)((size_t)TM * tileK * sizeof(Real) / 16);
@@ -999,6 +1033,7 @@ struct PlantArgs {
 // kernel waits for the rollout grid.
 struct PlantPre {
   double x[12];
+  double aux[6];  // Dyn::aux<double>(x): the plant state's trig, computed before the wait
   double ed[4];   // L_D z  (Sigma_D, harness.py:137)
   double mk[4];   // mu + L_J z', drawn every step (harness.py:139)
   int k;
@@ -1012,6 +1047,11 @@ __device__ void plant_prepare(const PlantArgs& a, PlantPre& pre) {
   const int k = L->step;
   pre.k = k;
   for (int i = 0; i < N; ++i) pre.x[i] = L->x[i];
+  {
+    const auto ax = Dyn::template aux<double>(pre.x, a.sp);
+    static_assert(sizeof(ax) <= sizeof(pre.aux), "plant trig");
+    memcpy(pre.aux, &ax, sizeof(ax));
+  }
   const StreamKey sk = make_stream_key(L->seed, 0);
   P4 r = draw(sk, kSlotPlant, 3u * k + 0u, 0u);
   float z[4];
@@ -1043,25 +1083,19 @@ __device__ void plant_prepare(const PlantArgs& a, PlantPre& pre) {
 // u_new is complete.
 // u_src: the finished control sequence (shared memory when the finalize is a
 // single CTA, else a.u_new in global memory, read past L1).
+// The plant state update of one control step (one thread): x <- Euler step from
+// the clamped u0 with the prepared noise (harness.py:137-148), history, and the
+// divergence check; returns false when the plant diverged (loop halted).
 template <class Dyn>
-__device__ void plant_finish(const PlantArgs& a, const PlantPre& pre, const double* u_src, bool u_src_global) {
+__device__ bool plant_advance(const PlantArgs& a, const PlantPre& pre, const double* u0, LoopState* L) {
   constexpr int N = Dyn::N, M = Dyn::M;
-  LoopState* L = a.loop + blockIdx.y;
-  double* const u_nom = a.u_nom + (size_t)blockIdx.y * a.T * M;
-  __shared__ int s_ok;
-  if (threadIdx.x == 0) {
-    const int k = pre.k;
-    L->t_end[k] = globaltimer();
-    double u0[M];
-    for (int j = 0; j < M; ++j) {
-      double v = u_src_global ? __ldcg(u_src + j) : u_src[j];
-      if (a.has_limits) v = fmin(fmax(v, a.u_lo[j]), a.u_hi[j]);  // harness.py:136
-      u0[j] = v;
-    }
+  const int k = pre.k;
+  {
     const bool jump = pre.jump != 0;
     double x[N];
     for (int i = 0; i < N; ++i) x[i] = pre.x[i];
-    const auto ax = Dyn::template aux<double>(x, a.sp);
+    typename Dyn::template Aux<double> ax;
+    memcpy(&ax, pre.aux, sizeof(ax));  // (computed before the grid dependency wait)
     double v[M];
     for (int j = 0; j < M; ++j) {
       const double e = (jump && a.jmode == 0) ? pre.ed[j] + pre.mk[j] : pre.ed[j];
@@ -1080,14 +1114,35 @@ __device__ void plant_finish(const PlantArgs& a, const PlantPre& pre, const doub
       L->halted = 1;
       L->status = 7;
       L->diverged_at = k;
-      s_ok = 0;
-    } else {
-      for (int i = 0; i < N; ++i) {
-        L->x[i] = x[i];
-        L->hist_states[(size_t)(k + 1) * N + i] = x[i];
-      }
-      s_ok = 1;
+      return false;
     }
+    for (int i = 0; i < N; ++i) {
+      L->x[i] = x[i];
+      L->hist_states[(size_t)(k + 1) * N + i] = x[i];
+    }
+    return true;
+  }
+}
+
+// One plant step from u_new[0] and the warm-start shift; run by one CTA after
+// u_new is complete.
+// u_src: the finished control sequence (shared memory when the finalize is a
+// single CTA, else a.u_new in global memory, read past L1).
+template <class Dyn>
+__device__ void plant_finish(const PlantArgs& a, const PlantPre& pre, const double* u_src, bool u_src_global) {
+  constexpr int M = Dyn::M;
+  LoopState* L = a.loop + blockIdx.y;
+  double* const u_nom = loop_unom(L, pre.k + 1, a.T * M);  // the next step's parity
+  __shared__ int s_ok;
+  if (threadIdx.x == 0) {
+    L->t_end[pre.k] = globaltimer();
+    double u0[M];
+    for (int j = 0; j < M; ++j) {
+      double v = u_src_global ? __ldcg(u_src + j) : u_src[j];
+      if (a.has_limits) v = fmin(fmax(v, a.u_lo[j]), a.u_hi[j]);  // harness.py:136
+      u0[j] = v;
+    }
+    s_ok = plant_advance<Dyn>(a, pre, u0, L) ? 1 : 0;
   }
   __syncthreads();
   if (!s_ok) return;
@@ -1097,6 +1152,7 @@ __device__ void plant_finish(const PlantArgs& a, const PlantPre& pre, const doub
                               : L->u_init[i - (TM - M)];  // warm_start_shift
   __syncthreads();
   if (threadIdx.x == 0) {
+    tl_stamp(L, kTlFinEnd);
     L->iteration += 1;  // ControllerState(..., k+1, cfg) (harness.py:150)
     L->step += 1;
     if (L->step >= L->max_steps) L->halted = 1;
@@ -1217,6 +1273,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
   double* const unew = a.u_new ? a.u_new + (size_t)trial * a.TM : nullptr;
   unsigned int* const counter = a.counter ? a.counter + trial : nullptr;
   LoopState* L = a.loop ? a.loop + trial : nullptr;
+  const double* const unom_in = L ? loop_unom(L, L->step, a.TM) : unom;  // (read before the wait: stable)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 #ifdef JM_FIN_STAMPS
   long long fin_ts[12];
@@ -1233,9 +1290,14 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
   const bool halted = (L != nullptr && L->halted) || (a.push_loop != nullptr && a.push_loop->halted);
   const int c0 = blockIdx.x * a.cols;
   const bool reduce_mode = a.rec_out != nullptr || a.push_peers != nullptr;
-  const double unom_c = (!reduce_mode && tid < a.cols && c0 + tid < a.TM) ? unom[c0 + tid] : 0.0;
+  const double unom_c = (!reduce_mode && tid < a.cols && c0 + tid < a.TM) ? unom_in[c0 + tid] : 0.0;
+  const uint64_t t_entry = globaltimer();
   grid_dep_wait();
   if (halted) return;
+  if (L != nullptr && L->tl != nullptr && blockIdx.x == 0 && tid == 0) {
+    L->tl[(size_t)L->step * kTlSlots + kTlFinEntry] = t_entry;
+    tl_stamp(L, kTlFinWait);
+  }
   const int rs = a.rec_stride;
   FIN_STAMP();
   if (a.wait_flags != nullptr) {  // every rank's CTA records arrive over NVLink (write_record)
@@ -1352,7 +1414,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
       fin_emit_record(a, c0, CUDART_INF, 0.0, 0.0, 0.0, nullptr);
       return;
     }
-    for (int c = c0 + tid; c < min(c0 + a.cols, a.TM); c += kFinThreads) unew[c] = unom[c];
+    for (int c = c0 + tid; c < min(c0 + a.cols, a.TM); c += kFinThreads) unew[c] = unom_in[c];
     return;
   }
   // columns: warps split records (several in flight), lanes split columns
@@ -1466,6 +1528,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
     }
   }
   if (L != nullptr) {
+    if (blockIdx.x == 0 && tid == 0) tl_stamp(L, kTlFinMerged);
     grid_dep_launch();  // the next control step's rollout may become resident
     if (gridDim.x == 1) {
       plant_finish<Dyn>(p, s_pre, s_unew, false);

@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(MAXT) rollout_kernel_ws(const RolloutArgs<Real
   const uint64_t iter = L ? L->iteration : (a.iteration_dev ? *a.iteration_dev : a.iteration);
   const double* x0 = L ? L->x : a.x0;
   if (L != nullptr && blockIdx.x == 0 && threadIdx.x == 0) L->t_start[L->step] = globaltimer();
-  rollout_prologue<M, Real>(a, a.u_nom + (size_t)blockIdx.y * TM, tab, Nacc, s_acc, Sg);
+  rollout_prologue<M, Real>(a, L ? loop_unom(L, L->step, TM) : a.u_nom + (size_t)blockIdx.y * TM, tab, Nacc, s_acc, Sg);
   __syncthreads();
 
   const bool producer = (int)threadIdx.x >= C;
@@ -654,14 +654,21 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
   SparseSmem sm{s_red, s_acc, s_cnt, reinterpret_cast<int*>(sb + pl.sigc), reinterpret_cast<float*>(sb + pl.sigw),
                 reinterpret_cast<double*>(sb + pl.sigw), sb + pl.scr, pl.chunk};
 
+  const uint64_t t_entry = globaltimer();
   grid_dep_wait();    // u_nom / x / iteration come from the previous control step
   grid_dep_launch();  // let the finalize grid get resident while the horizon runs
   LoopState* L = a.loop ? a.loop + blockIdx.y : nullptr;
   if (L != nullptr && L->halted) return;
   const uint64_t iter = L ? L->iteration : (a.iteration_dev ? *a.iteration_dev : a.iteration);
   const double* x0 = L ? L->x : a.x0;
-  if (L != nullptr && blockIdx.x == 0 && threadIdx.x == 0) L->t_start[L->step] = globaltimer();
-  rollout_prologue<M, Real>(a, a.u_nom + (size_t)blockIdx.y * TM, tab, Nacc, s_acc, Sg);
+  if (L != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
+    L->t_start[L->step] = globaltimer();
+    if (L->tl != nullptr) {
+      L->tl[(size_t)L->step * kTlSlots + kTlRollEntry] = t_entry;
+      tl_stamp(L, kTlRollWait);
+    }
+  }
+  rollout_prologue<M, Real>(a, L ? loop_unom(L, L->step, TM) : a.u_nom + (size_t)blockIdx.y * TM, tab, Nacc, s_acc, Sg);
   if (jumps) {  // the mark staging is zero outside event entries (jump_window_c)
     const int n4 = (int)((size_t)SPT * nwarps * 32 * a.jw_len * Q * sizeof(Real) / 16);
     float4* z4 = reinterpret_cast<float4*>(marks);
@@ -698,6 +705,7 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
   const StreamKey sk = make_stream_key(a.seeds[blockIdx.y], iter);
   double* const costs_out = gridDim.y > 1 ? nullptr : (a.costs_dev ? *a.costs_dev : a.costs);
   const int lane = threadIdx.x & 31;
+  if (blockIdx.x == 0 && threadIdx.x == 0) tl_stamp(L, kTlRollHorizon);
   Real* wdu[SPT];
 #pragma unroll
   for (int u = 0; u < SPT; ++u) wdu[u] = marks + (size_t)(threadIdx.x >> 5) * SPT * 32 * JW * Q + u;
@@ -879,6 +887,12 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
           }
         }
       }
+      if (threadIdx.x == 0) {  // (timeline: the first and the last CTA to finish the horizon)
+        tl_max(L, kTlRollHorizonEndMax);
+        if (L != nullptr && L->tl != nullptr)
+          atomicMax(reinterpret_cast<unsigned long long*>(L->tl) + (size_t)L->step * kTlSlots + kTlRollHorizonEndMin,
+                    ~(unsigned long long)globaltimer());
+      }
       // Once non-finite, an Euler state x += dx stays non-finite, so the final
       // state decides divergence (the reference checks every step).
       Real Sf[SPT];
@@ -921,6 +935,7 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
   }
   __syncthreads();
   write_record(a, s_acc, Nacc);
+  if (threadIdx.x == 0) tl_max(L, kTlRollEndMax);
 }
 
 }  // namespace jm
