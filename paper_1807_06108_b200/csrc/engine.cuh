@@ -418,9 +418,17 @@ class Engine final : public EngineBase {
     const PlantArgs p = plant_args(c, loop, f.u_new, u_nom_next);
     // the column-parallel finalize wherever no cross-GPU exchange is involved
     static const bool no_cols = std::getenv("JM_FIN_ONE_CTA") != nullptr;  // A/B: the one-CTA merge
-    if (!no_cols && f.rec_out == nullptr && f.push_peers == nullptr && f.wait_flags == nullptr) {
+    if (!no_cols && f.rec_out == nullptr && f.push_peers == nullptr && (f.wait_flags == nullptr || f.wait_gpu)) {
       f.cols = fincol_width(M);
       const int g = (c->TM + f.cols - 1) / f.cols;
+      // a plain launch, not a programmatic dependent one: resident early beside the
+      // rollout's CTAs, the finalize's CTAs measured 0.5 us slower per cfg1 step
+      // (tools/ab1.sh; JM_FIN_PDL=1 restores the early launch)
+      static const bool fin_pdl = std::getenv("JM_FIN_PDL") != nullptr;
+      if (!fin_pdl) {
+        finalize_cols<Dyn><<<dim3(g, c->launch_trials), dim3(fincol_threads(f.nrec)), 0, c->stream>>>(f, p);
+        return cudaGetLastError();
+      }
       return launch_pdl(finalize_cols<Dyn>, dim3(g, c->launch_trials), dim3(fincol_threads(f.nrec)), 0, c->stream,
                         f, p);
     }

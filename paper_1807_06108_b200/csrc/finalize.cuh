@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(512) finalize_cols(const FinArgs a, const Plan
   const int c0 = blockIdx.x * cw;
   const int ncol = min(cw, TM - c0);
   const int ntot = min(cw + M, TM - c0);  // this CTA's columns + the shift's halo
-  const double* recs = a.rec + (size_t)trial * a.nrec * rs;
+  const double* recs = a.rec + (size_t)trial * a.nrec * rs;  // (flag mode: parity slot added below)
   LoopState* L = a.loop ? a.loop + trial : nullptr;
   unsigned int* const counter = a.counter + trial;
   __shared__ double s_min[32];
@@ -62,16 +62,36 @@ __global__ void __launch_bounds__(512) finalize_cols(const FinArgs a, const Plan
   const uint64_t t_entry = globaltimer();
   const bool halted = L != nullptr && L->halted;
   const int step = L ? L->step : 0;
+  unsigned long long* const tlr = (blockIdx.x == 0 && tid == 0) ? tl_row(L, step) : nullptr;  // (tuning timeline)
   const double* unom = L ? loop_unom(L, step, TM) : a.u_nom + (size_t)trial * TM;
   double* const unew = a.u_new ? a.u_new + (size_t)trial * TM : nullptr;
   if (L != nullptr && !halted && blockIdx.x == 0 && tid == (int)blockDim.x - 1) plant_prepare<Dyn>(p, s_pre);
   const double un_c = (tid < ntot) ? unom[c0 + tid] : 0.0;
-  grid_dep_wait();
-  if (halted) return;
-  if (L != nullptr && L->tl != nullptr && blockIdx.x == 0 && tid == 0) {
-    L->tl[(size_t)step * kTlSlots + kTlFinEntry] = t_entry;
-    tl_stamp(L, kTlFinWait);
+  // touch this thread's record lines before the wait (address translation and the L2
+  // lines' home: the first accesses after the rollout's completion otherwise pay
+  // ~3k cycles; the data itself is read after the wait)
+  if (tid < a.nrec) {
+    const double* r = recs + (size_t)tid * rs;
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(r));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(r + 4 + c0));
   }
+  if (a.wait_flags != nullptr) {
+    // world-1 record exchange (jm_loop_rollout_push layout): every rollout CTA raised its
+    // record's epoch flag (release, GPU scope) -- wait for the flags instead of the whole
+    // grid's completion; the rollout's reads of the loop state precede its record
+    if (halted) return;
+    const uint32_t epoch = (uint32_t)step + 1u;
+    for (int r = tid; r < a.nrec; r += blockDim.x)
+      while (ld_acquire_gpu(a.wait_flags + r) < epoch) {
+      }
+    __syncthreads();
+    recs += (size_t)(epoch & 1u) * a.nrec * rs;
+  } else {
+    grid_dep_wait();
+  }
+  if (halted) return;
+  tl_put(tlr, kTlFinEntry, t_entry);
+  tl_put(tlr, kTlFinWait);
 
   // one record per thread (more than 1024 records: a strided loop): all loads at once
   double h0 = CUDART_INF, h1 = 0.0, h2 = 0.0, h3 = 0.0, col[kFinColsMax];
@@ -82,13 +102,13 @@ __global__ void __launch_bounds__(512) finalize_cols(const FinArgs a, const Plan
   if (one) {
     if (tid < a.nrec) {
       const double* r = recs + (size_t)tid * rs;
-      h0 = r[0];
-      h1 = r[1];
-      h2 = r[2];
-      h3 = r[3];
+      h0 = __ldcg(r);  // (L2: written by the rollout's CTAs on other SMs)
+      h1 = __ldcg(r + 1);
+      h2 = __ldcg(r + 2);
+      h3 = __ldcg(r + 3);
 #pragma unroll
       for (int j = 0; j < kFinColsMax; ++j)
-        if (j < ntot) col[j] = r[4 + c0 + j];
+        if (j < ntot) col[j] = __ldcg(r + 4 + c0 + j);
     }
     m = h0;
   } else {
@@ -168,7 +188,7 @@ __global__ void __launch_bounds__(512) finalize_cols(const FinArgs a, const Plan
     s_part[0][tid] = out;  // (delta, for the norms)
   }
   __syncthreads();
-  if (L != nullptr && blockIdx.x == 0 && tid == 0) tl_stamp(L, kTlFinMerged);
+  tl_put(tlr, kTlFinMerged);
   if (a.norms && viable && tid < ncol / M) {  // per_step_update_norm (controller.py:168)
     double s2 = 0.0;
     for (int j = 0; j < M; ++j) s2 += s_part[0][tid * M + j] * s_part[0][tid * M + j];
@@ -220,7 +240,7 @@ __global__ void __launch_bounds__(512) finalize_cols(const FinArgs a, const Plan
         __threadfence();
         *counter = 0u;
         if (L != nullptr) {
-          tl_stamp(L, kTlFinEnd);
+          tl_put(tl_row(L, step), kTlFinEnd);
           if (!L->halted) {
             L->iteration += 1;  // ControllerState(..., k+1, cfg) (harness.py:150)
             L->step += 1;

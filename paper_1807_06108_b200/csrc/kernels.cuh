@@ -100,14 +100,17 @@ __device__ __forceinline__ uint64_t globaltimer() {
   return t;
 }
 
-__device__ __forceinline__ void tl_stamp(LoopState* L, int slot) {
-  if (L != nullptr && L->tl != nullptr) L->tl[(size_t)L->step * kTlSlots + slot] = globaltimer();
+// a step's stamp row (null when the timeline is off), read once by the stamping thread
+__device__ __forceinline__ unsigned long long* tl_row(const LoopState* L, int step) {
+  return (L != nullptr && L->tl != nullptr) ? reinterpret_cast<unsigned long long*>(L->tl) + (size_t)step * kTlSlots
+                                            : nullptr;
 }
-__device__ __forceinline__ void tl_max(LoopState* L, int slot) {
-  if (L != nullptr && L->tl != nullptr) atomicMax(reinterpret_cast<unsigned long long*>(L->tl) + (size_t)L->step * kTlSlots + slot, (unsigned long long)globaltimer());
+__device__ __forceinline__ void tl_put(unsigned long long* row, int slot, uint64_t t) {
+  if (row != nullptr) row[slot] = t;
 }
-__device__ __forceinline__ void tl_min(LoopState* L, int slot) {
-  if (L != nullptr && L->tl != nullptr) atomicMin(reinterpret_cast<unsigned long long*>(L->tl) + (size_t)L->step * kTlSlots + slot, (unsigned long long)globaltimer());
+__device__ __forceinline__ void tl_put(unsigned long long* row, int slot) { tl_put(row, slot, globaltimer()); }
+__device__ __forceinline__ void tl_max(unsigned long long* row, int slot) {
+  if (row != nullptr) atomicMax(row + slot, (unsigned long long)globaltimer());
 }
 
 // Programmatic dependent launch (sm_90+): a kernel launched with
@@ -1152,7 +1155,7 @@ __device__ void plant_finish(const PlantArgs& a, const PlantPre& pre, const doub
                               : L->u_init[i - (TM - M)];  // warm_start_shift
   __syncthreads();
   if (threadIdx.x == 0) {
-    tl_stamp(L, kTlFinEnd);
+    tl_put(tl_row(L, L->step), kTlFinEnd);
     L->iteration += 1;  // ControllerState(..., k+1, cfg) (harness.py:150)
     L->step += 1;
     if (L->step >= L->max_steps) L->halted = 1;
@@ -1294,9 +1297,10 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
   const uint64_t t_entry = globaltimer();
   grid_dep_wait();
   if (halted) return;
-  if (L != nullptr && L->tl != nullptr && blockIdx.x == 0 && tid == 0) {
-    L->tl[(size_t)L->step * kTlSlots + kTlFinEntry] = t_entry;
-    tl_stamp(L, kTlFinWait);
+  if (blockIdx.x == 0 && tid == 0 && L != nullptr) {
+    unsigned long long* const row = tl_row(L, L->step);
+    tl_put(row, kTlFinEntry, t_entry);
+    tl_put(row, kTlFinWait);
   }
   const int rs = a.rec_stride;
   FIN_STAMP();
@@ -1528,7 +1532,7 @@ __global__ void __launch_bounds__(kFinThreads) finalize_kernel(const FinArgs a, 
     }
   }
   if (L != nullptr) {
-    if (blockIdx.x == 0 && tid == 0) tl_stamp(L, kTlFinMerged);
+    if (blockIdx.x == 0 && tid == 0) tl_put(tl_row(L, L->step), kTlFinMerged);
     grid_dep_launch();  // the next control step's rollout may become resident
     if (gridDim.x == 1) {
       plant_finish<Dyn>(p, s_pre, s_unew, false);

@@ -661,12 +661,12 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
   if (L != nullptr && L->halted) return;
   const uint64_t iter = L ? L->iteration : (a.iteration_dev ? *a.iteration_dev : a.iteration);
   const double* x0 = L ? L->x : a.x0;
+  // timeline row (tuning: JM_TIMELINE), read by each CTA's stamping thread only
+  unsigned long long* const tlr = (threadIdx.x == 0) ? tl_row(L, L ? L->step : 0) : nullptr;
   if (L != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
     L->t_start[L->step] = globaltimer();
-    if (L->tl != nullptr) {
-      L->tl[(size_t)L->step * kTlSlots + kTlRollEntry] = t_entry;
-      tl_stamp(L, kTlRollWait);
-    }
+    tl_put(tlr, kTlRollEntry, t_entry);
+    tl_put(tlr, kTlRollWait);
   }
   rollout_prologue<M, Real>(a, L ? loop_unom(L, L->step, TM) : a.u_nom + (size_t)blockIdx.y * TM, tab, Nacc, s_acc, Sg);
   if (jumps) {  // the mark staging is zero outside event entries (jump_window_c)
@@ -705,7 +705,7 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
   const StreamKey sk = make_stream_key(a.seeds[blockIdx.y], iter);
   double* const costs_out = gridDim.y > 1 ? nullptr : (a.costs_dev ? *a.costs_dev : a.costs);
   const int lane = threadIdx.x & 31;
-  if (blockIdx.x == 0 && threadIdx.x == 0) tl_stamp(L, kTlRollHorizon);
+  if (blockIdx.x == 0) tl_put(tlr, kTlRollHorizon);
   Real* wdu[SPT];
 #pragma unroll
   for (int u = 0; u < SPT; ++u) wdu[u] = marks + (size_t)(threadIdx.x >> 5) * SPT * 32 * JW * Q + u;
@@ -887,11 +887,9 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
           }
         }
       }
-      if (threadIdx.x == 0) {  // (timeline: the first and the last CTA to finish the horizon)
-        tl_max(L, kTlRollHorizonEndMax);
-        if (L != nullptr && L->tl != nullptr)
-          atomicMax(reinterpret_cast<unsigned long long*>(L->tl) + (size_t)L->step * kTlSlots + kTlRollHorizonEndMin,
-                    ~(unsigned long long)globaltimer());
+      if (tlr != nullptr) {  // (timeline: the first and the last CTA to finish the horizon)
+        tl_max(tlr, kTlRollHorizonEndMax);
+        atomicMax(tlr + kTlRollHorizonEndMin, ~(unsigned long long)globaltimer());
       }
       // Once non-finite, an Euler state x += dx stays non-finite, so the final
       // state decides divergence (the reference checks every step).
@@ -935,7 +933,7 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
   }
   __syncthreads();
   write_record(a, s_acc, Nacc);
-  if (threadIdx.x == 0) tl_max(L, kTlRollEndMax);
+  tl_max(tlr, kTlRollEndMax);
 }
 
 }  // namespace jm

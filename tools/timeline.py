@@ -34,6 +34,7 @@ def main(wl="cfg1", steps=40):
         ctx.check(lib.jm_loop_step(h))
     tl = np.zeros(steps * 12, dtype=np.uint64)
     ctx.check(lib.jm_loop_timeline(h, steps, tl.ctypes.data_as(C.POINTER(C.c_uint64))))
+    raw = tl.reshape(steps, 12)[:, 10:12].copy()
     tl = tl.reshape(steps, 12).astype(np.float64)
     tl[:, 3] = (2.0 ** 64 - 1) - tl[:, 3]  # stored as ~t (atomicMax of the complement)
     w = tl[steps // 4:]
@@ -41,8 +42,14 @@ def main(wl="cfg1", steps=40):
     rel = (w[:, :10] - base) / 1e3
     period = np.diff(w[:, 0]) / 1e3
     print(f"{wl}: K={cfg.samples_m} T={cfg.horizon_n}; step period {period.mean():.2f} us (rollout entry to entry)")
-    for i, n in enumerate(NAMES):
+    for i, n in enumerate(NAMES[:10]):
         print(f"  {n:16s} {rel[:, i].mean():8.2f} us  (sd {rel[:, i].std():.2f})")
+    if os.environ.get("JM_TL_PROBE"):
+        r = raw[steps // 4:]
+        hi = lambda v: (v >> np.uint64(32)).astype(float).mean()
+        lo = lambda v: (v & np.uint64(0xffffffff)).astype(float).mean()
+        print(f"  probe cycles: loads+warpmin {hi(r[:, 0]):.0f} barrier+min {lo(r[:, 0]):.0f} "
+              f"exp+sums {hi(r[:, 1]):.0f} update {lo(r[:, 1]):.0f}")
 
 
 if __name__ == "__main__":
