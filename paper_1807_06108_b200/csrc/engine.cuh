@@ -82,7 +82,7 @@ class Engine final : public EngineBase {
   // (jump-mark staging: 32 lanes x W steps x q per warp; marks_warps = the warps running jump windows)
   size_t plan_bytes(const jm_ctx* c, int tile, int marks_warps, int W, int nring, bool scr) const {
     const int nmarks = c->jthr ? marks_warps * 32 * W * q_of(c) : 0;
-    return smem_plan(c->TM, c->T * tab_stride<M>(), tile, nmarks, nring, scr ? c->TM * tile : 0, c->gap_n,
+    return smem_plan(c->TM, c->T * (2 * M + 1), tile, nmarks, nring, scr ? c->TM * tile : 0, c->gap_n,
                      (int)sizeof(Real))
         .total;
   }
@@ -95,7 +95,7 @@ class Engine final : public EngineBase {
   size_t ws_bytes(const jm_ctx* c, int tile, int W) const {
     const int nmarks = c->jthr ? tile * W * q_of(c) : 0;
     const int chunk = ws_chunk(tile, regen_items(c->T, 4 / Pad<M>::value));
-    return smem_plan(c->TM, c->T * tab_stride<M>(), tile, nmarks, ws_ring(c, tile), chunk * c->TM, c->gap_n,
+    return smem_plan(c->TM, c->T * (2 * M + 1), tile, nmarks, ws_ring(c, tile), chunk * c->TM, c->gap_n,
                      (int)sizeof(Real))
         .total;
   }
@@ -154,7 +154,7 @@ class Engine final : public EngineBase {
   size_t fast_bytes(const jm_ctx* c, int tile, int spt, int W, bool philox) const {
     const int nb = regen_items(c->T, fast_gs(philox));
     const int nmarks = (philox && c->jthr) ? tile * W * q_of(c) : 0;
-    return fast_plan(c->TM, c->T * tab_stride<M>(), tile, tile / spt, nb, nmarks, c->gap_n, (int)sizeof(Real)).total;
+    return fast_plan(c->TM, c->T * (2 * M + 1), tile, tile / spt, nb, nmarks, c->gap_n, (int)sizeof(Real)).total;
   }
 
   // warp-specialised kernel (Philox, non-trace): block = 2 x tile

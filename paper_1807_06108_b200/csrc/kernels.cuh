@@ -538,23 +538,13 @@ __device__ __forceinline__ void jump_window(JumpClock& c, int w0, int wend, int 
 }
 
 // ---------------------------------------------------------------- rollout
-// The per-step table row [u dt (m) | 1/2 u'Ru dt | lambda sqrt(dt) u (m)], padded
-// to a multiple of 4 Reals: a step reads it with aligned vector loads.
-#ifndef JM_TAB_PAD
-#define JM_TAB_PAD 1
-#endif
-template <int M>
-__host__ __device__ constexpr int tab_stride() {
-  return JM_TAB_PAD ? (2 * M + 1 + 3) & ~3 : 2 * M + 1;
-}
-
 // Common prologue: per-step table (clamped u, controller.py:128, hoisted into
 //   udt = u dt, a_t = 1/2 u'Ru dt, b_t = lambda u sqrt(dt)   (costs.py:98-111 times dt)),
 // accumulator reset and the gap table copy.
 template <int M, typename Real>
 __device__ __forceinline__ void rollout_prologue(const RolloutArgs<Real>& a, const double* u_nom, Real* tab,
                                                  double* Nacc, double* s_acc, uint32_t* S) {
-  constexpr int TS = tab_stride<M>();
+  constexpr int TS = 2 * M + 1;
   const int T = a.T;
   // read-only (.nc) loads, unrolled: the loop's global reads are issued
   // together instead of one round trip per iteration
@@ -695,7 +685,7 @@ __global__ void __launch_bounds__(kRolloutMaxThreads, (RolloutMinBlocks<Sys, Rea
   constexpr int MP = Pad<M>::value;
   constexpr int Q = (JM == 0) ? M : Dyn::QJ;
   constexpr int QP = Pad<Q>::value;
-  constexpr int TS = tab_stride<M>();
+  constexpr int TS = 2 * M + 1;
 
   extern __shared__ double smem_d[];
   __shared__ double s_red[4][32];

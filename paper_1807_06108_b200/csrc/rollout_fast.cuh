@@ -123,14 +123,8 @@ __device__ __forceinline__ void block_normals_v(const StreamKey& sk, uint32_t b,
 // 32-lane window each), (b) a buffer that stays zero outside event entries:
 // each lane first clears the entries of its previous window's events (prev),
 // instead of the warp zeroing every row of the window.
-// Entry (s, i, L) at wd[mark_slot<Q, ES>(s, i, L)]: 4-step packets per lane --
-// [s / 4][i][L][s % 4] -- so a 4-step group reads its marks with one 16-byte
-// load, and ES = SPT interleaves the two halves of a thread (both samples'
-// marks side by side).
-template <int Q, int ES>
-__device__ __forceinline__ int mark_slot(int s, int i, int L) {
-  return ((((s >> 2) * Q + i) * 32 + L) * 4 + (s & 3)) * ES;
-}
+// Entry (s, i, L) at wd[((s * Q + i) * 32 + L) * ES]: ES = SPT interleaves the
+// two halves of a thread (one 8-byte load reads both samples' marks).
 template <int Q, int QP, int JM, int ES, typename Real>
 __device__ __forceinline__ void jump_window_c(JumpClock& c, Mask128& prev, int w0, int wend, const StreamKey& sk,
                                               uint32_t kg, int kstride, const GapSampler& gs, const Real* Lj,
@@ -159,7 +153,7 @@ __device__ __forceinline__ void jump_window_c(JumpClock& c, Mask128& prev, int w
   for (Mask128 m = prev; m.lo | m.hi; mask_pop(m)) {
     const int s = mask_low(m);
 #pragma unroll
-    for (int i = 0; i < Q; ++i) wd[mark_slot<Q, ES>(s, i, lane)] = Real(0);
+    for (int i = 0; i < Q; ++i) wd[((s * Q + i) * 32 + lane) * ES] = Real(0);
   }
   prev = mask;
   __syncwarp();
@@ -180,7 +174,7 @@ __device__ __forceinline__ void jump_window_c(JumpClock& c, Mask128& prev, int w
       Real mk[Q];
       mark_of<Q, QP, Real>(sk, kg + (uint32_t)((L - lane) * kstride), eL, Lj, mu, mk, poisson, ct);
 #pragma unroll
-      for (int i = 0; i < Q; ++i) wd[mark_slot<Q, ES>(s, i, L)] = (JM == 1) ? rmul<Real>(jscale, mk[i]) : mk[i];
+      for (int i = 0; i < Q; ++i) wd[((s * Q + i) * 32 + L) * ES] = (JM == 1) ? rmul<Real>(jscale, mk[i]) : mk[i];
     }
   }
   __syncwarp();
@@ -389,7 +383,7 @@ __global__ void __launch_bounds__(MAXT) rollout_kernel_ws(const RolloutArgs<Real
   constexpr int MP = Pad<M>::value;
   constexpr int Q = (JM == 0) ? M : Dyn::QJ;
   constexpr int QP = Pad<Q>::value;
-  constexpr int TS = tab_stride<M>();
+  constexpr int TS = 2 * M + 1;
   constexpr int GW = WsShape<Sys, JM>::GW;
 
   extern __shared__ double smem_d[];
@@ -634,7 +628,7 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
   constexpr int MP = Pad<M>::value;
   constexpr int Q = (JM == 0) ? M : Dyn::QJ;
   constexpr int QP = Pad<Q>::value;
-  constexpr int TS = tab_stride<M>();
+  constexpr int TS = 2 * M + 1;
   // steps per noise group: one Philox block (4 normals); HBM mode: 4 steps of
   // the small systems, one quadrotor step (its loads are 7 words a step)
   constexpr int GS = PHILOX ? 4 / MP : (M >= 3 ? 1 : 4);
@@ -701,13 +695,6 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
   for (int i = 0; i < Q * Q; ++i) Lj[i] = a.Lj[i];
 #pragma unroll
   for (int i = 0; i < Q; ++i) mu[i] = a.mu_j[i];
-#ifndef JM_PIN_TK
-#define JM_PIN_TK 1
-#endif
-  if constexpr (JM_PIN_TK && SPT == 1 && sizeof(Real) == 4) {  // the packed sincos coefficient pairs (sincos_f32<true>)
-#pragma unroll
-    for (int i = 0; i < 3; ++i) pin(sp.tk[i]);
-  }
   S dt = a.dt, sdt = a.sdt, cq = a.cq;
   const S jscale = a.jscale;
   pin(dt);
@@ -744,12 +731,13 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
       for (int i = 0; i < N; ++i) x[i] = vcast<V>(x0[i]);
       V Sacc = vcast<V>(0.0);
       JumpClock clk[SPT];
-      int wnext = 0, wstart = 0;
-      // this lane's mark packets (both halves interleaved): packet (p, i) at wlane + (p * Q + i) * 128 * SPT
-      const Real* const wlane = wdu[0] + lane * 4 * SPT;
+      const Real* wl[SPT];
+      int wnext = 0;
 #pragma unroll
-      for (int u = 0; u < SPT; ++u)
+      for (int u = 0; u < SPT; ++u) {
+        wl[u] = wdu[u] + lane * SPT;
         if (jumps) clock_start(clk[u], sk, kg[u], gs);
+      }
 
       // one horizon step t with its eps_combined and state-jump increment
       auto step = [&](const int t, const V* eps, const V* sj, const bool has_sj) {
@@ -790,43 +778,20 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
       if constexpr (PHILOX) {
         V z[4], zn[4];
         block_normals_v(sk, 0u, kg, z);
-        V mg[GS][Q];  // the group's staged marks (zero where no event)
-        auto load_marks = [&](const int t0) {
-          const int rel = t0 - wstart;
-          const Real* pk = wlane + (size_t)(rel >> 2) * Q * 128 * SPT + (rel & 3) * SPT;
-#pragma unroll
-          for (int i = 0; i < Q; ++i) {
-            const Real* q = pk + i * 128 * SPT;
-            if constexpr (GS == 4 && SPT == 1 && sizeof(Real) == 4) {
-              const float4 v = *reinterpret_cast<const float4*>(q);
-              mg[0][i] = V(v.x);
-              mg[1][i] = V(v.y);
-              mg[2][i] = V(v.z);
-              mg[3][i] = V(v.w);
-            } else if constexpr (GS == 4 && SPT == 2) {
-              const float4 v0 = *reinterpret_cast<const float4*>(q);
-              const float4 v1 = *reinterpret_cast<const float4*>(q + 4);
-              mg[0][i] = F2(v0.x, v0.y);
-              mg[1][i] = F2(v0.z, v0.w);
-              mg[2][i] = F2(v1.x, v1.y);
-              mg[3][i] = F2(v1.z, v1.w);
-            } else {
-#pragma unroll
-              for (int s2 = 0; s2 < GS; ++s2) {
-                if constexpr (SPT == 2)
-                  mg[s2][i] = F2(*reinterpret_cast<const float2*>(q + s2 * 2));
-                else
-                  mg[s2][i] = V(q[s2]);
-              }
-            }
-          }
-        };
         auto noisy = [&](const int t, const int s2) {
           V eps[M], sj[Q];
           bool has_sj = false;
           chol_v<M>(Ld, z + s2 * MP, eps);
           if (jumps) {
-            const V* mv = mg[s2];
+            V mv[Q];  // the staged marks of both halves: one load (interleaved pairs)
+#pragma unroll
+            for (int i = 0; i < Q; ++i) {
+              if constexpr (SPT == 2)
+                mv[i] = F2(*reinterpret_cast<const float2*>(wl[0] + i * 32 * SPT));
+              else
+                mv[i] = wl[0][i * 32];
+            }
+            wl[0] += Q * 32 * SPT;
             if (JM == 0) {
 #pragma unroll
               for (int j = 0; j < M; ++j) eps[j] = vadd(eps[j], mv[j]);  // noise.py:156-157
@@ -840,14 +805,14 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
         };
         for (int t0 = 0; t0 < T; t0 += GS) {
           if (jumps && t0 == wnext) {
-            wstart = t0;
             wnext = t0 + JW;
 #pragma unroll
-            for (int u = 0; u < SPT; ++u)
+            for (int u = 0; u < SPT; ++u) {
               jump_window_c<Q, QP, JM, SPT, Real>(clk[u], prev[u], t0, min(wnext, T), sk, kg[u], SPT, gs, Lj, mu,
                                                   jscale, wdu[u], a.poisson != 0, a.cnt);
+              wl[u] = wdu[u] + lane * SPT;
+            }
           }
-          if (jumps) load_marks(t0);
           if (t0 + GS <= T) {
             if (t0 + GS < T) block_normals_v(sk, (uint32_t)((t0 + GS) / GS), kg, zn);
 #pragma unroll
