@@ -16,9 +16,12 @@ fully synthetic).  Between timed steps a 256 MiB memset evicts the 126 MB L2.
 from baseline/_ref, unmodified) on the host cores, on the reference-expressible
 twin of the same config (control-channel jumps; same K, T, model and per
 state-step work), one process per core.
-N > 1 (torchrun): weak scaling, K samples per GPU with global sample indices;
-per control step one all_gather of the (rho, Z, sum w^2, N[T*m]) records over
-NCCL, then every rank merges and applies the same update and plant step.
+N > 1 (torchrun): weak scaling (K samples per GPU) by default, strong scaling
+(BASELINE config 3: K in total, K/N per GPU) for cfg3 or --scaling strong;
+global sample indices; per control step one all_gather of the reduced
+(rho, Z, sum w^2, N[T*m]) record of each rank over NCCL (JM_EXCHANGE=p2p: the
+peer-memory exchange), then every rank merges and applies the same update and
+plant step.
 """
 
 from __future__ import annotations
@@ -60,7 +63,9 @@ def parse():
     p.add_argument("--noise", default="philox", choices=["philox", "hbm"])
     p.add_argument("--precision", default="f32", choices=["f32", "f64"])
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--samples", type=int, default=None, help="override K per GPU")
+    p.add_argument("--samples", type=int, default=None, help="override K (per GPU under weak scaling)")
+    p.add_argument("--scaling", default=None, choices=["weak", "strong"],
+                   help="N > 1: weak = K per GPU (default), strong = K in total, K/N per GPU (default for cfg3)")
     p.add_argument("--horizon", type=int, default=None, help="override T")
     p.add_argument("--block", type=int, default=0, help="override the rollout tile (block_threads, tuning)")
     p.add_argument("--nu", type=float, default=None, help="override the jump rate (tuning; 0 = no jumps)")

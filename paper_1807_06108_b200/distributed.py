@@ -11,24 +11,30 @@ exp(-(rho_r - rho)/lambda) (the finalize kernel) and applies the identical
 update, plant step and shift -- one collective instead of a MIN all-reduce
 followed by a SUM all-reduce.
 
-Two transports for that exchange:
-  "p2p"  (default when available) -- no collective library on the data path:
-         each rank owns a symmetric buffer (torch.distributed._symmetric_memory,
-         peer pointers over NVLink/NVSwitch); a one-CTA kernel stores the
-         rank's record straight into slot `rank` of every peer's buffer and
-         raises an epoch flag there, and the finalize kernel waits on its own
-         flags on the device (jm_loop_rollout_push / jm_loop_finish_peers) --
-         the step never returns to the host or a collective launch;
-  "nccl" -- all_gather_into_tensor of the records (the fallback).
+Sharding (`scaling`): "weak" -- K samples per GPU (rank r owns global samples
+[r K, (r+1) K)); "strong" -- BASELINE config 3's K/N split of a fixed global K
+(shard_strong: ragged when N does not divide K, the first K mod N ranks one
+sample more).
 
-The p2p exchange has two forms.  Flat (world < 6): the rollout kernel's CTAs
-push their own records, every rank merges world x grid of them.  Two-level
-(world >= 6, `two_level`; env JM_P2P_TWO_LEVEL=0/1 overrides): a reduce
-kernel merges the rank's CTA records into one and pushes that, every rank
-merges `world` records -- the NCCL transport's merge tree, bit for bit.
-Measured on one B200 (DESIGN 7b): the reduce kernel adds 5.8 us to a cfg1
-step (43.7 -> 49.5 us at world 1) while the flat merge grows by 1.6 / 5.2 /
-13.1 us at world 2 / 4 / 8 -- the crossover lies between 4 and 8.
+Two transports for the exchange:
+  "nccl" (default) -- a reduce kernel merges the rank's CTA records into one,
+         all_gather_into_tensor gathers the `world` records, the finalize
+         merges them: three kernels of ours plus the collective per step;
+  "p2p"  (JM_EXCHANGE=p2p) -- no collective library on the data path: each
+         rank owns a symmetric buffer (torch.distributed._symmetric_memory,
+         peer pointers over NVLink/NVSwitch); the rollout kernel's CTAs store
+         their records straight into every rank's buffer and raise epoch flags
+         there (system-scope release), the finalize waits on its own flags on
+         the device (jm_loop_rollout_push / jm_loop_finish_peers) -- the step
+         never returns to the host or a collective launch.  Two forms: flat
+         (world < 6: every rank merges world x grid CTA records) and two-level
+         (world >= 6 or strong scaling, `two_level`; JM_P2P_TWO_LEVEL=0/1
+         overrides: a reduce kernel pushes one record per rank -- the NCCL
+         transport's merge tree, bit for bit).  It has run at world 1 only
+         (this pod exposes one GPU), hence not the default.
+Every rank agrees on the transport before the first step (an all_reduce of
+each rank's setup result), so a rank whose peer-buffer setup failed cannot
+leave the others waiting in a different exchange.
 
 torch.distributed is the plumbing (process group, rendezvous of the symmetric
 buffers, streams); all arithmetic is in libjmppi.so.  The host-side logic here
@@ -55,12 +61,32 @@ def shard(k_per_rank: int, rank: int) -> Tuple[int, int]:
     return rank * k_per_rank, k_per_rank
 
 
+def shard_for(scaling: str, k: int, rank: int, world: int) -> Tuple[int, int]:
+    """(sample_offset, count): weak -- k samples per rank; strong -- k in total."""
+    if scaling == "weak":
+        return shard(k, rank)
+    if scaling == "strong":
+        return shard_strong(k, rank, world)
+    raise ValueError(f"scaling must be weak or strong, got {scaling!r}")
+
+
 def shard_strong(k_total: int, rank: int, world: int) -> Tuple[int, int]:
     """(sample_offset, count) when a fixed global K is split over `world` ranks."""
     base, rem = divmod(k_total, world)
     count = base + (1 if rank < rem else 0)
     offset = rank * base + min(rank, rem)
     return offset, count
+
+
+def agree(ok: bool, group=None) -> bool:
+    """True iff `ok` on every rank (an all_reduce MIN of a flag; CPU tensor under gloo)."""
+    import torch
+    import torch.distributed as dist
+
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else "cpu"
+    t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    return bool(t.item())
 
 
 def exchange_records(local, group=None):
@@ -108,14 +134,25 @@ class ShardedLoop:
     rank: int
     group: object = None
     transport: str = "nccl"
-    two_level: bool = None  # p2p only; None: use_two_level(world)
+    two_level: bool = None  # p2p only; None: use_two_level(world) (always two-level under strong scaling)
+    scaling: str = "weak"
+    k_total: int = 0
 
     @classmethod
-    def create(cls, task, cfg, rank: int, world: int, device: int, precision=None, group=None, transport="nccl"):
-        off, _ = shard(cfg.samples_m, rank)
-        ctx = engine.get_context(task.model, task.cost_model, cfg, precision=precision, sample_offset=off,
-                                 device=device)
-        return cls(ctx, world, rank, group, transport)
+    def create(cls, task, cfg, rank: int, world: int, device: int, precision=None, group=None, transport="nccl",
+               scaling="weak"):
+        off, cnt = shard_for(scaling, cfg.samples_m, rank, world)
+        ctx = engine.get_context(task.model, task.cost_model, cfg, samples=cnt, precision=precision,
+                                 sample_offset=off, device=device)
+        k_total = cfg.samples_m if scaling == "strong" else world * cfg.samples_m
+        # (ragged strong shards may differ in their CTA grids: one record per rank)
+        return cls(ctx, world, rank, group, transport, True if scaling == "strong" else None, scaling, k_total)
+
+    def launches_per_step(self) -> int:
+        """Kernels of ours per control step (the NCCL collective not counted)."""
+        if self.transport == "p2p":
+            return 3 if self.two_level else 2
+        return 3  # rollout, reduce, finalize
 
     def init(self, x0, u_init, seed: int, max_steps: int):
         import torch
@@ -137,20 +174,36 @@ class ShardedLoop:
         torch.cuda.synchronize(dev)
         if self.transport == "p2p":
             if self.two_level is None:
-                self.two_level = use_two_level(self.world)
-            self._init_peers(dev)
+                self.two_level = use_two_level(self.world)  # (a bad JM_P2P_TWO_LEVEL raises on every rank)
+            buf, err = None, None
+            try:  # the local half of the setup: the symmetric allocation
+                buf = self._alloc_peers(dev)
+            except (RuntimeError, OSError, ImportError, AttributeError) as exc:
+                err = exc
+            # every rank takes the same transport: p2p only if it could be set up everywhere
+            if agree(err is None, self.group):
+                self._init_peers(dev, buf)
+            else:
+                self.transport = "nccl"
+                self.p2p_error = err
 
-    def _init_peers(self, dev):
-        """Symmetric exchange buffers + their peer addresses (jm_peer_buffer_doubles layout)."""
+    def _alloc_peers(self, dev):
+        import torch
+        import torch.distributed._symmetric_memory as symm
+
+        n = int(self.ctx.lib.jm_peer_buffer_doubles(self.ctx.h, self.world))
+        buf = symm.empty(n, dtype=torch.float64, device=dev)
+        buf.zero_()  # epoch flags start at 0
+        torch.cuda.synchronize(dev)
+        return buf
+
+    def _init_peers(self, dev, buf):
+        """Rendezvous of the symmetric exchange buffers + their peer addresses (jm_peer_buffer_doubles layout)."""
         import torch
         import torch.distributed as dist
         import torch.distributed._symmetric_memory as symm
 
         lib, h = self.ctx.lib, self.ctx.h
-        n = int(lib.jm_peer_buffer_doubles(h, self.world))
-        buf = symm.empty(n, dtype=torch.float64, device=dev)
-        buf.zero_()  # epoch flags start at 0
-        torch.cuda.synchronize(dev)
         hdl = symm.rendezvous(buf, self.group if self.group is not None else dist.group.WORLD)
         ptrs = [int(p) for p in hdl.buffer_ptrs]
         off = buf.data_ptr() - ptrs[self.rank]  # the same offset in every rank's symmetric allocation
@@ -159,7 +212,7 @@ class ShardedLoop:
         torch.cuda.synchronize(dev)
         dist.barrier(group=self.group)  # every rank's flags are zero before anyone pushes
         # the whole step is device-side (no collective, no host wait): one CUDA
-        # graph of its four kernels, replayed per control step
+        # graph of its two (flat) or three (two-level) kernels, replayed per control step
         lib, h = self.ctx.lib, self.ctx.h
         self.graph = torch.cuda.CUDAGraph()
         if self.two_level:
@@ -207,9 +260,9 @@ class ShardedLoop:
 
 
 def bench_sharded(a, world: int, rank: int, local: int):
-    """bench.py entry for N > 1 (torchrun): weak scaling, K samples per GPU."""
+    """bench.py entry for N > 1 (torchrun): weak scaling (K samples per GPU) or
+    strong scaling (BASELINE config 3: K in total, K/N per GPU)."""
     import json
-    import time
 
     import torch
     import torch.distributed as dist
@@ -221,18 +274,13 @@ def bench_sharded(a, world: int, rank: int, local: int):
     idx = {"cfg0": 0, "cfg1": 1, "cfg2": 2, "cfg3": 3}[a.workload]
     task, cfg = jb.baseline_config(idx, K=a.samples, T=a.horizon)
     K, T = cfg.samples_m, cfg.horizon_n
+    scaling = getattr(a, "scaling", None) or ("strong" if idx == 3 else "weak")
     n_total = a.warmup + a.steps
-    transport = os.environ.get("JM_EXCHANGE", "p2p")
-    try:
-        loop = ShardedLoop.create(task, cfg, rank, world, local, precision=a.precision, transport=transport)
-        loop.init(task.x0, cfg.u_init, 0, 2 * n_total + 64)
-    except Exception as exc:  # symmetric memory unavailable: the NCCL all_gather path
-        if transport != "p2p":
-            raise
-        print(f"[bench] peer-memory exchange unavailable ({exc}); using NCCL all_gather", file=sys.stderr)
-        transport = "nccl"
-        loop = ShardedLoop.create(task, cfg, rank, world, local, precision=a.precision, transport=transport)
-        loop.init(task.x0, cfg.u_init, 0, 2 * n_total + 64)
+    transport = os.environ.get("JM_EXCHANGE", "nccl")
+    loop = ShardedLoop.create(task, cfg, rank, world, local, precision=a.precision, transport=transport,
+                              scaling=scaling)
+    loop.init(task.x0, cfg.u_init, 0, 2 * n_total + 64)  # (falls back to NCCL on every rank together)
+    k_local = loop.ctx.K
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     for _ in range(a.warmup):
         loop.step()
@@ -254,26 +302,29 @@ def bench_sharded(a, world: int, rank: int, local: int):
     times = [e0.elapsed_time(e1) for e0, e1 in evs]
     t = torch.tensor([float(np.mean(times))], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)  # max over ranks
+    kl = torch.tensor([k_local, -k_local], dtype=torch.int64, device="cuda")
+    dist.all_reduce(kl, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     x, it, st, halted, status = loop.read()
     if halted:
         raise RuntimeError(f"sharded loop halted (status {status})")
     if rank == 0:
-        value = world * K * T / (ms * 1e-3)
+        value = loop.k_total * T / (ms * 1e-3)
+        exch = (("two-level: one reduced record per rank" if loop.two_level else "flat: per-CTA records") +
+                " over peer memory (symmetric buffers, device-side epoch flags, no collective launch)"
+                if loop.transport == "p2p" else
+                "NCCL all_gather_into_tensor of one reduced record per rank")
         line = {"metric": "rollout state-steps/sec (K*T/s)", "value": value, "unit": "state-steps/s",
                 "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": a.precision,
+                "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": a.precision,
                 "data": "synthetic",
                 "config": {"workload": f"{a.workload}: BASELINE config {idx} closed-loop control step, "
-                                       f"K={K} per GPU (global {world * K}), T={T}, one exchange of the "
-                                       "weighting records per step",
-                           "exchange": ((("two-level: one reduced record per rank" if loop.two_level
-                                          else "flat: per-CTA records") +
-                                         " over peer memory (symmetric buffers, device-side epoch flags, "
-                                         "no collective launch)") if transport == "p2p"
-                                        else "NCCL all_gather_into_tensor"),
-                           "K_per_gpu": K, "T": T, "parallelism": f"dp{world}",
+                                       f"K={loop.k_total} in total ({'K/N' if scaling == 'strong' else 'K'} per GPU: "
+                                       f"{int(kl[0].item())}{'' if -int(kl[1].item()) == int(kl[0].item()) else ' / ' + str(-int(kl[1].item()))}), "
+                                       f"T={T}, one exchange of the weighting records per step",
+                           "K_total": loop.k_total, "K_per_gpu_max": int(kl[0].item()), "K_per_gpu_min": -int(kl[1].item()),
+                           "exchange": exch, "T": T, "parallelism": f"dp{world}",
                            "l2": "flushed (256 MiB fill) before each timed step"},
-                "mpc_iteration_latency_ms": ms, "gpu_launches": ((5 if loop.two_level else 4) if transport == "p2p" else 3) * a.steps}
+                "mpc_iteration_latency_ms": ms, "gpu_launches": loop.launches_per_step() * a.steps}
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()

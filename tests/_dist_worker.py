@@ -22,10 +22,17 @@ def main():
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from conftest import load_golden, oracle_spec
 
+    if os.environ.get("JM_AGREE"):  # transport agreement: rank 1 reports a failed setup
+        ok = jd.agree(rank != 1)
+        print(json.dumps({"rank": rank, "agree": ok, "all_ok": jd.agree(True)}))
+        dist.destroy_process_group()
+        return
     g = load_golden(os.environ["JM_CASE"])
     spec = oracle_spec(g["spec"])
-    k_local = int(os.environ["JM_K_LOCAL"])
-    off, cnt = jd.shard(k_local, rank)
+    if os.environ.get("JM_K_TOTAL"):  # strong scaling: a fixed global K split over the ranks (ragged)
+        off, cnt = jd.shard_for("strong", int(os.environ["JM_K_TOTAL"]), rank, world)
+    else:
+        off, cnt = jd.shard_for("weak", int(os.environ["JM_K_LOCAL"]), rank, world)
     Ld = np.linalg.cholesky(spec.c * spec.sigma_d)
     Lj = np.linalg.cholesky(spec.sigma_j)
     jthr = ps.jump_threshold(spec.nu * spec.dt) if spec.jump_enabled else 0
@@ -37,7 +44,7 @@ def main():
     gathered = jd.exchange_records(rec).numpy()
     u_new, rho, ess = om.combine_records(gathered, spec.lam, spec.dt, g["u_nom"])
     print(json.dumps({"rank": rank, "u_new": u_new.tolist(), "rho": rho, "ess": ess,
-                      "gathered_rho": gathered[:, 0].tolist()}))
+                      "gathered_rho": gathered[:, 0].tolist(), "offset": off, "count": cnt}))
     dist.destroy_process_group()
 
 

@@ -56,12 +56,10 @@ def test_record_merge_matches_unsharded_oracle():
     assert ess == pytest.approx(ref["ess"], rel=1e-12)
 
 
-@pytest.mark.parametrize("case", ["b_cartpole", "r_quadrotor_task"])
-def test_gloo_world2_exchange(case):
+def _run_world2(**extra):
     port = _free_port()
-    k_local = 48
-    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), WORLD_SIZE="2",
-               JM_CASE=case, JM_K_LOCAL=str(k_local), CUDA_VISIBLE_DEVICES="")
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), WORLD_SIZE="2", CUDA_VISIBLE_DEVICES="",
+               **{k: str(v) for k, v in extra.items()})
     procs = [subprocess.Popen([sys.executable, str(ROOT / "tests" / "_dist_worker.py")],
                               env=dict(env, RANK=str(r), LOCAL_RANK=str(r)), stdout=subprocess.PIPE,
                               stderr=subprocess.PIPE, text=True) for r in range(2)]
@@ -70,20 +68,49 @@ def test_gloo_world2_exchange(case):
         o, e = p.communicate(timeout=300)
         assert p.returncode == 0, e[-3000:]
         outs.append(json.loads(o.strip().splitlines()[-1]))
+    return outs
+
+
+@pytest.mark.parametrize("case,scaling", [("b_cartpole", "weak"), ("r_quadrotor_task", "weak"),
+                                          ("b_cartpole", "strong"), ("r_quadrotor_task", "strong")])
+def test_gloo_world2_exchange(case, scaling):
+    """Weak: 48 samples per rank.  Strong (BASELINE config 3's K/N split): 97
+    samples in total, ragged 49 + 48."""
+    if scaling == "weak":
+        k_global = 2 * 48
+        outs = _run_world2(JM_CASE=case, JM_K_LOCAL=48)
+    else:
+        k_global = 97
+        outs = _run_world2(JM_CASE=case, JM_K_TOTAL=k_global)
+        assert [(o["offset"], o["count"]) for o in outs] == [(0, 49), (49, 48)]
     # every rank merged the same records into the same update
     assert outs[0]["u_new"] == outs[1]["u_new"]
-    # ... equal to one unsharded iteration over the 2*k_local global samples
+    # ... equal to one unsharded iteration over the k_global global samples
     g = load_golden(case)
     spec = oracle_spec(g["spec"])
     Ld = np.linalg.cholesky(spec.c * spec.sigma_d)
     Lj = np.linalg.cholesky(spec.sigma_j)
     jthr = ps.jump_threshold(spec.nu * spec.dt) if spec.jump_enabled else 0
-    full = ps.device_noise(7, 3, 2 * k_local, spec.T, spec.m, spec.q, Ld, Lj, spec.mark_mean, jthr,
+    full = ps.device_noise(7, 3, k_global, spec.T, spec.m, spec.q, Ld, Lj, spec.mark_mean, jthr,
                            jump_channel=spec.jump_channel)
-    spec.K = 2 * k_local
+    spec.K = k_global
     ref = om.mppi_iteration_oracle(spec, g["x0"], g["u_nom"], full)
     assert np.allclose(np.array(outs[0]["u_new"]), ref["u_new"], rtol=1e-11, atol=1e-11)
     assert outs[0]["rho"] == pytest.approx(ref["min_cost"], rel=1e-13)
+
+
+def test_gloo_world2_transport_agreement():
+    """A rank whose peer-buffer setup failed pulls every rank onto the NCCL path."""
+    outs = _run_world2(JM_AGREE=1)
+    assert [o["agree"] for o in outs] == [False, False]
+    assert [o["all_ok"] for o in outs] == [True, True]
+
+
+def test_shard_for():
+    assert jd.shard_for("weak", 100, 2, 4) == (200, 100)
+    assert jd.shard_for("strong", 10, 3, 4) == (8, 2)
+    with pytest.raises(ValueError):
+        jd.shard_for("linear", 10, 0, 2)
 
 
 def test_two_level_exchange_policy():

@@ -276,9 +276,11 @@ def test_closed_loop_f32_runs_and_stays_finite(gpu_device):
     assert rec.wall_time_per_iteration.shape == (30,)
 
 
-def test_sharded_loop_world1_matches_graph_loop(gpu_device):
+@pytest.mark.parametrize("scaling", ["weak", "strong"])
+def test_sharded_loop_world1_matches_graph_loop(scaling, gpu_device):
     """The multi-GPU stage split (rollout+record, all_gather, merge/plant) over a
-    one-rank NCCL group reproduces the single-GPU graph loop."""
+    one-rank NCCL group reproduces the single-GPU graph loop (weak: K per rank;
+    strong: config 3's K/N split, the whole K at world 1)."""
     import os
     import socket
 
@@ -296,7 +298,8 @@ def test_sharded_loop_world1_matches_graph_loop(gpu_device):
     try:
         task, cfg = jb.baseline_config(0, K=2048, T=60, steps=12)
         rec = jb.run_trial(task, cfg, seed=5, precision="f64")
-        loop = jd.ShardedLoop.create(task, cfg, 0, 1, 0, precision="f64")
+        loop = jd.ShardedLoop.create(task, cfg, 0, 1, 0, precision="f64", scaling=scaling)
+        assert loop.k_total == 2048 and loop.ctx.K == 2048
         loop.init(task.x0, cfg.u_init, 5, 64)
         for _ in range(12):
             loop.step()
