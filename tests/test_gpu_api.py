@@ -420,3 +420,49 @@ def test_sharded_loop_world1_two_level_exchange_matches_nccl(gpu_device):
                 assert np.array_equal(a, b)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("idx,K,T,steps", [(0, 512, 30, 24), (2, 256, 20, 20)])
+def test_closed_loop_multistep_matches_oracle_loop(idx, K, T, steps, gpu_device):
+    """The device-resident loop (harness.py:131-150) step by step against an
+    oracle loop: at every control step k the oracle iteration (the restatement
+    of controller.py:103-181) runs from the loop's state on the device sampler's
+    noise table for iteration k and the oracle's own warm-started nominal
+    (controller.py:96-100), and must give the loop's applied control u0
+    (harness.py:136); the loop's plant step must equal the oracle Euler step
+    with the emulated plant stream (Sigma_D, not c Sigma_D; the jump drawn and
+    the mark always drawn, harness.py:137-139)."""
+    from paper_1807_06108_b200 import engine
+
+    task, cfg = jb.baseline_config(idx, K=K, T=T, steps=steps)
+    seed = 11
+    rec = jb.run_trial(task, cfg, seed=seed, precision="f64")
+    assert not rec.diverged
+    ctx = engine.get_context(task.model, task.cost_model, cfg, precision="f64")
+    spec = om.spec_from_plugins(task.model, task.cost_model, cfg)
+    m, q = spec.m, spec.q
+    Lp = np.linalg.cholesky(np.asarray(cfg.sigma_d, float))
+    Lj = np.linalg.cholesky(np.asarray(cfg.sigma_j, float))
+    mu = np.asarray(cfg.mark_mean, float)
+    key = ps.stream_key(seed, 0)
+    jthr = ps.jump_threshold(cfg.nu * cfg.dt)
+    u_nom = np.tile(np.asarray(cfg.u_init, float), (T, 1))
+    for k in range(steps):
+        x = rec.states[k]
+        out = om.mppi_iteration_oracle(spec, x, u_nom, ctx.sample_noise(seed, k), np.float64)
+        u0 = om.clamp(spec, out["u_new"][0])
+        # (f64 both sides; the two nominal chains drift apart by rounding, amplified by the
+        # upright cartpole's instability: ~3e-8 after 18 steps -- the single-iteration gate is 1e-9)
+        assert rel_err(rec.controls[k], u0, floor=1e-6) <= 1e-6, k
+        w = ps.draw(key, ps.SLOT_PLANT, np.array([3 * k, 3 * k + 1, 3 * k + 2], np.uint32), np.uint32(0))
+        z = np.concatenate([ps.box_muller(w[0][0], w[1][0]), ps.box_muller(w[2][0], w[3][0])])
+        zm = np.concatenate([ps.box_muller(w[0][2], w[1][2]), ps.box_muller(w[2][2], w[3][2])])
+        jump = int(w[0][1]) < jthr
+        assert rec.jump_indicators[k] == int(jump), k
+        ed = Lp @ z[:m]
+        mk = mu + Lj @ zm[:q]
+        x1 = om.step_batch(spec, x[None], rec.controls[k], ed[None], mk[None], np.array([1.0 if jump else 0.0]),
+                           cfg.dt, np.float64)[0]
+        # (the device's Box-Muller runs on MUFU lg2/sqrt/sincos: plant normals to ~1e-6)
+        assert np.allclose(rec.states[k + 1], x1, rtol=2e-5, atol=2e-6), k
+        u_nom = om.warm_start_shift(out["u_new"], cfg.u_init)
