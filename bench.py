@@ -73,7 +73,6 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--profile", action="store_true", help="ncu mode: no clock settle, e2e or CPU legs")
-    p.add_argument("--_cpu-worker", dest="cpu_worker", default=None, help=argparse.SUPPRESS)
     return p.parse_args()
 
 
@@ -110,9 +109,8 @@ def _twin_reference_objects(jm, system, K, T):
     return model, cost, cfg, x0
 
 
-def cpu_worker(spec_json: str):
-    """Child process: time `iters` reference iterations; prints seconds per iteration."""
-    spec = json.loads(spec_json)
+def _cpu_step_fn(spec):
+    """One reference iteration (+ shift) on this process's share of the samples."""
     jm, kind = _ref_import()
     if jm is None:  # oracle port (numpy restatement) -- only when baseline/_ref is absent
         from oracle import mppi as om
@@ -137,34 +135,55 @@ def cpu_worker(spec_json: str):
                                        master_seed=spec["seed"])
             jm.warm_start_shift(seq, cfg.u_init)
 
-    one(0)  # warm-up
-    times = []
+    return one, kind
+
+
+def _cpu_proc(spec, barrier, times, kinds, slot):
+    """Worker of run_cpu: every step starts and ends at a barrier across all workers, so
+    worker 0's clock around (barrier, step, barrier) is the wall clock of the whole step."""
+    one, kind = _cpu_step_fn(spec)
+    kinds[slot] = 1 if kind == "reference" else 0
+    one(0)  # warm-up (imports, allocator)
     for it in range(spec["iters"]):
+        barrier.wait()
         t0 = time.perf_counter()
         one(it + 1)
-        times.append(time.perf_counter() - t0)
-    print(json.dumps({"sec": times, "kind": kind}))
+        barrier.wait()
+        if slot == 0:
+            times[it] = time.perf_counter() - t0
 
 
 def run_cpu(system, K, T, iters, procs, seed=0):
-    """Run `procs` single-thread reference processes concurrently, each on K/procs samples."""
-    env = dict(os.environ, OMP_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1", MKL_NUM_THREADS="1",
-               CUDA_VISIBLE_DEVICES="")
+    """`procs` single-thread reference processes, each on K/procs samples, stepping in lockstep:
+    the step time is the synchronised wall clock of the slowest process, not a per-process timer."""
+    import multiprocessing as mp
+
     kp = max(1, K // procs)
-    spec = json.dumps({"system": system, "K": kp, "T": T, "iters": iters, "seed": seed})
-    t0 = time.perf_counter()
-    ps = [subprocess.Popen([sys.executable, str(ROOT / "bench.py"), "--_cpu-worker", spec], env=env,
-                           stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True) for _ in range(procs)]
-    outs = [p.communicate() for p in ps]
-    wall = time.perf_counter() - t0
-    res = []
-    for (o, e), p in zip(outs, ps):
-        if p.returncode != 0:
-            raise RuntimeError(f"cpu worker failed: {e[-2000:]}")
-        res.append(json.loads(o.strip().splitlines()[-1]))
-    # per step all processes run concurrently: step time = max over processes
-    per_step = [max(r["sec"][i] for r in res) for i in range(iters)]
-    return per_step, res[0]["kind"], kp * procs, wall
+    spec = {"system": system, "K": kp, "T": T, "iters": iters, "seed": seed}
+    keys = {"OMP_NUM_THREADS": "1", "OPENBLAS_NUM_THREADS": "1", "MKL_NUM_THREADS": "1", "CUDA_VISIBLE_DEVICES": ""}
+    saved = {k: os.environ.get(k) for k in keys}
+    os.environ.update(keys)  # inherited by the spawned workers (fresh interpreters: no CUDA state)
+    try:
+        ctx = mp.get_context("spawn")
+        barrier = ctx.Barrier(procs)
+        times = ctx.Array("d", iters)
+        kinds = ctx.Array("i", procs)
+        t0 = time.perf_counter()
+        ps = [ctx.Process(target=_cpu_proc, args=(spec, barrier, times, kinds, i)) for i in range(procs)]
+        for p in ps:
+            p.start()
+        for p in ps:
+            p.join()
+        wall = time.perf_counter() - t0
+    finally:
+        for k, v in saved.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    if any(p.exitcode != 0 for p in ps):
+        raise RuntimeError(f"cpu worker failed (exit codes {[p.exitcode for p in ps]})")
+    return list(times), ("reference" if kinds[0] else "port"), kp * procs, wall
 
 
 def _host_cpu():
@@ -200,7 +219,7 @@ def reference_arm(a):
     val = Kdone * T / (ms * 1e-3)
     sample = (f"reference jump_mppi.mppi_iteration + warm_start_shift ({'baseline/_ref' if kind == 'reference' else 'oracle port'}), "
               f"control-channel twin of {a.workload}: {procs} processes x {Kdone // procs} samples x T={T} per step "
-              f"(K={Kdone} of {K}), 1 thread each")
+              f"(K={Kdone} of {K}), 1 thread each, lockstep (barrier per step: synchronised wall clock)")
     line = {
         "impl": "reference", "metric": "rollout state-steps/sec (K*T/s)", "value": val, "unit": "state-steps/s",
         "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -470,9 +489,6 @@ def ours_arm(a):
 
 def main():
     a = parse()
-    if a.cpu_worker:
-        cpu_worker(a.cpu_worker)
-        return
     if a.impl == "reference":
         reference_arm(a)
         return

@@ -1,0 +1,18 @@
+#!/bin/bash
+# round-2 ncu captures (one rollout launch each): cfg1, cfg3, cartpole 2^20 HBM, cfg0, cfg2
+mkdir -p gpurun_out/prof
+run() { # name, bench args
+  name=$1; shift
+  B="python bench.py --steps 2 --warmup 1 --profile --no-cpu-baseline --no-e2e $*"
+  $B > gpurun_out/prof/plain_$name.log 2>&1 || return
+  ncu --set full --clock-control none --import-source on -k regex:rollout_ -s 2 -c 1 -o gpurun_out/prof/$name $B > gpurun_out/prof/ncu_$name.log 2>&1
+  python tools/ncu_summary.py gpurun_out/prof/$name.ncu-rep > gpurun_out/prof/$name.summary.txt 2>&1
+  python tools/ncu_stalls.py gpurun_out/prof/$name.ncu-rep 60 > gpurun_out/prof/$name.stalls.txt 2>&1
+  python tools/ncu_lines.py gpurun_out/prof/$name.ncu-rep 70 > gpurun_out/prof/$name.lines.txt 2>&1 || true
+}
+run cfg1 --workload cfg1
+run cfg3 --workload cfg3
+run hbm_cart1M --workload cfg1 --noise hbm --samples 1048576
+run cfg0 --workload cfg0
+run cfg2 --workload cfg2
+ls -la gpurun_out/prof
