@@ -282,23 +282,35 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- ours
-def traffic_from_profiles(workload, precision, noise):
-    f = ROOT / "profiles" / "traffic.json"
-    if not f.exists():
-        return None
+def kernel_source_hash():
+    """sha256 over the CUDA sources of libjmppi.so (csrc/*.cu, *.cuh, internal.h, include/jmppi.h):
+    the stamp profiles/kernel_counters.json carries, so a capture of an older kernel is refused."""
+    import hashlib
+
+    h = hashlib.sha256()
+    src = ROOT / "paper_1807_06108_b200" / "csrc"
+    files = sorted(list(src.glob("*.cu")) + list(src.glob("*.cuh")) + [src / "internal.h", ROOT / "include" / "jmppi.h"])
+    for f in files:
+        h.update(f.name.encode())
+        h.update(f.read_bytes())
+    return h.hexdigest()[:16]
+
+
+def counters_from_profiles(workload, precision, noise, K):
+    """ncu counters of the rollout kernel of this workload (dram bytes, warp instructions per
+    launch) from profiles/kernel_counters.json -- only if the capture was taken from the kernel
+    sources of this tree (src_hash) and at this K; else (None, reason)."""
+    f = ROOT / "profiles" / "kernel_counters.json"
     try:
         d = json.loads(f.read_text())
-        return d.get(f"{workload}/{precision}/{noise}")
     except (ValueError, OSError):
-        return None
-
-
-def instructions_from_profiles(workload, precision, noise):
-    f = ROOT / "profiles" / "instructions.json"
-    try:
-        return json.loads(f.read_text()).get(f"{workload}/{precision}/{noise}")
-    except (ValueError, OSError):
-        return None
+        return None, "no profiles/kernel_counters.json"
+    e = d.get("captures", {}).get(f"{workload}/{precision}/{noise}/K={K}")
+    if e is None:
+        return None, "no ncu capture of this workload"
+    if e.get("src_hash") != kernel_source_hash():
+        return None, f"stale: captured at kernel sources {e.get('src_hash')}, this tree is {kernel_source_hash()}"
+    return e, None
 
 
 def ours_arm(a):
@@ -401,8 +413,8 @@ def ours_arm(a):
     achieved = flops / (rms * 1e-3) / 1e12
     peak = peaks["fp32_tflops"]
     roof = {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-            "traffic": traffic_from_profiles(a.workload, a.precision, a.noise),
-            "kernel": "rollout_kernel", "kernel_ms": rms, "kernel_share_of_step": rms / ms,
+            "traffic": None,
+            "kernel": ctx.lib.jm_kernel_name(ctx.h).decode(), "kernel_ms": rms, "kernel_share_of_step": rms / ms,
             "flops_per_state_step": FLOPS_PER_STATE_STEP[system],
             "peak_source": "live FFMA microbenchmark (jm_microbench), no FP32 entry in MEASURED_PEAKS.json",
             "mufu_peak_tops": peaks["mufu_tops"], "fp64_peak_tflops": peaks["fp64_tflops"]}
@@ -415,7 +427,13 @@ def ours_arm(a):
     # issue-slot view of the same kernel: warp-instructions per state-step from the
     # committed ncu capture, and the rate at which 4 schedulers/SM issuing every
     # cycle would retire them -- what bounds this FP32-light, latency-bound loop
-    ninst = instructions_from_profiles(a.workload, a.precision, a.noise) if a.samples is None else None
+    cap, why = counters_from_profiles(a.workload, a.precision, a.noise, K)
+    if cap is None:
+        roof["traffic_note"] = why
+    else:
+        roof["traffic"] = cap.get("dram_bytes")
+        roof["traffic_source"] = cap.get("source")
+    ninst = cap.get("warp_instructions") if cap else None
     if ninst:
         ips = ninst / (K * T / 32.0)
         import torch
@@ -425,7 +443,7 @@ def ours_arm(a):
         roof["issue_slots"] = {"warp_instructions_per_state_step": ips, "ceiling_state_steps_per_s": ceil,
                                "achieved_state_steps_per_s": K * T / (rms * 1e-3),
                                "frac": K * T / (rms * 1e-3) / ceil,
-                               "source": "smsp__inst_executed of profiles/r1 capture; 4 issue slots/SM/cycle"}
+                               "source": f"smsp__inst_executed of {cap.get('source')}; 4 issue slots/SM/cycle"}
     if hbm:
         bpss = HBM_BYTES_PER_STATE_STEP[system] * (2 if a.precision == "f64" else 1)
         gbs = bpss * K * T / (rms * 1e-3) / 1e9
@@ -455,19 +473,24 @@ def ours_arm(a):
         ctrl = jb.initial_controller_state(cfg)
         x0 = np.asarray(task.x0, float)
         e2e = []
+        b0 = (C.c_int64(), C.c_int64())
+        b1 = (C.c_int64(), C.c_int64())
         for i in range(a.warmup + a.steps):
+            if i == a.warmup:
+                lib.jm_transfer_bytes(C.byref(b0[0]), C.byref(b0[1]))
             t0 = time.perf_counter()
             seq, diag = jb.mppi_iteration(ctrl, task.model, task.cost_model, x0, 0, precision=a.precision,
                                           device=local)
             ctrl = jb.ControllerState(jb.warm_start_shift(seq, cfg.u_init), ctrl.iteration_index + 1, cfg)
             e2e.append(time.perf_counter() - t0)
         e_ms = 1e3 * statistics.mean(e2e[a.warmup:])
-        m = cfg.control_dim
-        # one staged H2D of [x0|u_nom|mapping|u_init] and one D2H of
-        # [u_new|norms|diag|status|u_shift] (csrc/internal.h layout); the
-        # per-sample weights stay on the GPU until UpdateDiagnostics.weights is read
-        h2d = 8 * (48 + T * m)
-        d2h = 8 * (2 * T * m + T + 6)
+        # bytes the library moved during the timed iterations (jm_transfer_bytes counts every
+        # copy it issues): one staged block [x0|u_nom|mapping|u_init] in and one block
+        # [u_new|norms|diag|status|u_shift] out per iteration; the per-sample weights stay on the
+        # GPU until UpdateDiagnostics.weights is read
+        lib.jm_transfer_bytes(C.byref(b1[0]), C.byref(b1[1]))
+        h2d = (b1[0].value - b0[0].value) // a.steps
+        d2h = (b1[1].value - b0[1].value) // a.steps
         line["e2e"] = {"value": K * T / (e_ms * 1e-3), "unit": "state-steps/s", "h2d_bytes_per_step": h2d,
                        "d2h_bytes_per_step": d2h, "ms_per_step": e_ms,
                        "path": "paper_1807_06108_b200.mppi_iteration + warm_start_shift (numpy in/out), "

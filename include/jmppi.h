@@ -339,6 +339,10 @@ int jm_microbench(int device, double* fp32_tflops, double* mufu_tops, double* fp
  * times): "<kernel>/<noise>/<shape>/<precision>", e.g.
  * "rollout_kernel/philox/single_wave_smem/f32" (ncu -k regex:<kernel>). */
 const char* jm_kernel_name(const jm_ctx* ctx);
+/* Cumulative bytes this process has moved host->device / device->host through the
+ * library (explicit copies and the drop-in graph's zero-copy blocks); bench.py's
+ * e2e h2d/d2h_bytes_per_step are differences of these counters. */
+int jm_transfer_bytes(int64_t* h2d, int64_t* d2h);
 /* Number of kernel launches one jm_iteration_host / loop step enqueues. */
 int jm_launches_per_iteration(const jm_ctx* ctx, int32_t* iteration, int32_t* loop_step);
 

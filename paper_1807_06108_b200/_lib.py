@@ -119,6 +119,7 @@ SIGNATURES = {
     "jm_bench_iteration": (C.c_int, [_vp, _i32, _i64, _pd, _pd]),
     "jm_kernel_name": (C.c_char_p, [_vp]),
     "jm_launches_per_iteration": (C.c_int, [_vp, _pi32, _pi32]),
+    "jm_transfer_bytes": (C.c_int, [_pi64, _pi64]),
 }
 
 _lock = threading.Lock()

@@ -21,6 +21,22 @@ namespace {
 
 thread_local std::string g_err;
 
+// host<->device copy counters (jm_transfer_bytes): every explicit copy the library issues goes
+// through these wrappers; the drop-in graph's zero-copy blocks are counted in dropin_launch
+std::atomic<long long> g_h2d{0}, g_d2h{0};
+inline void count_xfer(size_t n, cudaMemcpyKind k) {
+  if (k == cudaMemcpyHostToDevice) g_h2d += (long long)n;
+  if (k == cudaMemcpyDeviceToHost) g_d2h += (long long)n;
+}
+inline cudaError_t xferAsync(void* d, const void* s, size_t n, cudaMemcpyKind k, cudaStream_t st) {
+  count_xfer(n, k);
+  return cudaMemcpyAsync(d, s, n, k, st);
+}
+inline cudaError_t xferSync(void* d, const void* s, size_t n, cudaMemcpyKind k) {
+  count_xfer(n, k);
+  return cudaMemcpy(d, s, n, k);
+}
+
 int fail(jm_ctx* c, int code, const char* fmt, ...) {
   char buf[512];
   va_list ap;
@@ -325,6 +341,10 @@ int dropin_launch(jm_ctx* ctx, const double* x0, const double* u_nom, const doub
   st[0] = 0;
   st[1] = 0;  // done word, raised by the finalize after its last output
   CK(cudaGraphLaunch(ge, ctx->stream));
+  // (zero-copy over PCIe: copy_block_kernel reads [x0|u_nom|mapping|u_init], the finalize
+  // writes [u_new|norms|diag|status|u_shift] into the pinned block)
+  g_h2d += (long long)(sizeof(double) * ctx->off_unew());
+  g_d2h += (long long)(sizeof(double) * (ctx->off_rec() - ctx->off_unew()));
   // spin on the done word (a stream synchronisation wakes the host several
   // microseconds later); fall back to the synchronisation after 2 s so a
   // faulting launch still reports its error
@@ -533,14 +553,14 @@ int jm_create(const jm_model_desc* model, const jm_cost_desc* cost, const jm_mpp
     std::vector<float> agf(ag.begin(), ag.end());
     e = cudaMalloc(&ctx->d_lin_d, sizeof(double) * ag.size());
     if (e == cudaSuccess) e = cudaMalloc(&ctx->d_lin_f, sizeof(float) * agf.size());
-    if (e == cudaSuccess) e = cudaMemcpy(ctx->d_lin_d, ag.data(), sizeof(double) * ag.size(), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(ctx->d_lin_f, agf.data(), sizeof(float) * agf.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = xferSync(ctx->d_lin_d, ag.data(), sizeof(double) * ag.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = xferSync(ctx->d_lin_f, agf.data(), sizeof(float) * agf.size(), cudaMemcpyHostToDevice);
   }
   if (e == cudaSuccess && ctx->jthr) {
     const std::vector<uint32_t> S = gap_table(p_event, ctx->T, &ctx->gap_inv);
     ctx->gap_n = (int)S.size();
     e = cudaMalloc(&ctx->d_gap, S.size() * sizeof(uint32_t));
-    if (e == cudaSuccess) e = cudaMemcpy(ctx->d_gap, S.data(), S.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = xferSync(ctx->d_gap, S.data(), S.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
   }
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = ctx->eng->configure(ctx);
@@ -655,7 +675,7 @@ int jm_iteration_host(jm_ctx* ctx, const double* x0, const double* u_nom, uint64
   std::memcpy(hs + ctx->off_unom(), u_nom, sizeof(double) * TM);
   if (mapping) std::memcpy(hs + ctx->off_map(), mapping, sizeof(double) * M * M);
   if (u_init) std::memcpy(hs + ctx->off_uinit(), u_init, sizeof(double) * M);
-  CK(cudaMemcpyAsync(ds, hs, sizeof(double) * ctx->off_unew(), cudaMemcpyHostToDevice, ctx->stream));
+  CK(xferAsync(ds, hs, sizeof(double) * ctx->off_unew(), cudaMemcpyHostToDevice, ctx->stream));
   jm::RolloutCall rc;
   rc.x0 = ds + ctx->off_x0();
   rc.u_nom = ds + ctx->off_unom();
@@ -665,12 +685,12 @@ int jm_iteration_host(jm_ctx* ctx, const double* x0, const double* u_nom, uint64
   if (hbm) {
     const size_t eb = (size_t)TM * K * ctx->real_size;
     if (!ctx->d_hbm_eps) CK(cudaMalloc(&ctx->d_hbm_eps, eb));
-    CK(cudaMemcpyAsync(ctx->d_hbm_eps, eps_c, eb, cudaMemcpyHostToDevice, ctx->stream));
+    CK(xferAsync(ctx->d_hbm_eps, eps_c, eb, cudaMemcpyHostToDevice, ctx->stream));
     rc.eps_in = ctx->d_hbm_eps;
     if (jump && ctx->model.jump_channel == JM_JUMP_STATE) {
       const size_t jb = (size_t)T * ctx->Q * K * ctx->real_size;
       if (!ctx->d_hbm_jump) CK(cudaMalloc(&ctx->d_hbm_jump, jb));
-      CK(cudaMemcpyAsync(ctx->d_hbm_jump, jump, jb, cudaMemcpyHostToDevice, ctx->stream));
+      CK(xferAsync(ctx->d_hbm_jump, jump, jb, cudaMemcpyHostToDevice, ctx->stream));
       rc.jump_in = ctx->d_hbm_jump;
     }
   }
@@ -693,20 +713,20 @@ int jm_iteration_host(jm_ctx* ctx, const double* x0, const double* u_nom, uint64
   if (weights_stash && !handle) {
     const int rs = stash_acquire(ctx, &handle);
     if (rs != JM_OK) return rs;
-    CK(cudaMemcpyAsync(ctx->stash[handle - 1], ctx->d_costs, sizeof(double) * K, cudaMemcpyDeviceToDevice,
+    CK(xferAsync(ctx->stash[handle - 1], ctx->d_costs, sizeof(double) * K, cudaMemcpyDeviceToDevice,
                        ctx->stream));
   }
   const size_t out_n = ctx->off_rec() - ctx->off_unew();
-  CK(cudaMemcpyAsync(hs + ctx->off_unew(), ds + ctx->off_unew(), sizeof(double) * out_n,
+  CK(xferAsync(hs + ctx->off_unew(), ds + ctx->off_unew(), sizeof(double) * out_n,
                      cudaMemcpyDeviceToHost, ctx->stream));
-  if (costs) CK(cudaMemcpyAsync(ctx->h_big, ctx->d_costs, sizeof(double) * K, cudaMemcpyDeviceToHost, ctx->stream));
+  if (costs) CK(xferAsync(ctx->h_big, ctx->d_costs, sizeof(double) * K, cudaMemcpyDeviceToHost, ctx->stream));
   if (weights)
-    CK(cudaMemcpyAsync(ctx->h_big + K, wdev, sizeof(double) * K, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(xferAsync(ctx->h_big + K, wdev, sizeof(double) * K, cudaMemcpyDeviceToHost, ctx->stream));
   if (states)
-    CK(cudaMemcpyAsync(states, ctx->d_states, sizeof(double) * (size_t)K * (T + 1) * N,
+    CK(xferAsync(states, ctx->d_states, sizeof(double) * (size_t)K * (T + 1) * N,
                        cudaMemcpyDeviceToHost, ctx->stream));
   if (diverged_step)
-    CK(cudaMemcpyAsync(diverged_step, ctx->d_div, sizeof(int64_t) * K, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(xferAsync(diverged_step, ctx->d_div, sizeof(int64_t) * K, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   const int32_t status = *reinterpret_cast<int32_t*>(hs + ctx->off_status());
   const DiagOut* dg = reinterpret_cast<const DiagOut*>(hs + ctx->off_diag());
@@ -734,7 +754,7 @@ int jm_upload_inputs(jm_ctx* ctx, const double* x0, const double* u_nom) {
   CK(cudaSetDevice(ctx->device));
   std::memcpy(ctx->h_small + ctx->off_x0(), x0, sizeof(double) * ctx->N);
   std::memcpy(ctx->h_small + ctx->off_unom(), u_nom, sizeof(double) * ctx->TM);
-  CK(cudaMemcpyAsync(ctx->d_small, ctx->h_small, sizeof(double) * ctx->off_map(), cudaMemcpyHostToDevice,
+  CK(xferAsync(ctx->d_small, ctx->h_small, sizeof(double) * ctx->off_map(), cudaMemcpyHostToDevice,
                      ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   return JM_OK;
@@ -751,6 +771,12 @@ int jm_iteration_dropin(jm_ctx* ctx, const double* x0, const double* u_nom, cons
   return JM_OK;
 }
 
+int jm_transfer_bytes(int64_t* h2d, int64_t* d2h) {
+  if (h2d) *h2d = (int64_t)g_h2d.load();
+  if (d2h) *d2h = (int64_t)g_d2h.load();
+  return JM_OK;
+}
+
 int64_t jm_dropin_doubles(const jm_ctx* ctx) { return ctx ? (int64_t)(ctx->off_rec() - ctx->off_unew()) : 0; }
 
 int jm_stash_fetch(jm_ctx* ctx, uint64_t handle, double min_cost, double normaliser, double* host) {
@@ -759,9 +785,9 @@ int jm_stash_fetch(jm_ctx* ctx, uint64_t handle, double min_cost, double normali
   // weights of the stashed costs (controller.py:62-71) with that iteration's rho and Z
   DiagOut* dd = reinterpret_cast<DiagOut*>(ctx->d_small + ctx->off_rec());  // scratch slot
   DiagOut hd{min_cost, 0.0, normaliser, 0};
-  CK(cudaMemcpyAsync(dd, &hd, sizeof(hd), cudaMemcpyHostToDevice, ctx->stream));
+  CK(xferAsync(dd, &hd, sizeof(hd), cudaMemcpyHostToDevice, ctx->stream));
   CK(launch_weights(ctx, ctx->stash[handle - 1], dd, ctx->d_weights));
-  CK(cudaMemcpyAsync(host, ctx->d_weights, sizeof(double) * ctx->K, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(xferAsync(host, ctx->d_weights, sizeof(double) * ctx->K, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   return JM_OK;
 }
@@ -856,11 +882,11 @@ int jm_shift_host(int device, int32_t T, int32_t m, const double* u, const doubl
     s_cap = need;
   }
   double *d_u = s_buf, *d_o = s_buf + TM, *d_i = s_buf + 2 * TM;
-  CK(cudaMemcpy(d_u, u, sizeof(double) * TM, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(d_i, u_init, sizeof(double) * m, cudaMemcpyHostToDevice));
+  CK(xferSync(d_u, u, sizeof(double) * TM, cudaMemcpyHostToDevice));
+  CK(xferSync(d_i, u_init, sizeof(double) * m, cudaMemcpyHostToDevice));
   jm::shift_kernel<<<(TM + 127) / 128, 128>>>(d_u, d_i, T, m, d_o);
   CK(cudaGetLastError());
-  CK(cudaMemcpy(out, d_o, sizeof(double) * TM, cudaMemcpyDeviceToHost));
+  CK(xferSync(out, d_o, sizeof(double) * TM, cudaMemcpyDeviceToHost));
   return JM_OK;
 }
 
@@ -872,12 +898,12 @@ int jm_compute_weights_host(int device, int64_t K, const double* costs, double l
   CK(dalloc(&d_c, (size_t)K));
   CK(dalloc(&d_w, (size_t)K));
   CK(dalloc(&d_o, 2));
-  CK(cudaMemcpy(d_c, costs, sizeof(double) * K, cudaMemcpyHostToDevice));
+  CK(xferSync(d_c, costs, sizeof(double) * K, cudaMemcpyHostToDevice));
   cw_kernel<<<1, 1024>>>(d_c, K, 1.0 / lambda_, d_w, d_o);
   CK(cudaGetLastError());
   double o[2];
-  CK(cudaMemcpy(weights, d_w, sizeof(double) * K, cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(o, d_o, sizeof(o), cudaMemcpyDeviceToHost));
+  CK(xferSync(weights, d_w, sizeof(double) * K, cudaMemcpyDeviceToHost));
+  CK(xferSync(o, d_o, sizeof(o), cudaMemcpyDeviceToHost));
   dfree(d_c);
   dfree(d_w);
   dfree(d_o);
@@ -900,21 +926,21 @@ int jm_update_controls_host(int device, int64_t K, int32_t T, int32_t m, const d
   CK(dalloc(&d_e, (size_t)K * TM));
   CK(dalloc(&d_u, (size_t)TM));
   CK(dalloc(&d_n, (size_t)TM));
-  CK(cudaMemcpy(d_c, costs, sizeof(double) * K, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(d_e, eps_c, sizeof(double) * K * TM, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(d_u, u_nom, sizeof(double) * TM, cudaMemcpyHostToDevice));
+  CK(xferSync(d_c, costs, sizeof(double) * K, cudaMemcpyHostToDevice));
+  CK(xferSync(d_e, eps_c, sizeof(double) * K * TM, cudaMemcpyHostToDevice));
+  CK(xferSync(d_u, u_nom, sizeof(double) * TM, cudaMemcpyHostToDevice));
   if (mapping) {
     CK(dalloc(&d_m, (size_t)m * m));
-    CK(cudaMemcpy(d_m, mapping, sizeof(double) * m * m, cudaMemcpyHostToDevice));
+    CK(xferSync(d_m, mapping, sizeof(double) * m * m, cudaMemcpyHostToDevice));
   }
   cw_kernel<<<1, 1024>>>(d_c, K, 1.0 / lambda_, d_w, d_o);
   CK(cudaGetLastError());
   wavg_kernel<<<(T + 127) / 128, 128>>>(d_w, d_e, K, TM, m, 1.0 / std::sqrt(dt), d_u, d_m, d_n);
   CK(cudaGetLastError());
   double o[2];
-  CK(cudaMemcpy(o, d_o, sizeof(o), cudaMemcpyDeviceToHost));
-  CK(cudaMemcpy(u_new, d_n, sizeof(double) * TM, cudaMemcpyDeviceToHost));
-  if (weights) CK(cudaMemcpy(weights, d_w, sizeof(double) * K, cudaMemcpyDeviceToHost));
+  CK(xferSync(o, d_o, sizeof(o), cudaMemcpyDeviceToHost));
+  CK(xferSync(u_new, d_n, sizeof(double) * TM, cudaMemcpyDeviceToHost));
+  if (weights) CK(xferSync(weights, d_w, sizeof(double) * K, cudaMemcpyDeviceToHost));
   for (double* p : {d_c, d_w, d_o, d_e, d_u, d_n, d_m}) dfree(p);
   if (o[0] == INFINITY) return fail(nullptr, JM_ERR_NO_VIABLE, "no viable rollout");
   return JM_OK;
@@ -958,10 +984,10 @@ int jm_sample_noise_host(jm_ctx* ctx, uint64_t seed, uint64_t iteration, double*
   na.eps_c = d_ec;
   na.ind = d_ind;
   CK(ctx->eng->noise(ctx, na));
-  if (eps_d) CK(cudaMemcpyAsync(eps_d, d_ed, sizeof(double) * KT * ctx->M, cudaMemcpyDeviceToHost, ctx->stream));
-  if (eps_j) CK(cudaMemcpyAsync(eps_j, d_ej, sizeof(double) * KT * ctx->Q, cudaMemcpyDeviceToHost, ctx->stream));
-  if (eps_c) CK(cudaMemcpyAsync(eps_c, d_ec, sizeof(double) * KT * ctx->M, cudaMemcpyDeviceToHost, ctx->stream));
-  if (indicators) CK(cudaMemcpyAsync(indicators, d_ind, sizeof(int64_t) * KT, cudaMemcpyDeviceToHost, ctx->stream));
+  if (eps_d) CK(xferAsync(eps_d, d_ed, sizeof(double) * KT * ctx->M, cudaMemcpyDeviceToHost, ctx->stream));
+  if (eps_j) CK(xferAsync(eps_j, d_ej, sizeof(double) * KT * ctx->Q, cudaMemcpyDeviceToHost, ctx->stream));
+  if (eps_c) CK(xferAsync(eps_c, d_ec, sizeof(double) * KT * ctx->M, cudaMemcpyDeviceToHost, ctx->stream));
+  if (indicators) CK(xferAsync(indicators, d_ind, sizeof(int64_t) * KT, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   for (void* p : {(void*)d_ed, (void*)d_ej, (void*)d_ec, (void*)d_ind}) dfree(p);
   return JM_OK;
@@ -1005,7 +1031,7 @@ int jm_loop_init(jm_ctx* ctx, const double* x0, const double* u_init, uint64_t s
         CK(dalloc(&ctx->d_self_push, (size_t)jm_peer_buffer_doubles(ctx, 1)));
         CK(dalloc(&ctx->d_self_base, 1));
         const unsigned long long base = reinterpret_cast<unsigned long long>(ctx->d_self_push);
-        CK(cudaMemcpy(ctx->d_self_base, &base, sizeof(base), cudaMemcpyHostToDevice));
+        CK(xferSync(ctx->d_self_base, &base, sizeof(base), cudaMemcpyHostToDevice));
       }
     }
     CK(dalloc(&ctx->d_hist, (size_t)(max_steps + 1) * N + (size_t)max_steps * M));
@@ -1043,9 +1069,9 @@ int jm_loop_init(jm_ctx* ctx, const double* x0, const double* u_init, uint64_t s
   CK(cudaMemsetAsync(ctx->d_counter, 0, sizeof(unsigned int), s));
   if (ctx->d_self_push)  // epochs restart at 1: clear the flags of the previous run
     CK(cudaMemsetAsync(ctx->d_self_push, 0, sizeof(double) * (size_t)jm_peer_buffer_doubles(ctx, 1), s));
-  CK(cudaMemcpyAsync(ctx->d_loop, &h, sizeof(h), cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(ctx->d_loop_unom, unom.data(), sizeof(double) * TM, cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(ctx->d_hist, x0, sizeof(double) * N, cudaMemcpyHostToDevice, s));
+  CK(xferAsync(ctx->d_loop, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+  CK(xferAsync(ctx->d_loop_unom, unom.data(), sizeof(double) * TM, cudaMemcpyHostToDevice, s));
+  CK(xferAsync(ctx->d_hist, x0, sizeof(double) * N, cudaMemcpyHostToDevice, s));
   CK(cudaStreamSynchronize(s));
   return capture_loop_graph(ctx);
 }
@@ -1156,7 +1182,7 @@ int jm_loop_read(jm_ctx* ctx, double* x_out, uint64_t* iteration_out, int32_t* s
   if (!ctx || !ctx->d_loop) return fail(ctx, JM_ERR_VALUE, "loop not initialised");
   CK(cudaSetDevice(ctx->device));
   LoopState h{};
-  CK(cudaMemcpyAsync(&h, ctx->d_loop, sizeof(h), cudaMemcpyDeviceToHost, ctx->own_stream));
+  CK(xferAsync(&h, ctx->d_loop, sizeof(h), cudaMemcpyDeviceToHost, ctx->own_stream));
   CK(cudaStreamSynchronize(ctx->own_stream));
   if (x_out) std::memcpy(x_out, h.x, sizeof(double) * ctx->N);
   if (iteration_out) *iteration_out = h.iteration;
@@ -1170,7 +1196,7 @@ int jm_loop_timeline(jm_ctx* ctx, int32_t steps, uint64_t* out) {
   if (!ctx || !out || steps < 1 || steps > ctx->loop_cap) return fail(ctx, JM_ERR_VALUE, "bad arguments");
   if (!ctx->d_tl) return fail(ctx, JM_ERR_UNSUPPORTED, "loop timeline off (set JM_TIMELINE=1 before jm_loop_init)");
   CK(cudaStreamSynchronize(ctx->stream));
-  CK(cudaMemcpy(out, ctx->d_tl, sizeof(uint64_t) * (size_t)steps * jm::kTlSlots, cudaMemcpyDeviceToHost));
+  CK(xferSync(out, ctx->d_tl, sizeof(uint64_t) * (size_t)steps * jm::kTlSlots, cudaMemcpyDeviceToHost));
   return JM_OK;
 }
 
@@ -1180,11 +1206,11 @@ int jm_loop_history(jm_ctx* ctx, int32_t steps, double* states, double* controls
   CK(cudaStreamSynchronize(ctx->stream));
   CK(cudaStreamSynchronize(ctx->own_stream));
   const int N = ctx->N, M = ctx->M;
-  if (states) CK(cudaMemcpy(states, ctx->d_hist, sizeof(double) * (size_t)(steps + 1) * N, cudaMemcpyDeviceToHost));
+  if (states) CK(xferSync(states, ctx->d_hist, sizeof(double) * (size_t)(steps + 1) * N, cudaMemcpyDeviceToHost));
   if (controls)
-    CK(cudaMemcpy(controls, ctx->d_hist + (size_t)(ctx->loop_cap + 1) * N, sizeof(double) * (size_t)steps * M,
+    CK(xferSync(controls, ctx->d_hist + (size_t)(ctx->loop_cap + 1) * N, sizeof(double) * (size_t)steps * M,
                   cudaMemcpyDeviceToHost));
-  if (jumps) CK(cudaMemcpy(jumps, ctx->d_hist_jumps, sizeof(int64_t) * (size_t)steps, cudaMemcpyDeviceToHost));
+  if (jumps) CK(xferSync(jumps, ctx->d_hist_jumps, sizeof(int64_t) * (size_t)steps, cudaMemcpyDeviceToHost));
   return JM_OK;
 }
 
@@ -1198,16 +1224,16 @@ int jm_closed_loop_host(jm_ctx* ctx, const double* x0, const double* u_init, uin
     if (r != JM_OK) return r;
   }
   LoopState h{};
-  CK(cudaMemcpyAsync(&h, ctx->d_loop, sizeof(h), cudaMemcpyDeviceToHost, ctx->own_stream));
+  CK(xferAsync(&h, ctx->d_loop, sizeof(h), cudaMemcpyDeviceToHost, ctx->own_stream));
   const int N = ctx->N, M = ctx->M;
   std::vector<double> hs((size_t)(steps + 1) * N), hc((size_t)steps * M);
   std::vector<int64_t> hj((size_t)steps);
   std::vector<uint64_t> ht(2 * (size_t)ctx->loop_cap);
-  CK(cudaMemcpyAsync(hs.data(), ctx->d_hist, sizeof(double) * hs.size(), cudaMemcpyDeviceToHost, ctx->own_stream));
-  CK(cudaMemcpyAsync(hc.data(), ctx->d_hist + (size_t)(ctx->loop_cap + 1) * N, sizeof(double) * hc.size(),
+  CK(xferAsync(hs.data(), ctx->d_hist, sizeof(double) * hs.size(), cudaMemcpyDeviceToHost, ctx->own_stream));
+  CK(xferAsync(hc.data(), ctx->d_hist + (size_t)(ctx->loop_cap + 1) * N, sizeof(double) * hc.size(),
                      cudaMemcpyDeviceToHost, ctx->own_stream));
-  CK(cudaMemcpyAsync(hj.data(), ctx->d_hist_jumps, sizeof(int64_t) * hj.size(), cudaMemcpyDeviceToHost, ctx->own_stream));
-  CK(cudaMemcpyAsync(ht.data(), ctx->d_hist_t, sizeof(uint64_t) * ht.size(), cudaMemcpyDeviceToHost, ctx->own_stream));
+  CK(xferAsync(hj.data(), ctx->d_hist_jumps, sizeof(int64_t) * hj.size(), cudaMemcpyDeviceToHost, ctx->own_stream));
+  CK(xferAsync(ht.data(), ctx->d_hist_t, sizeof(uint64_t) * ht.size(), cudaMemcpyDeviceToHost, ctx->own_stream));
   CK(cudaStreamSynchronize(ctx->own_stream));
   // steps actually executed (h.step), then the reference's post-divergence fill
   // (harness.py:144-148): states[k+1:] = states[k], controls[k+1:] = 0.
@@ -1283,9 +1309,9 @@ int jm_batch_loop_host(jm_ctx* ctx, int32_t trials, const double* x0, const doub
     for (int i = 0; i < N; ++i) hs0[(size_t)b * (S + 1) * N + i] = x0[(size_t)b * N + i];
   }
   cudaStream_t s = ctx->own_stream;
-  if (e == cudaSuccess) e = cudaMemcpyAsync(d_loop, hl.data(), sizeof(jm::LoopState) * B, cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(d_unom, unom.data(), sizeof(double) * unom.size(), cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(d_hs, hs0.data(), sizeof(double) * hs0.size(), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = xferAsync(d_loop, hl.data(), sizeof(jm::LoopState) * B, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = xferAsync(d_unom, unom.data(), sizeof(double) * unom.size(), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = xferAsync(d_hs, hs0.data(), sizeof(double) * hs0.size(), cudaMemcpyHostToDevice, s);
   // one control step of every trial = the two loop kernels with grid.y = B, captured once
   cudaGraph_t g = nullptr;
   cudaGraphExec_t ge = nullptr;
@@ -1325,11 +1351,11 @@ int jm_batch_loop_host(jm_ctx* ctx, int32_t trials, const double* x0, const doub
   std::vector<double> hs((size_t)B * (S + 1) * N), hc((size_t)B * S * M);
   std::vector<int64_t> hj((size_t)B * S);
   std::vector<uint64_t> ht((size_t)B * 2 * S);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(hl.data(), d_loop, sizeof(jm::LoopState) * B, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(hs.data(), d_hs, sizeof(double) * hs.size(), cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(hc.data(), d_hc, sizeof(double) * hc.size(), cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(hj.data(), d_hj, sizeof(int64_t) * hj.size(), cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(ht.data(), d_ht, sizeof(uint64_t) * ht.size(), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = xferAsync(hl.data(), d_loop, sizeof(jm::LoopState) * B, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = xferAsync(hs.data(), d_hs, sizeof(double) * hs.size(), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = xferAsync(hc.data(), d_hc, sizeof(double) * hc.size(), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = xferAsync(hj.data(), d_hj, sizeof(int64_t) * hj.size(), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = xferAsync(ht.data(), d_ht, sizeof(uint64_t) * ht.size(), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (ge) cudaGraphExecDestroy(ge);
   if (g) cudaGraphDestroy(g);

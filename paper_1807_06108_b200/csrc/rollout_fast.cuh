@@ -34,6 +34,10 @@
 
 namespace jm {
 
+#ifndef JM_HBM_DEPTH
+#define JM_HBM_DEPTH 2
+#endif
+constexpr int kHbmDepth = JM_HBM_DEPTH;  // HBM mode: noise groups in flight ahead of the one being consumed
 constexpr float kSparseCut = 55.0f;  // (S - rho) / lambda above which N drops the sample (w < e^-55)
 
 template <int SPT, typename Real>
@@ -858,32 +862,32 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
         constexpr int GE = GS * M, GJ = (JM == 1) ? GS * Q : 1;
         (void)EW;
         (void)JWD;
-        V e0[GE], e1[GE], j0[GJ], j1[GJ];
-        load_group(0, e0, j0);
-        load_group(GS, e1, j1);
-        for (int t0 = 0; t0 < T; t0 += GS) {
-          V en[GE], jn[GJ];
-          load_group(t0 + 2 * GS, en, jn);  // (clamped inside the horizon)
+        // a ring of kHbmDepth + 1 register buffers, the group loop unrolled over the ring so
+        // a buffer's role is a compile-time index (no register rotation moves): group g runs
+        // from buffer g % NB while group g + kHbmDepth is loaded into the buffer group g - 1
+        // has just released
+        constexpr int NB = kHbmDepth + 1;
+        V eb[NB][GE], jb[NB][GJ];
 #pragma unroll
-          for (int s2 = 0; s2 < GS; ++s2) {
-            if (GS == 1 || t0 + s2 < T) {
-              V sj[Q];
-              if (JM == 1) {
+        for (int d = 0; d < kHbmDepth; ++d) load_group(d * GS, eb[d], jb[d]);
+        for (int t0 = 0; t0 < T; t0 += NB * GS) {
 #pragma unroll
-                for (int i = 0; i < Q; ++i) sj[i] = jscale * j0[s2 * Q + i];
+          for (int r = 0; r < NB; ++r) {
+            const int tg = t0 + r * GS;
+            if (tg < T) {
+              load_group(tg + kHbmDepth * GS, eb[(r + kHbmDepth) % NB], jb[(r + kHbmDepth) % NB]);  // (clamped inside the horizon)
+#pragma unroll
+              for (int s2 = 0; s2 < GS; ++s2) {
+                if (GS == 1 || tg + s2 < T) {
+                  V sj[Q];
+                  if (JM == 1) {
+#pragma unroll
+                    for (int i = 0; i < Q; ++i) sj[i] = jscale * jb[r][s2 * Q + i];
+                  }
+                  step(tg + s2, eb[r] + s2 * M, sj, JM == 1 && hj);
+                }
               }
-              step(t0 + s2, e0 + s2 * M, sj, JM == 1 && hj);
             }
-          }
-#pragma unroll
-          for (int i = 0; i < GE; ++i) {
-            e0[i] = e1[i];
-            e1[i] = en[i];
-          }
-#pragma unroll
-          for (int i = 0; i < GJ; ++i) {
-            j0[i] = j1[i];
-            j1[i] = jn[i];
           }
         }
       }

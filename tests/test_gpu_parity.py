@@ -59,9 +59,22 @@ def test_f64_fed_noise_matches_reference(name, gpu_device):
 def test_f32_fed_noise_gate(name, gpu_device):
     g = load_golden(name)
     if name == "r_divergence":
-        pytest.skip("non-finite noise is a float64 semantics case (covered by the f64 test)")
+        pytest.skip("its 1e200 entry is not a float32 value; r_divergence_f32 is the fp32 divergence case")
     seq, diag, rollouts = run_golden(g, "f32")
     costs = np.array([r.cost for r in rollouts])
+    if name == "r_quadrotor_pitch_floor":
+        # cos(pitch) ~ 4e-7 sits below float32's resolution of the angle (ulp(pi/2) = 1.2e-7), so
+        # the band exit differs from the float64 reference by construction; what fp32 must show is
+        # that the floor is applied: no division by ~0, every cost and the update finite
+        assert np.isfinite(costs).all() and np.isfinite(seq.controls).all()
+        assert np.all(np.array([r.diverged_at is None for r in rollouts]))
+        return
+    if name == "r_divergence_f32":
+        div = np.array([-1 if r.diverged_at is None else r.diverged_at for r in rollouts])
+        assert np.array_equal(div, g["diverged"])
+        assert np.array_equal(np.isnan(seq.controls), np.isnan(g["u_new"]))
+        assert diag.weights[3] == 0.0 and diag.weights[7] == 0.0 and diag.weights[11] == 0.0
+        assert np.isfinite(costs[11]) and not np.isfinite(costs[[3, 7]]).any()
     ref = g["costs"]
     fin = np.isfinite(ref)
     rel = np.full(ref.shape, np.inf)
@@ -78,8 +91,9 @@ def test_f32_fed_noise_gate(name, gpu_device):
         f"heavy-sample cost error {rel[heavy].max():.3g} (numpy f32 {floor_heavy:.3g})")
     assert np.mean(rel <= 1e-4) >= min(0.98, np.mean(rel32[fin] <= 1e-4) - 0.01)
     dref = g["u_new"] - g["u_nom"]
-    err_np32 = normwise(o32["u_new"] - g["u_nom"], dref)
-    err_gpu = normwise(seq.controls - g["u_nom"], dref)
+    okc = np.isfinite(dref)  # (the divergence case: NaN steps compared above)
+    err_np32 = normwise((o32["u_new"] - g["u_nom"])[okc], dref[okc])
+    err_gpu = normwise((seq.controls - g["u_nom"])[okc], dref[okc])
     print(f"{name}: update err gpu f32 {err_gpu:.3g}, numpy f32 {err_np32:.3g}")
     assert err_gpu <= max(1e-4, 2.0 * err_np32)
 

@@ -36,7 +36,7 @@ def test_oracle_reproduces_reference(name):
         assert rel_err(out["states"], g["states"], floor=1e-9) <= max(tol, 1e-10)
 
 
-@pytest.mark.parametrize("name", [n for n in R_CASES if n != "r_divergence"])
+@pytest.mark.parametrize("name", [n for n in R_CASES if not n.startswith("r_divergence")])
 def test_sampler_restatement_is_bit_exact(name):
     g = load_golden(name)
     spec = oracle_spec(g["spec"])
@@ -97,3 +97,25 @@ def test_emulated_normals_moments():
     off = cov[~np.eye(4, dtype=bool)]
     assert np.all(np.abs(off) < 4 * np.sqrt(1.0 / n))
     assert np.all(np.abs(e.mean(0)) < 4 / np.sqrt(n))
+
+
+def test_f32_divergence_fixture_semantics():
+    """r_divergence_f32: the same semantics with values float32 holds (the f32 kernels' divergence case)."""
+    g = load_golden("r_divergence_f32")
+    assert g["diverged"][3] == 2 and g["diverged"][7] == 5 and g["diverged"][11] == -1
+    assert g["weights"][3] == 0.0 and g["weights"][7] == 0.0
+    assert np.isfinite(g["costs"][11]) and g["costs"][11] > 1e30 and g["weights"][11] == 0.0
+    assert np.float32(g["costs"][11]) < np.inf  # a finite float32 cost
+    assert np.isnan(g["u_new"][[2, 5]]).all() and np.isfinite(np.delete(g["u_new"], [2, 5])).all()
+
+
+def test_pitch_floor_fixture_reaches_both_signs():
+    """r_quadrotor_pitch_floor drives |cos(pitch)| < 1e-6 with both signs (jm/dynamics.py:293, :361-363)."""
+    g = load_golden("r_quadrotor_pitch_floor")
+    cp = np.cos(g["states"][:, :-1, 7])
+    band = np.abs(cp) < 1e-6
+    assert band.mean() > 0.2 and (band & (cp > 0)).any() and (band & (cp < 0)).any()
+    # the floor matters: without it the oracle's costs move far outside the parity tolerance
+    spec = oracle_spec(g["spec"])
+    out = om.mppi_iteration_oracle(spec, g["x0"], g["u_nom"], g["noise"], np.float64)
+    assert rel_err(out["costs"], g["costs"]) <= 1e-12
