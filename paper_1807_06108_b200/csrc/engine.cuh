@@ -126,22 +126,36 @@ class Engine final : public EngineBase {
                                     (std::is_same<Dyn, Cartpole>::value || std::is_same<Dyn, Quadrotor>::value);
   // (QUAD: the eps'eps term of the modified cost is formed -- c != 1, the general
   // channel, or fed noise, whose non-finite values must still poison the cost)
-  template <bool PH, int JM, int SPT, bool QUAD>
+  // (LDIAG: diagonal-Cholesky form, instantiated where it pays -- packed Philox kernels, m > 1)
+  static constexpr bool kDiagForm = kPackable && M > 1;
+  template <bool PH, int JM, int SPT, bool QUAD, bool LDIAG = false>
   static auto fast_kern() {
     if constexpr (SPT == 2 && kPackable)
-      return &rollout_fast<Sys, Real, PH, JM, 2, 256, QUAD>;
+      return &rollout_fast<Sys, Real, PH, JM, 2, 256, QUAD, LDIAG && PH && kDiagForm>;
     else
       return &rollout_fast<Sys, Real, PH, JM, 1, 512, QUAD>;
   }
   template <bool PH, int JM, int SPT>
-  static const void* fast_fn_q(bool quad) {
+  static const void* fast_fn_q(bool quad, bool ldiag = false) {
+    if constexpr (PH && SPT == 2 && kDiagForm) {
+      if (ldiag)
+        return quad ? reinterpret_cast<const void*>(fast_kern<PH, JM, SPT, true, true>())
+                    : reinterpret_cast<const void*>(fast_kern<PH, JM, SPT, false, true>());
+    }
     return quad ? reinterpret_cast<const void*>(fast_kern<PH, JM, SPT, true>())
                 : reinterpret_cast<const void*>(fast_kern<PH, JM, SPT, false>());
   }
-  static const void* fast_fn_rt(bool ph, int jm, int spt, bool quad) {
+  // the diffusion factor's strict lower triangle is all zero
+  static bool ld_diag(const jm_ctx* c) {
+    for (int i = 0; i < M; ++i)
+      for (int j = 0; j < i; ++j)
+        if (c->Ld[i * M + j] != 0.0) return false;
+    return true;
+  }
+  static const void* fast_fn_rt(bool ph, int jm, int spt, bool quad, bool ldiag) {
     if (ph) {
-      if (jm) return spt == 2 ? fast_fn_q<true, 1, 2>(quad) : fast_fn_q<true, 1, 1>(quad);
-      return spt == 2 ? fast_fn_q<true, 0, 2>(quad) : fast_fn_q<true, 0, 1>(quad);
+      if (jm) return spt == 2 ? fast_fn_q<true, 1, 2>(quad, ldiag) : fast_fn_q<true, 1, 1>(quad);
+      return spt == 2 ? fast_fn_q<true, 0, 2>(quad, ldiag) : fast_fn_q<true, 0, 1>(quad);
     }
     if (jm) return spt == 2 ? fast_fn_q<false, 1, 2>(true) : fast_fn_q<false, 1, 1>(true);
     return spt == 2 ? fast_fn_q<false, 0, 2>(true) : fast_fn_q<false, 0, 1>(true);
@@ -242,7 +256,7 @@ class Engine final : public EngineBase {
     e = sj ? set_attrs<1>(optin) : set_attrs<0>(optin);
     if (e != cudaSuccess) return e;
     if (ws) fn = sj ? reinterpret_cast<const void*>(ws_kern<1>()) : reinterpret_cast<const void*>(ws_kern<0>());
-    if (fast) fn = fast_fn_rt(philox, sj ? 1 : 0, spt, fast_quad(c));
+    if (fast) fn = fast_fn_rt(philox, sj ? 1 : 0, spt, fast_quad(c), ld_diag(c));
     e = raise_smem(fn, optin);
     if (e != cudaSuccess) return e;
     int occ = 0;
@@ -342,6 +356,13 @@ class Engine final : public EngineBase {
     RolloutArgs<Real> b = a;
     b.jw_len = c->jw_fast;
     dim3 grid(c->grid, c->launch_trials), block(c->block / SPT);
+    if constexpr (PH && SPT == 2 && kDiagForm) {
+      if (ld_diag(c)) {
+        if (fast_quad(c))
+          return launch_pdl(fast_kern<PH, JM, SPT, true, true>(), grid, block, c->fast_smem, c->stream, b);
+        return launch_pdl(fast_kern<PH, JM, SPT, false, true>(), grid, block, c->fast_smem, c->stream, b);
+      }
+    }
     if (fast_quad(c)) return launch_pdl(fast_kern<PH, JM, SPT, true>(), grid, block, c->fast_smem, c->stream, b);
     if constexpr (PH) return launch_pdl(fast_kern<PH, JM, SPT, false>(), grid, block, c->fast_smem, c->stream, b);
     return cudaErrorInvalidValue;

@@ -152,6 +152,13 @@ __host__ __device__ __forceinline__ int event_count(const StreamKey& sk, uint32_
 
 #ifdef __CUDACC__
 // Box-Muller on two words.  u1 in (0,1], angle uniform in [-pi, pi).
+// Resolution: both uniforms keep the top 23 bits of their word, so u1 >= 2^-23
+// and |z| <= sqrt(-2 ln 2^-23) = 5.65: the normal's tails beyond 5.65 sigma
+// (two-sided mass 1.6e-8, about one draw in 6e7; ~100 of the 6.6e9 draws of a
+// cfg1 iteration would have landed there) are folded onto the 2^23-point grid
+// below it, and the angle takes 2^23 values.  The reference's ziggurat has no
+// such cut; the moment / frequency tests (tests/test_gpu_api.py, G-stat in
+// tests/test_gpu_f32_gate.py) bound the effect on the control statistics.
 // MUFU lg2/sqrt/sin/cos: noise quality only needs ~1e-6 relative accuracy;
 // the fp64 kernels consume the very same float normals (cast), so both
 // precisions see identical noise for a given (seed, iteration).

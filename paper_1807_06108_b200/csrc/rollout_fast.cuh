@@ -622,7 +622,10 @@ __host__ __device__ __forceinline__ FastPlan fast_plan(int TM, int tabn, int til
 // inc) = inc exactly for finite noise); true: the term formed, eps' eps or, for
 // the general channel (costs.py:118-121, a rare plugin: a uniform branch),
 // eps' bb eps.  Separate kernels, so each carries one copy of the tile loop.
-template <class Sys, typename Real, bool PHILOX, int JM, int SPT, int MAXT, bool QUAD>
+// LDIAG: the diffusion Cholesky factor is diagonal (independent input channels, every BASELINE
+// config): eps_j = L_jj z_j, m multiplies instead of m (m + 1) / 2 multiply-adds -- the same
+// value as the dense product, whose off-diagonal terms add exact zeros.
+template <class Sys, typename Real, bool PHILOX, int JM, int SPT, int MAXT, bool QUAD, bool LDIAG = false>
 __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const RolloutArgs<Real> a) {
   using Dyn = typename Sys::Dyn;
   using Cost = typename Sys::Cost;
@@ -785,7 +788,12 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
         auto noisy = [&](const int t, const int s2) {
           V eps[M], sj[Q];
           bool has_sj = false;
-          chol_v<M>(Ld, z + s2 * MP, eps);
+          if constexpr (LDIAG) {
+#pragma unroll
+            for (int j = 0; j < M; ++j) eps[j] = Ld[j * M + j] * z[s2 * MP + j];
+          } else {
+            chol_v<M>(Ld, z + s2 * MP, eps);
+          }
           if (jumps) {
             V mv[Q];  // the staged marks of both halves: one load (interleaved pairs)
 #pragma unroll
