@@ -662,6 +662,21 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
                 reinterpret_cast<double*>(sb + pl.sigw), sb + pl.scr, pl.chunk};
 
   const uint64_t t_entry = globaltimer();
+  if (a.loop != nullptr) {
+    // closed loop: pull the lines the prologue reads one after another (LoopState, then the
+    // nominal sequence of the parity LoopState::step selects -- both parities sit at
+    // u_nom + trial * 2 TM) into L2 side by side, so a cold start pays one DRAM round trip
+    // instead of two dependent ones (an L2 prefetch of lines the previous step's finalize is
+    // still writing is harmless: L2 is the point of coherence)
+    const char* lp = reinterpret_cast<const char*>(a.loop + blockIdx.y);
+    const char* up = reinterpret_cast<const char*>(a.u_nom + (size_t)blockIdx.y * 2 * TM);
+    const int nl = (2 * TM * (int)sizeof(double) + 127) / 128;
+    const int i = (int)threadIdx.x;
+    if (i < 2)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(lp + 128 * i));
+    else if (i - 2 < nl)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(up + 128 * (i - 2)));
+  }
   grid_dep_wait();    // u_nom / x / iteration come from the previous control step
   grid_dep_launch();  // let the finalize grid get resident while the horizon runs
   LoopState* L = a.loop ? a.loop + blockIdx.y : nullptr;

@@ -31,6 +31,28 @@ def test_trajectory_csv_round_trip_and_layout(tmp_path):
     assert p.read_bytes() == q.read_bytes()  # deterministic bytes
 
 
+def test_csv_bytes_equal_the_reference_writers(tmp_path):
+    """tests/golden/csv/*.csv were written by the reference's own jm/io.py:47-84 (oracle/gen_golden_csv.py,
+    run in the build container) from these seeded records: this package's writers give the same bytes."""
+    from pathlib import Path
+
+    from oracle.gen_golden_csv import SUMMARY, synthetic_records
+
+    gold = Path(__file__).parent / "golden" / "csv"
+    recs = [TrialRecord("c", k, s, c, j, ok, np.zeros(len(c))) for k, (s, c, j, ok) in enumerate(synthetic_records())]
+    p = tmp_path / "trajectory.csv"
+    jio.write_trajectory_csv(recs, str(p), ["x", "xd", "th", "thd"], ["F"], 0.02)
+    assert p.read_bytes() == (gold / "trajectory.csv").read_bytes()
+    q = tmp_path / "summary.csv"
+    jio.write_summary_csv([jio.SummaryRow(*r) for r in SUMMARY], str(q))
+    assert q.read_bytes() == (gold / "summary.csv").read_bytes()
+    # and this package's readers parse the reference's files exactly
+    cols = jio.read_trajectory_csv(str(gold / "trajectory.csv"))
+    assert np.array_equal(cols["x"].reshape(3, 5), np.stack([r.states[:5, 0] for r in recs]))
+    back = jio.read_summary_csv(str(gold / "summary.csv"))
+    assert back[2]["seed"] == 2**40 + 1 and back[1]["total_variance"] == 1.0 / 3.0
+
+
 def test_summary_csv_round_trip(tmp_path):
     rows = [jio.SummaryRow("cartpole", "new", 0.25, 2.0, 1000, 8, 0.875, 12.5, 3.25, 42),
             jio.SummaryRow("cartpole", "old", 0.25, 2.0, 1000, 8, 0.5, 1.0 / 3.0, 3.5, 42)]

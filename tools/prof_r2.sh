@@ -17,3 +17,4 @@ run hbm_cart1M cfg1/f32/hbm/K=1048576 --workload cfg1 --noise hbm --samples 1048
 run cfg0 cfg0/f32/philox/K=1024 --workload cfg0
 run cfg2 cfg2/f32/philox/K=8192 --workload cfg2
 ls -la gpurun_out/prof
+cp gpurun_out/prof/kernel_counters.json profiles/kernel_counters.json
