@@ -131,7 +131,7 @@ class Engine final : public EngineBase {
   template <bool PH, int JM, int SPT, bool QUAD, bool LDIAG = false>
   static auto fast_kern() {
     if constexpr (SPT == 2 && kPackable)
-      return &rollout_fast<Sys, Real, PH, JM, 2, 256, QUAD, LDIAG && PH && kDiagForm>;
+      return &rollout_fast<Sys, Real, PH, JM, 2, kPackedThreads, QUAD, LDIAG && PH && kDiagForm>;
     else
       return &rollout_fast<Sys, Real, PH, JM, 1, 512, QUAD>;
   }
@@ -210,7 +210,7 @@ class Engine final : public EngineBase {
         const int per = (K + sms - 1) / sms;
         block = std::max(32 * spt, ((per + 32 * spt - 1) / (32 * spt)) * (32 * spt));
       } else {
-        block = 256 * spt;
+        block = (spt == 2 ? kPackedThreads : 256) * spt;
       }
     }
     const bool ws = philox && 2 * block <= kWsMaxThreads && (ws_env < 0 ? block <= kWsMaxTile : ws_env == 1);

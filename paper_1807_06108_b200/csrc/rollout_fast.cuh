@@ -34,6 +34,10 @@
 
 namespace jm {
 
+#ifndef JM_PACKED_THREADS
+#define JM_PACKED_THREADS 256
+#endif
+constexpr int kPackedThreads = JM_PACKED_THREADS;  // threads per CTA of the two-samples-per-thread kernels (2 CTAs per SM)
 #ifndef JM_HBM_DEPTH
 #define JM_HBM_DEPTH 2
 #endif
