@@ -266,24 +266,13 @@ int stash_acquire(jm_ctx* ctx, uint64_t* handle) {
 // seed is a kernel parameter (uniform-register Philox keys): one graph per seed, a few
 // kept (a controller keeps its seed: run_trial, the CLI bench loop).
 constexpr size_t kIterGraphs = 8;
-int capture_iteration_graph(jm_ctx* ctx, uint64_t seed, cudaGraphExec_t* out) {
-  auto& v = ctx->iter_execs;
-  for (size_t i = 0; i < v.size(); ++i)
-    if (v[i].first == seed) {
-      *out = v[i].second;
-      if (i + 1 != v.size()) std::rotate(v.begin() + i, v.begin() + i + 1, v.end());  // most recent last
-      return JM_OK;
-    }
-  if (v.size() >= kIterGraphs) {
-    cudaGraphExecDestroy(v.front().second);
-    v.erase(v.begin());
-  }
-  cudaStream_t saved = ctx->stream;
-  ctx->stream = ctx->own_stream;
+// the drop-in iteration's three launches on ctx->stream: one-CTA zero-copy read of the staged
+// input block, rollout (costs straight into the stash buffer the block names), finalize
+// writing its outputs and the done word into the pinned block
+cudaError_t enqueue_dropin_iteration(jm_ctx* ctx, uint64_t seed) {
   double* ds = ctx->d_small;
   double* hs = ctx->h_small;
   uint64_t* words = reinterpret_cast<uint64_t*>(ds + ctx->off_x0());
-  CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
   jm::copy_block_kernel<<<1, 256, 0, ctx->stream>>>(hs, ds, (int)ctx->off_unew());
   cudaError_t e = cudaGetLastError();
   jm::RolloutCall rc;
@@ -305,6 +294,25 @@ int capture_iteration_graph(jm_ctx* ctx, uint64_t seed, cudaGraphExec_t* out) {
     f.done = reinterpret_cast<int32_t*>(hs + ctx->off_status()) + 1;
     e = ctx->eng->finalize(ctx, f, nullptr, nullptr);
   }
+  return e;
+}
+
+int capture_iteration_graph(jm_ctx* ctx, uint64_t seed, cudaGraphExec_t* out) {
+  auto& v = ctx->iter_execs;
+  for (size_t i = 0; i < v.size(); ++i)
+    if (v[i].first == seed) {
+      *out = v[i].second;
+      if (i + 1 != v.size()) std::rotate(v.begin() + i, v.begin() + i + 1, v.end());  // most recent last
+      return JM_OK;
+    }
+  if (v.size() >= kIterGraphs) {
+    cudaGraphExecDestroy(v.front().second);
+    v.erase(v.begin());
+  }
+  cudaStream_t saved = ctx->stream;
+  ctx->stream = ctx->own_stream;
+  CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  cudaError_t e = enqueue_dropin_iteration(ctx, seed);
   cudaGraph_t g = nullptr;
   cudaError_t e2 = cudaStreamEndCapture(ctx->stream, &g);
   ctx->stream = saved;
@@ -324,8 +332,10 @@ int capture_iteration_graph(jm_ctx* ctx, uint64_t seed, cudaGraphExec_t* out) {
 // (h_small from off_unew on).
 int dropin_launch(jm_ctx* ctx, const double* x0, const double* u_nom, const double* u_init, uint64_t seed,
                   uint64_t iteration, uint64_t* weights_stash) {
+  // JM_DROPIN_DIRECT=1 (tuning): three stream launches instead of one graph launch
+  static const bool direct = std::getenv("JM_DROPIN_DIRECT") != nullptr && std::atoi(std::getenv("JM_DROPIN_DIRECT")) != 0;
   cudaGraphExec_t ge = nullptr;
-  int r = capture_iteration_graph(ctx, seed, &ge);
+  int r = direct ? JM_OK : capture_iteration_graph(ctx, seed, &ge);
   if (r != JM_OK) return r;
   uint64_t handle = 0;
   r = stash_acquire(ctx, &handle);
@@ -340,7 +350,10 @@ int dropin_launch(jm_ctx* ctx, const double* x0, const double* u_nom, const doub
   volatile int32_t* st = reinterpret_cast<volatile int32_t*>(hs + ctx->off_status());
   st[0] = 0;
   st[1] = 0;  // done word, raised by the finalize after its last output
-  CK(cudaGraphLaunch(ge, ctx->stream));
+  if (direct)
+    CK(enqueue_dropin_iteration(ctx, seed));
+  else
+    CK(cudaGraphLaunch(ge, ctx->stream));
   // (zero-copy over PCIe: copy_block_kernel reads [x0|u_nom|mapping|u_init], the finalize
   // writes [u_new|norms|diag|status|u_shift] into the pinned block)
   g_h2d += (long long)(sizeof(double) * ctx->off_unew());
