@@ -167,8 +167,8 @@ class Engine final : public EngineBase {
   int fast_gs(bool philox) const { return philox ? 4 / Pad<M>::value : (M >= 3 ? 1 : 4); }
   size_t fast_bytes(const jm_ctx* c, int tile, int spt, int W, bool philox) const {
     const int nb = regen_items(c->T, fast_gs(philox));
-    const int nmarks = (philox && c->jthr) ? tile * W * q_of(c) : 0;
-    return fast_plan(c->TM, c->T * (2 * M + 1), tile, tile / spt, nb, nmarks, c->gap_n, (int)sizeof(Real)).total;
+    const size_t mbytes = (philox && c->jthr) ? fast_marks_bytes(tile, tile / spt / 32, W, q_of(c), (int)sizeof(Real)) : 0;
+    return fast_plan(c->TM, c->T * (2 * M + 1), tile, tile / spt, nb, mbytes, c->gap_n, (int)sizeof(Real)).total;
   }
 
   // warp-specialised kernel (Philox, non-trace): block = 2 x tile
@@ -244,6 +244,12 @@ class Engine final : public EngineBase {
       // multi-wave: two CTAs per SM must fit; single wave: the whole SM
       const size_t fbudget = (c->ntiles <= sms) ? cap : std::min(cap, (size_t)optin / 2 - 2048);
       WF = std::min(128, (c->T + 3) / 4 * 4);
+      // (JM_JW_NOCAP=1, tests: windows as long as the memory allows whatever the rate, so a warp's
+      // window overflows its mark table and the halve-and-redo path runs)
+      static const bool jw_nocap = std::getenv("JM_JW_NOCAP") != nullptr && std::atoi(std::getenv("JM_JW_NOCAP")) != 0;
+      if (philox && c->jthr && marks_indexed(q_of(c)) && !jw_nocap) WF = std::min(WF, marks_window_cap(c->jthr, spt));
+      static const int jw_env = std::getenv("JM_JW") ? std::atoi(std::getenv("JM_JW")) : 0;  // A/B: window length
+      if (jw_env >= 4) WF = std::min(WF, jw_env / 4 * 4);
       while (WF > 8 && fast_bytes(c, block, spt, WF, philox) > fbudget) WF -= 4;
       (void)budget;
       fsmem = fast_bytes(c, block, spt, WF, philox);

@@ -125,6 +125,34 @@ __device__ __forceinline__ void block_normals_v(const StreamKey& sk, uint32_t b,
   box_muller2(r0.z, r1.z, r0.w, r1.w, z[2], z[3]);
 }
 
+// ---------------------------------------------------------------- mark staging, two forms
+// Dense (q = 1): one Real per (step, sample) of the window, zero where no event.
+// Indexed (q >= 2): one BYTE per (step, thread) -- 0, or the entry of the warp's compact mark
+// table holding the q values of that step's event for each of the thread's SPT samples (zero
+// for a sample without one; entry 0 is all zero), laid out [i][half] so a step still reads
+// each component of both halves with one load -- a window costs tile / SPT x W bytes instead
+// of tile x W x q Reals and reaches ~10 times further for the same shared memory (quadrotor,
+// q = 3, two CTAs per SM: 128 steps instead of 12; each window costs a clock pass, a prefix
+// scan and a cooperative mark pass of fixed latency).  A warp's window holds at most
+// kMarkCap - 1 entries; the launch sizes W from nu dt so that is ~1.6x the expected count,
+// and a window that still overflows is halved and redone from the saved clocks (exact for
+// any rate: one step of a warp has at most 32 entries).
+constexpr int kMarkCap = 256;
+__host__ __device__ constexpr bool marks_indexed(int q) { return q >= 2; }
+__host__ __device__ __forceinline__ size_t fast_marks_bytes(int tile, int nwarps, int W, int q, int rs) {
+  if (W <= 0) return 0;
+  if (!marks_indexed(q)) return (size_t)rs * tile * W * q;
+  const int spt = tile / (nwarps * 32);
+  return (((size_t)nwarps * 32 * W + 15) & ~(size_t)15) + (size_t)rs * nwarps * kMarkCap * q * spt;
+}
+// the longest indexed window whose expected event count per warp stays below ~5/8 of the table
+// (p = nu dt as jthr / 2^32; spt samples per lane)
+__host__ __device__ __forceinline__ int marks_window_cap(uint32_t jthr, int spt) {
+  const double ev_per_step = 32.0 * spt * (double)jthr / 4294967296.0;  // (jthr = ceil(p 2^24) << 8)
+  const double w = 160.0 / (ev_per_step > 1e-12 ? ev_per_step : 1e-12);
+  return w >= 128.0 ? 128 : (w < 4.0 ? 4 : ((int)w & ~3));
+}
+
 // ---------------------------------------------------------------- jump windows (clearing form)
 // jump_window (kernels.cuh) with (a) the owner lane's sample at kg + (L - lane)
 // * kstride (two samples per thread: the even / odd samples of a warp form one
@@ -186,6 +214,120 @@ __device__ __forceinline__ void jump_window_c(JumpClock& c, Mask128& prev, int w
     }
   }
   __syncwarp();
+}
+
+// ---------------------------------------------------------------- jump window, indexed staging
+// The events of [w0, wend) of one sample: its clock advanced past the window, the event
+// steps as a mask relative to w0; returns their number.
+__device__ __forceinline__ int window_events(JumpClock& c, int w0, int wend, const StreamKey& sk, uint32_t kg,
+                                             const GapSampler& gs, Mask128& mask) {
+  mask = Mask128{0ull, 0ull};
+  int n = 0;
+  while (__any_sync(0xFFFFFFFFu, c.tj < wend)) {
+    if (c.tj < wend) {
+      mask_set(mask, c.tj - w0);
+      ++n;
+      clock_next(c, sk, kg, gs);
+    }
+  }
+  return n;
+}
+
+// One window of a warp's 32 threads x SPT samples (lane's samples kg0 + u) in ONE cooperative
+// pass: the (thread, step) pairs with an event on either sample form one list (by lane, then
+// time), lane j computes entry j's mark(s) into table entry 1 + j -- tabw[((1 + j) * Q + i) *
+// SPT + u], zero for a sample without an event at that step -- and stores that byte at
+// ib[(step - w0) * 32 + lane].  Returns the window's end (<= wend_max; shorter only after an
+// overflow, a multiple of `gran` steps past w0).
+__device__ __forceinline__ int mask_count_below(const Mask128& m, int s) {  // set bits below bit s
+  const uint64_t lo = s >= 64 ? m.lo : (m.lo & ((1ull << s) - 1ull));
+  const uint64_t hi = s >= 64 ? (m.hi & ((1ull << (s - 64)) - 1ull)) : 0ull;
+  return __popcll(lo) + __popcll(hi);
+}
+__device__ __forceinline__ bool mask_test(const Mask128& m, int s) {
+  return ((s >= 64 ? m.hi >> (s - 64) : m.lo >> s) & 1ull) != 0ull;
+}
+
+template <int Q, int QP, int JM, int SPT, typename Real>
+__device__ __forceinline__ int jump_window_idx(JumpClock* c, Mask128& prev, int w0, int wend_max, int gran,
+                                               const StreamKey& sk, uint32_t kg0, const GapSampler& gs,
+                                               const Real* Lj, const Real* mu, Real jscale, uint8_t* ib, Real* tabw,
+                                               bool poisson, const CountTable& ct) {
+  const int lane = threadIdx.x & 31;
+  int wend = wend_max;
+  Mask128 mask[SPT], um;
+  uint32_t e0[SPT];
+  int nl, inc, tot;
+  for (;;) {
+    JumpClock saved[SPT];
+    um = Mask128{0ull, 0ull};
+#pragma unroll
+    for (int u = 0; u < SPT; ++u) {
+      saved[u] = c[u];
+      e0[u] = c[u].e;
+      window_events(c[u], w0, wend, sk, kg0 + (uint32_t)u, gs, mask[u]);
+      um.lo |= mask[u].lo;
+      um.hi |= mask[u].hi;
+    }
+    nl = __popcll(um.lo) + __popcll(um.hi);
+    inc = nl;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+      if (lane >= o) inc += v;
+    }
+    tot = __shfl_sync(0xFFFFFFFFu, inc, 31);
+    if (tot < kMarkCap) break;  // (uniform)
+    // overflow: redo a window half as long from the saved clocks
+#pragma unroll
+    for (int u = 0; u < SPT; ++u) c[u] = saved[u];
+    const int half = ((wend - w0) / 2 / gran) * gran;
+    wend = w0 + (half > gran ? half : gran);
+  }
+  const int off = inc - nl;
+  __syncwarp();  // the previous window's bytes have been read
+  for (Mask128 m = prev; m.lo | m.hi; mask_pop(m)) ib[mask_low(m) * 32 + lane] = 0;
+  prev = um;
+  __syncwarp();
+  for (int j0 = 0; j0 < tot; j0 += 32) {
+    const int j = j0 + lane;
+    int L = 0;  // owner lane of entry j: the last lane with off <= j
+#pragma unroll
+    for (int bb = 16; bb > 0; bb >>= 1) {
+      const int oc = __shfl_sync(0xFFFFFFFFu, off, L + bb);
+      if (oc <= j) L += bb;
+    }
+    const int k = j - __shfl_sync(0xFFFFFFFFu, off, L);
+    Mask128 mL[SPT];
+    uint32_t eL[SPT];
+    Mask128 uL{0ull, 0ull};
+#pragma unroll
+    for (int u = 0; u < SPT; ++u) {
+      mL[u] = mask_shfl(mask[u], L);
+      eL[u] = __shfl_sync(0xFFFFFFFFu, e0[u], L);
+      uL.lo |= mL[u].lo;
+      uL.hi |= mL[u].hi;
+    }
+    if (j < tot) {
+      for (int r = 0; r < k; ++r) mask_pop(uL);
+      const int sidx = mask_low(uL);
+      Real* const ent = tabw + (size_t)(1 + j) * Q * SPT;
+#pragma unroll
+      for (int u = 0; u < SPT; ++u) {
+        Real mk[Q];
+#pragma unroll
+        for (int i = 0; i < Q; ++i) mk[i] = Real(0);
+        if (mask_test(mL[u], sidx))
+          mark_of<Q, QP, Real>(sk, kg0 + (uint32_t)((L - lane) * SPT + u),
+                               eL[u] + (uint32_t)mask_count_below(mL[u], sidx), Lj, mu, mk, poisson, ct);
+#pragma unroll
+        for (int i = 0; i < Q; ++i) ent[i * SPT + u] = (JM == 1) ? rmul<Real>(jscale, mk[i]) : mk[i];
+      }
+      ib[sidx * 32 + L] = (uint8_t)(1 + j);
+    }
+  }
+  __syncwarp();
+  return wend;
 }
 
 // ---------------------------------------------------------------- regeneration
@@ -590,13 +732,13 @@ __global__ void __launch_bounds__(MAXT) rollout_kernel_ws(const RolloutArgs<Real
 
 
 // ---------------------------------------------------------------- shared memory plan (fast kernel)
-//   Nacc (TM doubles) | marks (SPT x nwarps x 32 x W x q Real) | step table (T x (2m+1) Real) |
+//   Nacc (TM doubles) | mark staging (fast_marks_bytes) | step table (T x (2m+1) Real) |
 //   sig_col (tile int) | sig_w (tile double) | scratch (chunk x TM Real) | gap table (uint32)
 struct FastPlan {
   size_t nacc, marks, tab, sigc, sigw, scr, gap, total;
   int chunk;
 };
-__host__ __device__ __forceinline__ FastPlan fast_plan(int TM, int tabn, int tile, int nthreads, int nb, int nmarks,
+__host__ __device__ __forceinline__ FastPlan fast_plan(int TM, int tabn, int tile, int nthreads, int nb, size_t mbytes,
                                                        int ngap, int rs) {
   FastPlan p;
   p.chunk = nthreads / nb > 1 ? nthreads / nb : 1;
@@ -605,7 +747,7 @@ __host__ __device__ __forceinline__ FastPlan fast_plan(int TM, int tabn, int til
   p.nacc = o;
   o = al16(o + sizeof(double) * (size_t)TM);
   p.marks = o;
-  o = al16(o + (size_t)rs * nmarks);
+  o = al16(o + mbytes);
   p.tab = o;
   o = al16(o + (size_t)rs * tabn);
   p.sigc = o;
@@ -655,8 +797,11 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
   const int nb = regen_items(T, GS);
   // (batched old/new variants: the "old" trials' sampler draws no jumps)
   const bool jumps = PHILOX && a.jump_on && (a.loop == nullptr || a.loop[blockIdx.y].sampler_jumps);
-  const FastPlan pl = fast_plan(TM, T * TS, tileK, nthreads, nb, jumps ? SPT * nwarps * 32 * a.jw_len * Q : 0,
-                                a.gap_n, (int)sizeof(Real));
+  constexpr bool IDX = PHILOX && marks_indexed(Q);  // indexed mark staging (q >= 2)
+  static_assert(!IDX || GS * 32 < kMarkCap, "one group of steps must fit the mark table");
+  const FastPlan pl = fast_plan(TM, T * TS, tileK, nthreads, nb,
+                                jumps ? fast_marks_bytes(tileK, nwarps, a.jw_len, Q, (int)sizeof(Real)) : 0, a.gap_n,
+                                (int)sizeof(Real));
   char* const sb = reinterpret_cast<char*>(smem_d);
   double* Nacc = reinterpret_cast<double*>(sb + pl.nacc);
   Real* tab = reinterpret_cast<Real*>(sb + pl.tab);
@@ -695,10 +840,17 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
     tl_put(tlr, kTlRollWait);
   }
   rollout_prologue<M, Real>(a, L ? loop_unom(L, L->step, TM) : a.u_nom + (size_t)blockIdx.y * TM, tab, Nacc, s_acc, Sg);
-  if (jumps) {  // the mark staging is zero outside event entries (jump_window_c)
-    const int n4 = (int)((size_t)SPT * nwarps * 32 * a.jw_len * Q * sizeof(Real) / 16);
+  // indexed staging: bytes [warp][step][lane][half], then the warps' mark tables
+  uint8_t* const ibw = reinterpret_cast<uint8_t*>(marks) + (size_t)(threadIdx.x >> 5) * 32 * a.jw_len;
+  Real* const tabw =
+      reinterpret_cast<Real*>(reinterpret_cast<char*>(marks) + (((size_t)nthreads * a.jw_len + 15) & ~(size_t)15)) +
+      (size_t)(threadIdx.x >> 5) * kMarkCap * Q * SPT;
+  if (jumps) {  // the mark staging is zero outside event entries (jump_window_c / jump_window_idx)
+    const size_t zb = IDX ? (size_t)nthreads * a.jw_len : (size_t)SPT * nwarps * 32 * a.jw_len * Q * sizeof(Real);
+    const int n4 = (int)((zb + 15) / 16);
     float4* z4 = reinterpret_cast<float4*>(marks);
     for (int i = threadIdx.x; i < n4; i += nthreads) z4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (IDX && (threadIdx.x & 31) < Q * SPT) tabw[threadIdx.x & 31] = Real(0);  // entry 0: no event
   }
   __syncthreads();
 
@@ -758,6 +910,7 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
       V Sacc = vcast<V>(0.0);
       JumpClock clk[SPT];
       const Real* wl[SPT];
+      const uint8_t* il = ibw + lane;
       int wnext = 0;
 #pragma unroll
       for (int u = 0; u < SPT; ++u) {
@@ -802,60 +955,88 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
       };
 
       if constexpr (PHILOX) {
-        V z[4], zn[4];
-        block_normals_v(sk, 0u, kg, z);
-        auto noisy = [&](const int t, const int s2) {
-          V eps[M], sj[Q];
-          bool has_sj = false;
-          if constexpr (LDIAG) {
-#pragma unroll
-            for (int j = 0; j < M; ++j) eps[j] = Ld[j * M + j] * z[s2 * MP + j];
-          } else {
-            chol_v<M>(Ld, z + s2 * MP, eps);
-          }
-          if (jumps) {
-            V mv[Q];  // the staged marks of both halves: one load (interleaved pairs)
-#pragma unroll
-            for (int i = 0; i < Q; ++i) {
-              if constexpr (SPT == 2)
-                mv[i] = F2(*reinterpret_cast<const float2*>(wl[0] + i * 32 * SPT));
-              else
-                mv[i] = wl[0][i * 32];
-            }
-            wl[0] += Q * 32 * SPT;
-            if (JM == 0) {
-#pragma unroll
-              for (int j = 0; j < M; ++j) eps[j] = vadd(eps[j], mv[j]);  // noise.py:156-157
+        // the horizon, unswitched on the sampler's jumps (a uniform run-time flag): each form is
+        // straight-line per noise group, so the next group's Philox block overlaps the dynamics
+        auto horizon = [&](auto jtag) {
+          constexpr bool J = decltype(jtag)::value;
+          V z[4], zn[4];
+          block_normals_v(sk, 0u, kg, z);
+          auto noisy = [&](const int t, const int s2) {
+            V eps[M], sj[Q];
+            bool has_sj = false;
+            if constexpr (LDIAG) {
+  #pragma unroll
+              for (int j = 0; j < M; ++j) eps[j] = Ld[j * M + j] * z[s2 * MP + j];
             } else {
+              chol_v<M>(Ld, z + s2 * MP, eps);
+            }
+            if constexpr (J) {
+              V mv[Q];  // the staged marks of both halves: one load (interleaved pairs)
+              if constexpr (IDX) {
+                // the step's table entry (0: none) of this thread, then its samples' marks
+              const uint32_t ii = *il;
+              il += 32;
 #pragma unroll
-              for (int i = 0; i < Q; ++i) sj[i] = mv[i];
-              has_sj = true;
+              for (int i = 0; i < Q; ++i) {
+                if constexpr (SPT == 2)
+                  mv[i] = F2(*reinterpret_cast<const float2*>(tabw + (ii * Q + i) * 2));
+                else
+                  mv[i] = tabw[ii * Q + i];
+              }
+              } else {
+  #pragma unroll
+                for (int i = 0; i < Q; ++i) {
+                  if constexpr (SPT == 2)
+                    mv[i] = F2(*reinterpret_cast<const float2*>(wl[0] + i * 32 * SPT));
+                  else
+                    mv[i] = wl[0][i * 32];
+                }
+                wl[0] += Q * 32 * SPT;
+              }
+              if (JM == 0) {
+  #pragma unroll
+                for (int j = 0; j < M; ++j) eps[j] = vadd(eps[j], mv[j]);  // noise.py:156-157
+              } else {
+  #pragma unroll
+                for (int i = 0; i < Q; ++i) sj[i] = mv[i];
+                has_sj = true;
+              }
+            }
+            step(t, eps, sj, has_sj);
+          };
+          for (int t0 = 0; t0 < T; t0 += GS) {
+            if (J && t0 == wnext) {
+              if constexpr (IDX) {
+                wnext = jump_window_idx<Q, QP, JM, SPT, Real>(clk, prev[0], t0, min(t0 + JW, T), GS, sk, kg[0], gs, Lj, mu,
+                                                              jscale, ibw, tabw, a.poisson != 0, a.cnt);
+                il = ibw + lane;
+              } else {
+                wnext = t0 + JW;
+  #pragma unroll
+                for (int u = 0; u < SPT; ++u) {
+                  jump_window_c<Q, QP, JM, SPT, Real>(clk[u], prev[u], t0, min(wnext, T), sk, kg[u], SPT, gs, Lj, mu,
+                                                      jscale, wdu[u], a.poisson != 0, a.cnt);
+                  wl[u] = wdu[u] + lane * SPT;
+                }
+              }
+            }
+            if (t0 + GS <= T) {
+              block_normals_v(sk, (uint32_t)((t0 + GS) / GS), kg, zn);  // (unconditional: one spare block at the horizon's end keeps the group one basic block)
+  #pragma unroll
+              for (int s2 = 0; s2 < GS; ++s2) noisy(t0 + s2, s2);
+  #pragma unroll
+              for (int i = 0; i < 4; ++i) z[i] = zn[i];
+            } else {
+  #pragma unroll
+              for (int s2 = 0; s2 < GS; ++s2)
+                if (t0 + s2 < T) noisy(t0 + s2, s2);
             }
           }
-          step(t, eps, sj, has_sj);
         };
-        for (int t0 = 0; t0 < T; t0 += GS) {
-          if (jumps && t0 == wnext) {
-            wnext = t0 + JW;
-#pragma unroll
-            for (int u = 0; u < SPT; ++u) {
-              jump_window_c<Q, QP, JM, SPT, Real>(clk[u], prev[u], t0, min(wnext, T), sk, kg[u], SPT, gs, Lj, mu,
-                                                  jscale, wdu[u], a.poisson != 0, a.cnt);
-              wl[u] = wdu[u] + lane * SPT;
-            }
-          }
-          if (t0 + GS <= T) {
-            if (t0 + GS < T) block_normals_v(sk, (uint32_t)((t0 + GS) / GS), kg, zn);
-#pragma unroll
-            for (int s2 = 0; s2 < GS; ++s2) noisy(t0 + s2, s2);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) z[i] = zn[i];
-          } else {
-#pragma unroll
-            for (int s2 = 0; s2 < GS; ++s2)
-              if (t0 + s2 < T) noisy(t0 + s2, s2);
-          }
-        }
+        if (jumps)
+          horizon(std::true_type{});
+        else
+          horizon(std::false_type{});
       } else {
         // HBM wire format eps[(t*M + j)*K + k], jump[(t*Q + i)*K + k]: a thread's
         // SPT samples are adjacent columns (one 8-byte load for both), groups

@@ -106,3 +106,22 @@ def test_noise_wire_file_replays_the_device_stream(gpu_device, tmp_path):
     b, _ = jb.mppi_iteration(ctrl, model, cost, g["x0"], 21, noise=jio.from_wire(ec, jw), precision="f64")
     # the file holds fp32 values: agreement to fp32 resolution of the noise
     assert rel_err(b.controls, a.controls, floor=1e-3) <= 1e-5
+
+
+def test_mark_table_overflow_path(gpu_device):
+    """jump_window_idx's halve-and-redo path (csrc/rollout_fast.cuh): with JM_JW_NOCAP=1 the windows ignore
+    the rate, a warp's window overflows its 255-entry mark table, and the results must not change --
+    tests/_overflow_worker.py checks the fp64 kernel against the oracle and the packed fp32 kernel
+    against the HBM kernel.  (A subprocess: the switch is read once per process.)"""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    env = {k: v for k, v in os.environ.items() if k not in ("JM_WS", "JM_SPT", "JM_NO_EPS_SMEM", "JM_JW")}
+    env.update(JM_JW_NOCAP="1", PYTHONPATH=f"{root}{os.pathsep}{root / 'tests'}")  # (the default kernel choice)
+    r = subprocess.run([sys.executable, str(root / "tests" / "_overflow_worker.py")], env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    assert "overflow path ok" in r.stdout
