@@ -1004,33 +1004,39 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
             }
             step(t, eps, sj, has_sj);
           };
-          for (int t0 = 0; t0 < T; t0 += GS) {
-            if (J && t0 == wnext) {
+          // outer loop: one jump window (the whole horizon without jumps); inner loop: its noise
+          // groups, nothing but the groups -- the window code stays out of the hot loop's live ranges
+          for (int w0 = 0; w0 < T;) {
+            int wend = T;
+            if constexpr (J) {
               if constexpr (IDX) {
-                wnext = jump_window_idx<Q, QP, JM, SPT, Real>(clk, prev[0], t0, min(t0 + JW, T), GS, sk, kg[0], gs, Lj, mu,
-                                                              jscale, ibw, tabw, a.poisson != 0, a.cnt);
+                wend = jump_window_idx<Q, QP, JM, SPT, Real>(clk, prev[0], w0, min(w0 + JW, T), GS, sk, kg[0], gs, Lj, mu,
+                                                             jscale, ibw, tabw, a.poisson != 0, a.cnt);
                 il = ibw + lane;
               } else {
-                wnext = t0 + JW;
-  #pragma unroll
+                wend = min(w0 + JW, T);
+#pragma unroll
                 for (int u = 0; u < SPT; ++u) {
-                  jump_window_c<Q, QP, JM, SPT, Real>(clk[u], prev[u], t0, min(wnext, T), sk, kg[u], SPT, gs, Lj, mu,
-                                                      jscale, wdu[u], a.poisson != 0, a.cnt);
+                  jump_window_c<Q, QP, JM, SPT, Real>(clk[u], prev[u], w0, wend, sk, kg[u], SPT, gs, Lj, mu, jscale,
+                                                      wdu[u], a.poisson != 0, a.cnt);
                   wl[u] = wdu[u] + lane * SPT;
                 }
               }
             }
-            if (t0 + GS <= T) {
-              block_normals_v(sk, (uint32_t)((t0 + GS) / GS), kg, zn);  // (unconditional: one spare block at the horizon's end keeps the group one basic block)
-  #pragma unroll
+            int t0 = w0;
+            for (; t0 + GS <= wend; t0 += GS) {
+              block_normals_v(sk, (uint32_t)((t0 + GS) / GS), kg, zn);  // (one spare block at the horizon's end)
+#pragma unroll
               for (int s2 = 0; s2 < GS; ++s2) noisy(t0 + s2, s2);
-  #pragma unroll
+#pragma unroll
               for (int i = 0; i < 4; ++i) z[i] = zn[i];
-            } else {
-  #pragma unroll
+            }
+            if (t0 < wend) {  // (the horizon's last, partial group: wend == T)
+#pragma unroll
               for (int s2 = 0; s2 < GS; ++s2)
                 if (t0 + s2 < T) noisy(t0 + s2, s2);
             }
+            w0 = wend;
           }
         };
         if (jumps)
