@@ -1023,14 +1023,18 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
                 }
               }
             }
-            int t0 = w0;
-            for (; t0 + GS <= wend; t0 += GS) {
-              block_normals_v(sk, (uint32_t)((t0 + GS) / GS), kg, zn);  // (one spare block at the horizon's end)
+            // (windows start on group boundaries: the group index form lets the compiler see
+            // t0 = GS g, so the step table's rows of a group are read with vector loads)
+            int g = w0 / GS;
+            for (; (g + 1) * GS <= wend; ++g) {
+              const int t0 = g * GS;
+              block_normals_v(sk, (uint32_t)(g + 1), kg, zn);  // (one spare block at the horizon's end)
 #pragma unroll
               for (int s2 = 0; s2 < GS; ++s2) noisy(t0 + s2, s2);
 #pragma unroll
               for (int i = 0; i < 4; ++i) z[i] = zn[i];
             }
+            const int t0 = g * GS;
             if (t0 < wend) {  // (the horizon's last, partial group: wend == T)
 #pragma unroll
               for (int s2 = 0; s2 < GS; ++s2)
