@@ -1065,49 +1065,57 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
             return V(__ldg(p));
           }
         };
-        auto load_group = [&](int g0, V* ze, V* zj) {
-#pragma unroll
-          for (int s2 = 0; s2 < GS; ++s2) {
-            const int t = min(g0 + s2, T - 1);
-#pragma unroll
-            for (int j = 0; j < M; ++j) ze[s2 * M + j] = load(pe + (size_t)t * rowe + (size_t)j * K);
-            if (JM == 1) {
-#pragma unroll
-              for (int i = 0; i < Q; ++i) zj[s2 * Q + i] = hj ? load(pj + (size_t)t * rowj + (size_t)i * K) : vcast<V>(0.0);
+        // the horizon, unswitched on whether a jump tensor was fed (a uniform run-time flag)
+        auto horizon = [&](auto jtag) {
+          constexpr bool HJ = decltype(jtag)::value;
+          auto load_group = [&](int g0, V* ze, V* zj) {
+  #pragma unroll
+            for (int s2 = 0; s2 < GS; ++s2) {
+              const int t = min(g0 + s2, T - 1);
+  #pragma unroll
+              for (int j = 0; j < M; ++j) ze[s2 * M + j] = load(pe + (size_t)t * rowe + (size_t)j * K);
+              if (JM == 1) {
+  #pragma unroll
+                for (int i = 0; i < Q; ++i) zj[s2 * Q + i] = HJ ? load(pj + (size_t)t * rowj + (size_t)i * K) : vcast<V>(0.0);
+              }
             }
-          }
-        };
-        constexpr int GE = GS * M, GJ = (JM == 1) ? GS * Q : 1;
-        (void)EW;
-        (void)JWD;
-        // a ring of kHbmDepth + 1 register buffers, the group loop unrolled over the ring so
-        // a buffer's role is a compile-time index (no register rotation moves): group g runs
-        // from buffer g % NB while group g + kHbmDepth is loaded into the buffer group g - 1
-        // has just released
-        constexpr int NB = kHbmDepth + 1;
-        V eb[NB][GE], jb[NB][GJ];
-#pragma unroll
-        for (int d = 0; d < kHbmDepth; ++d) load_group(d * GS, eb[d], jb[d]);
-        for (int t0 = 0; t0 < T; t0 += NB * GS) {
-#pragma unroll
-          for (int r = 0; r < NB; ++r) {
-            const int tg = t0 + r * GS;
-            if (tg < T) {
-              load_group(tg + kHbmDepth * GS, eb[(r + kHbmDepth) % NB], jb[(r + kHbmDepth) % NB]);  // (clamped inside the horizon)
-#pragma unroll
-              for (int s2 = 0; s2 < GS; ++s2) {
-                if (GS == 1 || tg + s2 < T) {
-                  V sj[Q];
-                  if (JM == 1) {
-#pragma unroll
-                    for (int i = 0; i < Q; ++i) sj[i] = jscale * jb[r][s2 * Q + i];
+          };
+          constexpr int GE = GS * M, GJ = (JM == 1) ? GS * Q : 1;
+          (void)EW;
+          (void)JWD;
+          // a ring of kHbmDepth + 1 register buffers, the group loop unrolled over the ring so
+          // a buffer's role is a compile-time index (no register rotation moves): group g runs
+          // from buffer g % NB while group g + kHbmDepth is loaded into the buffer group g - 1
+          // has just released
+          constexpr int NB = kHbmDepth + 1;
+          V eb[NB][GE], jb[NB][GJ];
+  #pragma unroll
+          for (int d = 0; d < kHbmDepth; ++d) load_group(d * GS, eb[d], jb[d]);
+          for (int t0 = 0; t0 < T; t0 += NB * GS) {
+  #pragma unroll
+            for (int r = 0; r < NB; ++r) {
+              const int tg = t0 + r * GS;
+              if (tg < T) {
+                load_group(tg + kHbmDepth * GS, eb[(r + kHbmDepth) % NB], jb[(r + kHbmDepth) % NB]);  // (clamped inside the horizon)
+  #pragma unroll
+                for (int s2 = 0; s2 < GS; ++s2) {
+                  if (GS == 1 || tg + s2 < T) {
+                    V sj[Q];
+                    if (JM == 1) {
+  #pragma unroll
+                      for (int i = 0; i < Q; ++i) sj[i] = jscale * jb[r][s2 * Q + i];
+                    }
+                    step(tg + s2, eb[r] + s2 * M, sj, JM == 1 && HJ);
                   }
-                  step(tg + s2, eb[r] + s2 * M, sj, JM == 1 && hj);
                 }
               }
             }
           }
-        }
+        };
+        if (hj)
+          horizon(std::true_type{});
+        else
+          horizon(std::false_type{});
       }
       if (tlr != nullptr) {  // (timeline: the first and the last CTA to finish the horizon)
         tl_max(tlr, kTlRollHorizonEndMax);
