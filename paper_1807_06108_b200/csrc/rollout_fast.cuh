@@ -961,14 +961,14 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
           constexpr bool J = decltype(jtag)::value;
           V z[4], zn[4];
           block_normals_v(sk, 0u, kg, z);
-          auto noisy = [&](const int t, const int s2) {
+          auto noisy = [&](const int t, const int s2, const V* zz) {
             V eps[M], sj[Q];
             bool has_sj = false;
             if constexpr (LDIAG) {
   #pragma unroll
-              for (int j = 0; j < M; ++j) eps[j] = Ld[j * M + j] * z[s2 * MP + j];
+              for (int j = 0; j < M; ++j) eps[j] = Ld[j * M + j] * zz[s2 * MP + j];
             } else {
-              chol_v<M>(Ld, z + s2 * MP, eps);
+              chol_v<M>(Ld, zz + s2 * MP, eps);
             }
             if constexpr (J) {
               V mv[Q];  // the staged marks of both halves: one load (interleaved pairs)
@@ -1026,11 +1026,24 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
             // (windows start on group boundaries: the group index form lets the compiler see
             // t0 = GS g, so the step table's rows of a group are read with vector loads)
             int g = w0 / GS;
-            for (; (g + 1) * GS <= wend; ++g) {
-              const int t0 = g * GS;
-              block_normals_v(sk, (uint32_t)(g + 1), kg, zn);  // (one spare block at the horizon's end)
+            // two groups per trip, the normal buffers z / zn swapping roles (no register copies;
+            // the BASELINE systems in fp32 -- elsewhere the longer body only adds register pressure)
+            if constexpr (std::is_same<Real, float>::value && Dyn::kPairGroups) {
+              for (; (g + 2) * GS <= wend; g += 2) {
+                const int t0 = g * GS;
+                block_normals_v(sk, (uint32_t)(g + 1), kg, zn);
 #pragma unroll
-              for (int s2 = 0; s2 < GS; ++s2) noisy(t0 + s2, s2);
+                for (int s2 = 0; s2 < GS; ++s2) noisy(t0 + s2, s2, z);
+                block_normals_v(sk, (uint32_t)(g + 2), kg, z);  // (one spare block at the horizon's end)
+#pragma unroll
+                for (int s2 = 0; s2 < GS; ++s2) noisy(t0 + GS + s2, s2, zn);
+              }
+            }
+            for (; (g + 1) * GS <= wend; ++g) {  // (the window's odd group; every group of the other systems)
+              const int t0 = g * GS;
+              block_normals_v(sk, (uint32_t)(g + 1), kg, zn);
+#pragma unroll
+              for (int s2 = 0; s2 < GS; ++s2) noisy(t0 + s2, s2, z);
 #pragma unroll
               for (int i = 0; i < 4; ++i) z[i] = zn[i];
             }
@@ -1038,7 +1051,7 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
             if (t0 < wend) {  // (the horizon's last, partial group: wend == T)
 #pragma unroll
               for (int s2 = 0; s2 < GS; ++s2)
-                if (t0 + s2 < T) noisy(t0 + s2, s2);
+                if (t0 + s2 < T) noisy(t0 + s2, s2, z);
             }
             w0 = wend;
           }
@@ -1087,16 +1100,18 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
           // a buffer's role is a compile-time index (no register rotation moves): group g runs
           // from buffer g % NB while group g + kHbmDepth is loaded into the buffer group g - 1
           // has just released
-          constexpr int NB = kHbmDepth + 1;
+          // (fp64, the strict-parity precision: one group ahead -- its buffers are twice the registers)
+          constexpr int DEPTH = sizeof(Real) == 8 ? 1 : kHbmDepth;
+          constexpr int NB = DEPTH + 1;
           V eb[NB][GE], jb[NB][GJ];
   #pragma unroll
-          for (int d = 0; d < kHbmDepth; ++d) load_group(d * GS, eb[d], jb[d]);
+          for (int d = 0; d < DEPTH; ++d) load_group(d * GS, eb[d], jb[d]);
           for (int t0 = 0; t0 < T; t0 += NB * GS) {
   #pragma unroll
             for (int r = 0; r < NB; ++r) {
               const int tg = t0 + r * GS;
               if (tg < T) {
-                load_group(tg + kHbmDepth * GS, eb[(r + kHbmDepth) % NB], jb[(r + kHbmDepth) % NB]);  // (clamped inside the horizon)
+                load_group(tg + DEPTH * GS, eb[(r + DEPTH) % NB], jb[(r + DEPTH) % NB]);  // (clamped inside the horizon)
   #pragma unroll
                 for (int s2 = 0; s2 < GS; ++s2) {
                   if (GS == 1 || tg + s2 < T) {
