@@ -16,5 +16,5 @@ run cfg3 cfg3/f32/philox/K=1048576 --workload cfg3
 run hbm_cart1M cfg1/f32/hbm/K=1048576 --workload cfg1 --noise hbm --samples 1048576
 run cfg0 cfg0/f32/philox/K=1024 --workload cfg0
 run cfg2 cfg2/f32/philox/K=8192 --workload cfg2
-ls -la gpurun_out/prof
+ls -la gpurun_out/prof; mkdir -p /tmp/reps && mv gpurun_out/prof/*.ncu-rep /tmp/reps/ 2>/dev/null || true
 cp gpurun_out/prof/kernel_counters.json profiles/kernel_counters.json
