@@ -207,3 +207,30 @@ def test_linear_6x3_long_horizon_with_mapping(gpu_device):
         tol = G_DOUBLE if prec == "f64" else 1e-4
         assert normwise(seq.controls - u_nom, out["u_new"] - u_nom) <= tol, prec
         assert np.allclose(diag.per_step_update_norm, out["norms"], rtol=10 * tol, atol=1e-12), prec
+
+
+@pytest.mark.parametrize("name,K,T,p", [("r_linear_4x2", 20000, 51, 0.08), ("r_linear_6x3", 24000, 37, 0.06),
+                                        ("r_quadrotor_task", 24000, 45, 0.09)])
+def test_indexed_mark_staging_shapes(name, K, T, p, gpu_device):
+    """rollout_fast's indexed mark staging (q >= 2, csrc/rollout_fast.cuh jump_window_idx) on the plugins
+    whose noise groups span 2 steps (m = 2), 1 step (m = 3, 4) and on horizons that end inside a group:
+    the fp64 Philox iteration of the non-warp-specialised kernel against the oracle fed the device
+    sampler's table of the same stream."""
+    import dataclasses
+
+    from paper_1807_06108_b200 import engine
+
+    g, s, model, cost, cfg = _philox_setup(name, K=K, T=T)
+    nu = p / s["dt"]
+    cfg = dataclasses.replace(cfg, nu=nu)  # a few jump events per sample and horizon
+    u_nom = np.resize(g["u_nom"], (T, s["m"]))
+    ctrl = jb.ControllerState(jb.ControlSequence(u_nom, s["dt"]), 2, cfg)
+    ctx = engine.get_context(model, cost, cfg, precision="f64")
+    assert ctx.kernel_name().startswith("rollout_fast/philox/single_wave/f64"), ctx.kernel_name()
+    seq, diag = jb.mppi_iteration(ctrl, model, cost, g["x0"], 5, precision="f64")
+    noise = jb.sample_noise_batch(jb.RngStream(5, 2), cfg, K, model=model, precision="f64")
+    assert 0.2 * nu * s["dt"] < (noise[1] != 0).mean() < 5.0 * nu * s["dt"]
+    ref = om.mppi_iteration_oracle(om.spec_from_plugins(model, cost, cfg), g["x0"], u_nom, noise)
+    assert normwise(seq.controls - u_nom, ref["u_new"] - u_nom) <= 1e-9
+    assert diag.min_cost == pytest.approx(ref["min_cost"], rel=1e-9)
+    assert diag.effective_sample_size == pytest.approx(ref["ess"], rel=1e-8)
