@@ -127,7 +127,11 @@ class Engine final : public EngineBase {
   // (QUAD: the eps'eps term of the modified cost is formed -- c != 1, the general
   // channel, or fed noise, whose non-finite values must still poison the cost)
   // (LDIAG: diagonal-Cholesky form, instantiated where it pays -- packed Philox kernels, m > 1)
+  #ifdef JM_NO_LDIAG
+  static constexpr bool kDiagForm = false;
+#else
   static constexpr bool kDiagForm = kPackable && M > 1;
+#endif
   template <bool PH, int JM, int SPT, bool QUAD, bool LDIAG = false>
   static auto fast_kern() {
     if constexpr (SPT == 2 && kPackable)

@@ -254,13 +254,29 @@ __device__ __forceinline__ void apply_chol(const Real* L, const float* z, Real* 
   }
 }
 
+template <typename Real>
+__device__ __forceinline__ Real radd(Real a, Real b);  // uncontracted add / mul: every kernel
+template <>                                            // (and the oracle) rounds them alike
+__device__ __forceinline__ float radd<float>(float a, float b) { return __fadd_rn(a, b); }
+template <>
+__device__ __forceinline__ double radd<double>(double a, double b) { return __dadd_rn(a, b); }
+template <typename Real>
+__device__ __forceinline__ Real rmul(Real a, Real b);
+template <>
+__device__ __forceinline__ float rmul<float>(float a, float b) { return __fmul_rn(a, b); }
+template <>
+__device__ __forceinline__ double rmul<double>(double a, double b) { return __dmul_rn(a, b); }
+
 // marks = mu + Lj z
 template <int Q, typename Real>
 __device__ __forceinline__ void apply_marks(const Real* Lj, const Real* mu, const float* z, Real* mk) {
   Real c[Q];
   apply_chol<Q, Real>(Lj, z, c);
 #pragma unroll
-  for (int i = 0; i < Q; ++i) mk[i] = mu[i] + c[i];
+  // (an uncontracted add: c[0] is a bare product, and a compiler free to fuse mu + L z into one
+  // fma in some inlining contexts and not in others would give the sampler, the rollout's mark
+  // pass and the regeneration marks that differ in the last bit)
+  for (int i = 0; i < Q; ++i) mk[i] = radd<Real>(mu[i], c[i]);
 }
 
 template <int Q>
@@ -415,18 +431,6 @@ __host__ __device__ __forceinline__ SmemPlan smem_plan(int TM, int tabn, int til
 // dense per-warp buffer wd[(s*Q + i)*32 + lane] (zero where no event), so a
 // step adds its staged value with one conflict-free shared-memory load and
 // no branch.  State jumps (JM = 1) are staged pre-scaled (jscale * mark).
-template <typename Real>
-__device__ __forceinline__ Real radd(Real a, Real b);  // uncontracted add / mul: every kernel
-template <>                                            // (and the oracle) rounds them alike
-__device__ __forceinline__ float radd<float>(float a, float b) { return __fadd_rn(a, b); }
-template <>
-__device__ __forceinline__ double radd<double>(double a, double b) { return __dadd_rn(a, b); }
-template <typename Real>
-__device__ __forceinline__ Real rmul(Real a, Real b);
-template <>
-__device__ __forceinline__ float rmul<float>(float a, float b) { return __fmul_rn(a, b); }
-template <>
-__device__ __forceinline__ double rmul<double>(double a, double b) { return __dmul_rn(a, b); }
 
 // Mark of jump event e: mu + Lj z, or -- Poisson counts -- the sum of the
 // event's n arrivals' iid N(mu, Sigma_J) marks, n mu + sqrt(n) Lj z (n = 1

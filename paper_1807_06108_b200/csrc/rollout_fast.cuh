@@ -67,6 +67,19 @@ __device__ __forceinline__ V vcast(R s) {
 __device__ __forceinline__ float vadd(float a, float b) { return __fadd_rn(a, b); }
 __device__ __forceinline__ double vadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ F2 vadd(F2 a, F2 b) { return a + b; }
+// eps_d + eps_j (control-channel marks): two scalar __fadd_rn, not one packed add.  The f32x2 add
+// -- the __fadd2_rn builtin, and inline `add.rn.f32x2` alike -- was fused with the packed multiply
+// before it (eps = L z, then + mark became one FFMA2), moving eps_c by an ulp against the sampler's
+// scalar sum on most events (tests/test_gpu_fullsize.py
+// test_philox_and_hbm_kernels_agree_control_channel_jumps pins it).  The state-jump sum x + H mark
+// keeps vadd: what precedes it is an fma, which cannot absorb an add.
+__device__ __forceinline__ float vadd_exact(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double vadd_exact(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ F2 vadd_exact(F2 a, F2 b) { return F2(__fadd_rn(a.v.x, b.v.x), __fadd_rn(a.v.y, b.v.y)); }
+// jscale * mark of the fed-noise path, per half for the same reason (the Philox path stages rmul(jscale, mark))
+__device__ __forceinline__ float vmul_exact(float s, float a) { return __fmul_rn(s, a); }
+__device__ __forceinline__ double vmul_exact(double s, double a) { return __dmul_rn(s, a); }
+__device__ __forceinline__ F2 vmul_exact(float s, F2 a) { return F2(__fmul_rn(s, a.v.x), __fmul_rn(s, a.v.y)); }
 
 // eps = L z, fixed fma order (apply_chol in kernels.cuh: the same operations per sample)
 template <int M, typename V, typename S>
@@ -995,7 +1008,7 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
               }
               if (JM == 0) {
   #pragma unroll
-                for (int j = 0; j < M; ++j) eps[j] = vadd(eps[j], mv[j]);  // noise.py:156-157
+                for (int j = 0; j < M; ++j) eps[j] = vadd_exact(eps[j], mv[j]);  // noise.py:156-157
               } else {
   #pragma unroll
                 for (int i = 0; i < Q; ++i) sj[i] = mv[i];
@@ -1118,7 +1131,7 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
                     V sj[Q];
                     if (JM == 1) {
   #pragma unroll
-                      for (int i = 0; i < Q; ++i) sj[i] = jscale * jb[r][s2 * Q + i];
+                      for (int i = 0; i < Q; ++i) sj[i] = vmul_exact(jscale, jb[r][s2 * Q + i]);  // (a bare packed product could fuse into the add)
                     }
                     step(tg + s2, eb[r] + s2 * M, sj, JM == 1 && HJ);
                   }

@@ -135,3 +135,29 @@ def test_philox_and_hbm_kernels_agree_on_the_same_noise(idx, K, T, gpu_device):
     assert a.diag.min_cost == b.diag.min_cost and a.diag.n_finite == b.diag.n_finite
     scale = np.abs(a.u_new - u_nom).max()
     assert np.abs(a.u_new - b.u_new).max() <= 2e-6 * scale
+
+
+def test_philox_and_hbm_kernels_agree_control_channel_jumps(gpu_device):
+    """The same cross-check on the reference's own (control-channel) jump model at a multi-wave shape:
+    the quadrotor task's marks ride on eps_combined (noise.py:156-157), q = m = 4 -- the packed kernel's
+    indexed mark staging with the marks added to the noise instead of the state."""
+    import dataclasses
+
+    from conftest import load_golden, plugins
+
+    g = load_golden("r_quadrotor_task")
+    s = g["spec"]
+    K, T = 80000, 50
+    model, cost, cfg = plugins(s, K=K, T=T)
+    cfg = dataclasses.replace(cfg, nu=0.08 / s["dt"])
+    u_nom = np.resize(g["u_nom"], (T, s["m"]))
+    cp = engine.get_context(model, cost, cfg, precision="f32")
+    assert cp.kernel_name().startswith("rollout_fast/philox/multi_wave/f32/spt2"), cp.kernel_name()
+    a = cp.iteration(g["x0"], u_nom, 3, 1, want_costs=True, want_weights=False)
+    eps_d, ind, eps_j, eps_c = cp.sample_noise(3, 1)
+    assert 0.05 < (ind != 0).mean() < 0.11
+    ch = engine.get_context(model, cost, cfg, precision="f32", hbm=True)
+    b = ch.iteration(g["x0"], u_nom, 3, 1, eps_c=ch.step_major(eps_c, cp.M), want_costs=True, want_weights=False)
+    assert np.array_equal(a.costs, b.costs)
+    scale = np.abs(a.u_new - u_nom).max()
+    assert np.abs(a.u_new - b.u_new).max() <= 2e-6 * scale

@@ -226,7 +226,10 @@ def test_indexed_mark_staging_shapes(name, K, T, p, gpu_device):
     u_nom = np.resize(g["u_nom"], (T, s["m"]))
     ctrl = jb.ControllerState(jb.ControlSequence(u_nom, s["dt"]), 2, cfg)
     ctx = engine.get_context(model, cost, cfg, precision="f64")
-    assert ctx.kernel_name().startswith("rollout_fast/philox/single_wave/f64"), ctx.kernel_name()
+    import os
+
+    if not any(k in os.environ for k in ("JM_WS", "JM_SPT")):  # (tests/test_gpu_variants.py forces other kernels)
+        assert ctx.kernel_name().startswith("rollout_fast/philox/single_wave/f64"), ctx.kernel_name()
     seq, diag = jb.mppi_iteration(ctrl, model, cost, g["x0"], 5, precision="f64")
     noise = jb.sample_noise_batch(jb.RngStream(5, 2), cfg, K, model=model, precision="f64")
     assert 0.2 * nu * s["dt"] < (noise[1] != 0).mean() < 5.0 * nu * s["dt"]
