@@ -328,7 +328,8 @@ def ours_arm(a):
     if world > 1 or os.environ.get("JM_SHARDED_BENCH"):  # (the env var: exercise the sharded path at N=1)
         from paper_1807_06108_b200 import distributed as jd
 
-        return jd.bench_sharded(a, world, rank, local)
+        return jd.bench_sharded(a, world, rank, local, clock_sampler=ClockSampler,
+                                flops_per_state_step=FLOPS_PER_STATE_STEP)
 
     w = WORKLOADS[a.workload]
     idx = w["index"]

@@ -259,10 +259,11 @@ class ShardedLoop:
         return x, it.value, st.value, hal.value, status.value
 
 
-def bench_sharded(a, world: int, rank: int, local: int):
+def bench_sharded(a, world: int, rank: int, local: int, clock_sampler=None, flops_per_state_step=None):
     """bench.py entry for N > 1 (torchrun): weak scaling (K samples per GPU) or
     strong scaling (BASELINE config 3: K in total, K/N per GPU)."""
     import json
+    import time
 
     import torch
     import torch.distributed as dist
@@ -279,26 +280,57 @@ def bench_sharded(a, world: int, rank: int, local: int):
     transport = os.environ.get("JM_EXCHANGE", "nccl")
     loop = ShardedLoop.create(task, cfg, rank, world, local, precision=a.precision, transport=transport,
                               scaling=scaling)
-    loop.init(task.x0, cfg.u_init, 0, 2 * n_total + 64)  # (falls back to NCCL on every rank together)
+    kSettleMax = 20000
+    loop.init(task.x0, cfg.u_init, 0, 3 * n_total + 64 + kSettleMax)  # (falls back to NCCL on every rank together)
     k_local = loop.ctx.K
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    t_w = time.perf_counter()
     for _ in range(a.warmup):
         loop.step()
     torch.cuda.synchronize()
+    tw = torch.tensor([(time.perf_counter() - t_w) / max(1, a.warmup)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(tw, op=dist.ReduceOp.MAX)
+    n_settle = int(min(kSettleMax, max(0.0, 1.0 / max(float(tw.item()), 1e-6)))) if clock_sampler is not None else 0
     # the timed steps are enqueued back to back (no host round trip between
     # them, as the device-resident loop runs); per step an L2 flush outside the
     # step's event pair; barrier + synchronize around the whole region
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    import contextlib
+
+    sampler = clock_sampler(local) if (clock_sampler is not None and rank == 0) else contextlib.nullcontext()
     dist.barrier()
     torch.cuda.synchronize()
-    for i in range(a.steps):
-        with torch.cuda.stream(loop.stream):
-            flush.fill_(i & 0xFF)  # evict L2 between timed steps
-        evs[i][0].record(loop.stream)  # events on the stream the kernels run on
+    with sampler as clk:
+        # ~1 s of untimed steps so rank 0's clock record covers a loaded GPU: the same count on
+        # every rank (the exchange is collective), from the slowest rank's warm-up pace
+        for _ in range(n_settle):
+            loop.step()
+        torch.cuda.synchronize()
+        for i in range(a.steps):
+            with torch.cuda.stream(loop.stream):
+                flush.fill_(i & 0xFF)  # evict L2 between timed steps
+            evs[i][0].record(loop.stream)  # events on the stream the kernels run on
+            loop.step()
+            evs[i][1].record(loop.stream)
+        torch.cuda.synchronize()
+    dist.barrier()
+    # end to end through the public sharded API: per step the loop's step() and a host read of the
+    # plant state it produced (loop.read(): the step's result, device -> host), host wall clock,
+    # barrier on both sides, max over ranks; the closed loop has no per-step host input
+    h0, d0 = C.c_int64(), C.c_int64()
+    h1, d1 = C.c_int64(), C.c_int64()
+    loop.ctx.lib.jm_transfer_bytes(C.byref(h0), C.byref(d0))
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(a.steps):
         loop.step()
-        evs[i][1].record(loop.stream)
-    torch.cuda.synchronize()
+        loop.read()
+    e2e_s = (time.perf_counter() - t0) / a.steps
     dist.barrier()
+    loop.ctx.lib.jm_transfer_bytes(C.byref(h1), C.byref(d1))
+    te = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_s = float(te.item())
     times = [e0.elapsed_time(e1) for e0, e1 in evs]
     t = torch.tensor([float(np.mean(times))], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)  # max over ranks
@@ -326,5 +358,21 @@ def bench_sharded(a, world: int, rank: int, local: int):
                            "exchange": exch, "T": T, "parallelism": f"dp{world}",
                            "l2": "flushed (256 MiB fill) before each timed step"},
                 "mpc_iteration_latency_ms": ms, "gpu_launches": loop.launches_per_step() * a.steps}
+        line["e2e"] = {"value": loop.k_total * T / e2e_s, "unit": "state-steps/s",
+                       "h2d_bytes_per_step": (h1.value - h0.value) // a.steps,
+                       "d2h_bytes_per_step": (d1.value - d0.value) // a.steps, "ms_per_step": 1e3 * e2e_s,
+                       "path": "ShardedLoop.step() + ShardedLoop.read() (plant state to the host) per control step; "
+                               "the closed loop has no per-step host input"}
+        if flops_per_state_step is not None:
+            # whole-job FP32 rate over the whole step (rollout + exchange + finalize: the rollout kernel is not
+            # timed separately here) against N x the live FFMA peak of rank 0's GPU
+            peak = engine.microbench(local)["fp32_tflops"] * world
+            ach = flops_per_state_step[task.name] * loop.k_total * T / (ms * 1e-3) / 1e12
+            line["roofline"] = {"bound": "fp32", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                                "traffic": None, "kernel": loop.ctx.kernel_name() + " (timed: the whole control step)",
+                                "flops_per_state_step": flops_per_state_step[task.name]}
+        cs = clk.summary() if clk is not None else None
+        if cs:
+            line["clocks"] = cs
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
