@@ -137,6 +137,7 @@ class ShardedLoop:
     two_level: bool = None  # p2p only; None: use_two_level(world) (always two-level under strong scaling)
     scaling: str = "weak"
     k_total: int = 0
+    nccl_graph: object = None  # NCCL transport: the captured step (None: not tried yet; False: direct enqueue)
 
     @classmethod
     def create(cls, task, cfg, rank: int, world: int, device: int, precision=None, group=None, transport="nccl",
@@ -232,10 +233,49 @@ class ShardedLoop:
             if self.transport == "p2p":
                 self.graph.replay()
                 return
+            if self.nccl_graph is None:
+                if self._capture_nccl_step():
+                    return  # (the capture's eager step was this control step)
+            if self.nccl_graph:
+                self.nccl_graph.replay()
+                return
             self.ctx.check(lib.jm_loop_rollout(h, C.c_void_p(self.record.data_ptr())))
             gathered = exchange_records(self.record, self.group)
             self.ctx.check(lib.jm_loop_finish(h, C.c_void_p(gathered.data_ptr()), self.world))
         self._keep = gathered  # alive until the stream consumed it
+
+    def _capture_nccl_step(self):
+        """The NCCL transport's step (rollout + reduce, all_gather_into_tensor, finalize) as one CUDA
+        graph, replayed per control step: one launch instead of three enqueues and a collective call.
+        NCCL collectives are capturable; every rank captures the same sequence.  JM_NCCL_GRAPH=0, or a
+        capture that fails on any rank (all ranks then agree to enqueue directly), keeps the direct form."""
+        import torch
+        import torch.distributed as dist
+
+        lib, h = self.ctx.lib, self.ctx.h
+        self.nccl_graph = False
+        want = os.environ.get("JM_NCCL_GRAPH", "1") != "0" and self.record.is_cuda
+        ok, graph, stepped = want, None, False
+        if want:
+            dev = self.record.device
+            self.gathered = torch.empty((self.world,) + tuple(self.record.shape), dtype=self.record.dtype, device=dev)
+            try:
+                # one eager step first: NCCL's lazy communicator setup must not happen under capture
+                self.ctx.check(lib.jm_loop_rollout(h, C.c_void_p(self.record.data_ptr())))
+                dist.all_gather_into_tensor(self.gathered, self.record, group=self.group)
+                self.ctx.check(lib.jm_loop_finish(h, C.c_void_p(self.gathered.data_ptr()), self.world))
+                torch.cuda.synchronize(dev)
+                stepped = True
+                graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(graph, stream=self.stream):
+                    self.ctx.check(lib.jm_loop_rollout(h, C.c_void_p(self.record.data_ptr())))
+                    dist.all_gather_into_tensor(self.gathered, self.record, group=self.group)
+                    self.ctx.check(lib.jm_loop_finish(h, C.c_void_p(self.gathered.data_ptr()), self.world))
+            except (RuntimeError, OSError) as exc:
+                ok, self.nccl_graph_error = False, exc
+        if agree(ok, self.group) and want:
+            self.nccl_graph = graph
+        return stepped
 
     def history(self, steps: int):
         """(states (steps+1, n), controls (steps, m), jumps (steps,)) of the loop so far."""
