@@ -808,12 +808,13 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
   const int nthreads = blockDim.x, nwarps = nthreads >> 5;
   const int tileK = SPT * nthreads;
   const int nb = regen_items(T, GS);
-  // (batched old/new variants: the "old" trials' sampler draws no jumps)
-  const bool jumps = PHILOX && a.jump_on && (a.loop == nullptr || a.loop[blockIdx.y].sampler_jumps);
   constexpr bool IDX = PHILOX && marks_indexed(Q);  // indexed mark staging (q >= 2)
   static_assert(!IDX || GS * 32 < kMarkCap, "one group of steps must fit the mark table");
+  // (the plan depends on kernel parameters only: nothing is read from memory before the
+  // prefetches below are in flight)
+  const bool stage = PHILOX && a.jump_on;
   const FastPlan pl = fast_plan(TM, T * TS, tileK, nthreads, nb,
-                                jumps ? fast_marks_bytes(tileK, nwarps, a.jw_len, Q, (int)sizeof(Real)) : 0, a.gap_n,
+                                stage ? fast_marks_bytes(tileK, nwarps, a.jw_len, Q, (int)sizeof(Real)) : 0, a.gap_n,
                                 (int)sizeof(Real));
   char* const sb = reinterpret_cast<char*>(smem_d);
   double* Nacc = reinterpret_cast<double*>(sb + pl.nacc);
@@ -839,10 +840,26 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
     else if (i - 2 < nl)
       asm volatile("prefetch.global.L2 [%0];" ::"l"(up + 128 * (i - 2)));
   }
+  // indexed staging: bytes [warp][step][lane][half], then the warps' mark tables
+  uint8_t* const ibw = reinterpret_cast<uint8_t*>(marks) + (size_t)(threadIdx.x >> 5) * 32 * a.jw_len;
+  Real* const tabw =
+      reinterpret_cast<Real*>(reinterpret_cast<char*>(marks) + (((size_t)nthreads * a.jw_len + 15) & ~(size_t)15)) +
+      (size_t)(threadIdx.x >> 5) * kMarkCap * Q * SPT;
+  if (stage) {  // the mark staging is zero outside event entries (jump_window_c / jump_window_idx); zeroed
+                // before the grid wait: shared memory is ours, and the stores overlap the prefetches'
+                // (and, in the closed loop, the previous finalize's) latency
+    const size_t zb = IDX ? (size_t)nthreads * a.jw_len : (size_t)SPT * nwarps * 32 * a.jw_len * Q * sizeof(Real);
+    const int n4 = (int)((zb + 15) / 16);
+    float4* z4 = reinterpret_cast<float4*>(marks);
+    for (int i = threadIdx.x; i < n4; i += nthreads) z4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (IDX && (threadIdx.x & 31) < Q * SPT) tabw[threadIdx.x & 31] = Real(0);  // entry 0: no event
+  }
   grid_dep_wait();    // u_nom / x / iteration come from the previous control step
   grid_dep_launch();  // let the finalize grid get resident while the horizon runs
   LoopState* L = a.loop ? a.loop + blockIdx.y : nullptr;
   if (L != nullptr && L->halted) return;
+  // (batched old/new variants: the "old" trials' sampler draws no jumps)
+  const bool jumps = stage && (L == nullptr || L->sampler_jumps);
   const uint64_t iter = L ? L->iteration : (a.iteration_dev ? *a.iteration_dev : a.iteration);
   const double* x0 = L ? L->x : a.x0;
   // timeline row (tuning: JM_TIMELINE), read by each CTA's stamping thread only
@@ -853,18 +870,6 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
     tl_put(tlr, kTlRollWait);
   }
   rollout_prologue<M, Real>(a, L ? loop_unom(L, L->step, TM) : a.u_nom + (size_t)blockIdx.y * TM, tab, Nacc, s_acc, Sg);
-  // indexed staging: bytes [warp][step][lane][half], then the warps' mark tables
-  uint8_t* const ibw = reinterpret_cast<uint8_t*>(marks) + (size_t)(threadIdx.x >> 5) * 32 * a.jw_len;
-  Real* const tabw =
-      reinterpret_cast<Real*>(reinterpret_cast<char*>(marks) + (((size_t)nthreads * a.jw_len + 15) & ~(size_t)15)) +
-      (size_t)(threadIdx.x >> 5) * kMarkCap * Q * SPT;
-  if (jumps) {  // the mark staging is zero outside event entries (jump_window_c / jump_window_idx)
-    const size_t zb = IDX ? (size_t)nthreads * a.jw_len : (size_t)SPT * nwarps * 32 * a.jw_len * Q * sizeof(Real);
-    const int n4 = (int)((zb + 15) / 16);
-    float4* z4 = reinterpret_cast<float4*>(marks);
-    for (int i = threadIdx.x; i < n4; i += nthreads) z4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (IDX && (threadIdx.x & 31) < Q * SPT) tabw[threadIdx.x & 31] = Real(0);  // entry 0: no event
-  }
   __syncthreads();
 
   using S = Real;  // parameter type (scalar_t<V>)
