@@ -609,47 +609,55 @@ __global__ void __launch_bounds__(MAXT) rollout_kernel_ws(const RolloutArgs<Real
       const Real* wl = wd + (c & 31);
       int wnext = 0;
       if (jumps) clock_start(clk, sk, kg, gs);
-      for (int g = 0; g < G; ++g) {
-        const int slot = g % kWsBuf;
-        const int t0 = 4 * g;
-        if (jumps && t0 == wnext) {
-          wnext = t0 + JW;
-          jump_window<Q, QP, JM, Real>(clk, t0, min(wnext, T), JW, sk, kg, gs, Lj, mu, jscale, wd, a.poisson != 0,
-                                       a.cnt);
-          wl = wd + (c & 31);
-        }
-        float z[4 * MP];
-        group_normals<MP>(sk, (uint32_t)t0, kg, z);
-        Real eps[4][M], sj[4][Q];
-#pragma unroll
-        for (int s = 0; s < 4; ++s) {
-          apply_chol<M, Real>(Ld, z + s * MP, eps[s]);
-#pragma unroll
-          for (int i = 0; i < Q; ++i) sj[s][i] = Real(0);
-          if (jumps) {  // staged marks (zero where no event, and past T)
-            if (JM == 0) {
-#pragma unroll
-              for (int j = 0; j < M; ++j) eps[s][j] = radd<Real>(eps[s][j], wl[j * 32]);  // noise.py:156-157
-            } else {
-#pragma unroll
-              for (int i = 0; i < Q; ++i) sj[s][i] = wl[i * 32];
+      // the producers' horizon, unswitched on the sampler's jump flag
+      auto produce = [&](auto jtag) {
+        constexpr bool J = decltype(jtag)::value;
+        for (int g = 0; g < G; ++g) {
+          const int slot = g % kWsBuf;
+          const int t0 = 4 * g;
+          if (J && t0 == wnext) {
+            wnext = t0 + JW;
+            jump_window<Q, QP, JM, Real>(clk, t0, min(wnext, T), JW, sk, kg, gs, Lj, mu, jscale, wd, a.poisson != 0,
+                                         a.cnt);
+            wl = wd + (c & 31);
+          }
+          float z[4 * MP];
+          group_normals<MP>(sk, (uint32_t)t0, kg, z);
+          Real eps[4][M], sj[4][Q];
+  #pragma unroll
+          for (int s = 0; s < 4; ++s) {
+            apply_chol<M, Real>(Ld, z + s * MP, eps[s]);
+  #pragma unroll
+            for (int i = 0; i < Q; ++i) sj[s][i] = Real(0);
+            if constexpr (J) {  // staged marks (zero where no event, and past T)
+              if (JM == 0) {
+  #pragma unroll
+                for (int j = 0; j < M; ++j) eps[s][j] = radd<Real>(eps[s][j], wl[j * 32]);  // noise.py:156-157
+              } else {
+  #pragma unroll
+                for (int i = 0; i < Q; ++i) sj[s][i] = wl[i * 32];
+              }
+              wl += Q * 32;
             }
-            wl += Q * 32;
           }
-        }
-        if (g >= kWsBuf) named_sync(1 + kWsBuf + slot, nb);  // slot drained by the consumers
-        Real* rs = ring + (size_t)slot * GW * C + c;
-#pragma unroll
-        for (int s = 0; s < 4; ++s) {
-#pragma unroll
-          for (int j = 0; j < M; ++j) rs[(s * M + j) * C] = eps[s][j];
-          if (JM == 1) {
-#pragma unroll
-            for (int i = 0; i < Q; ++i) rs[(4 * M + s * Q + i) * C] = sj[s][i];
+          if (g >= kWsBuf) named_sync(1 + kWsBuf + slot, nb);  // slot drained by the consumers
+          Real* rs = ring + (size_t)slot * GW * C + c;
+  #pragma unroll
+          for (int s = 0; s < 4; ++s) {
+  #pragma unroll
+            for (int j = 0; j < M; ++j) rs[(s * M + j) * C] = eps[s][j];
+            if (JM == 1) {
+  #pragma unroll
+              for (int i = 0; i < Q; ++i) rs[(4 * M + s * Q + i) * C] = sj[s][i];
+            }
           }
+          named_arrive(1 + slot, nb);  // slot full
         }
-        named_arrive(1 + slot, nb);  // slot full
-      }
+      };
+      if (jumps)
+        produce(std::true_type{});
+      else
+        produce(std::false_type{});
     } else {
       SysParams<Real> sp = a.sp;
 #pragma unroll
@@ -669,46 +677,55 @@ __global__ void __launch_bounds__(MAXT) rollout_kernel_ws(const RolloutArgs<Real
 #pragma unroll
       for (int i = 0; i < N; ++i) x[i] = Real(x0[i]);
       Real S = Real(0);
-      auto step = [&](const int t, const Real* eps, const Real* sj) {
-        const auto ax = Dyn::template aux<Real, true>(x, sp);
-        const Real qv = Cost::template q<Dyn, Real>(x, ax, sp);
-        const Real* st = tab + t * TS;
-        Real inc = fma(qv, dt, st[M]);
-        const Real quad = a.general ? noise_quad<M, Real, true>(a, eps) : noise_quad<M, Real, false>(a, eps);
-#pragma unroll
-        for (int j = 0; j < M; ++j) inc = fma(st[M + 1 + j], eps[j], inc);
-        S += fma(cq, quad, inc);  // costs.py:98-111 times dt
-        Real v[M];
-#pragma unroll
-        for (int j = 0; j < M; ++j) v[j] = fma(eps[j], sdt, st[j]);
-        Dyn::template advance<Real>(x, ax, v, dt, sp);  // dynamics.py:130-135
-        if (JM == 1) {
-#pragma unroll
-          for (int i = 0; i < Q; ++i) x[Dyn::jump_row(i)] = radd<Real>(x[Dyn::jump_row(i)], sj[i]);  // x + H (ind * mark)
+      // the consumers' horizon, unswitched on the general-channel flag (a uniform run-time branch
+      // inside the step would split the 4-step group's basic block)
+      auto consume = [&](auto gtag) {
+        constexpr bool GEN = decltype(gtag)::value;
+        auto step = [&](const int t, const Real* eps, const Real* sj) {
+          const auto ax = Dyn::template aux<Real, true>(x, sp);
+          const Real qv = Cost::template q<Dyn, Real>(x, ax, sp);
+          const Real* st = tab + t * TS;
+          Real inc = fma(qv, dt, st[M]);
+          const Real quad = noise_quad<M, Real, GEN>(a, eps);
+  #pragma unroll
+          for (int j = 0; j < M; ++j) inc = fma(st[M + 1 + j], eps[j], inc);
+          S += fma(cq, quad, inc);  // costs.py:98-111 times dt
+          Real v[M];
+  #pragma unroll
+          for (int j = 0; j < M; ++j) v[j] = fma(eps[j], sdt, st[j]);
+          Dyn::template advance<Real>(x, ax, v, dt, sp);  // dynamics.py:130-135
+          if (JM == 1) {
+  #pragma unroll
+            for (int i = 0; i < Q; ++i) x[Dyn::jump_row(i)] = radd<Real>(x[Dyn::jump_row(i)], sj[i]);  // x + H (ind * mark)
+          }
+        };
+        for (int g = 0; g < G; ++g) {
+          const int slot = g % kWsBuf;
+          named_sync(1 + slot, nb);
+          const Real* rs = ring + (size_t)slot * GW * C + c;
+          Real e[4 * M], jv[(JM == 1) ? 4 * Q : 1];
+  #pragma unroll
+          for (int i = 0; i < 4 * M; ++i) e[i] = rs[i * C];
+          if (JM == 1) {
+  #pragma unroll
+            for (int i = 0; i < 4 * Q; ++i) jv[i] = rs[(4 * M + i) * C];
+          }
+          if (g < G - kWsBuf) named_arrive(1 + kWsBuf + slot, nb);
+          const int t0 = 4 * g;
+          if (t0 + 4 <= T) {
+  #pragma unroll
+            for (int s = 0; s < 4; ++s) step(t0 + s, e + s * M, jv + (JM == 1 ? s * Q : 0));
+          } else {
+  #pragma unroll
+            for (int s = 0; s < 4; ++s)
+              if (t0 + s < T) step(t0 + s, e + s * M, jv + (JM == 1 ? s * Q : 0));
+          }
         }
       };
-      for (int g = 0; g < G; ++g) {
-        const int slot = g % kWsBuf;
-        named_sync(1 + slot, nb);
-        const Real* rs = ring + (size_t)slot * GW * C + c;
-        Real e[4 * M], jv[(JM == 1) ? 4 * Q : 1];
-#pragma unroll
-        for (int i = 0; i < 4 * M; ++i) e[i] = rs[i * C];
-        if (JM == 1) {
-#pragma unroll
-          for (int i = 0; i < 4 * Q; ++i) jv[i] = rs[(4 * M + i) * C];
-        }
-        if (g < G - kWsBuf) named_arrive(1 + kWsBuf + slot, nb);
-        const int t0 = 4 * g;
-        if (t0 + 4 <= T) {
-#pragma unroll
-          for (int s = 0; s < 4; ++s) step(t0 + s, e + s * M, jv + (JM == 1 ? s * Q : 0));
-        } else {
-#pragma unroll
-          for (int s = 0; s < 4; ++s)
-            if (t0 + s < T) step(t0 + s, e + s * M, jv + (JM == 1 ? s * Q : 0));
-        }
-      }
+      if (a.general)
+        consume(std::true_type{});
+      else
+        consume(std::false_type{});
       bool fin = true;
 #pragma unroll
       for (int i = 0; i < N; ++i) fin = fin && isfinite(x[i]);
