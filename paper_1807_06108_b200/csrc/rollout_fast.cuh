@@ -954,7 +954,9 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
       }
 
       // one horizon step t with its eps_combined and state-jump increment
-      auto step = [&](const int t, const V* eps, const V* sj, const bool has_sj) {
+      // (gen: the general-channel form eps' bb eps, a compile-time tag -- a uniform run-time branch
+      // here would split every step's basic block)
+      auto step = [&](auto gen, const int t, const V* eps, const V* sj, const bool has_sj) {
         const auto ax = Dyn::template aux<V, true>(x, sp);
         const V qv = Cost::template q<Dyn, V>(x, ax, sp);
         const Real* st = tab + t * TS;
@@ -967,7 +969,7 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
           V quad = eps[0] * eps[0];
 #pragma unroll
           for (int j = 1; j < M; ++j) quad = fma(eps[j], eps[j], quad);
-          if (a.general) {  // eps' bb eps (costs.py:118-121)
+          if constexpr (decltype(gen)::value) {  // eps' bb eps (costs.py:118-121)
             quad = vcast<V>(0.0);
 #pragma unroll
             for (int i = 0; i < M; ++i) {
@@ -992,7 +994,7 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
       if constexpr (PHILOX) {
         // the horizon, unswitched on the sampler's jumps (a uniform run-time flag): each form is
         // straight-line per noise group, so the next group's Philox block overlaps the dynamics
-        auto horizon = [&](auto jtag) {
+        auto horizon = [&](auto jtag, auto gtag) {
           constexpr bool J = decltype(jtag)::value;
           V z[4], zn[4];
           block_normals_v(sk, 0u, kg, z);
@@ -1037,7 +1039,7 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
                 has_sj = true;
               }
             }
-            step(t, eps, sj, has_sj);
+            step(gtag, t, eps, sj, has_sj);
           };
           // outer loop: one jump window (the whole horizon without jumps); inner loop: its noise
           // groups, nothing but the groups -- the window code stays out of the hot loop's live ranges
@@ -1091,10 +1093,21 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
             w0 = wend;
           }
         };
-        if (jumps)
-          horizon(std::true_type{});
-        else
-          horizon(std::false_type{});
+        // (the general-channel form exists only in the QUAD kernels)
+        const bool gen = QUAD && a.general;
+        if (jumps) {
+          if (gen) {
+            if constexpr (QUAD) horizon(std::true_type{}, std::true_type{});
+          } else {
+            horizon(std::true_type{}, std::false_type{});
+          }
+        } else {
+          if (gen) {
+            if constexpr (QUAD) horizon(std::false_type{}, std::true_type{});
+          } else {
+            horizon(std::false_type{}, std::false_type{});
+          }
+        }
       } else {
         // HBM wire format eps[(t*M + j)*K + k], jump[(t*Q + i)*K + k]: a thread's
         // SPT samples are adjacent columns (one 8-byte load for both), groups
@@ -1114,7 +1127,7 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
           }
         };
         // the horizon, unswitched on whether a jump tensor was fed (a uniform run-time flag)
-        auto horizon = [&](auto jtag) {
+        auto horizon = [&](auto jtag, auto gtag) {
           constexpr bool HJ = decltype(jtag)::value;
           auto load_group = [&](int g0, V* ze, V* zj) {
   #pragma unroll
@@ -1155,17 +1168,27 @@ __global__ void __launch_bounds__(MAXT, (SPT == 2 ? 2 : 1)) rollout_fast(const R
   #pragma unroll
                       for (int i = 0; i < Q; ++i) sj[i] = vmul_exact(jscale, jb[r][s2 * Q + i]);  // (a bare packed product could fuse into the add)
                     }
-                    step(tg + s2, eb[r] + s2 * M, sj, JM == 1 && HJ);
+                    step(gtag, tg + s2, eb[r] + s2 * M, sj, JM == 1 && HJ);
                   }
                 }
               }
             }
           }
         };
-        if (hj)
-          horizon(std::true_type{});
-        else
-          horizon(std::false_type{});
+        const bool gen = QUAD && a.general;
+        if (hj) {
+          if (gen) {
+            if constexpr (QUAD) horizon(std::true_type{}, std::true_type{});
+          } else {
+            horizon(std::true_type{}, std::false_type{});
+          }
+        } else {
+          if (gen) {
+            if constexpr (QUAD) horizon(std::false_type{}, std::true_type{});
+          } else {
+            horizon(std::false_type{}, std::false_type{});
+          }
+        }
       }
       if (tlr != nullptr) {  // (timeline: the first and the last CTA to finish the horizon)
         tl_max(tlr, kTlRollHorizonEndMax);
