@@ -129,7 +129,9 @@ def test_device_poisson_moments(gpu_device):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("name,K", [("b_cartpole", 256), ("b_cartpole", 8192), ("r_cartpole_task", 2048),
-                                    ("b_quadrotor", 1024), ("r_quadrotor_task", 8192)])
+                                    ("b_quadrotor", 1024), ("r_quadrotor_task", 8192),
+                                    # (rollout_fast with the indexed mark staging: state and control-channel marks)
+                                    ("b_quadrotor", 24000), ("r_quadrotor_task", 24000)])
 def test_f64_poisson_iteration_matches_oracle(name, K, gpu_device):
     """The rollout kernels (warp-specialised and main, per K) consume exactly
     the Poisson noise sample_noise_batch exports."""
