@@ -113,14 +113,19 @@ def test_full_size_properties(case, idx, K, T, variant, gpu_device):
     assert np.abs(du_merged - du).max() <= 2e-6 * scale
 
 
-@pytest.mark.parametrize("idx,K,T", [(1, 65536, 100), (3, 32768, 200)])
-def test_philox_and_hbm_kernels_agree_on_the_same_noise(idx, K, T, gpu_device):
+@pytest.mark.parametrize("idx,K,T,process", [(1, 65536, 100, "bernoulli"), (3, 32768, 200, "bernoulli"),
+                                             (3, 80000, 30, "poisson"), (1, 160000, 40, "poisson")])
+def test_philox_and_hbm_kernels_agree_on_the_same_noise(idx, K, T, process, gpu_device):
     """The two product kernels against each other at BASELINE shapes: the device sampler's table of
     stream (seed, iteration) -- the very draws the Philox kernel makes in registers -- fed to the
     HBM kernel in the fp32 wire format gives the same per-sample costs bit for bit (the same
     arithmetic per sample; with c = 1 the eps'eps term the fed-noise kernel forms is multiplied by
     an exact 0) and the same update to the fp32 exponentials' rounding."""
+    import dataclasses
+
     task, cfg = jb.baseline_config(idx, K=K, T=T)
+    if process == "poisson":  # compound-Poisson arrival counts, at a rate where multi-arrival steps occur
+        cfg = dataclasses.replace(cfg, nu=0.09 / cfg.dt, jump_process="poisson")
     seed, it = 5, 2
     u_nom = np.tile(np.atleast_1d(np.asarray(cfg.u_init, float)), (T, 1))
     cp = engine.get_context(task.model, task.cost_model, cfg, precision="f32")
